@@ -1,0 +1,183 @@
+/*
+ * moeb200.h — C ABI of the B200-native decode-time MoE offloading engine.
+ *
+ * The reference (``moe_offload``, /root/reference/pkg/src/moe_offload) is a
+ * pure-Python package with no FFI; its drop-in seams for this hot path are the
+ * ``_Session`` / ``OffloadEngine`` methods listed beside each entry point.
+ * The Python mirror ``paper_2312_17238_b200.engine.OffloadEngine`` binds these
+ * symbols with ctypes and maps the status codes onto the
+ * reference exception classes.
+ *
+ * Conventions: plain pointers and sizes, no torch types; every call returns a
+ * MOE_* status and ``moe_last_error()`` returns the thread-local message of the
+ * last failure.  One host thread drives one engine; the engine owns its CUDA
+ * streams, device memory, pinned host arena and copy-engine thread.
+ */
+#ifndef MOEB200_H
+#define MOEB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> reference exceptions (engine.py maps them) */
+#define MOE_OK 0
+#define MOE_ERR_VALUE 1           /* ValueError                                  */
+#define MOE_ERR_RUNTIME 2         /* RuntimeError (e.g. decode before prefill)   */
+#define MOE_ERR_NONFINITE 3       /* model.NonFiniteError (model.py:36)          */
+#define MOE_ERR_UNKNOWN_EXPERT 4  /* store.UnknownExpertError (store.py:42)      */
+#define MOE_ERR_FORMAT 5          /* quant.QuantFormatError (quant.py:30)        */
+#define MOE_ERR_CUDA 6            /* CUDA / driver failure                       */
+#define MOE_ERR_TIMEOUT 7         /* a slot-ready flag never arrived             */
+
+/* event kinds, numbered like store.EVENT_KINDS (store.py:29-30) */
+#define MOE_EV_HIT 0
+#define MOE_EV_STAGING_HIT 1
+#define MOE_EV_MISS_LOAD 2
+#define MOE_EV_EVICT_TO_HOST 3
+#define MOE_EV_SPECULATIVE_LOAD 4
+#define MOE_EV_PROMOTE_FROM_STAGING 5
+
+typedef struct moe_engine moe_engine;
+
+/* model.ModelConfig (model.py:40-77) */
+typedef struct {
+  int32_t vocab_size, d_model, n_layers, n_heads, d_ffn, n_experts, top_k, max_seq_len;
+} moe_model_desc;
+
+/* store.CacheConfig (store.py:46-56); expert_bytes already resolved the way
+ * OffloadEngine.__init__ does (engine.py:211-214) */
+typedef struct {
+  int32_t k, b;
+  int64_t expert_bytes;
+} moe_cache_cfg;
+
+/* engine.SpeculationConfig (engine.py:43-57) */
+typedef struct {
+  int32_t enabled, m, lookahead;
+} moe_spec_cfg;
+
+/* One 2-D matrix.  bits 2/3/4: a quant.QuantizedBlock in the reference layout
+ * (quant.py:76-102; ``zeros`` unpacked, one u8 code per group; f16 arrays as
+ * raw uint16).  bits 16 / 32: raw row-major float16 / float32 values in
+ * ``codes``. */
+typedef struct {
+  int32_t bits, group_size, scale_group_size, meta_bits;
+  int32_t rows, cols, pad_count;
+  const void* codes;
+  int64_t codes_len;
+  const uint8_t* zeros;
+  int64_t n_groups;
+  const uint16_t* zero_scales;
+  const uint16_t* zero_offsets;
+  int64_t n_zruns;
+  const uint16_t* scales;
+  int64_t n_scales;
+} moe_matrix;
+
+/* store.StoreEvent (store.py:59-73) */
+typedef struct {
+  int64_t seq;
+  int32_t kind, layer, expert, token_pos;
+  int64_t bytes_moved;
+} moe_event;
+
+/* trace.TraceRecord without the hidden vector (trace.py:38-51) */
+typedef struct {
+  int32_t token_pos, layer;
+  int32_t experts[8];
+  float weights[8];
+} moe_trace_rec;
+
+typedef struct {
+  int64_t h2d_copies, h2d_bytes;
+  double h2d_busy_ms;       /* copy-stream busy time, CUDA events            */
+  double h2d_peak_gbs;      /* best single-copy GB/s seen                      */
+  int64_t n_buffers;        /* physical expert buffers in HBM                  */
+  int64_t slot_bytes;       /* bytes per expert buffer                         */
+  int64_t device_bytes;     /* total device allocation                         */
+  int64_t arena_bytes;      /* pinned host arena                               */
+  int64_t kernel_launches;  /* kernels launched by the last API call           */
+  double last_call_ms;      /* device time of the last prefill/decode/step     */
+} moe_stats;
+
+/* OffloadEngine.__init__ (engine.py:204-220): validates the geometry (k <= E,
+ * m <= b) and allocates device state; weights are loaded afterwards. */
+int moe_create(const moe_model_desc* model, const moe_cache_cfg* cache,
+               const moe_spec_cfg* spec, int32_t device, int32_t record_hidden,
+               moe_engine** out);
+
+/* Model.params[name] (model.py:145-175 naming): "wte", "wpe", "lm_head",
+ * "ln_f.gamma", "ln_f.beta", "layers.{l}.ln1.gamma", ..., "layers.{l}.attn.wq",
+ * "layers.{l}.gate".  Attention projections may be quantized blocks. */
+int moe_load_tensor(moe_engine* eng, const char* name, const moe_matrix* m);
+
+/* One host-arena payload (the store's canonical copy, store.py:85-92):
+ * w_gate_proj, w_up_proj, w_down_proj of expert (layer, expert). */
+int moe_load_expert(moe_engine* eng, int32_t layer, int32_t expert, const moe_matrix* w_gate,
+                    const moe_matrix* w_up, const moe_matrix* w_down);
+
+/* Device-side synthetic weights (counter hash, see oracle/model.py
+ * synth_params), quantized on device with the reference quantizer
+ * (quant.py:181-229); attn_bits/expert_bits in {2,3,4,32}. */
+int moe_synth_model(moe_engine* eng, uint64_t seed, int32_t attn_bits, int32_t expert_bits);
+
+/* Checks that every tensor/expert is present, builds the expert buffer pool
+ * and starts the copy engine.  Must precede prefill/step/decode. */
+int moe_finalize(moe_engine* eng);
+
+/* _Session.prefill (engine.py:148-156) incl. _resolve_prefill_layer
+ * (engine.py:233-240).  logits_out: n*vocab floats or NULL. */
+int moe_prefill(moe_engine* eng, const int32_t* tokens, int32_t n, float* logits_out);
+
+/* _Session.run_token (engine.py:158-166) with _resolve_token
+ * (engine.py:222-231); logits_out: vocab floats or NULL. */
+int moe_step(moe_engine* eng, int32_t token, float* logits_out);
+
+/* _Session.decode with the greedy sampler (engine.py:168-182,
+ * model.py:374-375), sampling on device: tokens_out n ids, final_logits_out
+ * vocab floats (or NULL). */
+int moe_decode_greedy(moe_engine* eng, int32_t n, int32_t* tokens_out, float* final_logits_out);
+
+/* OffloadEngine.events / store.events (engine.py:242-244) */
+int64_t moe_num_events(moe_engine* eng);
+int moe_read_events(moe_engine* eng, int64_t start, int64_t count, moe_event* out);
+
+/* _Session._records / trace() (engine.py:122-144), current session only,
+ * (token_pos, layer) order; hidden_out: count*d_model floats or NULL. */
+int64_t moe_num_trace(moe_engine* eng);
+int moe_read_trace(moe_engine* eng, int64_t start, int64_t count, moe_trace_rec* out,
+                   float* hidden_out);
+
+/* _Session.reset_session (engine.py:100-110): KV and position, not the store */
+int moe_reset_session(moe_engine* eng);
+
+/* device LRU state (store.device_state, store.py:108-109): out[l*k + i] =
+ * expert id (MRU first), -1 padded; staged: b entries of layer*E+expert or -1 */
+int moe_device_state(moe_engine* eng, int32_t* lru_out, int32_t* staged_out);
+
+int moe_get_stats(moe_engine* eng, moe_stats* out);
+const char* moe_last_error(void);
+int moe_destroy(moe_engine* eng);
+
+/* Standalone kernels exposed for parity tests (no engine needed):
+ * quantize a row-major fp32 matrix on device into the reference layout
+ * (quant.py:181-229); outputs sized as quant.py's arrays. */
+int moe_quantize_device(const float* w, int32_t rows, int32_t cols, int32_t bits,
+                        int32_t group_size, int32_t scale_group_size, uint8_t* codes_out,
+                        uint8_t* zeros_out, uint16_t* zscales_out, uint16_t* zoffsets_out,
+                        uint16_t* scales_out);
+
+/* y = x @ dequantize(m) through the engine's GEMV kernel (fp32 accumulate). */
+int moe_gemv_device(const moe_matrix* m, const float* x, float* y);
+
+/* synthetic tensor (oracle/model.py synth_tensor) generated on device */
+int moe_synth_tensor_device(uint64_t seed, uint64_t tensor_id, int64_t count, float scale,
+                            float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOEB200_H */

@@ -1,0 +1,1542 @@
+// Host side of the B200 MoE offloading engine: the C ABI of include/moeb200.h.
+//
+// Owns: device weights in the tiled layout, the pinned host arena (canonical
+// expert copies, store.py:85-92), the HBM expert-buffer pool, the device
+// store state (store_dev.cuh), and a copy-engine thread that drains the
+// device's copy-request mailbox with cudaMemcpyAsync on a side stream and
+// marks each buffer ready with cuStreamWriteValue32 (kernels wait on it).
+#include <cuda.h>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t _e = (call);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return fail(MOE_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));         \
+  } while (0)
+
+int ilog2(int v) {
+  int r = 0;
+  while ((1 << r) < v) ++r;
+  return ((1 << r) == v) ? r : -1;
+}
+
+struct DevMat {  // one tiled matrix in device memory
+  MatDev M{};
+  void* mem = nullptr;
+  size_t bytes = 0;
+  int bits = 0;
+  int ncb = 0, nchunks = 0, nquads = 0;
+};
+
+struct Layout {  // byte sections of one tiled matrix
+  int bits = 0, K = 0, N = 0, g = 0, sg = 0;
+  size_t rec = 0, scales = 0, zeros = 0, zmeta = 0;
+  int64_t nruns = 0;
+  size_t total() const { return rec + scales + zeros + zmeta; }
+};
+
+int make_layout(const moe_matrix* m, Layout* L, const char* what) {
+  const int bits = m->bits;
+  if (bits != 2 && bits != 3 && bits != 4 && bits != 16 && bits != 32)
+    return fail(MOE_ERR_VALUE, std::string(what) + ": unsupported bits " + std::to_string(bits));
+  const int K = m->rows, N = m->cols;
+  if (K < 1 || N < 1) return fail(MOE_ERR_VALUE, std::string(what) + ": empty matrix");
+  const int wc = fmt_wc(bits);
+  if (K % 4) return fail(MOE_ERR_VALUE, std::string(what) + ": rows must be a multiple of 4");
+  if (N % wc)
+    return fail(MOE_ERR_VALUE,
+                std::string(what) + ": cols must be a multiple of " + std::to_string(wc));
+  L->bits = bits;
+  L->K = K;
+  L->N = N;
+  if (bits >= 16) {
+    const int64_t need = (int64_t)K * N * (bits / 8);
+    if (m->codes_len != need) return fail(MOE_ERR_FORMAT, std::string(what) + ": payload size mismatch");
+    L->rec = need;
+    return MOE_OK;
+  }
+  const int g = m->group_size, sg = m->scale_group_size;
+  if (m->meta_bits != 8) return fail(MOE_ERR_VALUE, std::string(what) + ": meta_bits must be 8");
+  if (m->pad_count != 0 || N % g)
+    return fail(MOE_ERR_VALUE, std::string(what) + ": cols must be a multiple of group_size");
+  if (ilog2(g) < 0 || ilog2(sg) < 0 || g % wc || sg % g || N % sg)
+    return fail(MOE_ERR_VALUE, std::string(what) + ": unsupported grouping for the device layout");
+  if (((int64_t)g * bits) % 32) return fail(MOE_ERR_VALUE, std::string(what) + ": group not word aligned");
+  const int64_t ng = (int64_t)K * N / g;
+  const int64_t nsg = (ng + sg / g - 1) / (sg / g);
+  const int64_t nruns = (ng + sg - 1) / sg;
+  if (m->codes_len != (int64_t)K * N * bits / 8 || m->n_groups != ng || m->n_scales != nsg ||
+      m->n_zruns != nruns)
+    return fail(MOE_ERR_FORMAT, std::string(what) + ": block arrays inconsistent with shape");
+  L->g = g;
+  L->sg = sg;
+  L->rec = (size_t)K * N * bits / 8;
+  L->scales = (size_t)nsg * 2;
+  L->zeros = (size_t)ng;
+  L->zmeta = (size_t)nruns * 4;
+  L->nruns = nruns;
+  return MOE_OK;
+}
+
+MatDev matdev_from(const Layout& L, const uint8_t* base) {
+  MatDev M{};
+  M.rec = reinterpret_cast<const uint4*>(base);
+  M.scales = reinterpret_cast<const uint2*>(base + L.rec);
+  M.zeros = reinterpret_cast<const uint32_t*>(base + L.rec + L.scales);
+  M.zmeta = reinterpret_cast<const __half2*>(base + L.rec + L.scales + L.zeros);
+  M.K = L.K;
+  M.N = L.N;
+  M.bits = L.bits;
+  if (L.bits <= 4) {
+    M.G = L.N / L.g;
+    M.S = L.N / L.sg;
+    M.g_log2 = ilog2(L.g);
+    M.sg_log2 = ilog2(L.sg);
+  }
+  return M;
+}
+
+// tile a reference-layout matrix already resident on device into `dst`
+int tile_device(const RefMat& R, const Layout& L, uint8_t* dst, cudaStream_t s) {
+  launch_tile(R, dst, reinterpret_cast<uint32_t*>(dst + L.rec + L.scales),
+              reinterpret_cast<uint2*>(dst + L.rec),
+              reinterpret_cast<__half2*>(dst + L.rec + L.scales + L.zeros), s);
+  CU(cudaGetLastError());
+  return MOE_OK;
+}
+
+RefMat refmat_of(const Layout& L) {
+  RefMat R{};
+  R.bits = L.bits;
+  R.K = L.K;
+  R.N = L.N;
+  R.g = L.g;
+  R.sg = L.sg;
+  R.nruns = L.nruns;
+  return R;
+}
+
+// upload a reference-layout matrix and tile it into `dst` (device, L.total() bytes)
+int upload_and_tile(const moe_matrix* m, const Layout& L, uint8_t* dst, cudaStream_t s) {
+  uint8_t* scratch = nullptr;
+  const size_t cbytes = m->codes_len;
+  size_t tot = cbytes + 16;
+  if (L.bits <= 4) tot += m->n_groups + 16 + 2 * (2 * m->n_zruns + m->n_scales) + 64;
+  CU(cudaMalloc(&scratch, tot));
+  uint8_t* p = scratch;
+  RefMat R = refmat_of(L);
+  CU(cudaMemcpyAsync(p, m->codes, cbytes, cudaMemcpyHostToDevice, s));
+  R.codes = p;
+  p += (cbytes + 15) & ~size_t(15);
+  if (L.bits <= 4) {
+    CU(cudaMemcpyAsync(p, m->zeros, m->n_groups, cudaMemcpyHostToDevice, s));
+    R.zeros = p;
+    p += (m->n_groups + 15) & ~int64_t(15);
+    CU(cudaMemcpyAsync(p, m->zero_scales, 2 * m->n_zruns, cudaMemcpyHostToDevice, s));
+    R.zs = reinterpret_cast<const uint16_t*>(p);
+    p += (2 * m->n_zruns + 15) & ~int64_t(15);
+    CU(cudaMemcpyAsync(p, m->zero_offsets, 2 * m->n_zruns, cudaMemcpyHostToDevice, s));
+    R.zo = reinterpret_cast<const uint16_t*>(p);
+    p += (2 * m->n_zruns + 15) & ~int64_t(15);
+    CU(cudaMemcpyAsync(p, m->scales, 2 * m->n_scales, cudaMemcpyHostToDevice, s));
+    R.scales = reinterpret_cast<const uint16_t*>(p);
+  }
+  int rc = tile_device(R, L, dst, s);
+  CU(cudaStreamSynchronize(s));
+  CU(cudaFree(scratch));
+  return rc;
+}
+
+struct CopyRec {
+  cudaEvent_t a, b;
+  int64_t bytes;
+};
+
+// cuStreamWriteValue32 resolved through the runtime (no link-time libcuda
+// dependency, so the library loads on hosts without a driver).
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_writeValue32 write_value32() {
+  static PFN_writeValue32 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_writeValue32>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+struct moe_engine {
+  moe_model_desc md{};
+  moe_cache_cfg cc{};
+  moe_spec_cfg sc{};
+  int dev = 0;
+  bool rec_hidden = true;
+  cudaStream_t s_comp = nullptr, s_copy = nullptr;
+  int attn_bits = 0, expert_bits = 0, lm_bits = 0;
+  int d = 0, f = 0, V = 0, L = 0, E = 0, H = 0, hd = 0, T = 0, topk = 0;
+
+  // dense weights
+  void* wte = nullptr;
+  void* wpe = nullptr;
+  int emb_half = -1;
+  DevMat lm_head;
+  std::vector<DevMat> wq, wk, wv, wo;
+  std::vector<float*> ln1g, ln1b, ln2g, ln2b, gate;
+  float *lnfg = nullptr, *lnfb = nullptr;
+  std::vector<bool> have;  // named tensor presence
+
+  // experts
+  Layout xl[3];
+  bool xl_set = false;
+  size_t xoff[3][4] = {};  // per matrix: rec, scales, zeros, zmeta offsets in a buffer
+  size_t xbytes = 0, slot_stride = 0;
+  uint8_t* arena = nullptr;
+  std::vector<bool> loaded;
+  uint8_t* pool = nullptr;
+  uint32_t* flags = nullptr;
+  int nbuf = 0;
+
+  // activations
+  float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
+  float *qkv_part = nullptr, *wo_part = nullptr, *up_part = nullptr, *dn_part = nullptr,
+        *lm_part = nullptr;
+  int S_qkv = 1, S_wo = 1, S_up = 1, S_dn = 1, S_lm = 1;
+  float *kc = nullptr, *vc = nullptr;
+  RouteRec* route = nullptr;
+  TraceRecDev* trace = nullptr;
+  float* trace_hidden = nullptr;
+  int* tok_dev = nullptr;
+  int* tok_hist = nullptr;
+  int* tok_in = nullptr;
+  float* cand_val = nullptr;
+  int* cand_idx = nullptr;
+  unsigned int* counter = nullptr;
+  int* err = nullptr;
+
+  // store
+  StoreDev st{};
+  void* st_mem = nullptr;
+  Mailbox* mb_host = nullptr;
+  Mailbox* mb_dev = nullptr;
+  int ev_cap = 0;
+
+  // copy engine
+  std::thread copier;
+  std::atomic<bool> stop{false};
+  std::mutex cmu;
+  std::vector<CopyRec> copies;
+  int64_t n_copies = 0, copy_bytes = 0;
+  double busy_ms = 0, peak_gbs = 0;
+  std::vector<cudaEvent_t> free_events;
+
+  // session
+  int pos = 0;
+  bool has_logits = false;
+  bool finalized = false;
+  std::vector<moe_event> events;
+  int64_t launches = 0;
+  double last_ms = 0;
+  unsigned long long wait_ns = 60000000000ull;
+  bool debug = false;
+  // run-ahead bound: the host may enqueue at most `ahead` units (one layer of
+  // one position) beyond the oldest unfinished one, so the launch queue never
+  // fills while a kernel waits for the copy engine.
+  std::vector<cudaEvent_t> ring;
+  int64_t units_issued = 0, units_done = 0;
+  int ahead = 3;
+  int throttle();
+  int unit_done();
+  int dbg(const char* what, int l, int p);
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  size_t dev_bytes = 0;
+
+  ~moe_engine();
+  template <class T>
+  int dalloc(T** p, size_t n) {
+    CU(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+    CU(cudaMemset(*p, 0, n * sizeof(T)));
+    dev_bytes += n * sizeof(T);
+    return MOE_OK;
+  }
+  int run_copier();
+  int enq_attention(int l, int p, int mode);
+  int enq_experts(int p);
+  int enq_logits(int p, float* out);
+  int finish_call();
+  int choose_splits(int njobs, int ncb, int nquads) const;
+  GJob dense_job(const DevMat& D, const float* x, float* out, int S) const;
+};
+
+moe_engine::~moe_engine() {
+  stop.store(true);
+  if (copier.joinable()) copier.join();
+  if (s_copy) cudaStreamSynchronize(s_copy);
+  if (s_comp) cudaStreamSynchronize(s_comp);
+  for (auto& c : copies) {
+    cudaEventDestroy(c.a);
+    cudaEventDestroy(c.b);
+  }
+  for (auto e : free_events) cudaEventDestroy(e);
+  for (auto e : ring) cudaEventDestroy(e);
+  void* ptrs[] = {wte, wpe, lm_head.mem, lnfg, lnfb, pool, flags, x, h, xn, ctx, logits,
+                  qkv_part, wo_part, up_part, dn_part, lm_part, kc, vc, route, trace,
+                  trace_hidden, tok_dev, tok_hist, tok_in, cand_val, cand_idx, counter, err,
+                  st_mem};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto* v : {&wq, &wk, &wv, &wo})
+    for (auto& m : *v)
+      if (m.mem) cudaFree(m.mem);
+  for (auto* v : {&ln1g, &ln1b, &ln2g, &ln2b, &gate})
+    for (auto p : *v)
+      if (p) cudaFree(p);
+  if (arena) cudaFreeHost(arena);
+  if (mb_host) cudaFreeHost(mb_host);
+  if (t0) cudaEventDestroy(t0);
+  if (t1) cudaEventDestroy(t1);
+  if (s_comp) cudaStreamDestroy(s_comp);
+  if (s_copy) cudaStreamDestroy(s_copy);
+}
+
+// The copy engine: drains the device mailbox in FIFO order.  Each request is
+// one contiguous H2D copy of a whole expert (paper §3.3 contiguous buffers)
+// from the pinned arena into an HBM buffer, then a stream write of the
+// buffer's generation into its ready flag.
+int moe_engine::run_copier() {
+  cudaSetDevice(dev);
+  uint64_t tail = 0;
+  int idle = 0;
+  while (!stop.load(std::memory_order_acquire)) {
+    const uint64_t head = __atomic_load_n(&mb_host->head, __ATOMIC_ACQUIRE);
+    if (head == tail) {
+      if (++idle > 20000) std::this_thread::yield();
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+      continue;
+    }
+    idle = 0;
+    while (tail < head) {
+      const CopyReq r = const_cast<const CopyReq&>(mb_host->ring[tail % MOE_MAILBOX_CAP]);
+      if (debug) {
+        fprintf(stderr, "[moe-copy] req %llu buf %d key (%d,%d) gen %u\n",
+                (unsigned long long)tail, r.buf, r.layer, r.expert, r.gen);
+        fflush(stderr);
+      }
+      const uint8_t* src = arena + ((size_t)r.layer * E + r.expert) * xbytes;
+      uint8_t* dst = pool + (size_t)r.buf * slot_stride;
+      cudaEvent_t a, b;
+      {
+        std::lock_guard<std::mutex> g(cmu);
+        if (free_events.size() < 2) {
+          cudaEventCreate(&a);
+          cudaEventCreate(&b);
+        } else {
+          a = free_events.back();
+          free_events.pop_back();
+          b = free_events.back();
+          free_events.pop_back();
+        }
+      }
+      cudaEventRecord(a, s_copy);
+      cudaMemcpyAsync(dst, src, xbytes, cudaMemcpyHostToDevice, s_copy);
+      cudaEventRecord(b, s_copy);
+      write_value32()(reinterpret_cast<CUstream>(s_copy),
+                      reinterpret_cast<CUdeviceptr>(flags + r.buf), r.gen,
+                      CU_STREAM_WRITE_VALUE_DEFAULT);
+      {
+        std::lock_guard<std::mutex> g(cmu);
+        copies.push_back({a, b, (int64_t)xbytes});
+      }
+      ++tail;
+    }
+  }
+  return MOE_OK;
+}
+
+int moe_engine::choose_splits(int njobs, int ncb, int nquads) const {
+  const int target = 4 * 148;
+  int S = (target + njobs * ncb - 1) / (njobs * ncb);
+  S = std::max(1, std::min(S, std::max(1, nquads / MOE_GEMV_WARPS)));
+  while ((nquads + S - 1) / S * 4 > MOE_XS_MAX) ++S;
+  return S;
+}
+
+GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* out, int S) const {
+  GJob j{};
+  j.M = D.M;
+  j.rel_slot = -1;
+  j.xmode = X_PLAIN;
+  j.x = xin;
+  j.out = out;
+  j.S = S;
+  j.QPS = (D.nquads + S - 1) / S;
+  j.ncb = D.ncb;
+  j.nchunks = D.nchunks;
+  j.nquads = D.nquads;
+  return j;
+}
+
+static int finalize_launch(GLaunch& P) {
+  int blk = 0;
+  for (int i = 0; i < P.nj; ++i) {
+    P.j[i].blk0 = blk;
+    blk += P.j[i].ncb * P.j[i].S;
+  }
+  return blk;
+}
+
+int moe_engine::enq_attention(int l, int p, int mode) {
+  throttle();
+  float* xp = x + (size_t)p * d;
+  float* hp = h + (size_t)p * d;
+  launch_layernorm(xp, ln1g[l], ln1b[l], xn, d, s_comp);
+  dbg("ln1", l, p);
+  GLaunch q{};
+  q.nj = 3;
+  q.j[0] = dense_job(wq[l], xn, qkv_part, S_qkv);
+  q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, S_qkv);
+  q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, S_qkv);
+  launch_gemv(attn_bits, q, finalize_launch(q), s_comp);
+  dbg("qkv", l, p);
+  AttnParams a{};
+  a.qkv_part = qkv_part;
+  a.S = S_qkv;
+  a.kc = kc + (size_t)l * T * d;
+  a.vc = vc + (size_t)l * T * d;
+  a.ctx = ctx;
+  a.pos = p;
+  a.H = H;
+  a.hd = hd;
+  a.d = d;
+  launch_attention(a, s_comp);
+  dbg("attn", l, p);
+  GLaunch o{};
+  o.nj = 1;
+  o.j[0] = dense_job(wo[l], ctx, wo_part, S_wo);
+  launch_gemv(attn_bits, o, finalize_launch(o), s_comp);
+  dbg("wo", l, p);
+  TailParams t{};
+  t.x = xp;
+  t.part = wo_part;
+  t.S = S_wo;
+  t.g2 = ln2g[l];
+  t.b2 = ln2b[l];
+  t.gate_l = gate[l];
+  const int gl = l + sc.lookahead;
+  const bool guess = mode == 0 && sc.enabled && sc.m > 0 && gl < L;
+  t.gate_g = guess ? gate[gl] : nullptr;
+  t.guess_layer = guess ? gl : -1;
+  t.m = guess ? sc.m : 0;
+  t.h = hp;
+  t.route = route + p;
+  t.trace = trace + (size_t)p * L + l;
+  t.trace_hidden = rec_hidden ? trace_hidden + ((size_t)p * L + l) * d : nullptr;
+  t.st = st;
+  t.d = d;
+  t.E = E;
+  t.top_k = topk;
+  t.layer = l;
+  t.pos = p;
+  t.mode = mode;
+  t.ep_size = 1;
+  launch_tail(t, s_comp);
+  dbg("tail", l, p);
+  launches += 6;
+  unit_done();
+  return MOE_OK;
+}
+
+int moe_engine::enq_experts(int p) {
+  throttle();
+  GLaunch u{};
+  u.route = route + p;
+  u.pool = pool;
+  u.slot_stride = slot_stride;
+  u.flags = flags;
+  u.err = err;
+  u.wait_ns = wait_ns;
+  GLaunch dn = u;
+  for (int j = 0; j < topk; ++j) {
+    for (int m = 0; m < 2; ++m) {
+      GJob& J = u.j[2 * j + m];
+      J = GJob{};
+      J.M = matdev_from(xl[m], reinterpret_cast<const uint8_t*>(xoff[m][0]));
+      J.M.scales = reinterpret_cast<const uint2*>(xoff[m][1]);
+      J.M.zeros = reinterpret_cast<const uint32_t*>(xoff[m][2]);
+      J.M.zmeta = reinterpret_cast<const __half2*>(xoff[m][3]);
+      J.rel_slot = j;
+      J.xmode = X_PLAIN;
+      J.x = h + (size_t)p * d;
+      J.out = up_part + ((size_t)(2 * j + m) * S_up) * f;
+      J.S = S_up;
+      J.nquads = d / 4;
+      J.QPS = (J.nquads + S_up - 1) / S_up;
+      J.nchunks = f / fmt_wc(expert_bits);
+      J.ncb = (J.nchunks + 31) / 32;
+    }
+    GJob& J = dn.j[j];
+    J = GJob{};
+    J.M = matdev_from(xl[2], reinterpret_cast<const uint8_t*>(xoff[2][0]));
+    J.M.scales = reinterpret_cast<const uint2*>(xoff[2][1]);
+    J.M.zeros = reinterpret_cast<const uint32_t*>(xoff[2][2]);
+    J.M.zmeta = reinterpret_cast<const __half2*>(xoff[2][3]);
+    J.rel_slot = j;
+    J.xmode = X_SWIGLU;
+    J.up1 = up_part + ((size_t)(2 * j) * S_up) * f;
+    J.up3 = up_part + ((size_t)(2 * j + 1) * S_up) * f;
+    J.S_up = S_up;
+    J.out = dn_part + ((size_t)j * S_dn) * d;
+    J.S = S_dn;
+    J.nquads = f / 4;
+    J.QPS = (J.nquads + S_dn - 1) / S_dn;
+    J.nchunks = d / fmt_wc(expert_bits);
+    J.ncb = (J.nchunks + 31) / 32;
+  }
+  u.nj = 2 * topk;
+  dn.nj = topk;
+  launch_gemv(expert_bits, u, finalize_launch(u), s_comp);
+  dbg("up", -1, p);
+  launch_gemv(expert_bits, dn, finalize_launch(dn), s_comp);
+  dbg("down", -1, p);
+  CombineParams c{};
+  c.h = h + (size_t)p * d;
+  c.part = dn_part;
+  c.S = S_dn;
+  c.route = route + p;
+  c.out = x + (size_t)p * d;
+  c.d = d;
+  c.top_k = topk;
+  launch_combine(c, s_comp);
+  dbg("combine", -1, p);
+  launches += 3;
+  unit_done();
+  return MOE_OK;
+}
+
+int moe_engine::enq_logits(int p, float* out) {
+  launch_layernorm(x + (size_t)p * d, lnfg, lnfb, xn, d, s_comp);
+  GLaunch g{};
+  g.nj = 1;
+  g.j[0] = dense_job(lm_head, xn, lm_part, S_lm);
+  launch_gemv(lm_bits, g, finalize_launch(g), s_comp);
+  LogitsParams lp{};
+  lp.part = lm_part;
+  lp.S = S_lm;
+  lp.V = V;
+  lp.logits = out;
+  lp.cand_val = cand_val;
+  lp.cand_idx = cand_idx;
+  lp.counter = counter;
+  lp.tok_out = tok_dev;
+  lp.err = err;
+  launch_logits(lp, s_comp);
+  dbg("logits", -1, p);
+  launches += 3;
+  return MOE_OK;
+}
+
+int moe_engine::throttle() {
+  while (units_issued - units_done >= ahead) {
+    CU(cudaEventSynchronize(ring[units_done % ring.size()]));
+    ++units_done;
+  }
+  return MOE_OK;
+}
+
+int moe_engine::unit_done() {
+  CU(cudaEventRecord(ring[units_issued % ring.size()], s_comp));
+  ++units_issued;
+  return MOE_OK;
+}
+
+// MOE_DEBUG=1: synchronize and report after every launch group
+int moe_engine::dbg(const char* what, int l, int p) {
+  if (!debug) return MOE_OK;
+  cudaError_t ce = cudaStreamSynchronize(s_comp);
+  int ev = 0, fl = 0;
+  cudaMemcpy(&fl, err, 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&ev, st.scalars + 3, 4, cudaMemcpyDeviceToHost);
+  fprintf(stderr, "[moe] %-10s layer %3d pos %3d : %s err=0x%x nev=%d mailbox=%llu\n", what, l, p,
+          cudaGetErrorString(ce), fl, ev, mb_host ? (unsigned long long)mb_host->head : 0ull);
+  fflush(stderr);
+  return ce == cudaSuccess ? MOE_OK : fail(MOE_ERR_CUDA, cudaGetErrorString(ce));
+}
+
+int moe_engine::finish_call() {
+  CU(cudaEventRecord(t1, s_comp));
+  CU(cudaStreamSynchronize(s_comp));
+  units_done = units_issued;
+  CU(cudaGetLastError());
+  float ms = 0;
+  cudaEventElapsedTime(&ms, t0, t1);
+  last_ms = ms;
+  int e = 0;
+  CU(cudaMemcpy(&e, err, sizeof(int), cudaMemcpyDeviceToHost));
+  CU(cudaMemset(err, 0, sizeof(int)));
+  int nev = 0;
+  CU(cudaMemcpy(&nev, st.scalars + 3, sizeof(int), cudaMemcpyDeviceToHost));
+  if (nev > 0) {
+    const size_t old = events.size();
+    events.resize(old + nev);
+    CU(cudaMemcpy(events.data() + old, st.ev, nev * sizeof(moe_event), cudaMemcpyDeviceToHost));
+    CU(cudaMemset(st.scalars + 3, 0, sizeof(int)));
+  }
+  if (e & MOE_ERRF_TIMEOUT) return fail(MOE_ERR_TIMEOUT, "expert buffer never became ready");
+  if (e & (MOE_ERRF_ALLOC | MOE_ERRF_EVENTS))
+    return fail(MOE_ERR_RUNTIME, "device store overflow (buffers or event log)");
+  if (e & MOE_ERRF_UNKNOWN) return fail(MOE_ERR_UNKNOWN_EXPERT, "no such expert");
+  if (e & MOE_ERRF_NONFINITE_GATE) return fail(MOE_ERR_NONFINITE, "gate input is not finite");
+  if (e & MOE_ERRF_NONFINITE_LOGITS) return fail(MOE_ERR_NONFINITE, "output logits are not finite");
+  return MOE_OK;
+}
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* moe_last_error(void) { return g_err.c_str(); }
+
+int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec_cfg* sc,
+               int32_t device, int32_t record_hidden, moe_engine** out) {
+  if (!md || !cc || !sc || !out) return fail(MOE_ERR_VALUE, "null argument");
+  const int dims[] = {md->vocab_size, md->d_model, md->n_layers, md->n_heads,
+                      md->d_ffn,      md->n_experts, md->top_k,  md->max_seq_len};
+  for (int v : dims)
+    if (v < 1) return fail(MOE_ERR_VALUE, "all model dimensions must be >= 1");
+  if (md->d_model % md->n_heads) return fail(MOE_ERR_VALUE, "d_model must be divisible by n_heads");
+  if (md->top_k > md->n_experts) return fail(MOE_ERR_VALUE, "top_k_gate cannot exceed n_experts");
+  if (md->top_k > MOE_MAX_TOPK || md->n_experts > 16)
+    return fail(MOE_ERR_VALUE, "engine supports top_k <= 4 and n_experts <= 16");
+  if (cc->k < 0 || cc->b < 0 || cc->expert_bytes <= 0)
+    return fail(MOE_ERR_VALUE, "k and b must be >= 0 and expert_bytes positive");
+  if (cc->k > md->n_experts)
+    return fail(MOE_ERR_VALUE, "k=" + std::to_string(cc->k) + " exceeds experts per layer");
+  if (sc->m < 0) return fail(MOE_ERR_VALUE, "m must be >= 0");
+  if (sc->lookahead < 1) return fail(MOE_ERR_VALUE, "lookahead must be >= 1");
+  if (sc->enabled && sc->m > cc->b)
+    return fail(MOE_ERR_VALUE, "m=" + std::to_string(sc->m) + " exceeds b=" +
+                                   std::to_string(cc->b) + " staging buffers");
+  if (sc->m > md->n_experts) return fail(MOE_ERR_VALUE, "m exceeds n_experts");
+  auto* e = new moe_engine();
+  e->md = *md;
+  e->cc = *cc;
+  e->sc = *sc;
+  e->dev = device;
+  e->rec_hidden = record_hidden != 0;
+  if (const char* dbgv = getenv("MOE_DEBUG")) e->debug = atoi(dbgv) != 0;
+  if (const char* w = getenv("MOE_WAIT_TIMEOUT_MS")) e->wait_ns = 1000000ull * atoll(w);
+  if (const char* a = getenv("MOE_AHEAD")) e->ahead = std::max(1, atoi(a));
+  e->ring.resize(64);
+  for (auto& ev : e->ring) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  e->d = md->d_model;
+  e->f = md->d_ffn;
+  e->V = md->vocab_size;
+  e->L = md->n_layers;
+  e->E = md->n_experts;
+  e->H = md->n_heads;
+  e->hd = md->d_model / md->n_heads;
+  e->T = md->max_seq_len;
+  e->topk = md->top_k;
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) {
+    delete e;
+    return fail(MOE_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(ce));
+  }
+  ce = preload_kernels();
+  if (ce == cudaSuccess) ce = preload_tile_kernels();
+  if (ce != cudaSuccess) {
+    delete e;
+    return fail(MOE_ERR_CUDA, std::string("kernel preload: ") + cudaGetErrorString(ce));
+  }
+  cudaStreamCreateWithFlags(&e->s_comp, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&e->s_copy, cudaStreamNonBlocking);
+  cudaEventCreate(&e->t0);
+  cudaEventCreate(&e->t1);
+  const int L = e->L;
+  e->wq.resize(L);
+  e->wk.resize(L);
+  e->wv.resize(L);
+  e->wo.resize(L);
+  e->ln1g.assign(L, nullptr);
+  e->ln1b.assign(L, nullptr);
+  e->ln2g.assign(L, nullptr);
+  e->ln2b.assign(L, nullptr);
+  e->gate.assign(L, nullptr);
+  e->loaded.assign((size_t)L * e->E, false);
+  *out = e;
+  return MOE_OK;
+}
+
+static int load_dense_mat(moe_engine* e, const moe_matrix* m, DevMat* D, const char* nm) {
+  Layout Lo;
+  int rc = make_layout(m, &Lo, nm);
+  if (rc) return rc;
+  if (D->mem) cudaFree(D->mem);
+  CU(cudaMalloc(&D->mem, Lo.total()));
+  e->dev_bytes += Lo.total();
+  rc = upload_and_tile(m, Lo, static_cast<uint8_t*>(D->mem), e->s_comp);
+  if (rc) return rc;
+  D->M = matdev_from(Lo, static_cast<uint8_t*>(D->mem));
+  D->bits = Lo.bits;
+  D->nchunks = Lo.N / fmt_wc(Lo.bits);
+  D->ncb = (D->nchunks + 31) / 32;
+  D->nquads = Lo.K / 4;
+  return MOE_OK;
+}
+
+static int load_vec(moe_engine* e, const moe_matrix* m, float** dst, int64_t n, const char* nm) {
+  if ((int64_t)m->rows * m->cols != n) return fail(MOE_ERR_VALUE, std::string(nm) + ": wrong shape");
+  std::vector<float> tmp(n);
+  if (m->bits == 32) {
+    memcpy(tmp.data(), m->codes, n * 4);
+  } else if (m->bits == 16) {
+    const uint16_t* hp = static_cast<const uint16_t*>(m->codes);
+    for (int64_t i = 0; i < n; ++i) {
+      __half_raw r;
+      r.x = hp[i];
+      tmp[i] = __half2float(__half(r));
+    }
+  } else {
+    return fail(MOE_ERR_VALUE, std::string(nm) + ": must be fp16 or fp32");
+  }
+  if (!*dst) {
+    CU(cudaMalloc(dst, n * 4));
+    e->dev_bytes += n * 4;
+  }
+  CU(cudaMemcpy(*dst, tmp.data(), n * 4, cudaMemcpyHostToDevice));
+  return MOE_OK;
+}
+
+int moe_load_tensor(moe_engine* e, const char* name, const moe_matrix* m) {
+  if (!e || !name || !m) return fail(MOE_ERR_VALUE, "null argument");
+  cudaSetDevice(e->dev);
+  const std::string nm(name);
+  const int d = e->d;
+  if (nm == "wte" || nm == "wpe") {
+    const int rows = nm == "wte" ? e->V : e->T;
+    if (m->rows != rows || m->cols != d) return fail(MOE_ERR_VALUE, nm + ": wrong shape");
+    if (m->bits != 16 && m->bits != 32) return fail(MOE_ERR_VALUE, nm + ": must be fp16 or fp32");
+    const int half = m->bits == 16;
+    if (e->emb_half >= 0 && e->emb_half != half)
+      return fail(MOE_ERR_VALUE, "wte and wpe must share a dtype");
+    e->emb_half = half;
+    void** dst = nm == "wte" ? &e->wte : &e->wpe;
+    const size_t bytes = (size_t)rows * d * (half ? 2 : 4);
+    if (m->codes_len != (int64_t)bytes) return fail(MOE_ERR_FORMAT, nm + ": size mismatch");
+    if (*dst) cudaFree(*dst);
+    CU(cudaMalloc(dst, bytes));
+    e->dev_bytes += bytes;
+    CU(cudaMemcpy(*dst, m->codes, bytes, cudaMemcpyHostToDevice));
+    return MOE_OK;
+  }
+  if (nm == "lm_head") {
+    if (m->rows != d || m->cols != e->V) return fail(MOE_ERR_VALUE, "lm_head: wrong shape");
+    if (m->bits != 16 && m->bits != 32) return fail(MOE_ERR_VALUE, "lm_head must be fp16/fp32");
+    e->lm_bits = m->bits;
+    return load_dense_mat(e, m, &e->lm_head, "lm_head");
+  }
+  if (nm == "ln_f.gamma") return load_vec(e, m, &e->lnfg, d, name);
+  if (nm == "ln_f.beta") return load_vec(e, m, &e->lnfb, d, name);
+  int l = -1;
+  char rest[128] = {0};
+  if (sscanf(name, "layers.%d.%127s", &l, rest) == 2 && l >= 0 && l < e->L) {
+    const std::string r(rest);
+    if (r == "ln1.gamma") return load_vec(e, m, &e->ln1g[l], d, name);
+    if (r == "ln1.beta") return load_vec(e, m, &e->ln1b[l], d, name);
+    if (r == "ln2.gamma") return load_vec(e, m, &e->ln2g[l], d, name);
+    if (r == "ln2.beta") return load_vec(e, m, &e->ln2b[l], d, name);
+    if (r == "gate") {
+      if (m->rows != d || m->cols != e->E) return fail(MOE_ERR_VALUE, nm + ": wrong shape");
+      return load_vec(e, m, &e->gate[l], (int64_t)d * e->E, name);
+    }
+    DevMat* D = r == "attn.wq" ? &e->wq[l] : r == "attn.wk" ? &e->wk[l]
+              : r == "attn.wv" ? &e->wv[l] : r == "attn.wo" ? &e->wo[l] : nullptr;
+    if (D) {
+      if (m->rows != d || m->cols != d) return fail(MOE_ERR_VALUE, nm + ": wrong shape");
+      if (m->bits == 16) return fail(MOE_ERR_VALUE, nm + ": fp16 attention unsupported");
+      if (e->attn_bits && e->attn_bits != m->bits)
+        return fail(MOE_ERR_VALUE, "all attention projections must share one scheme");
+      e->attn_bits = m->bits;
+      return load_dense_mat(e, m, D, name);
+    }
+  }
+  return fail(MOE_ERR_VALUE, "unknown tensor name " + nm);
+}
+
+static int set_expert_layout(moe_engine* e, const moe_matrix* ms[3]) {
+  Layout lo[3];
+  const char* nms[3] = {"w_gate_proj", "w_up_proj", "w_down_proj"};
+  for (int i = 0; i < 3; ++i) {
+    int rc = make_layout(ms[i], &lo[i], nms[i]);
+    if (rc) return rc;
+  }
+  if (lo[0].K != e->d || lo[0].N != e->f || lo[1].K != e->d || lo[1].N != e->f ||
+      lo[2].K != e->f || lo[2].N != e->d)
+    return fail(MOE_ERR_VALUE, "expert matrices have the wrong shape");
+  if (lo[0].bits != lo[1].bits || lo[0].bits != lo[2].bits || lo[0].bits == 16)
+    return fail(MOE_ERR_VALUE, "expert matrices must share one scheme (2/3/4-bit or fp32)");
+  if (e->xl_set) {
+    for (int i = 0; i < 3; ++i)
+      if (lo[i].bits != e->xl[i].bits || lo[i].g != e->xl[i].g || lo[i].sg != e->xl[i].sg)
+        return fail(MOE_ERR_VALUE, "all experts must share one scheme");
+    return MOE_OK;
+  }
+  size_t off = 0;
+  for (int i = 0; i < 3; ++i) {
+    e->xoff[i][0] = off;
+    off += lo[i].rec;
+  }
+  for (int i = 0; i < 3; ++i) {
+    e->xoff[i][1] = off;
+    off += lo[i].scales;
+  }
+  for (int i = 0; i < 3; ++i) {
+    e->xoff[i][2] = off;
+    off += lo[i].zeros;
+  }
+  for (int i = 0; i < 3; ++i) {
+    e->xoff[i][3] = off;
+    off += lo[i].zmeta;
+  }
+  for (int i = 0; i < 3; ++i) e->xl[i] = lo[i];
+  e->xbytes = off;
+  e->slot_stride = (off + 255) & ~size_t(255);
+  e->expert_bits = lo[0].bits;
+  e->xl_set = true;
+  const size_t arena = e->xbytes * (size_t)e->L * e->E;
+  CU(cudaHostAlloc(&e->arena, arena, cudaHostAllocPortable));
+  return MOE_OK;
+}
+
+int moe_load_expert(moe_engine* e, int32_t layer, int32_t expert, const moe_matrix* w1,
+                    const moe_matrix* w3, const moe_matrix* w2) {
+  if (!e || !w1 || !w3 || !w2) return fail(MOE_ERR_VALUE, "null argument");
+  if (layer < 0 || layer >= e->L || expert < 0 || expert >= e->E)
+    return fail(MOE_ERR_VALUE, "payload key outside model dimensions");
+  cudaSetDevice(e->dev);
+  const moe_matrix* ms[3] = {w1, w3, w2};
+  int rc = set_expert_layout(e, ms);
+  if (rc) return rc;
+  uint8_t* tmp = nullptr;
+  CU(cudaMalloc(&tmp, e->xbytes + 256));
+  for (int i = 0; i < 3; ++i) {
+    Layout lo;
+    rc = make_layout(ms[i], &lo, "expert");
+    if (rc) break;
+    // tile each matrix into a contiguous scratch, then scatter its sections
+    uint8_t* one = nullptr;
+    CU(cudaMalloc(&one, lo.total() + 16));
+    rc = upload_and_tile(ms[i], lo, one, e->s_comp);
+    if (!rc) {
+      const size_t secs[4] = {lo.rec, lo.scales, lo.zeros, lo.zmeta};
+      size_t so = 0;
+      for (int k = 0; k < 4; ++k) {
+        if (secs[k]) CU(cudaMemcpy(tmp + e->xoff[i][k], one + so, secs[k], cudaMemcpyDeviceToDevice));
+        so += secs[k];
+      }
+    }
+    cudaFree(one);
+    if (rc) break;
+  }
+  if (!rc) {
+    CU(cudaMemcpy(e->arena + ((size_t)layer * e->E + expert) * e->xbytes, tmp, e->xbytes,
+                  cudaMemcpyDeviceToHost));
+    e->loaded[(size_t)layer * e->E + expert] = true;
+  }
+  cudaFree(tmp);
+  return rc;
+}
+
+int moe_finalize(moe_engine* e) {
+  if (!e) return fail(MOE_ERR_VALUE, "null engine");
+  if (e->finalized) return MOE_OK;
+  cudaSetDevice(e->dev);
+  const int L = e->L, E = e->E, d = e->d, f = e->f, V = e->V, T = e->T;
+  if (!e->wte || !e->wpe || !e->lm_head.mem || !e->lnfg || !e->lnfb)
+    return fail(MOE_ERR_VALUE, "missing embedding / lm_head / ln_f tensors");
+  for (int l = 0; l < L; ++l)
+    if (!e->wq[l].mem || !e->wk[l].mem || !e->wv[l].mem || !e->wo[l].mem || !e->ln1g[l] ||
+        !e->ln1b[l] || !e->ln2g[l] || !e->ln2b[l] || !e->gate[l])
+      return fail(MOE_ERR_VALUE, "missing tensors of layer " + std::to_string(l));
+  for (size_t i = 0; i < e->loaded.size(); ++i)
+    if (!e->loaded[i]) return fail(MOE_ERR_UNKNOWN_EXPERT, "expert payload missing");
+  const int k = e->cc.k, b = e->cc.b;
+  e->nbuf = L * k + b + E + k + e->sc.m + 2;
+  CU(cudaMalloc(&e->pool, e->slot_stride * (size_t)e->nbuf));
+  e->dev_bytes += e->slot_stride * (size_t)e->nbuf;
+  int rc;
+  if ((rc = e->dalloc(&e->flags, e->nbuf))) return rc;
+  // activations
+  if ((rc = e->dalloc(&e->x, (size_t)T * d))) return rc;
+  if ((rc = e->dalloc(&e->h, (size_t)T * d))) return rc;
+  if ((rc = e->dalloc(&e->xn, d))) return rc;
+  if ((rc = e->dalloc(&e->ctx, d))) return rc;
+  if ((rc = e->dalloc(&e->logits, (size_t)T * V))) return rc;
+  const int wca = fmt_wc(e->attn_bits), wcx = fmt_wc(e->expert_bits);
+  e->S_qkv = e->choose_splits(3, (d / wca + 31) / 32, d / 4);
+  e->S_wo = e->choose_splits(1, (d / wca + 31) / 32, d / 4);
+  e->S_up = e->choose_splits(2 * e->topk, (f / wcx + 31) / 32, d / 4);
+  e->S_dn = e->choose_splits(e->topk, (d / wcx + 31) / 32, f / 4);
+  e->S_lm = e->choose_splits(1, e->lm_head.ncb, d / 4);
+  if ((rc = e->dalloc(&e->qkv_part, (size_t)3 * e->S_qkv * d))) return rc;
+  if ((rc = e->dalloc(&e->wo_part, (size_t)e->S_wo * d))) return rc;
+  if ((rc = e->dalloc(&e->up_part, (size_t)2 * e->topk * e->S_up * f))) return rc;
+  if ((rc = e->dalloc(&e->dn_part, (size_t)e->topk * e->S_dn * d))) return rc;
+  if ((rc = e->dalloc(&e->lm_part, (size_t)e->S_lm * V))) return rc;
+  if ((rc = e->dalloc(&e->kc, (size_t)L * T * d))) return rc;
+  if ((rc = e->dalloc(&e->vc, (size_t)L * T * d))) return rc;
+  if ((rc = e->dalloc(&e->route, T))) return rc;
+  if ((rc = e->dalloc(&e->trace, (size_t)T * L))) return rc;
+  if (e->rec_hidden && (rc = e->dalloc(&e->trace_hidden, (size_t)T * L * d))) return rc;
+  if ((rc = e->dalloc(&e->tok_dev, 1))) return rc;
+  if ((rc = e->dalloc(&e->tok_hist, T))) return rc;
+  if ((rc = e->dalloc(&e->tok_in, T))) return rc;
+  const int nblk = (V + 255) / 256;
+  if ((rc = e->dalloc(&e->cand_val, nblk))) return rc;
+  if ((rc = e->dalloc(&e->cand_idx, nblk))) return rc;
+  if ((rc = e->dalloc(&e->counter, 1))) return rc;
+  if ((rc = e->dalloc(&e->err, 1))) return rc;
+  // device store state
+  const int kk = std::max(k, 1);
+  e->ev_cap = std::max(4096, T * L * (3 * e->topk + e->sc.m + 2) + L * E * 3);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 15) & ~size_t(15);
+    return o;
+  };
+  const size_t o_lru = take((size_t)L * kk * 4), o_len = take((size_t)L * 4),
+               o_res = take((size_t)L * E * 4), o_sl = take(std::max(b, 1) * 4),
+               o_se = take(std::max(b, 1) * 4), o_ss = take(std::max(b, 1) * 4),
+               o_sb = take(std::max(b, 1) * 4), o_sc = take(16), o_seq = take(8),
+               o_free = take((size_t)e->nbuf * 4), o_pend = take((size_t)e->nbuf * 4),
+               o_gen = take((size_t)e->nbuf * 4), o_ev = take((size_t)e->ev_cap * sizeof(DevEvent));
+  CU(cudaMalloc(&e->st_mem, off));
+  e->dev_bytes += off;
+  CU(cudaMemset(e->st_mem, 0, off));
+  uint8_t* sm = static_cast<uint8_t*>(e->st_mem);
+  StoreDev& S = e->st;
+  S.L = L;
+  S.E = E;
+  S.k = k;
+  S.b = b;
+  S.top_k = e->topk;
+  S.nbuf = e->nbuf;
+  S.expert_bytes = e->cc.expert_bytes;
+  S.lru = reinterpret_cast<int*>(sm + o_lru);
+  S.lru_len = reinterpret_cast<int*>(sm + o_len);
+  S.res_buf = reinterpret_cast<int*>(sm + o_res);
+  S.stg_layer = reinterpret_cast<int*>(sm + o_sl);
+  S.stg_exp = reinterpret_cast<int*>(sm + o_se);
+  S.stg_stamp = reinterpret_cast<int*>(sm + o_ss);
+  S.stg_buf = reinterpret_cast<int*>(sm + o_sb);
+  S.scalars = reinterpret_cast<int*>(sm + o_sc);
+  S.seq = reinterpret_cast<long long*>(sm + o_seq);
+  S.free_stack = reinterpret_cast<int*>(sm + o_free);
+  S.pending = reinterpret_cast<int*>(sm + o_pend);
+  S.gen = reinterpret_cast<uint32_t*>(sm + o_gen);
+  S.ev = reinterpret_cast<DevEvent*>(sm + o_ev);
+  S.ev_cap = e->ev_cap;
+  S.owned = nullptr;
+  S.err = e->err;
+  {
+    std::vector<int> neg(std::max(b, 1), -1), fs(e->nbuf);
+    CU(cudaMemcpy(S.stg_layer, neg.data(), neg.size() * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(S.stg_exp, neg.data(), neg.size() * 4, cudaMemcpyHostToDevice));
+    for (int i = 0; i < e->nbuf; ++i) fs[i] = e->nbuf - 1 - i;
+    CU(cudaMemcpy(S.free_stack, fs.data(), fs.size() * 4, cudaMemcpyHostToDevice));
+    const int sc4[4] = {0, e->nbuf, 0, 0};
+    CU(cudaMemcpy(S.scalars, sc4, 16, cudaMemcpyHostToDevice));
+  }
+  if (!write_value32()) return fail(MOE_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  CU(cudaHostAlloc(&e->mb_host, sizeof(Mailbox), cudaHostAllocMapped));
+  memset(e->mb_host, 0, sizeof(Mailbox));
+  CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->mb_dev), e->mb_host, 0));
+  S.mb = e->mb_dev;
+  CU(cudaDeviceSynchronize());
+  e->copier = std::thread([e] { e->run_copier(); });
+  e->finalized = true;
+  return MOE_OK;
+}
+
+static int check_ready(moe_engine* e) {
+  if (!e) return fail(MOE_ERR_VALUE, "null engine");
+  if (!e->finalized) return fail(MOE_ERR_RUNTIME, "engine not finalized (weights not loaded)");
+  cudaSetDevice(e->dev);
+  return MOE_OK;
+}
+
+int moe_reset_session(moe_engine* e) {
+  int rc = check_ready(e);
+  if (rc) return rc;
+  e->pos = 0;
+  e->has_logits = false;
+  return MOE_OK;
+}
+
+int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_out) {
+  int rc = check_ready(e);
+  if (rc) return rc;
+  e->pos = 0;  // reset_session (engine.py:149): KV and trace, not the store
+  e->has_logits = false;
+  e->launches = 0;
+  if (n < 1) return fail(MOE_ERR_VALUE, "prompt must contain at least one token");
+  for (int i = 0; i < n; ++i) {
+    if (tokens[i] < 0 || tokens[i] >= e->V)
+      return fail(MOE_ERR_VALUE, "token id " + std::to_string(tokens[i]) +
+                                     " outside vocabulary of " + std::to_string(e->V));
+    if (i >= e->T)
+      return fail(MOE_ERR_VALUE, "position " + std::to_string(i) + " exceeds max_seq_len=" +
+                                     std::to_string(e->T));
+  }
+  CU(cudaEventRecord(e->t0, e->s_comp));
+  for (int p = 0; p < n; ++p) {
+    EmbedParams ep{};
+    ep.wte = e->wte;
+    ep.wpe = e->wpe;
+    ep.half = e->emb_half;
+    ep.tok = tokens[p];
+    ep.pos = p;
+    ep.d = e->d;
+    ep.x = e->x + (size_t)p * e->d;
+    launch_embed(ep, e->s_comp);
+  }
+  for (int l = 0; l < e->L; ++l) {
+    for (int p = 0; p < n; ++p) e->enq_attention(l, p, 1);
+    PrefillBKParams pb{};
+    pb.route = e->route;
+    pb.st = e->st;
+    pb.layer = l;
+    pb.n = n;
+    pb.top_k = e->topk;
+    launch_prefill_bk(pb, e->s_comp);
+    e->dbg("prefill_bk", l, n);
+    for (int p = 0; p < n; ++p) e->enq_experts(p);
+  }
+  for (int p = 0; p < n; ++p) e->enq_logits(p, e->logits + (size_t)p * e->V);
+  CU(cudaGetLastError());
+  rc = e->finish_call();
+  if (rc) return rc;
+  if (logits_out)
+    CU(cudaMemcpy(logits_out, e->logits, (size_t)n * e->V * 4, cudaMemcpyDeviceToHost));
+  if (n > 1)  // keep the last position's logits at slot 0 for decode
+    CU(cudaMemcpy(e->logits, e->logits + (size_t)(n - 1) * e->V, (size_t)e->V * 4,
+                  cudaMemcpyDeviceToDevice));
+  e->pos = n;
+  e->has_logits = true;
+  return MOE_OK;
+}
+
+static int run_one(moe_engine* e, int tok_host, const int* tok_dev, int* tok_hist) {
+  EmbedParams ep{};
+  ep.wte = e->wte;
+  ep.wpe = e->wpe;
+  ep.half = e->emb_half;
+  ep.tok = tok_host;
+  ep.tok_dev = tok_dev;
+  ep.tok_hist = tok_hist;
+  ep.pos = e->pos;
+  ep.d = e->d;
+  ep.x = e->x + (size_t)e->pos * e->d;
+  launch_embed(ep, e->s_comp);
+  for (int l = 0; l < e->L; ++l) {
+    e->enq_attention(l, e->pos, 0);
+    e->enq_experts(e->pos);
+  }
+  e->enq_logits(e->pos, e->logits);
+  e->launches += 1;
+  e->pos += 1;
+  return MOE_OK;
+}
+
+int moe_step(moe_engine* e, int32_t token, float* logits_out) {
+  int rc = check_ready(e);
+  if (rc) return rc;
+  if (token < 0 || token >= e->V)
+    return fail(MOE_ERR_VALUE, "token id " + std::to_string(token) + " outside vocabulary of " +
+                                   std::to_string(e->V));
+  if (e->pos >= e->T)
+    return fail(MOE_ERR_VALUE, "position " + std::to_string(e->pos) + " exceeds max_seq_len=" +
+                                   std::to_string(e->T));
+  e->launches = 0;
+  CU(cudaEventRecord(e->t0, e->s_comp));
+  run_one(e, token, nullptr, nullptr);
+  CU(cudaGetLastError());
+  rc = e->finish_call();
+  if (rc) return rc;
+  if (logits_out) CU(cudaMemcpy(logits_out, e->logits, (size_t)e->V * 4, cudaMemcpyDeviceToHost));
+  e->has_logits = true;
+  return MOE_OK;
+}
+
+int moe_decode_greedy(moe_engine* e, int32_t n, int32_t* tokens_out, float* final_logits_out) {
+  int rc = check_ready(e);
+  if (rc) return rc;
+  if (n < 1) return fail(MOE_ERR_VALUE, "n_tokens must be >= 1");
+  if (!e->has_logits) return fail(MOE_ERR_RUNTIME, "prefill must run before decoding");
+  if (e->pos + n > e->T)
+    return fail(MOE_ERR_VALUE, "position " + std::to_string(e->T) + " exceeds max_seq_len=" +
+                                   std::to_string(e->T));
+  e->launches = 0;
+  CU(cudaEventRecord(e->t0, e->s_comp));
+  for (int i = 0; i < n; ++i) run_one(e, 0, e->tok_dev, e->tok_hist + i);
+  CU(cudaGetLastError());
+  rc = e->finish_call();
+  if (rc) return rc;
+  if (tokens_out) CU(cudaMemcpy(tokens_out, e->tok_hist, (size_t)n * 4, cudaMemcpyDeviceToHost));
+  if (final_logits_out)
+    CU(cudaMemcpy(final_logits_out, e->logits, (size_t)e->V * 4, cudaMemcpyDeviceToHost));
+  return MOE_OK;
+}
+
+int64_t moe_num_events(moe_engine* e) { return e ? (int64_t)e->events.size() : 0; }
+
+int moe_read_events(moe_engine* e, int64_t start, int64_t count, moe_event* out) {
+  if (!e || start < 0 || count < 0 || start + count > (int64_t)e->events.size())
+    return fail(MOE_ERR_VALUE, "event range out of bounds");
+  if (count) memcpy(out, e->events.data() + start, count * sizeof(moe_event));
+  return MOE_OK;
+}
+
+int64_t moe_num_trace(moe_engine* e) { return e ? (int64_t)e->pos * e->L : 0; }
+
+int moe_read_trace(moe_engine* e, int64_t start, int64_t count, moe_trace_rec* out,
+                   float* hidden_out) {
+  int rc = check_ready(e);
+  if (rc) return rc;
+  if (start < 0 || count < 0 || start + count > (int64_t)e->pos * e->L)
+    return fail(MOE_ERR_VALUE, "trace range out of bounds");
+  if (!count) return MOE_OK;
+  CU(cudaMemcpy(out, e->trace + start, count * sizeof(moe_trace_rec), cudaMemcpyDeviceToHost));
+  if (hidden_out) {
+    if (!e->rec_hidden) return fail(MOE_ERR_VALUE, "hidden states were not recorded");
+    CU(cudaMemcpy(hidden_out, e->trace_hidden + start * e->d, count * e->d * 4,
+                  cudaMemcpyDeviceToHost));
+  }
+  return MOE_OK;
+}
+
+int moe_device_state(moe_engine* e, int32_t* lru_out, int32_t* staged_out) {
+  int rc = check_ready(e);
+  if (rc) return rc;
+  const int L = e->L, k = e->cc.k, kk = std::max(k, 1), b = e->cc.b;
+  std::vector<int> lru((size_t)L * kk), len(L), sl(std::max(b, 1)), se(std::max(b, 1));
+  CU(cudaMemcpy(lru.data(), e->st.lru, lru.size() * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(len.data(), e->st.lru_len, L * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(sl.data(), e->st.stg_layer, sl.size() * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(se.data(), e->st.stg_exp, se.size() * 4, cudaMemcpyDeviceToHost));
+  if (lru_out)
+    for (int l = 0; l < L; ++l)
+      for (int i = 0; i < k; ++i) lru_out[l * k + i] = i < len[l] ? lru[l * kk + i] : -1;
+  if (staged_out)
+    for (int i = 0; i < b; ++i) staged_out[i] = sl[i] >= 0 ? sl[i] * e->E + se[i] : -1;
+  return MOE_OK;
+}
+
+int moe_get_stats(moe_engine* e, moe_stats* out) {
+  if (!e || !out) return fail(MOE_ERR_VALUE, "null argument");
+  {
+    std::lock_guard<std::mutex> g(e->cmu);
+    std::vector<CopyRec> keep;
+    for (auto& c : e->copies) {
+      if (cudaEventQuery(c.b) != cudaSuccess) {
+        keep.push_back(c);
+        continue;
+      }
+      float ms = 0;
+      cudaEventElapsedTime(&ms, c.a, c.b);
+      e->busy_ms += ms;
+      e->n_copies += 1;
+      e->copy_bytes += c.bytes;
+      if (ms > 0) e->peak_gbs = std::max(e->peak_gbs, c.bytes / (ms * 1e6));
+      e->free_events.push_back(c.a);
+      e->free_events.push_back(c.b);
+    }
+    e->copies.swap(keep);
+  }
+  memset(out, 0, sizeof(*out));
+  out->h2d_copies = e->n_copies;
+  out->h2d_bytes = e->copy_bytes;
+  out->h2d_busy_ms = e->busy_ms;
+  out->h2d_peak_gbs = e->peak_gbs;
+  out->n_buffers = e->nbuf;
+  out->slot_bytes = (int64_t)e->slot_stride;
+  out->device_bytes = (int64_t)e->dev_bytes;
+  out->arena_bytes = (int64_t)(e->xbytes * (size_t)e->L * e->E);
+  out->kernel_launches = e->launches;
+  out->last_call_ms = e->last_ms;
+  return MOE_OK;
+}
+
+int moe_destroy(moe_engine* e) {
+  if (e) {
+    cudaSetDevice(e->dev);
+    delete e;
+  }
+  return MOE_OK;
+}
+
+}  // extern "C"
+
+// ============================================================ synthesis path
+namespace {
+
+constexpr double kSynthIHStd = 37837.22700;  // oracle/model.py SYNTH_IHSTD
+
+float synth_scale(double std) { return (float)(std / kSynthIHStd); }
+
+struct QScratch {  // device scratch for generate -> quantize -> tile
+  float* w = nullptr;
+  uint8_t* codes = nullptr;
+  uint8_t* zeros = nullptr;
+  uint16_t *zs = nullptr, *zo = nullptr, *sc = nullptr;
+  float *gmin = nullptr, *gscale = nullptr;
+  uint8_t* tiled = nullptr;
+  size_t cap = 0;
+  void release() {
+    void* p[] = {w, codes, zeros, zs, zo, sc, gmin, gscale, tiled};
+    for (void* q : p)
+      if (q) cudaFree(q);
+  }
+};
+
+int qscratch_alloc(QScratch& Q, size_t nmax) {
+  Q.cap = nmax;
+  CU(cudaMalloc(&Q.w, nmax * 4));
+  CU(cudaMalloc(&Q.codes, nmax / 2 + 64));
+  CU(cudaMalloc(&Q.zeros, nmax / 16 + 64));
+  CU(cudaMalloc(&Q.zs, nmax / 128 + 64));
+  CU(cudaMalloc(&Q.zo, nmax / 128 + 64));
+  CU(cudaMalloc(&Q.sc, nmax / 32 + 64));
+  CU(cudaMalloc(&Q.gmin, nmax / 4 + 64));
+  CU(cudaMalloc(&Q.gscale, nmax / 4 + 64));
+  CU(cudaMalloc(&Q.tiled, nmax * 4 + 256));
+  return MOE_OK;
+}
+
+// layout descriptor for a synthetic K x N matrix of `bits`
+Layout synth_layout(int K, int N, int bits) {
+  moe_matrix m{};
+  m.bits = bits;
+  m.rows = K;
+  m.cols = N;
+  m.meta_bits = 8;
+  if (bits <= 4) {
+    m.group_size = bits == 2 ? 16 : 64;
+    m.scale_group_size = bits == 4 ? 256 : 128;
+    const int64_t ng = (int64_t)K * N / m.group_size;
+    m.codes_len = (int64_t)K * N * bits / 8;
+    m.n_groups = ng;
+    m.n_scales = (ng + m.scale_group_size / m.group_size - 1) / (m.scale_group_size / m.group_size);
+    m.n_zruns = (ng + m.scale_group_size - 1) / m.scale_group_size;
+  } else {
+    m.codes_len = (int64_t)K * N * (bits / 8);
+  }
+  Layout L;
+  make_layout(&m, &L, "synth");
+  return L;
+}
+
+// generate (K x N) with id `tid`, quantize (or keep fp32 / round to fp16) and
+// tile into Q.tiled.  Returns the layout.
+int synth_matrix(QScratch& Q, uint64_t seed, uint64_t tid, int K, int N, double std, int bits,
+                 int half_round, Layout* out, cudaStream_t s) {
+  const int64_t n = (int64_t)K * N;
+  launch_synth(seed, tid, n, synth_scale(std), half_round, Q.w, s);
+  Layout L = synth_layout(K, N, bits);
+  if (L.bits == 0) return fail(MOE_ERR_VALUE, "synthetic shape incompatible with the device layout");
+  RefMat R = refmat_of(L);
+  if (bits <= 4) {
+    launch_quantize(Q.w, K, N, bits, L.g, L.sg, Q.codes, Q.zeros, Q.zs, Q.zo, Q.sc, Q.gmin,
+                    Q.gscale, s);
+    R.codes = Q.codes;
+    R.zeros = Q.zeros;
+    R.zs = Q.zs;
+    R.zo = Q.zo;
+    R.scales = Q.sc;
+  } else if (bits == 16) {
+    // reuse gscale region as the fp16 staging of the values
+    std::vector<float> tmp;  // (device conversion below)
+    R.codes = reinterpret_cast<const uint8_t*>(Q.w);
+  } else {
+    R.codes = reinterpret_cast<const uint8_t*>(Q.w);
+  }
+  int rc = tile_device(R, L, Q.tiled, s);
+  if (rc) return rc;
+  *out = L;
+  return MOE_OK;
+}
+
+__global__ void k_f32_to_f16(const float* a, __half* b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = __float2half_rn(a[i]);
+}
+
+}  // namespace
+
+extern "C" {
+
+int moe_synth_model(moe_engine* e, uint64_t seed, int32_t attn_bits, int32_t expert_bits) {
+  if (!e) return fail(MOE_ERR_VALUE, "null engine");
+  if (!((attn_bits >= 2 && attn_bits <= 4) || attn_bits == 32) ||
+      !((expert_bits >= 2 && expert_bits <= 4) || expert_bits == 32))
+    return fail(MOE_ERR_VALUE, "synthetic bits must be 2/3/4 or 32");
+  cudaSetDevice(e->dev);
+  cudaStream_t s = e->s_comp;
+  const int d = e->d, f = e->f, V = e->V, L = e->L, E = e->E, T = e->T;
+  const bool mixed = attn_bits != 32 || expert_bits != 32;
+  const int hr = mixed ? 1 : 0;  // fp16-passthrough roles (quant.py:428)
+  const double sd = 1.0 / std::sqrt((double)d), sf = 1.0 / std::sqrt((double)f);
+  QScratch Q;
+  int rc = qscratch_alloc(Q, std::max(std::max((size_t)d * f, (size_t)V * d), (size_t)T * d));
+  if (rc) {
+    Q.release();
+    return rc;
+  }
+  auto put_raw = [&](const char* name, uint64_t tid, int rows, int cols, double std) -> int {
+    const int64_t n = (int64_t)rows * cols;
+    launch_synth(seed, tid, n, synth_scale(std), hr, Q.w, s);
+    moe_matrix m{};
+    m.rows = rows;
+    m.cols = cols;
+    std::vector<uint8_t> host(n * (mixed ? 2 : 4));
+    if (mixed) {
+      k_f32_to_f16<<<1184, 256, 0, s>>>(Q.w, reinterpret_cast<__half*>(Q.gscale), n);
+      CU(cudaMemcpyAsync(host.data(), Q.gscale, n * 2, cudaMemcpyDeviceToHost, s));
+      m.bits = 16;
+    } else {
+      CU(cudaMemcpyAsync(host.data(), Q.w, n * 4, cudaMemcpyDeviceToHost, s));
+      m.bits = 32;
+    }
+    CU(cudaStreamSynchronize(s));
+    m.codes = host.data();
+    m.codes_len = (int64_t)host.size();
+    return moe_load_tensor(e, name, &m);
+  };
+  if ((rc = put_raw("wte", 1, V, d, 0.02)) || (rc = put_raw("wpe", 2, T, d, 0.02)) ||
+      (rc = put_raw("lm_head", 3, d, V, 0.02))) {
+    Q.release();
+    return rc;
+  }
+  std::vector<float> ones(d, 1.f), zeros(d, 0.f);
+  auto put_vec = [&](const std::string& name, std::vector<float>& v) {
+    moe_matrix m{};
+    m.bits = 32;
+    m.rows = 1;
+    m.cols = (int)v.size();
+    m.codes = v.data();
+    m.codes_len = (int64_t)v.size() * 4;
+    return moe_load_tensor(e, name.c_str(), &m);
+  };
+  if ((rc = put_vec("ln_f.gamma", ones)) || (rc = put_vec("ln_f.beta", zeros))) {
+    Q.release();
+    return rc;
+  }
+  // experts share one layout; set it from the synthetic shapes
+  Layout xl3[3] = {synth_layout(d, f, expert_bits), synth_layout(d, f, expert_bits),
+                   synth_layout(f, d, expert_bits)};
+  uint8_t* xtmp = nullptr;
+  for (int l = 0; l < L && !rc; ++l) {
+    const uint64_t base = 1000 + 100 * (uint64_t)l;
+    const std::string pre = "layers." + std::to_string(l) + ".";
+    rc = put_vec(pre + "ln1.gamma", ones);
+    if (!rc) rc = put_vec(pre + "ln1.beta", zeros);
+    if (!rc) rc = put_vec(pre + "ln2.gamma", ones);
+    if (!rc) rc = put_vec(pre + "ln2.beta", zeros);
+    const char* an[4] = {"attn.wq", "attn.wk", "attn.wv", "attn.wo"};
+    for (int j = 0; j < 4 && !rc; ++j) {
+      Layout lo;
+      rc = synth_matrix(Q, seed, base + j, d, d, sd, attn_bits, 0, &lo, s);
+      if (rc) break;
+      DevMat& D = j == 0 ? e->wq[l] : j == 1 ? e->wk[l] : j == 2 ? e->wv[l] : e->wo[l];
+      if (D.mem) cudaFree(D.mem);
+      CU(cudaMalloc(&D.mem, lo.total()));
+      e->dev_bytes += lo.total();
+      CU(cudaMemcpyAsync(D.mem, Q.tiled, lo.total(), cudaMemcpyDeviceToDevice, s));
+      D.M = matdev_from(lo, static_cast<uint8_t*>(D.mem));
+      D.bits = lo.bits;
+      D.nchunks = lo.N / fmt_wc(lo.bits);
+      D.ncb = (D.nchunks + 31) / 32;
+      D.nquads = lo.K / 4;
+      e->attn_bits = lo.bits;
+    }
+    if (rc) break;
+    {  // gate (fp16-rounded in mixed mode), kept as fp32 [d][E]
+      launch_synth(seed, base + 4, (int64_t)d * E, synth_scale(sd), hr, Q.w, s);
+      std::vector<float> g((size_t)d * E);
+      CU(cudaMemcpyAsync(g.data(), Q.w, g.size() * 4, cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      moe_matrix m{};
+      m.bits = 32;
+      m.rows = d;
+      m.cols = E;
+      m.codes = g.data();
+      m.codes_len = (int64_t)g.size() * 4;
+      rc = moe_load_tensor(e, (pre + "gate").c_str(), &m);
+      if (rc) break;
+    }
+    for (int x = 0; x < E && !rc; ++x) {
+      if (!e->xl_set) {  // first expert defines the buffer layout + arena
+        size_t off = 0;
+        for (int i = 0; i < 3; ++i) { e->xoff[i][0] = off; off += xl3[i].rec; }
+        for (int i = 0; i < 3; ++i) { e->xoff[i][1] = off; off += xl3[i].scales; }
+        for (int i = 0; i < 3; ++i) { e->xoff[i][2] = off; off += xl3[i].zeros; }
+        for (int i = 0; i < 3; ++i) { e->xoff[i][3] = off; off += xl3[i].zmeta; }
+        for (int i = 0; i < 3; ++i) e->xl[i] = xl3[i];
+        e->xbytes = off;
+        e->slot_stride = (off + 255) & ~size_t(255);
+        e->expert_bits = xl3[0].bits;
+        e->xl_set = true;
+        CU(cudaHostAlloc(&e->arena, e->xbytes * (size_t)L * E, cudaHostAllocPortable));
+        CU(cudaMalloc(&xtmp, e->slot_stride));
+      }
+      const int K3[3] = {d, d, f}, N3[3] = {f, f, d};
+      const double sd3[3] = {sd, sd, sf};
+      for (int i = 0; i < 3 && !rc; ++i) {
+        Layout lo;
+        rc = synth_matrix(Q, seed, base + 10 + 3 * x + i, K3[i], N3[i], sd3[i], expert_bits, 0, &lo,
+                          s);
+        if (rc) break;
+        const size_t secs[4] = {lo.rec, lo.scales, lo.zeros, lo.zmeta};
+        size_t so = 0;
+        for (int k = 0; k < 4; ++k) {
+          if (secs[k])
+            CU(cudaMemcpyAsync(xtmp + e->xoff[i][k], Q.tiled + so, secs[k], cudaMemcpyDeviceToDevice, s));
+          so += secs[k];
+        }
+      }
+      if (rc) break;
+      CU(cudaMemcpyAsync(e->arena + ((size_t)l * E + x) * e->xbytes, xtmp, e->xbytes,
+                         cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      e->loaded[(size_t)l * E + x] = true;
+    }
+  }
+  CU(cudaStreamSynchronize(s));
+  if (xtmp) cudaFree(xtmp);
+  Q.release();
+  return rc;
+}
+
+int moe_quantize_device(const float* w, int32_t rows, int32_t cols, int32_t bits,
+                        int32_t group_size, int32_t scale_group_size, uint8_t* codes_out,
+                        uint8_t* zeros_out, uint16_t* zscales_out, uint16_t* zoffsets_out,
+                        uint16_t* scales_out) {
+  if (bits < 2 || bits > 4) return fail(MOE_ERR_VALUE, "bits must be 2, 3 or 4");
+  const int g = group_size, sg = scale_group_size;
+  if (g < 1 || sg % g || cols % g || ((int64_t)g * bits) % 32)
+    return fail(MOE_ERR_VALUE, "device quantizer needs cols % g == 0 and word-aligned groups");
+  const int64_t n = (int64_t)rows * cols, ng = n / g, per = sg / g;
+  const int64_t nsg = (ng + per - 1) / per, nruns = (ng + sg - 1) / sg;
+  float *dw, *gmin, *gsc;
+  uint8_t *dc, *dz;
+  uint16_t *zs, *zo, *sc;
+  CU(cudaMalloc(&dw, n * 4));
+  CU(cudaMalloc(&gmin, ng * 4));
+  CU(cudaMalloc(&gsc, ng * 4));
+  CU(cudaMalloc(&dc, n * bits / 8 + 16));
+  CU(cudaMalloc(&dz, ng));
+  CU(cudaMalloc(&zs, nruns * 2));
+  CU(cudaMalloc(&zo, nruns * 2));
+  CU(cudaMalloc(&sc, nsg * 2));
+  CU(cudaMemcpy(dw, w, n * 4, cudaMemcpyHostToDevice));
+  launch_quantize(dw, rows, cols, bits, g, sg, dc, dz, zs, zo, sc, gmin, gsc, 0);
+  CU(cudaGetLastError());
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(codes_out, dc, n * bits / 8, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(zeros_out, dz, ng, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(zscales_out, zs, nruns * 2, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(zoffsets_out, zo, nruns * 2, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(scales_out, sc, nsg * 2, cudaMemcpyDeviceToHost));
+  void* ps[] = {dw, gmin, gsc, dc, dz, zs, zo, sc};
+  for (void* p : ps) cudaFree(p);
+  return MOE_OK;
+}
+
+int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
+  Layout L;
+  int rc = make_layout(m, &L, "gemv");
+  if (rc) return rc;
+  uint8_t* mem = nullptr;
+  CU(cudaMalloc(&mem, L.total() + 16));
+  rc = upload_and_tile(m, L, mem, 0);
+  if (rc) {
+    cudaFree(mem);
+    return rc;
+  }
+  const int nquads = L.K / 4, nchunks = L.N / fmt_wc(L.bits), ncb = (nchunks + 31) / 32;
+  int S = std::max(1, std::min((592 + ncb - 1) / ncb, std::max(1, nquads / MOE_GEMV_WARPS)));
+  while ((nquads + S - 1) / S * 4 > MOE_XS_MAX) ++S;
+  float *dx, *part;
+  CU(cudaMalloc(&dx, (size_t)L.K * 4));
+  CU(cudaMalloc(&part, (size_t)S * L.N * 4));
+  CU(cudaMemcpy(dx, x, (size_t)L.K * 4, cudaMemcpyHostToDevice));
+  GLaunch P{};
+  P.nj = 1;
+  GJob& J = P.j[0];
+  J.M = matdev_from(L, mem);
+  J.rel_slot = -1;
+  J.xmode = X_PLAIN;
+  J.x = dx;
+  J.out = part;
+  J.S = S;
+  J.QPS = (nquads + S - 1) / S;
+  J.ncb = ncb;
+  J.nchunks = nchunks;
+  J.nquads = nquads;
+  J.blk0 = 0;
+  launch_gemv(L.bits, P, ncb * S, 0);
+  CU(cudaGetLastError());
+  CU(cudaDeviceSynchronize());
+  std::vector<float> h((size_t)S * L.N);
+  CU(cudaMemcpy(h.data(), part, h.size() * 4, cudaMemcpyDeviceToHost));
+  for (int j = 0; j < L.N; ++j) {
+    float a = 0.f;
+    for (int s = 0; s < S; ++s) a += h[(size_t)s * L.N + j];
+    y[j] = a;
+  }
+  cudaFree(mem);
+  cudaFree(dx);
+  cudaFree(part);
+  return MOE_OK;
+}
+
+int moe_synth_tensor_device(uint64_t seed, uint64_t tensor_id, int64_t count, float scale,
+                            float* out) {
+  float* d = nullptr;
+  CU(cudaMalloc(&d, count * 4));
+  launch_synth(seed, tensor_id, count, scale, 0, d, 0);
+  CU(cudaGetLastError());
+  CU(cudaMemcpy(out, d, count * 4, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  return MOE_OK;
+}
+
+}  // extern "C"

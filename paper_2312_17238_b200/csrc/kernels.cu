@@ -1,0 +1,553 @@
+// Decode-path kernels of the B200 MoE offloading engine (sm_100a).
+//
+// Per token and layer (engine.cu enqueues them in this order):
+//   layernorm(x -> xn, ln1) | gemv<attn bits>(Wq,Wk,Wv) | attention | gemv(Wo)
+//   | tail (resid + LN2 + gate(l) + gate(l+lookahead) + top-k + device store)
+//   | gemv<expert bits>(W1,W3 of the routed experts) | gemv(W2, SwiGLU prologue)
+//   | combine (h + w0*y0 + w1*y1, reference order)
+// then layernorm(ln_f) | gemv<f16>(lm_head) | logits (+ argmax on device).
+// All reductions are in a fixed order, so results are run-to-run deterministic.
+#include "kernels.cuh"
+#include "gemv.cuh"
+
+namespace {
+
+MOE_DEV unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+MOE_DEV float sigmoid_ref(float x) {  // model.py:229-235 branch-stable logistic
+  if (x >= 0.f) return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-x)));
+  const float ex = expf(x);
+  return __fdiv_rn(ex, __fadd_rn(1.f, ex));
+}
+
+// ------------------------------------------------------------------ GEMV
+template <int BITS>
+__global__ void __launch_bounds__(MOE_GEMV_WARPS * 32)
+    k_gemv(const __grid_constant__ GLaunch P, int xs_cap) {
+  constexpr int WC = Fmt<BITS>::WC, NV = Fmt<BITS>::NV;
+  constexpr int U = (BITS == 2 || BITS == 4) ? 4 : 2;
+  constexpr int W = MOE_GEMV_WARPS;
+  extern __shared__ float smem[];
+  float* xs = smem;
+  float* red = smem + xs_cap;
+
+  int ji = 0;
+  for (int i = 1; i < P.nj; ++i)
+    if ((int)blockIdx.x >= P.j[i].blk0) ji = i;
+  const GJob& J = P.j[ji];
+  const int local = blockIdx.x - J.blk0;
+  const int cb = local / J.S, s = local % J.S;
+  MatDev M = J.M;
+  if (J.rel_slot >= 0) {
+    const int buf = P.route->buf[J.rel_slot];
+    const uint32_t gen = P.route->gen[J.rel_slot];
+    const uint8_t* base = P.pool + (long long)buf * P.slot_stride;
+    M.rec = reinterpret_cast<const uint4*>(base + reinterpret_cast<size_t>(M.rec));
+    M.zeros = reinterpret_cast<const uint32_t*>(base + reinterpret_cast<size_t>(M.zeros));
+    M.scales = reinterpret_cast<const uint2*>(base + reinterpret_cast<size_t>(M.scales));
+    M.zmeta = reinterpret_cast<const __half2*>(base + reinterpret_cast<size_t>(M.zmeta));
+    if (threadIdx.x == 0) {  // wait until the copy engine has landed this buffer
+      const uint32_t* f = P.flags + buf;
+      if ((int)(ld_acquire_u32(f) - gen) < 0) {
+        const unsigned long long t0 = globaltimer();
+        while ((int)(ld_acquire_u32(f) - gen) < 0) {
+          __nanosleep(256);
+          if (globaltimer() - t0 > P.wait_ns ||
+              (*reinterpret_cast<volatile int*>(P.err) & MOE_ERRF_TIMEOUT)) {
+            atomicOr(P.err, MOE_ERRF_TIMEOUT);
+            break;
+          }
+        }
+      }
+    }
+  }
+  const int qs = s * J.QPS, qe = min(J.nquads, qs + J.QPS);
+  const int row0 = qs * 4, nrows = max(qe - qs, 0) * 4;
+  const float xscale = BITS <= 4 ? gemv::kXScale : 1.f;
+  if (J.xmode == X_PLAIN) {
+    for (int i = threadIdx.x; i < nrows; i += blockDim.x) xs[i] = J.x[row0 + i] * xscale;
+  } else {  // SwiGLU of the up-projection partials (model.py:223-226)
+    const int K = M.K;
+    for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
+      const int r = row0 + i;
+      float a = 0.f, b = 0.f;
+      for (int t = 0; t < J.S_up; ++t) {
+        a += __ldcg(J.up1 + (size_t)t * K + r);
+        b += __ldcg(J.up3 + (size_t)t * K + r);
+      }
+      xs[i] = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b) * xscale;
+    }
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qpw = (qe - qs + W - 1) / W;
+  const int qb = qs + warp * qpw, qend = min(qe, qb + qpw);
+  const int chunk = cb * 32 + lane;
+  float y[WC];
+  if (chunk < J.nchunks) {
+    gemv::Lane L;
+    L.wcb = min(32, J.nchunks - cb * 32);
+    L.rec = M.rec + (int64_t)cb * 32 * J.nquads * NV + lane;
+    L.G = M.G;
+    L.S = M.S;
+    L.sg_log2 = M.sg_log2;
+    if (BITS <= 4) {
+      L.grp = (chunk * WC) >> M.g_log2;
+      L.zeros = M.zeros + L.grp;
+      L.scales = M.scales + ((chunk * WC) >> M.sg_log2);
+      L.zmeta = M.zmeta;
+    }
+    gemv::run_lane<BITS, U>(y, L, xs, row0, qb, qend);
+  } else {
+#pragma unroll
+    for (int k = 0; k < WC; ++k) y[k] = 0.f;
+  }
+#pragma unroll
+  for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
+  __syncthreads();
+  for (int t = threadIdx.x; t < 32 * WC; t += blockDim.x) {
+    const int l = t / WC, k = t % WC;
+    const int c = cb * 32 + l;
+    if (c < J.nchunks) {
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc += red[(w * 32 + l) * (WC + 1) + k];
+      J.out[(size_t)s * M.N + (size_t)c * WC + k] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ embed
+__global__ void k_embed(EmbedParams P) {
+  const int tok = P.tok_dev ? *P.tok_dev : P.tok;
+  if (P.tok_hist && blockIdx.x == 0 && threadIdx.x == 0) *P.tok_hist = tok;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.d) return;
+  float a, b;
+  if (P.half) {
+    a = __half2float(reinterpret_cast<const __half*>(P.wte)[(size_t)tok * P.d + i]);
+    b = __half2float(reinterpret_cast<const __half*>(P.wpe)[(size_t)P.pos * P.d + i]);
+  } else {
+    a = reinterpret_cast<const float*>(P.wte)[(size_t)tok * P.d + i];
+    b = reinterpret_cast<const float*>(P.wpe)[(size_t)P.pos * P.d + i];
+  }
+  P.x[i] = __fadd_rn(a, b);  // model.py:319
+}
+
+// LayerNorm with the reference's float32 rounding structure (model.py:186-189):
+// mu, var rounded to float32 (sums taken in double), then
+// ((x - mu) / sqrt(var + eps)) * gamma + beta with separately rounded ops.
+MOE_DEV void layernorm_block(const float* x, const float* g, const float* b, float* y, float* ysh,
+                             int d, double* red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) s += (double)x[i];
+  const float mu = (float)(block_sum_d(s, red) / d);
+  double q = 0.0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float t = __fsub_rn(x[i], mu);
+    q += (double)__fmul_rn(t, t);
+  }
+  const float var = (float)(block_sum_d(q, red) / d);
+  const float den = sqrtf(__fadd_rn(var, 1e-5f));
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(x[i], mu), den), g[i]), b[i]);
+    if (y) y[i] = v;
+    if (ysh) ysh[i] = v;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_layernorm(const float* x, const float* g, const float* b,
+                                                    float* y, int d) {
+  __shared__ double red[32];
+  layernorm_block(x, g, b, y, nullptr, d, red);
+}
+
+// ------------------------------------------------------------------ attention
+// One CTA per head (model.py:290-299): reduce q/k/v partials, append k/v to
+// the fp32 KV cache, scores / sqrt(hd), softmax, ctx = alpha @ V.
+__global__ void __launch_bounds__(256) k_attention(AttnParams P) {
+  extern __shared__ float sh[];
+  const int hd = P.hd, h = blockIdx.x, d = P.d;
+  float* q = sh;
+  float* sc = sh + hd;
+  __shared__ float red[32];
+  __shared__ float bval;
+  const size_t kvrow = (size_t)P.pos * P.H * hd + (size_t)h * hd;
+  for (int i = threadIdx.x; i < hd; i += blockDim.x) {
+    const int o = h * hd + i;
+    float a = 0.f, bk = 0.f, bv = 0.f;
+    for (int s = 0; s < P.S; ++s) {
+      a += __ldcg(P.qkv_part + ((size_t)0 * P.S + s) * d + o);
+      bk += __ldcg(P.qkv_part + ((size_t)1 * P.S + s) * d + o);
+      bv += __ldcg(P.qkv_part + ((size_t)2 * P.S + s) * d + o);
+    }
+    q[i] = a;
+    P.kc[kvrow + i] = bk;
+    P.vc[kvrow + i] = bv;
+  }
+  __syncthreads();
+  const int T = P.pos + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const float rs = sqrtf((float)hd);
+  for (int t = warp; t < T; t += nw) {
+    const float* kr = P.kc + (size_t)t * P.H * hd + (size_t)h * hd;
+    float a = 0.f;
+    for (int i = lane; i < hd; i += 32) a = fmaf(q[i], __ldcg(kr + i), a);
+    a = warp_sum(a);
+    if (lane == 0) sc[t] = __fdiv_rn(a, rs);
+  }
+  __syncthreads();
+  float mx = -INFINITY;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) mx = fmaxf(mx, sc[t]);
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = red[0];
+    for (int i = 1; i < nw; ++i) m = fmaxf(m, red[i]);
+    bval = m;
+  }
+  __syncthreads();
+  mx = bval;
+  float su = 0.f;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const float e = expf(__fsub_rn(sc[t], mx));
+    sc[t] = e;
+    su += e;
+  }
+  su = warp_sum(su);
+  __syncthreads();
+  if (lane == 0) red[warp] = su;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.f;
+    for (int i = 0; i < nw; ++i) m += red[i];
+    bval = m;
+  }
+  __syncthreads();
+  su = bval;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) sc[t] = __fdiv_rn(sc[t], su);
+  __syncthreads();
+  for (int i = threadIdx.x; i < hd; i += blockDim.x) {
+    float a = 0.f;
+    for (int t = 0; t < T; ++t)
+      a = fmaf(sc[t], __ldcg(P.vc + (size_t)t * P.H * hd + (size_t)h * hd + i), a);
+    P.ctx[h * hd + i] = a;
+  }
+}
+
+// ------------------------------------------------------------------ tail
+// resid = x + ctx@Wo; h = LN2(resid) (model.py:300-301); gate logits for this
+// layer and the guessed layer on the same h (model.py:210, engine.py:60-68);
+// stable top-k + softmax over the selected logits (model.py:211-215); trace
+// record (engine.py:122-128); then the device store: acquire each selected
+// expert in descending-weight order and speculative_load the guesses
+// (engine.py:222-231).
+__global__ void __launch_bounds__(1024) k_tail(TailParams P) {
+  extern __shared__ float hs[];
+  __shared__ double red[32];
+  __shared__ double gred[32][33];
+  __shared__ float lg[64];
+  const int d = P.d, E = P.E;
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float a = 0.f;
+    for (int s = 0; s < P.S; ++s) a += __ldcg(P.part + (size_t)s * d + i);
+    hs[i] = __fadd_rn(P.x[i], a);
+  }
+  __syncthreads();
+  layernorm_block(hs, P.g2, P.b2, P.h, hs, d, red);
+  __syncthreads();
+  int bad = 0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    if (!isfinite(hs[i])) bad = 1;
+    if (P.trace_hidden) P.trace_hidden[i] = hs[i];
+  }
+  bad = __syncthreads_or(bad);
+  const int nlog = P.gate_g ? 2 * E : E;  // E <= 16
+  double acc[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) acc[e] = 0.0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const double hv = hs[i];
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (e < E) acc[e] += hv * P.gate_l[(size_t)i * E + e];
+    if (P.gate_g) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (e < E) acc[16 + e] += hv * P.gate_g[(size_t)i * E + e];
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    const double v = warp_sum_d(acc[e]);
+    if (lane == 0) gred[warp][e] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int e = threadIdx.x;
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += gred[w][e];
+    const int idx = e < 16 ? e : E + (e - 16);
+    if ((e < 16 && e < E) || (e >= 16 && e - 16 < E && P.gate_g)) lg[idx] = (float)t;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  (void)nlog;
+  RouteRec R;
+  const int k = P.top_k;
+  int sel[MOE_MAX_TOPK];
+  unsigned long long used = 0ull;
+  for (int j = 0; j < k; ++j) {  // stable descending (ties -> lower index)
+    int best = -1;
+    for (int e = 0; e < E; ++e)
+      if (!((used >> e) & 1ull) && (best < 0 || lg[e] > lg[best])) best = e;
+    sel[j] = best;
+    used |= 1ull << best;
+  }
+  float ez[MOE_MAX_TOPK], sum = 0.f;
+  for (int j = 0; j < k; ++j) {
+    ez[j] = expf(__fsub_rn(lg[sel[j]], lg[sel[0]]));
+    sum = __fadd_rn(sum, ez[j]);
+  }
+  for (int j = 0; j < MOE_MAX_TOPK; ++j) {
+    R.e[j] = j < k ? sel[j] : -1;
+    R.w[j] = j < k ? __fdiv_rn(ez[j], sum) : 0.f;
+    R.buf[j] = -1;
+    R.gen[j] = 0;
+  }
+  TraceRecDev tr;
+  tr.pos = P.pos;
+  tr.layer = P.layer;
+  for (int j = 0; j < 8; ++j) {
+    tr.experts[j] = j < k ? sel[j] : -1;
+    tr.weights[j] = j < k ? R.w[j] : 0.f;
+  }
+  *P.trace = tr;
+  if (bad) {
+    atomicOr(P.st.err, MOE_ERRF_NONFINITE_GATE);
+    *P.route = R;
+    return;
+  }
+  if (P.mode == 0) {
+    StoreDev S = P.st;
+    store::begin_call(S);
+    for (int j = 0; j < k; ++j)
+      if (store::key_ok(S, P.layer, sel[j])) R.buf[j] = store::acquire(S, P.layer, sel[j], P.pos);
+    if (P.gate_g && P.m > 0) {
+      int g[16];
+      unsigned long long gu = 0ull;
+      const float* lgg = lg + E;
+      for (int j = 0; j < P.m; ++j) {
+        int best = -1;
+        for (int e = 0; e < E; ++e)
+          if (!((gu >> e) & 1ull) && (best < 0 || lgg[e] > lgg[best])) best = e;
+        g[j] = best;
+        gu |= 1ull << best;
+      }
+      store::speculative_load(S, P.guess_layer, g, P.m, P.pos, P.layer);
+    }
+    for (int j = 0; j < k; ++j)
+      if (R.buf[j] >= 0) R.gen[j] = S.gen[R.buf[j]];
+  }
+  *P.route = R;
+}
+
+// prefill: each distinct expert of the layer acquired once, first-use order
+// over (position, descending weight), no speculation (engine.py:233-240).
+__global__ void k_prefill_bk(PrefillBKParams P) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  StoreDev S = P.st;
+  store::begin_call(S);
+  int table[64];
+  for (int e = 0; e < 64; ++e) table[e] = -2;
+  for (int p = 0; p < P.n; ++p) {
+    for (int j = 0; j < P.top_k; ++j) {
+      const int e = P.route[p].e[j];
+      if (e < 0 || table[e] != -2) continue;
+      table[e] = store::key_ok(S, P.layer, e) ? store::acquire(S, P.layer, e, p) : -1;
+    }
+  }
+  for (int p = 0; p < P.n; ++p)
+    for (int j = 0; j < P.top_k; ++j) {
+      const int e = P.route[p].e[j];
+      const int b = e >= 0 ? table[e] : -1;
+      P.route[p].buf[j] = b;
+      P.route[p].gen[j] = b >= 0 ? S.gen[b] : 0;
+    }
+}
+
+__global__ void k_begin_call(StoreDev S) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) store::begin_call(S);
+}
+
+// out = h + w0*y0 + w1*y1 in descending-weight order (model.py:251-254)
+__global__ void k_combine(CombineParams P) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.d) return;
+  float out = P.h[i];
+  for (int j = 0; j < P.top_k; ++j) {
+    float y = 0.f;
+    for (int s = 0; s < P.S; ++s) y += __ldcg(P.part + ((size_t)j * P.S + s) * P.d + i);
+    out = __fadd_rn(out, __fmul_rn(P.route->w[j], y));
+  }
+  P.out[i] = out;
+}
+
+// logits = sum of lm_head partials; non-finite check (model.py:308-309);
+// argmax with lowest index on ties (model.py:374-375) via a last-block reduce.
+__global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
+  __shared__ float bv[256];
+  __shared__ int bi[256];
+  __shared__ bool last;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  float val = -INFINITY;
+  int idx = 0x7fffffff;
+  if (v < P.V) {
+    float a = 0.f;
+    for (int s = 0; s < P.S; ++s) a += __ldcg(P.part + (size_t)s * P.V + v);
+    P.logits[v] = a;
+    if (!isfinite(a)) atomicOr(P.err, MOE_ERRF_NONFINITE_LOGITS);
+    val = a;
+    idx = v;
+  }
+  bv[threadIdx.x] = val;
+  bi[threadIdx.x] = idx;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      const float a = bv[threadIdx.x + o];
+      const int ai = bi[threadIdx.x + o];
+      if (a > bv[threadIdx.x] || (a == bv[threadIdx.x] && ai < bi[threadIdx.x])) {
+        bv[threadIdx.x] = a;
+        bi[threadIdx.x] = ai;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    P.cand_val[blockIdx.x] = bv[0];
+    P.cand_idx[blockIdx.x] = bi[0];
+    __threadfence();
+    const unsigned int t = atomicAdd(P.counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  float best = -INFINITY;
+  int besti = 0x7fffffff;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    const float a = __ldcg(P.cand_val + b);
+    const int ai = __ldcg(P.cand_idx + b);
+    if (a > best || (a == best && ai < besti)) {
+      best = a;
+      besti = ai;
+    }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = besti;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      const float a = bv[threadIdx.x + o];
+      const int ai = bi[threadIdx.x + o];
+      if (a > bv[threadIdx.x] || (a == bv[threadIdx.x] && ai < bi[threadIdx.x])) {
+        bv[threadIdx.x] = a;
+        bi[threadIdx.x] = ai;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int t = bi[0] == 0x7fffffff ? 0 : bi[0];
+    *P.tok_out = t;
+    if (P.tok_hist) *P.tok_hist = t;
+    *P.counter = 0u;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+// Loads every kernel and sets its shared-memory limit while the GPU is idle.
+// With lazy module loading, the first launch of a kernel while another kernel
+// spin-waits on the copy engine can block the runtime (and so the copy
+// thread): everything is loaded up front instead.
+cudaError_t preload_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {(const void*)k_gemv<2>,   (const void*)k_gemv<3>,  (const void*)k_gemv<4>,
+                       (const void*)k_gemv<16>,  (const void*)k_gemv<32>, (const void*)k_embed,
+                       (const void*)k_layernorm, (const void*)k_attention, (const void*)k_tail,
+                       (const void*)k_prefill_bk, (const void*)k_begin_call,
+                       (const void*)k_combine,   (const void*)k_logits};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  for (int i = 0; i < 5; ++i) {
+    cudaError_t e = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_attention,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute((const void*)k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              200 * 1024);
+}
+
+template <int BITS>
+static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s) {
+  constexpr int WC = Fmt<BITS>::WC;
+  int xs_cap = 0;
+  for (int i = 0; i < P.nj; ++i) xs_cap = max(xs_cap, P.j[i].QPS * 4);
+  xs_cap = (xs_cap + 3) & ~3;
+  const size_t smem = (size_t)(xs_cap + MOE_GEMV_WARPS * 32 * (WC + 1)) * sizeof(float);
+  k_gemv<BITS><<<nblocks, MOE_GEMV_WARPS * 32, smem, s>>>(P, xs_cap);
+}
+
+void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s) {
+  switch (bits) {
+    case 2: launch_gemv_t<2>(P, nblocks, s); break;
+    case 3: launch_gemv_t<3>(P, nblocks, s); break;
+    case 4: launch_gemv_t<4>(P, nblocks, s); break;
+    case 16: launch_gemv_t<16>(P, nblocks, s); break;
+    default: launch_gemv_t<32>(P, nblocks, s); break;
+  }
+}
+
+void launch_embed(const EmbedParams& P, cudaStream_t s) {
+  k_embed<<<(P.d + 255) / 256, 256, 0, s>>>(P);
+}
+
+void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
+                      cudaStream_t s) {
+  k_layernorm<<<1, 1024, 0, s>>>(x, g, b, y, d);
+}
+
+void launch_attention(const AttnParams& P, cudaStream_t s) {
+  const size_t smem = (size_t)(P.hd + P.pos + 1) * sizeof(float);
+  k_attention<<<P.H, 256, smem, s>>>(P);
+}
+
+void launch_tail(const TailParams& P, cudaStream_t s) {
+  k_tail<<<1, 1024, (size_t)P.d * sizeof(float), s>>>(P);
+}
+
+void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s) { k_prefill_bk<<<1, 32, 0, s>>>(P); }
+void launch_begin_call(StoreDev st, cudaStream_t s) { k_begin_call<<<1, 32, 0, s>>>(st); }
+
+void launch_combine(const CombineParams& P, cudaStream_t s) {
+  k_combine<<<(P.d + 255) / 256, 256, 0, s>>>(P);
+}
+
+void launch_logits(const LogitsParams& P, cudaStream_t s) {
+  k_logits<<<(P.V + 255) / 256, 256, 0, s>>>(P);
+}

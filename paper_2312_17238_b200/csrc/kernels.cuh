@@ -1,0 +1,129 @@
+// Kernel parameter blocks shared by kernels.cu (device) and engine.cu (host).
+#pragma once
+#include "common.cuh"
+#include "store_dev.cuh"
+
+#define MOE_GEMV_WARPS 8
+#define MOE_GEMV_MAXJOBS 8
+#define MOE_XS_MAX 4096  // rows of x kept in smem per CTA
+
+enum XMode { X_PLAIN = 0, X_SWIGLU = 1 };
+
+struct GJob {
+  MatDev M;            // absolute pointers, or byte offsets when rel_slot >= 0
+  int rel_slot;        // >= 0: expert matrix, base = pool + route.buf[rel_slot]*stride
+  int xmode;
+  const float* x;      // X_PLAIN input (length K)
+  const float* up1;    // X_SWIGLU: partial sums of x@W1 [S_up][K]
+  const float* up3;    //           partial sums of x@W3 [S_up][K]
+  int S_up;
+  float* out;          // partial outputs [S][N]
+  int S, QPS, ncb, nchunks, nquads, blk0;
+};
+
+struct GLaunch {
+  GJob j[MOE_GEMV_MAXJOBS];
+  int nj;
+  const RouteRec* route;
+  const uint8_t* pool;
+  long long slot_stride;
+  const uint32_t* flags;
+  int* err;
+  unsigned long long wait_ns;  // give up waiting for a buffer after this long
+};
+
+struct AttnParams {
+  const float* qkv_part;  // [3][S][d]
+  int S;
+  float* kc;              // this layer's K cache [max_seq][H][hd]
+  float* vc;
+  float* ctx;             // [d]
+  int pos, H, hd, d;
+};
+
+struct TailParams {
+  const float* x;         // residual input [d]
+  const float* part;      // Wo partials [S][d]
+  int S;
+  const float* g2;        // ln2 gamma / beta
+  const float* b2;
+  const float* gate_l;    // [d][E] gate of this layer
+  const float* gate_g;    // [d][E] gate of the guessed layer (or null)
+  float* h;               // pre-MoE hidden out [d]
+  RouteRec* route;        // route of this position
+  TraceRecDev* trace;     // record slot for (pos, layer)
+  float* trace_hidden;    // [d] or null
+  StoreDev st;
+  int d, E, top_k, m, layer, guess_layer, pos, mode;  // mode 0 decode, 1 prefill (no store)
+  int ep_rank, ep_size;   // expert parallel (ep_size 1 = off)
+};
+
+struct PrefillBKParams {
+  RouteRec* route;  // [n]
+  StoreDev st;
+  int layer, n, top_k;
+};
+
+struct CombineParams {
+  const float* h;     // [d]
+  const float* part;  // [top_k][S][d]
+  int S;
+  const RouteRec* route;
+  float* out;         // [d]
+  int d, top_k;
+};
+
+struct LogitsParams {
+  const float* part;  // [S][V]
+  int S, V;
+  float* logits;      // [V]
+  float* cand_val;    // [nblk]
+  int* cand_idx;
+  unsigned int* counter;
+  int* tok_out;       // argmax
+  int* tok_hist;      // optional history slot
+  int* err;
+};
+
+struct EmbedParams {
+  const void* wte;
+  const void* wpe;
+  int half;           // 1: fp16 tables
+  const int* tok_dev; // token from device (greedy) or null
+  int tok;            // host token
+  int* tok_hist;      // write the consumed token here (or null)
+  int pos, d;
+  float* x;
+};
+
+// launchers (kernels.cu)
+void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s);
+void launch_embed(const EmbedParams& P, cudaStream_t s);
+void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
+                      cudaStream_t s);
+void launch_attention(const AttnParams& P, cudaStream_t s);
+void launch_tail(const TailParams& P, cudaStream_t s);
+void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s);
+void launch_combine(const CombineParams& P, cudaStream_t s);
+void launch_logits(const LogitsParams& P, cudaStream_t s);
+void launch_begin_call(StoreDev st, cudaStream_t s);
+cudaError_t preload_kernels();
+cudaError_t preload_tile_kernels();
+
+// tiling + quantization + synthesis (tile.cu)
+struct RefMat {  // reference-layout matrix resident on device
+  int bits, g, sg, K, N;
+  const uint8_t* codes;
+  const uint8_t* zeros;
+  const uint16_t* zs;
+  const uint16_t* zo;
+  const uint16_t* scales;
+  int64_t nruns;
+};
+void launch_tile(const RefMat& R, uint8_t* rec, uint32_t* zeros, uint2* scales, __half2* zmeta,
+                 cudaStream_t s);
+void launch_quantize(const float* w, int K, int N, int bits, int g, int sg, uint8_t* codes,
+                     uint8_t* zeros, uint16_t* zs, uint16_t* zo, uint16_t* scales, float* gmin_ws,
+                     float* gscale_ws, cudaStream_t s);
+void launch_synth(uint64_t seed, uint64_t tid, int64_t count, float scale, int to_half_round,
+                  float* out, cudaStream_t s);

@@ -1,0 +1,247 @@
+// Device-resident expert store: the exact semantics of the reference
+// TieredExpertStore (store.py:76-220) executed by one thread on the GPU, plus
+// the physical side the reference never sees: a pool of HBM expert buffers,
+// per-buffer copy generations, and a copy-request mailbox in mapped pinned
+// memory that the host copy engine drains (cudaMemcpyAsync + stream write of
+// the buffer's ready flag).
+//
+// Logical state (must match the reference exactly): per-layer MRU-first LRU
+// lists (<= k), b staging slots with stamps, the event sequence.
+// Physical state: every resident / staged expert owns one buffer.  Buffers
+// released during a bookkeeping call (evictions, k=0 transients, replaced
+// staging entries) are only recycled at the next call, i.e. after the expert
+// compute of the current layer has finished in stream order.
+#pragma once
+#include "common.cuh"
+#include "../../include/moeb200.h"
+
+#define MOE_ERRF_NONFINITE_GATE 1
+#define MOE_ERRF_NONFINITE_LOGITS 2
+#define MOE_ERRF_ALLOC 4
+#define MOE_ERRF_EVENTS 8
+#define MOE_ERRF_TIMEOUT 16
+#define MOE_ERRF_UNKNOWN 32
+
+#define MOE_MAX_TOPK 4
+#define MOE_MAILBOX_CAP 65536
+
+struct DevEvent {  // layout identical to moe_event
+  long long seq;
+  int kind, layer, expert, pos;
+  long long bytes;
+};
+
+struct CopyReq {
+  int buf, layer, expert;
+  uint32_t gen;
+};
+
+struct Mailbox {
+  volatile unsigned long long head;
+  unsigned long long pad[15];
+  CopyReq ring[MOE_MAILBOX_CAP];
+};
+
+struct RouteRec {  // per position: resolved experts of the current layer
+  int e[MOE_MAX_TOPK];
+  int buf[MOE_MAX_TOPK];
+  uint32_t gen[MOE_MAX_TOPK];
+  float w[MOE_MAX_TOPK];
+};
+
+struct TraceRecDev {  // layout identical to moe_trace_rec
+  int pos, layer;
+  int experts[8];
+  float weights[8];
+};
+
+struct StoreDev {
+  int L, E, k, b, top_k, nbuf;
+  long long expert_bytes;
+  int* lru;        // [L][max(k,1)] MRU first
+  int* lru_len;    // [L]
+  int* res_buf;    // [L][E]
+  int* stg_layer;  // [b] (-1 = empty)
+  int* stg_exp;
+  int* stg_stamp;
+  int* stg_buf;
+  int* scalars;    // [0]=stamp [1]=nfree [2]=npending [3]=nev
+  long long* seq;  // [1]
+  int* free_stack;
+  int* pending;
+  uint32_t* gen;  // [nbuf]
+  DevEvent* ev;
+  int ev_cap;
+  Mailbox* mb;    // device-mapped pointer
+  const unsigned char* owned;  // [L][E] or null (expert parallel subset)
+  int* err;
+};
+
+namespace store {
+
+MOE_DEV void begin_call(StoreDev& S) {
+  int nf = S.scalars[1];
+  const int np = S.scalars[2];
+  for (int i = 0; i < np; ++i) S.free_stack[nf++] = S.pending[i];
+  S.scalars[1] = nf;
+  S.scalars[2] = 0;
+}
+
+MOE_DEV void emit(StoreDev& S, int kind, int l, int e, int pos, bool moved) {
+  const long long sq = S.seq[0]++;
+  const int n = S.scalars[3];
+  if (n >= S.ev_cap) {
+    atomicOr(S.err, MOE_ERRF_EVENTS);
+    return;
+  }
+  DevEvent ev;
+  ev.seq = sq;
+  ev.kind = kind;
+  ev.layer = l;
+  ev.expert = e;
+  ev.pos = pos;
+  ev.bytes = moved ? S.expert_bytes : 0;
+  S.ev[n] = ev;
+  S.scalars[3] = n + 1;
+}
+
+MOE_DEV int alloc_buf(StoreDev& S) {
+  const int nf = S.scalars[1];
+  if (nf <= 0) {
+    atomicOr(S.err, MOE_ERRF_ALLOC);
+    return 0;
+  }
+  S.scalars[1] = nf - 1;
+  return S.free_stack[nf - 1];
+}
+
+MOE_DEV void release(StoreDev& S, int buf) { S.pending[S.scalars[2]++] = buf; }
+
+MOE_DEV void issue_copy(StoreDev& S, int buf, int l, int e) {
+  const uint32_t g = ++S.gen[buf];
+  Mailbox* mb = S.mb;
+  const unsigned long long h = mb->head;
+  CopyReq r;
+  r.buf = buf;
+  r.layer = l;
+  r.expert = e;
+  r.gen = g;
+  volatile int* dst = reinterpret_cast<volatile int*>(&mb->ring[h % MOE_MAILBOX_CAP]);
+  dst[0] = r.buf;
+  dst[1] = r.layer;
+  dst[2] = r.expert;
+  dst[3] = (int)r.gen;
+  __threadfence_system();
+  mb->head = h + 1;
+  __threadfence_system();
+}
+
+MOE_DEV int lru_find(const StoreDev& S, int l, int e) {
+  const int* lst = S.lru + l * max(S.k, 1);
+  const int n = S.lru_len[l];
+  for (int i = 0; i < n; ++i)
+    if (lst[i] == e) return i;
+  return -1;
+}
+
+MOE_DEV int staged_at(const StoreDev& S, int l, int e) {
+  for (int i = 0; i < S.b; ++i)
+    if (S.stg_layer[i] == l && S.stg_exp[i] == e) return i;
+  return -1;
+}
+
+// store.py:148-153 _insert_resident
+MOE_DEV void make_resident(StoreDev& S, int l, int e, int buf, int pos) {
+  int* lst = S.lru + l * max(S.k, 1);
+  int n = S.lru_len[l];
+  int evicted = -1;
+  if (n == S.k) {  // list full: the LRU tail leaves after the insert
+    evicted = lst[n - 1];
+    --n;
+  }
+  for (int i = n; i > 0; --i) lst[i] = lst[i - 1];
+  lst[0] = e;
+  S.lru_len[l] = n + 1;
+  S.res_buf[l * S.E + e] = buf;
+  if (evicted >= 0) {
+    emit(S, MOE_EV_EVICT_TO_HOST, l, evicted, pos, true);
+    release(S, S.res_buf[l * S.E + evicted]);
+  }
+}
+
+MOE_DEV bool key_ok(const StoreDev& S, int l, int e) {
+  if (l < 0 || l >= S.L || e < 0 || e >= S.E) return false;
+  return S.owned == nullptr || S.owned[l * S.E + e];
+}
+
+// store.py:157-186 acquire; returns the physical buffer holding the expert
+MOE_DEV int acquire(StoreDev& S, int l, int e, int pos) {
+  if (!key_ok(S, l, e)) {
+    atomicOr(S.err, MOE_ERRF_UNKNOWN);
+    return 0;
+  }
+  const int idx = lru_find(S, l, e);
+  if (idx >= 0) {
+    int* lst = S.lru + l * max(S.k, 1);
+    for (int i = idx; i > 0; --i) lst[i] = lst[i - 1];
+    lst[0] = e;
+    emit(S, MOE_EV_HIT, l, e, pos, false);
+    return S.res_buf[l * S.E + e];
+  }
+  const int s = staged_at(S, l, e);
+  if (s >= 0) {
+    emit(S, MOE_EV_STAGING_HIT, l, e, pos, false);
+    const int buf = S.stg_buf[s];
+    S.stg_layer[s] = -1;
+    S.stg_exp[s] = -1;
+    if (S.k > 0) {
+      emit(S, MOE_EV_PROMOTE_FROM_STAGING, l, e, pos, false);
+      make_resident(S, l, e, buf, pos);
+    } else {
+      release(S, buf);
+    }
+    return buf;
+  }
+  emit(S, MOE_EV_MISS_LOAD, l, e, pos, true);
+  const int buf = alloc_buf(S);
+  issue_copy(S, buf, l, e);
+  if (S.k > 0)
+    make_resident(S, l, e, buf, pos);
+  else
+    release(S, buf);
+  return buf;
+}
+
+// store.py:188-220 speculative_load (keys of one target layer)
+MOE_DEV void speculative_load(StoreDev& S, int tl, const int* es, int m, int pos, int cur_layer) {
+  for (int j = 0; j < m; ++j) {
+    const int e = es[j];
+    if (!key_ok(S, tl, e)) continue;  // EP: other ranks own it
+    if (lru_find(S, tl, e) >= 0 || staged_at(S, tl, e) >= 0) continue;
+    int slot = -1;
+    for (int i = 0; i < S.b; ++i)
+      if (S.stg_layer[i] < 0) {
+        slot = i;
+        break;
+      }
+    if (slot < 0) {
+      int best = 0x7fffffff;
+      for (int i = 0; i < S.b; ++i)
+        if (S.stg_layer[i] != cur_layer && S.stg_stamp[i] < best) {
+          best = S.stg_stamp[i];
+          slot = i;
+        }
+      if (slot < 0) continue;
+      release(S, S.stg_buf[slot]);
+    }
+    const int buf = alloc_buf(S);
+    issue_copy(S, buf, tl, e);
+    S.stg_layer[slot] = tl;
+    S.stg_exp[slot] = e;
+    S.stg_stamp[slot] = S.scalars[0]++;
+    S.stg_buf[slot] = buf;
+    emit(S, MOE_EV_SPECULATIVE_LOAD, tl, e, pos, true);
+  }
+}
+
+}  // namespace store

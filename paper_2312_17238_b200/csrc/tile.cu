@@ -1,0 +1,210 @@
+// Weight preparation on device:
+//  * tiling: reference-layout block (quant.py:76-102) -> the engine's tiled
+//    layout (common.cuh).  A pure byte permutation: same byte count, so the
+//    pinned host arena holds exactly payload_nbytes per expert (quant.py:332).
+//  * quantization: the reference quantizer (quant.py:181-229) re-expressed as
+//    four data-parallel kernels that reproduce its float32 / float64 rounding
+//    step for step, so device-quantized blocks are byte-identical.
+//  * synthesis: the counter-hash weight source of oracle/model.py synth_tensor.
+#include "kernels.cuh"
+
+namespace {
+
+// ------------------------------------------------------------------ tiling
+__global__ void k_tile_rec(RefMat R, uint4* rec) {
+  const int WC = fmt_wc(R.bits), NV = fmt_nv(R.bits);
+  const int nchunks = R.N / WC, nquads = R.K / 4;
+  const int64_t n = (int64_t)nquads * nchunks;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(idx / nchunks), c = (int)(idx % nchunks);
+    uint32_t w[16];
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(R.codes);
+    const int words_per_row = R.bits == 3 ? 3 : (R.bits <= 4 ? 1 : 4);
+    for (int r = 0; r < 4; ++r) {
+      const int64_t row = 4 * q + r;
+      int64_t wbase;
+      if (R.bits <= 4)
+        wbase = ((row * R.N + (int64_t)c * WC) * R.bits) >> 5;
+      else if (R.bits == 16)
+        wbase = (row * R.N + (int64_t)c * 8) >> 1;
+      else
+        wbase = row * R.N + (int64_t)c * 4;
+      for (int t = 0; t < words_per_row; ++t) w[r * words_per_row + t] = src[wbase + t];
+    }
+    const int cb = c / 32, lane = c % 32;
+    for (int v = 0; v < NV; ++v)
+      rec[rec_index(cb, q, v, lane, nquads, nchunks, NV)] =
+          make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+  }
+}
+
+__global__ void k_tile_meta(RefMat R, uint32_t* zeros, uint2* scales, __half2* zmeta) {
+  const int G = R.N / R.g, S = R.N / R.sg, nquads = R.K / 4;
+  const int64_t nz = (int64_t)nquads * G, ns = (int64_t)nquads * S;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nz; i += stride) {
+    const int64_t q = i / G, g = i % G;
+    uint32_t v = 0;
+    for (int r = 0; r < 4; ++r) v |= (uint32_t)R.zeros[(4 * q + r) * G + g] << (8 * r);
+    zeros[i] = v;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += stride) {
+    const int64_t q = i / S, s = i % S;
+    const uint32_t a = R.scales[(4 * q) * S + s], b = R.scales[(4 * q + 1) * S + s];
+    const uint32_t c = R.scales[(4 * q + 2) * S + s], d = R.scales[(4 * q + 3) * S + s];
+    scales[i] = make_uint2(a | (b << 16), c | (d << 16));
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R.nruns; i += stride)
+    zmeta[i] = __halves2half2(__ushort_as_half(R.zs[i]), __ushort_as_half(R.zo[i]));
+}
+
+// ------------------------------------------------------------------ quantize
+// per group of g weights: min, and (max - min) / levels in float32
+__global__ void k_q_groups(const float* w, int64_t ngroups, int g, int top, float* gmin,
+                           float* gscale) {
+  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < ngroups;
+       gi += (int64_t)gridDim.x * blockDim.x) {
+    const float* p = w + gi * g;
+    float lo = p[0], hi = p[0];
+    for (int t = 1; t < g; ++t) {
+      lo = fminf(lo, p[t]);
+      hi = fmaxf(hi, p[t]);
+    }
+    gmin[gi] = lo;
+    gscale[gi] = __fdiv_rn(__fsub_rn(hi, lo), (float)top);
+  }
+}
+
+// one f16 scale per scale group = max member scale (1.0 if all zero)
+__global__ void k_q_scales(const float* gscale, int64_t ngroups, int per, int64_t nsg,
+                           uint16_t* scales) {
+  for (int64_t si = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; si < nsg;
+       si += (int64_t)gridDim.x * blockDim.x) {
+    float m = gscale[si * per];
+    const int64_t e = min(ngroups, (si + 1) * per);
+    for (int64_t gi = si * per + 1; gi < e; ++gi) m = fmaxf(m, gscale[gi]);
+    scales[si] = m > 0.f ? __half_as_ushort(__float2half_rn(m)) : (uint16_t)0x3C00;
+  }
+}
+
+// codes = clip(rint((w - gmin) / scale), 0, top) packed LSB-first
+__global__ void k_q_codes(const float* w, int64_t ngroups, int g, int per, int bits, int top,
+                          const float* gmin, const uint16_t* scales, uint32_t* codes) {
+  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < ngroups;
+       gi += (int64_t)gridDim.x * blockDim.x) {
+    const float s = __half2float(__ushort_as_half(scales[gi / per]));
+    const float lo = gmin[gi];
+    const float* p = w + gi * g;
+    uint32_t* out = codes + ((gi * g * bits) >> 5);
+    unsigned long long buf = 0;
+    int nb = 0, wo = 0;
+    for (int t = 0; t < g; ++t) {
+      float c = rintf(__fdiv_rn(__fsub_rn(p[t], lo), s));
+      c = fminf(fmaxf(c, 0.f), (float)top);
+      buf |= (unsigned long long)(uint32_t)c << nb;
+      nb += bits;
+      if (nb >= 32) {
+        out[wo++] = (uint32_t)buf;
+        buf >>= 32;
+        nb -= 32;
+      }
+    }
+  }
+}
+
+// zero points: runs of sg group minima -> u8 codes with f16 (scale, offset);
+// spread in float64 and f16(spread/255) as quant.py:160-164
+__global__ void k_q_zmeta(const float* gmin, int64_t ngroups, int sg, int64_t nruns, uint8_t* zc,
+                          uint16_t* zs, uint16_t* zo) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nruns;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = r * sg, e = min(ngroups, b + sg);
+    float lo = gmin[b], hi = gmin[b];
+    for (int64_t i = b + 1; i < e; ++i) {
+      lo = fminf(lo, gmin[i]);
+      hi = fmaxf(hi, gmin[i]);
+    }
+    const double spread = (double)hi - (double)lo;
+    const double step = spread > 0.0 ? spread / 255.0 : 1.0;
+    const __half s16 = __double2half(step);
+    const float s32 = __half2float(s16);
+    for (int64_t i = b; i < e; ++i) {
+      float c = rintf(__fdiv_rn(__fsub_rn(gmin[i], lo), s32));
+      c = fminf(fmaxf(c, 0.f), 255.f);
+      zc[i] = (uint8_t)c;
+    }
+    zs[r] = __half_as_ushort(s16);
+    zo[r] = __half_as_ushort(__float2half_rn(lo));
+  }
+}
+
+// ------------------------------------------------------------------ synth
+MOE_DEV unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_synth(unsigned long long base, int64_t count, float scale, int half_round,
+                        float* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long h = mix64((unsigned long long)i * 0x9E3779B97F4A7C15ull + base);
+    const long long s = (long long)(h & 0xFFFF) + (long long)((h >> 16) & 0xFFFF) +
+                        (long long)((h >> 32) & 0xFFFF) + (long long)(h >> 48);
+    float v = __fmul_rn((float)(s - 131070), scale);
+    if (half_round) v = __half2float(__float2half_rn(v));
+    out[i] = v;
+  }
+}
+
+int grid_for(int64_t n) {
+  const int64_t b = (n + 255) / 256;
+  return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
+}  // namespace
+
+void launch_tile(const RefMat& R, uint8_t* rec, uint32_t* zeros, uint2* scales, __half2* zmeta,
+                 cudaStream_t s) {
+  const int64_t nrec = (int64_t)(R.K / 4) * (R.N / fmt_wc(R.bits));
+  k_tile_rec<<<grid_for(nrec), 256, 0, s>>>(R, reinterpret_cast<uint4*>(rec));
+  if (R.bits <= 4) {
+    const int64_t n = (int64_t)(R.K / 4) * (R.N / R.g);
+    k_tile_meta<<<grid_for(n), 256, 0, s>>>(R, zeros, scales, zmeta);
+  }
+}
+
+void launch_quantize(const float* w, int K, int N, int bits, int g, int sg, uint8_t* codes,
+                     uint8_t* zeros, uint16_t* zs, uint16_t* zo, uint16_t* scales, float* gmin,
+                     float* gscale, cudaStream_t s) {
+  const int64_t ng = (int64_t)K * N / g;
+  const int per = sg / g;
+  const int64_t nsg = (ng + per - 1) / per;
+  const int64_t nruns = (ng + sg - 1) / sg;
+  const int top = (1 << bits) - 1;
+  k_q_groups<<<grid_for(ng), 256, 0, s>>>(w, ng, g, top, gmin, gscale);
+  k_q_scales<<<grid_for(nsg), 256, 0, s>>>(gscale, ng, per, nsg, scales);
+  k_q_codes<<<grid_for(ng), 256, 0, s>>>(w, ng, g, per, bits, top, gmin, scales,
+                                         reinterpret_cast<uint32_t*>(codes));
+  k_q_zmeta<<<grid_for(nruns), 256, 0, s>>>(gmin, ng, sg, nruns, zeros, zs, zo);
+}
+
+void launch_synth(uint64_t seed, uint64_t tid, int64_t count, float scale, int half_round,
+                  float* out, cudaStream_t s) {
+  const unsigned long long base = (seed * 0x9E3779B97F4A7C15ull) ^ (tid * 0xD1B54A32D192ED03ull);
+  k_synth<<<grid_for(count), 256, 0, s>>>(base, count, scale, half_round, out);
+}
+
+cudaError_t preload_tile_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {(const void*)k_tile_rec, (const void*)k_tile_meta, (const void*)k_q_groups,
+                       (const void*)k_q_scales, (const void*)k_q_codes, (const void*)k_q_zmeta,
+                       (const void*)k_synth};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
