@@ -159,6 +159,12 @@ int moe_reset_session(moe_engine* eng);
 int moe_device_state(moe_engine* eng, int32_t* lru_out, int32_t* staged_out);
 
 int moe_get_stats(moe_engine* eng, moe_stats* out);
+
+/* Profiling: when on, every GEMV launch is bracketed by CUDA events on the
+ * compute stream; moe_kernel_times returns summed milliseconds and launch
+ * counts per class [qkv, wo, expert_up, expert_down, lm_head] (5 entries). */
+int moe_set_profiling(moe_engine* eng, int32_t on);
+int moe_kernel_times(moe_engine* eng, double* ms_out, int64_t* count_out);
 const char* moe_last_error(void);
 int moe_destroy(moe_engine* eng);
 

@@ -272,6 +272,39 @@ struct moe_engine {
   int ahead = 3;
   int throttle();
   int unit_done();
+  // per-class GEMV timing with CUDA events on the compute stream (profiling)
+  enum { K_QKV = 0, K_WO, K_UP, K_DOWN, K_LM, K_N };
+  bool prof = false;
+  std::vector<cudaEvent_t> pev;  // pairs
+  std::vector<int> pcls;
+  size_t pused = 0;
+  double prof_ms[K_N] = {};
+  int64_t prof_cnt[K_N] = {};
+  void prof_begin(int c) {
+    if (!prof) return;
+    if (pused + 2 > pev.size()) {
+      const size_t old = pev.size();
+      pev.resize(old + 256);
+      pcls.resize(pev.size() / 2);
+      for (size_t i = old; i < pev.size(); ++i) cudaEventCreate(&pev[i]);
+    }
+    pcls[pused / 2] = c;
+    cudaEventRecord(pev[pused], s_comp);
+  }
+  void prof_end(int) {
+    if (!prof) return;
+    cudaEventRecord(pev[pused + 1], s_comp);
+    pused += 2;
+  }
+  void prof_collect() {
+    for (size_t i = 0; i < pused; i += 2) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pev[i], pev[i + 1]);
+      prof_ms[pcls[i / 2]] += ms;
+      prof_cnt[pcls[i / 2]] += 1;
+    }
+    pused = 0;
+  }
   int dbg(const char* what, int l, int p);
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   size_t dev_bytes = 0;
@@ -304,6 +337,7 @@ moe_engine::~moe_engine() {
   }
   for (auto e : free_events) cudaEventDestroy(e);
   for (auto e : ring) cudaEventDestroy(e);
+  for (auto e : pev) cudaEventDestroy(e);
   void* ptrs[] = {wte, wpe, lm_head.mem, lnfg, lnfb, pool, flags, x, h, xn, ctx, logits,
                   qkv_part, wo_part, up_part, dn_part, lm_part, kc, vc, route, trace,
                   trace_hidden, tok_dev, tok_hist, tok_in, cand_val, cand_idx, counter, err,
@@ -423,7 +457,9 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   q.j[0] = dense_job(wq[l], xn, qkv_part, S_qkv);
   q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, S_qkv);
   q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, S_qkv);
+  prof_begin(K_QKV);
   launch_gemv(attn_bits, q, finalize_launch(q), s_comp);
+  prof_end(K_QKV);
   dbg("qkv", l, p);
   AttnParams a{};
   a.qkv_part = qkv_part;
@@ -440,7 +476,9 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   GLaunch o{};
   o.nj = 1;
   o.j[0] = dense_job(wo[l], ctx, wo_part, S_wo);
+  prof_begin(K_WO);
   launch_gemv(attn_bits, o, finalize_launch(o), s_comp);
+  prof_end(K_WO);
   dbg("wo", l, p);
   TailParams t{};
   t.x = xp;
@@ -479,9 +517,6 @@ int moe_engine::enq_experts(int p) {
   u.route = route + p;
   u.pool = pool;
   u.slot_stride = slot_stride;
-  u.flags = flags;
-  u.err = err;
-  u.wait_ns = wait_ns;
   GLaunch dn = u;
   for (int j = 0; j < topk; ++j) {
     for (int m = 0; m < 2; ++m) {
@@ -521,9 +556,15 @@ int moe_engine::enq_experts(int p) {
   }
   u.nj = 2 * topk;
   dn.nj = topk;
+  launch_wait_ready(route + p, topk, flags, err, wait_ns, s_comp);
+  dbg("wait", -1, p);
+  prof_begin(K_UP);
   launch_gemv(expert_bits, u, finalize_launch(u), s_comp);
+  prof_end(K_UP);
   dbg("up", -1, p);
+  prof_begin(K_DOWN);
   launch_gemv(expert_bits, dn, finalize_launch(dn), s_comp);
+  prof_end(K_DOWN);
   dbg("down", -1, p);
   CombineParams c{};
   c.h = h + (size_t)p * d;
@@ -545,7 +586,9 @@ int moe_engine::enq_logits(int p, float* out) {
   GLaunch g{};
   g.nj = 1;
   g.j[0] = dense_job(lm_head, xn, lm_part, S_lm);
+  prof_begin(K_LM);
   launch_gemv(lm_bits, g, finalize_launch(g), s_comp);
+  prof_end(K_LM);
   LogitsParams lp{};
   lp.part = lm_part;
   lp.S = S_lm;
@@ -593,6 +636,7 @@ int moe_engine::finish_call() {
   CU(cudaEventRecord(t1, s_comp));
   CU(cudaStreamSynchronize(s_comp));
   units_done = units_issued;
+  prof_collect();
   CU(cudaGetLastError());
   float ms = 0;
   cudaEventElapsedTime(&ms, t0, t1);
@@ -1194,6 +1238,25 @@ int moe_get_stats(moe_engine* e, moe_stats* out) {
   return MOE_OK;
 }
 
+int moe_set_profiling(moe_engine* e, int32_t on) {
+  if (!e) return fail(MOE_ERR_VALUE, "null engine");
+  e->prof = on != 0;
+  for (int i = 0; i < moe_engine::K_N; ++i) {
+    e->prof_ms[i] = 0;
+    e->prof_cnt[i] = 0;
+  }
+  return MOE_OK;
+}
+
+int moe_kernel_times(moe_engine* e, double* ms_out, int64_t* count_out) {
+  if (!e) return fail(MOE_ERR_VALUE, "null engine");
+  for (int i = 0; i < moe_engine::K_N; ++i) {
+    if (ms_out) ms_out[i] = e->prof_ms[i];
+    if (count_out) count_out[i] = e->prof_cnt[i];
+  }
+  return MOE_OK;
+}
+
 int moe_destroy(moe_engine* e) {
   if (e) {
     cudaSetDevice(e->dev);
@@ -1328,8 +1391,8 @@ int moe_synth_model(moe_engine* e, uint64_t seed, int32_t attn_bits, int32_t exp
     m.cols = cols;
     std::vector<uint8_t> host(n * (mixed ? 2 : 4));
     if (mixed) {
-      k_f32_to_f16<<<1184, 256, 0, s>>>(Q.w, reinterpret_cast<__half*>(Q.gscale), n);
-      CU(cudaMemcpyAsync(host.data(), Q.gscale, n * 2, cudaMemcpyDeviceToHost, s));
+      k_f32_to_f16<<<1184, 256, 0, s>>>(Q.w, reinterpret_cast<__half*>(Q.tiled), n);
+      CU(cudaMemcpyAsync(host.data(), Q.tiled, n * 2, cudaMemcpyDeviceToHost, s));
       m.bits = 16;
     } else {
       CU(cudaMemcpyAsync(host.data(), Q.w, n * 4, cudaMemcpyDeviceToHost, s));
@@ -1370,7 +1433,6 @@ int moe_synth_model(moe_engine* e, uint64_t seed, int32_t attn_bits, int32_t exp
     if (!rc) rc = put_vec(pre + "ln1.beta", zeros);
     if (!rc) rc = put_vec(pre + "ln2.gamma", ones);
     if (!rc) rc = put_vec(pre + "ln2.beta", zeros);
-    const char* an[4] = {"attn.wq", "attn.wk", "attn.wv", "attn.wo"};
     for (int j = 0; j < 4 && !rc; ++j) {
       Layout lo;
       rc = synth_matrix(Q, seed, base + j, d, d, sd, attn_bits, 0, &lo, s);

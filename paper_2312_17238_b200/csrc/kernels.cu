@@ -44,26 +44,11 @@ __global__ void __launch_bounds__(MOE_GEMV_WARPS * 32)
   MatDev M = J.M;
   if (J.rel_slot >= 0) {
     const int buf = P.route->buf[J.rel_slot];
-    const uint32_t gen = P.route->gen[J.rel_slot];
     const uint8_t* base = P.pool + (long long)buf * P.slot_stride;
     M.rec = reinterpret_cast<const uint4*>(base + reinterpret_cast<size_t>(M.rec));
     M.zeros = reinterpret_cast<const uint32_t*>(base + reinterpret_cast<size_t>(M.zeros));
     M.scales = reinterpret_cast<const uint2*>(base + reinterpret_cast<size_t>(M.scales));
     M.zmeta = reinterpret_cast<const __half2*>(base + reinterpret_cast<size_t>(M.zmeta));
-    if (threadIdx.x == 0) {  // wait until the copy engine has landed this buffer
-      const uint32_t* f = P.flags + buf;
-      if ((int)(ld_acquire_u32(f) - gen) < 0) {
-        const unsigned long long t0 = globaltimer();
-        while ((int)(ld_acquire_u32(f) - gen) < 0) {
-          __nanosleep(256);
-          if (globaltimer() - t0 > P.wait_ns ||
-              (*reinterpret_cast<volatile int*>(P.err) & MOE_ERRF_TIMEOUT)) {
-            atomicOr(P.err, MOE_ERRF_TIMEOUT);
-            break;
-          }
-        }
-      }
-    }
   }
   const int qs = s * J.QPS, qe = min(J.nquads, qs + J.QPS);
   const int row0 = qs * 4, nrows = max(qe - qs, 0) * 4;
@@ -118,6 +103,29 @@ __global__ void __launch_bounds__(MOE_GEMV_WARPS * 32)
 #pragma unroll
       for (int w = 0; w < W; ++w) acc += red[(w * 32 + l) * (WC + 1) + k];
       J.out[(size_t)s * M.N + (size_t)c * WC + k] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ wait
+// Blocks the compute stream until every expert buffer of this position's route
+// has landed (copy engine -> cuStreamWriteValue32 of the buffer generation).
+// One thread per routed expert; hits pass straight through.
+__global__ void k_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int* err,
+                             unsigned long long wait_ns) {
+  const int j = threadIdx.x;
+  if (j >= n) return;
+  const int buf = route->buf[j];
+  if (buf < 0) return;
+  const uint32_t gen = route->gen[j];
+  const uint32_t* f = flags + buf;
+  if ((int)(ld_acquire_u32(f) - gen) >= 0) return;
+  const unsigned long long t0 = globaltimer();
+  while ((int)(ld_acquire_u32(f) - gen) < 0) {
+    __nanosleep(200);
+    if (globaltimer() - t0 > wait_ns) {
+      atomicOr(err, MOE_ERRF_TIMEOUT);
+      return;
     }
   }
 }
@@ -486,7 +494,7 @@ cudaError_t preload_kernels() {
                        (const void*)k_gemv<16>,  (const void*)k_gemv<32>, (const void*)k_embed,
                        (const void*)k_layernorm, (const void*)k_attention, (const void*)k_tail,
                        (const void*)k_prefill_bk, (const void*)k_begin_call,
-                       (const void*)k_combine,   (const void*)k_logits};
+                       (const void*)k_combine,   (const void*)k_logits, (const void*)k_wait_ready};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -543,6 +551,11 @@ void launch_tail(const TailParams& P, cudaStream_t s) {
 
 void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s) { k_prefill_bk<<<1, 32, 0, s>>>(P); }
 void launch_begin_call(StoreDev st, cudaStream_t s) { k_begin_call<<<1, 32, 0, s>>>(st); }
+
+void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int* err,
+                       unsigned long long wait_ns, cudaStream_t s) {
+  k_wait_ready<<<1, 32, 0, s>>>(route, n, flags, err, wait_ns);
+}
 
 void launch_combine(const CombineParams& P, cudaStream_t s) {
   k_combine<<<(P.d + 255) / 256, 256, 0, s>>>(P);

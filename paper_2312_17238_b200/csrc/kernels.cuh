@@ -27,9 +27,6 @@ struct GLaunch {
   const RouteRec* route;
   const uint8_t* pool;
   long long slot_stride;
-  const uint32_t* flags;
-  int* err;
-  unsigned long long wait_ns;  // give up waiting for a buffer after this long
 };
 
 struct AttnParams {
@@ -105,6 +102,8 @@ void launch_attention(const AttnParams& P, cudaStream_t s);
 void launch_tail(const TailParams& P, cudaStream_t s);
 void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s);
 void launch_combine(const CombineParams& P, cudaStream_t s);
+void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int* err,
+                       unsigned long long wait_ns, cudaStream_t s);
 void launch_logits(const LogitsParams& P, cudaStream_t s);
 void launch_begin_call(StoreDev st, cudaStream_t s);
 cudaError_t preload_kernels();
