@@ -155,8 +155,13 @@ def run_b200(args, rank, world):
     s0 = eng.stats()
     L = _lib.lib()
     _lib.check(L.moe_set_profiling(eng._h, 1))
+    ncu_range = os.environ.get("MOE_NCU_RANGE") == "1"  # ncu --profile-from-start off
     with ClockSampler(args.device) as clk:
+        if ncu_range:
+            _lib.check(L.moe_profiler_range(1))
         res = eng.decode(args.steps)
+        if ncu_range:
+            _lib.check(L.moe_profiler_range(0))
     s1 = eng.stats()
     ms_tot = s1["last_call_ms"]
     kms = (C.c_double * 5)()

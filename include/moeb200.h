@@ -165,6 +165,9 @@ int moe_get_stats(moe_engine* eng, moe_stats* out);
  * counts per class [qkv, wo, expert_up, expert_down, lm_head] (5 entries). */
 int moe_set_profiling(moe_engine* eng, int32_t on);
 int moe_kernel_times(moe_engine* eng, double* ms_out, int64_t* count_out);
+/* cudaProfilerStart/Stop, so `ncu --profile-from-start off` captures only the
+ * bench's timed decode region. */
+int moe_profiler_range(int32_t on);
 const char* moe_last_error(void);
 int moe_destroy(moe_engine* eng);
 

@@ -6,6 +6,7 @@
 // device's copy-request mailbox with cudaMemcpyAsync on a side stream and
 // marks each buffer ready with cuStreamWriteValue32 (kernels wait on it).
 #include <cuda.h>
+#include <cuda_profiler_api.h>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -1254,6 +1255,11 @@ int moe_kernel_times(moe_engine* e, double* ms_out, int64_t* count_out) {
     if (ms_out) ms_out[i] = e->prof_ms[i];
     if (count_out) count_out[i] = e->prof_cnt[i];
   }
+  return MOE_OK;
+}
+
+int moe_profiler_range(int32_t on) {
+  CU(on ? cudaProfilerStart() : cudaProfilerStop());
   return MOE_OK;
 }
 
