@@ -186,6 +186,35 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y);
 int moe_synth_tensor_device(uint64_t seed, uint64_t tensor_id, int64_t count, float scale,
                             float* out);
 
+/* ------------------------------------------------------------------------
+ * Host execution of the device store (store_dev.cuh), for CPU tests and the
+ * expert-parallel ownership logic.  Runs the very functions the bookkeeping
+ * kernels run (store::resolve_token / resolve_prefill), so it replaces the
+ * reference TieredExpertStore (store.py:76-220) driven the way
+ * OffloadEngine._resolve_token / _resolve_prefill_layer drive it
+ * (engine.py:222-240).  `owned` (L*E bytes or NULL) restricts the store to
+ * one expert-parallel rank's keys. */
+typedef struct moe_store_sim moe_store_sim;
+int moe_store_sim_create(int32_t n_layers, int32_t n_experts, int32_t k, int32_t b,
+                         int64_t expert_bytes, int32_t top_k, int32_t m, const uint8_t* owned,
+                         moe_store_sim** out);
+/* one decode layer: acquire experts[0..k) then speculative_load guesses[0..m)
+ * of guess_layer (-1: none); bufs_out[k] physical buffers (-1: not owned) */
+int moe_store_sim_token(moe_store_sim* s, int32_t layer, int32_t pos, const int32_t* experts,
+                        int32_t k, const int32_t* guesses, int32_t m, int32_t guess_layer,
+                        int32_t* bufs_out);
+/* one prefill layer: experts[n][k]; bufs_out[n][k] */
+int moe_store_sim_prefill(moe_store_sim* s, int32_t layer, const int32_t* experts, int32_t n,
+                          int32_t k, int32_t* bufs_out);
+int64_t moe_store_sim_num_events(moe_store_sim* s);
+int moe_store_sim_events(moe_store_sim* s, moe_event* out, int64_t cap);
+int moe_store_sim_state(moe_store_sim* s, int32_t* lru_out, int32_t* staged_out,
+                        int32_t* content_out, int32_t* res_buf_out, int32_t* stg_buf_out,
+                        int32_t* nbuf_out);
+int64_t moe_store_sim_copies(moe_store_sim* s);
+const char* moe_store_sim_last_error(void);
+int moe_store_sim_destroy(moe_store_sim* s);
+
 #ifdef __cplusplus
 }
 #endif

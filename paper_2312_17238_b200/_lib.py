@@ -90,6 +90,15 @@ SIGNATURES = {
     "moe_quantize_device": (I32, [FP, I32, I32, I32, I32, I32, P, P, P, P, P]),
     "moe_gemv_device": (I32, [C.POINTER(Matrix), FP, FP]),
     "moe_synth_tensor_device": (I32, [U64, U64, I64, C.c_float, FP]),
+    "moe_store_sim_create": (I32, [I32, I32, I32, I32, I64, I32, I32, P, C.POINTER(P)]),
+    "moe_store_sim_token": (I32, [P, I32, I32, IP, I32, IP, I32, I32, IP]),
+    "moe_store_sim_prefill": (I32, [P, I32, IP, I32, I32, IP]),
+    "moe_store_sim_num_events": (I64, [P]),
+    "moe_store_sim_events": (I32, [P, C.POINTER(Event), I64]),
+    "moe_store_sim_state": (I32, [P, IP, IP, IP, IP, IP, IP]),
+    "moe_store_sim_copies": (I64, [P]),
+    "moe_store_sim_last_error": (C.c_char_p, []),
+    "moe_store_sim_destroy": (I32, [P]),
 }
 
 _lib = None

@@ -345,24 +345,21 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   }
   if (P.mode == 0) {
     StoreDev S = P.st;
-    store::begin_call(S);
-    for (int j = 0; j < k; ++j)
-      if (store::key_ok(S, P.layer, sel[j])) R.buf[j] = store::acquire(S, P.layer, sel[j], P.pos);
+    int g[16];
+    int m = 0;
     if (P.gate_g && P.m > 0) {
-      int g[16];
       unsigned long long gu = 0ull;
       const float* lgg = lg + E;
-      for (int j = 0; j < P.m; ++j) {
+      for (int j = 0; j < P.m; ++j) {  // top-m, ties -> lower index (engine.py:60-68)
         int best = -1;
         for (int e = 0; e < E; ++e)
           if (!((gu >> e) & 1ull) && (best < 0 || lgg[e] > lgg[best])) best = e;
         g[j] = best;
         gu |= 1ull << best;
       }
-      store::speculative_load(S, P.guess_layer, g, P.m, P.pos, P.layer);
+      m = P.m;
     }
-    for (int j = 0; j < k; ++j)
-      if (R.buf[j] >= 0) R.gen[j] = S.gen[R.buf[j]];
+    store::resolve_token(S, P.layer, sel, k, g, m, m ? P.guess_layer : -1, P.pos, R.buf, R.gen);
   }
   *P.route = R;
 }
@@ -372,23 +369,13 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
 __global__ void k_prefill_bk(PrefillBKParams P) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   StoreDev S = P.st;
-  store::begin_call(S);
-  int table[64];
-  for (int e = 0; e < 64; ++e) table[e] = -2;
-  for (int p = 0; p < P.n; ++p) {
-    for (int j = 0; j < P.top_k; ++j) {
-      const int e = P.route[p].e[j];
-      if (e < 0 || table[e] != -2) continue;
-      table[e] = store::key_ok(S, P.layer, e) ? store::acquire(S, P.layer, e, p) : -1;
-    }
-  }
-  for (int p = 0; p < P.n; ++p)
-    for (int j = 0; j < P.top_k; ++j) {
-      const int e = P.route[p].e[j];
-      const int b = e >= 0 ? table[e] : -1;
-      P.route[p].buf[j] = b;
-      P.route[p].gen[j] = b >= 0 ? S.gen[b] : 0;
-    }
+  RouteRec* R = P.route;
+  store::resolve_prefill(
+      S, P.layer, P.n, P.top_k, [&](int p, int j) { return R[p].e[j]; },
+      [&](int p, int j, int b, uint32_t g) {
+        R[p].buf[j] = b;
+        R[p].gen[j] = g;
+      });
 }
 
 __global__ void k_begin_call(StoreDev S) {

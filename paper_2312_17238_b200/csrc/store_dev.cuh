@@ -77,9 +77,30 @@ struct StoreDev {
   int* err;
 };
 
+// Every store operation is __host__ __device__: the engine runs it on one GPU
+// thread (k_tail / k_prefill_bk); the host simulator (store_sim.cu) runs the
+// very same code on the CPU so the bookkeeping is testable without a GPU.
+#define MOE_HD __host__ __device__ __forceinline__
+
 namespace store {
 
-MOE_DEV void begin_call(StoreDev& S) {
+MOE_HD void flag_err(StoreDev& S, int f) {
+#ifdef __CUDA_ARCH__
+  atomicOr(S.err, f);
+#else
+  __atomic_fetch_or(S.err, f, __ATOMIC_RELAXED);
+#endif
+}
+
+MOE_HD void fence_system() {
+#ifdef __CUDA_ARCH__
+  fence_system();
+#else
+  __atomic_thread_fence(__ATOMIC_SEQ_CST);
+#endif
+}
+
+MOE_HD void begin_call(StoreDev& S) {
   int nf = S.scalars[1];
   const int np = S.scalars[2];
   for (int i = 0; i < np; ++i) S.free_stack[nf++] = S.pending[i];
@@ -87,11 +108,11 @@ MOE_DEV void begin_call(StoreDev& S) {
   S.scalars[2] = 0;
 }
 
-MOE_DEV void emit(StoreDev& S, int kind, int l, int e, int pos, bool moved) {
+MOE_HD void emit(StoreDev& S, int kind, int l, int e, int pos, bool moved) {
   const long long sq = S.seq[0]++;
   const int n = S.scalars[3];
   if (n >= S.ev_cap) {
-    atomicOr(S.err, MOE_ERRF_EVENTS);
+    flag_err(S, MOE_ERRF_EVENTS);
     return;
   }
   DevEvent ev;
@@ -105,19 +126,19 @@ MOE_DEV void emit(StoreDev& S, int kind, int l, int e, int pos, bool moved) {
   S.scalars[3] = n + 1;
 }
 
-MOE_DEV int alloc_buf(StoreDev& S) {
+MOE_HD int alloc_buf(StoreDev& S) {
   const int nf = S.scalars[1];
   if (nf <= 0) {
-    atomicOr(S.err, MOE_ERRF_ALLOC);
+    flag_err(S, MOE_ERRF_ALLOC);
     return 0;
   }
   S.scalars[1] = nf - 1;
   return S.free_stack[nf - 1];
 }
 
-MOE_DEV void release(StoreDev& S, int buf) { S.pending[S.scalars[2]++] = buf; }
+MOE_HD void release(StoreDev& S, int buf) { S.pending[S.scalars[2]++] = buf; }
 
-MOE_DEV void issue_copy(StoreDev& S, int buf, int l, int e) {
+MOE_HD void issue_copy(StoreDev& S, int buf, int l, int e) {
   const uint32_t g = ++S.gen[buf];
   Mailbox* mb = S.mb;
   const unsigned long long h = mb->head;
@@ -131,28 +152,28 @@ MOE_DEV void issue_copy(StoreDev& S, int buf, int l, int e) {
   dst[1] = r.layer;
   dst[2] = r.expert;
   dst[3] = (int)r.gen;
-  __threadfence_system();
+  fence_system();
   mb->head = h + 1;
-  __threadfence_system();
+  fence_system();
 }
 
-MOE_DEV int lru_find(const StoreDev& S, int l, int e) {
-  const int* lst = S.lru + l * max(S.k, 1);
+MOE_HD int lru_find(const StoreDev& S, int l, int e) {
+  const int* lst = S.lru + l * (S.k > 1 ? S.k : 1);
   const int n = S.lru_len[l];
   for (int i = 0; i < n; ++i)
     if (lst[i] == e) return i;
   return -1;
 }
 
-MOE_DEV int staged_at(const StoreDev& S, int l, int e) {
+MOE_HD int staged_at(const StoreDev& S, int l, int e) {
   for (int i = 0; i < S.b; ++i)
     if (S.stg_layer[i] == l && S.stg_exp[i] == e) return i;
   return -1;
 }
 
 // store.py:148-153 _insert_resident
-MOE_DEV void make_resident(StoreDev& S, int l, int e, int buf, int pos) {
-  int* lst = S.lru + l * max(S.k, 1);
+MOE_HD void make_resident(StoreDev& S, int l, int e, int buf, int pos) {
+  int* lst = S.lru + l * (S.k > 1 ? S.k : 1);
   int n = S.lru_len[l];
   int evicted = -1;
   if (n == S.k) {  // list full: the LRU tail leaves after the insert
@@ -169,20 +190,20 @@ MOE_DEV void make_resident(StoreDev& S, int l, int e, int buf, int pos) {
   }
 }
 
-MOE_DEV bool key_ok(const StoreDev& S, int l, int e) {
+MOE_HD bool key_ok(const StoreDev& S, int l, int e) {
   if (l < 0 || l >= S.L || e < 0 || e >= S.E) return false;
   return S.owned == nullptr || S.owned[l * S.E + e];
 }
 
 // store.py:157-186 acquire; returns the physical buffer holding the expert
-MOE_DEV int acquire(StoreDev& S, int l, int e, int pos) {
+MOE_HD int acquire(StoreDev& S, int l, int e, int pos) {
   if (!key_ok(S, l, e)) {
-    atomicOr(S.err, MOE_ERRF_UNKNOWN);
+    flag_err(S, MOE_ERRF_UNKNOWN);
     return 0;
   }
   const int idx = lru_find(S, l, e);
   if (idx >= 0) {
-    int* lst = S.lru + l * max(S.k, 1);
+    int* lst = S.lru + l * (S.k > 1 ? S.k : 1);
     for (int i = idx; i > 0; --i) lst[i] = lst[i - 1];
     lst[0] = e;
     emit(S, MOE_EV_HIT, l, e, pos, false);
@@ -213,7 +234,7 @@ MOE_DEV int acquire(StoreDev& S, int l, int e, int pos) {
 }
 
 // store.py:188-220 speculative_load (keys of one target layer)
-MOE_DEV void speculative_load(StoreDev& S, int tl, const int* es, int m, int pos, int cur_layer) {
+MOE_HD void speculative_load(StoreDev& S, int tl, const int* es, int m, int pos, int cur_layer) {
   for (int j = 0; j < m; ++j) {
     const int e = es[j];
     if (!key_ok(S, tl, e)) continue;  // EP: other ranks own it
@@ -242,6 +263,46 @@ MOE_DEV void speculative_load(StoreDev& S, int tl, const int* es, int m, int pos
     S.stg_buf[slot] = buf;
     emit(S, MOE_EV_SPECULATIVE_LOAD, tl, e, pos, true);
   }
+}
+
+// One decode layer's bookkeeping, in the order of OffloadEngine._resolve_token
+// (engine.py:222-231): acquire the selected experts in descending-weight
+// order, then speculative_load the top-m guesses for layer + lookahead.
+// bufs/gens receive the physical buffer (and its copy generation) of each
+// selected expert; -1 for experts another EP rank owns.
+MOE_HD void resolve_token(StoreDev& S, int layer, const int* sel, int k, const int* guesses,
+                          int m, int guess_layer, int pos, int* bufs, uint32_t* gens) {
+  begin_call(S);
+  for (int j = 0; j < k; ++j) {
+    const bool in_range = layer >= 0 && layer < S.L && sel[j] >= 0 && sel[j] < S.E;
+    // out of range -> UnknownExpertError; in range but another rank's -> -1
+    bufs[j] = (!in_range || key_ok(S, layer, sel[j])) ? acquire(S, layer, sel[j], pos) : -1;
+  }
+  if (guess_layer >= 0 && m > 0) speculative_load(S, guess_layer, guesses, m, pos, layer);
+  for (int j = 0; j < k; ++j) gens[j] = bufs[j] >= 0 ? S.gen[bufs[j]] : 0u;
+}
+
+// One prefill layer (engine.py:233-240): every distinct expert acquired once,
+// first-use order over (position, descending weight), no speculation.
+// get(p, j) -> routed expert id; put(p, j, buf, gen) receives the buffer.
+#pragma nv_exec_check_disable
+template <class Get, class Put>
+MOE_HD void resolve_prefill(StoreDev& S, int layer, int n, int k, Get get, Put put) {
+  begin_call(S);
+  int table[64];
+  for (int e = 0; e < 64; ++e) table[e] = -2;
+  for (int p = 0; p < n; ++p)
+    for (int j = 0; j < k; ++j) {
+      const int e = get(p, j);
+      if (e < 0 || table[e] != -2) continue;
+      table[e] = key_ok(S, layer, e) ? acquire(S, layer, e, p) : -1;
+    }
+  for (int p = 0; p < n; ++p)
+    for (int j = 0; j < k; ++j) {
+      const int e = get(p, j);
+      const int b = e >= 0 ? table[e] : -1;
+      put(p, j, b, b >= 0 ? S.gen[b] : 0u);
+    }
 }
 
 }  // namespace store

@@ -11,6 +11,12 @@ if ROOT not in sys.path:
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
+def pytest_sessionstart(session):
+    """(Re)build libmoeb200.so when a source is newer (no-op otherwise)."""
+    from paper_2312_17238_b200 import build
+    build.build()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libmoeb200.so")
 

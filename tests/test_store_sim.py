@@ -1,0 +1,147 @@
+"""The engine's device store code (csrc/store_dev.cuh), executed on the host,
+against the oracle store and the reference's golden event logs (CPU).
+
+Same functions the k_tail / k_prefill_bk kernels run, so this pins the
+product bookkeeping — event grammar, LRU order, staging replacement, seq
+numbering — without a GPU, and checks the physical buffer invariants the
+reference never has to care about (k < top_k, k = 0 transients, staging
+slot recycling within one layer).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.store import KINDS, CacheConfig as OCache, ExpertStore
+from paper_2312_17238_b200.api import CacheConfig
+from paper_2312_17238_b200.store_sim import DeviceStoreSim
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rows(events):
+    return [[e.seq, KINDS.index(e.kind), e.key.layer, e.key.expert, e.token_pos, e.bytes_moved]
+            for e in events]
+
+
+def orows(events):
+    return [[sq, KINDS.index(k), l, e, p, b] for sq, k, l, e, p, b in events]
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_device_store_matches_reference_golden(i):
+    with open(os.path.join(GOLDEN, "store_golden.json")) as fh:
+        c = json.load(fh)[i]
+    s = DeviceStoreSim(c["L"], c["E"], CacheConfig(c["k"], c["b"], 64), top_k=1, m=2)
+    for op in c["ops"]:
+        if op[0] == "spec":
+            _, pos, cur, keys = op
+            tgt = keys[0][0]
+            s.resolve_token(cur, pos, [], [k[1] for k in keys], tgt)
+        else:
+            _, pos, l, e = op
+            buf = s.resolve_token(l, pos, [e])
+            assert s.buffers()["content"][buf[0]] == l * c["E"] + e
+        s.audit()
+    assert rows(s.events) == c["events"]
+    assert {str(l): [k.expert for k in v] for l, v in s.device_state().items()} == \
+        c["device_state"]
+    assert [list(k) for k in s.staged_keys()] == c["staged"]
+
+
+GEOMS = [(k, b, m) for k in (0, 1, 2, 4, 8) for b in (0, 1, 2, 4) for m in (0, 1, 2) if m <= b]
+
+
+@pytest.mark.parametrize("k,b,m", GEOMS)
+def test_decode_sequences_match_oracle_and_buffers_hold_keys(k, b, m):
+    L, E, T = 4, 8, 40
+    rng = np.random.default_rng(1000 * k + 10 * b + m)
+    sim = DeviceStoreSim(L, E, CacheConfig(k, b, 4096), top_k=2, m=m)
+    ref = ExpertStore(L, E, OCache(k, b, 4096))
+    for pos in range(T):
+        for l in range(L):
+            ex = [int(x) for x in rng.choice(E, 2, replace=False)]
+            g = [int(x) for x in rng.choice(E, m, replace=False)] if m else []
+            gl = l + 1 if (m and l + 1 < L) else -1
+            bufs = sim.resolve_token(l, pos, ex, g if gl >= 0 else [], gl)
+            for e in ex:
+                ref.acquire(l, e, pos)
+            if gl >= 0:
+                ref.speculative_load([(gl, x) for x in g], pos, current_layer=l)
+            content = sim.buffers()["content"]
+            for e, bf in zip(ex, bufs):      # the routed buffer holds the routed expert
+                assert content[bf] == l * E + e
+            assert len(set(bufs.tolist())) == 2
+    assert rows(sim.events) == orows(ref.events)
+    assert {l: tuple(x.expert for x in v) for l, v in sim.device_state().items()} == \
+        ref.device_state()
+    assert tuple(tuple(x) for x in sim.staged_keys()) == ref.staged_keys()
+    sim.audit()
+    n_loads = sum(1 for e in ref.events if e[1] in ("miss_load", "speculative_load"))
+    assert sim.copies == n_loads  # one H2D copy per MISS_LOAD / SPECULATIVE_LOAD, none per evict
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 8])
+def test_prefill_dedupe_matches_oracle(k):
+    L, E, n = 3, 8, 17
+    rng = np.random.default_rng(k)
+    sim = DeviceStoreSim(L, E, CacheConfig(k, 4, 64), top_k=2)
+    ref = ExpertStore(L, E, OCache(k, 4, 64))
+    for l in range(L):
+        ex = np.stack([rng.choice(E, 2, replace=False) for _ in range(n)]).astype(np.int32)
+        bufs = sim.resolve_prefill(l, ex)
+        seen = set()
+        for p in range(n):
+            for e in ex[p]:
+                if int(e) not in seen:
+                    ref.acquire(l, int(e), p)
+                    seen.add(int(e))
+        content = sim.buffers()["content"]
+        for p in range(n):
+            for j in range(2):
+                assert content[bufs[p, j]] == l * E + ex[p, j]
+    assert rows(sim.events) == orows(ref.events)
+
+
+def test_unknown_expert_raises():
+    from paper_2312_17238_b200 import UnknownExpertError
+    sim = DeviceStoreSim(2, 8, CacheConfig(2, 4, 64))
+    with pytest.raises(UnknownExpertError):
+        sim.resolve_token(0, 0, [9])
+
+
+def test_ep_rank_store_equals_oracle_on_owned_subset():
+    """Expert parallel: each rank's store is the reference store over its owned
+    keys; together the ranks resolve every routed expert once."""
+    from paper_2312_17238_b200.expert_parallel import owned_keys
+    L, E, N = 3, 8, 4
+    rng = np.random.default_rng(7)
+    ops = []
+    for pos in range(30):
+        for l in range(L):
+            ops.append((l, pos, [int(x) for x in rng.choice(E, 2, replace=False)],
+                        [int(x) for x in rng.choice(E, 2, replace=False)]))
+    resolved = {}
+    for r in range(N):
+        own = owned_keys(L, E, r, N)
+        sim = DeviceStoreSim(L, E, CacheConfig(1, 2, 64), top_k=2, m=2, owned=own)
+        ref = ExpertStore(L, E, OCache(1, 2, 64), owned=own)
+        for l, pos, ex, g in ops:
+            gl = l + 1 if l + 1 < L else -1
+            bufs = sim.resolve_token(l, pos, ex, g if gl >= 0 else [], gl)
+            for e, bf in zip(ex, bufs):
+                if (l, e) in own:
+                    ref.acquire(l, e, pos)
+                    assert bf >= 0
+                    resolved[(l, pos, e)] = resolved.get((l, pos, e), 0) + 1
+                else:
+                    assert bf == -1
+            if gl >= 0:
+                keys = [(gl, x) for x in g if (gl, x) in own]
+                if keys:
+                    ref.speculative_load(keys, pos, current_layer=l)
+        assert rows(sim.events) == orows(ref.events)
+        sim.audit()
+    assert len(resolved) == len(ops) * 2 and set(resolved.values()) == {1}
