@@ -1,0 +1,91 @@
+"""Expert-parallel host logic on CPU: world_size 2 over gloo (127.0.0.1).
+
+Each rank owns half of every layer's experts, computes the SwiGLU output of
+the routed experts it owns into a (top_k, d) slot buffer (zero elsewhere),
+sum-exchanges it, and applies the reference-ordered combine.  The result
+must equal the single-process moe_forward (model.py:238-254) bit for bit,
+because exactly one rank contributes each slot and x + 0 is exact.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2312_17238_b200.expert_parallel import (local_cache_k, owned_experts, owned_keys,
+                                                   owned_mask, owner_of)
+
+
+def test_partition_covers_every_expert_once():
+    for E in (8, 16):
+        for N in (1, 2, 4, 8):
+            seen = []
+            for r in range(N):
+                seen += owned_experts(E, r, N)
+                assert owned_mask(3, E, r, N).sum() == 3 * len(owned_experts(E, r, N))
+            assert sorted(seen) == list(range(E))
+            assert all(owner_of(e, E, N) in range(N) for e in range(E))
+    assert owned_keys(2, 8, 1, 2) == {(l, e) for l in range(2) for e in (4, 5, 6, 7)}
+    assert local_cache_k(4, 8, 2) == 2 and local_cache_k(2, 8, 8) == 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import model as OM
+    from paper_2312_17238_b200.expert_parallel import combine, owned_experts, slot_exchange
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = OM.ModelConfig(vocab_size=32, d_model=64, n_layers=2, n_heads=2, d_ffn=96,
+                             n_experts=8)
+        m = OM.Model(cfg, OM.init_params(cfg))
+        rng = np.random.default_rng(0)          # same h on every rank (replicated dense path)
+        mine = set(owned_experts(cfg.n_experts, rank, world))
+        results = []
+        for layer in range(cfg.n_layers):
+            for _ in range(5):
+                h = rng.normal(size=cfg.d_model).astype(np.float32)
+                out = OM.gate(m, layer, h)
+                slots = np.zeros((len(out.experts), cfg.d_model), np.float32)
+                for j, e in enumerate(out.experts):
+                    if e in mine:
+                        slots[j] = OM.swiglu(*m.expert(layer, e), h)
+
+                def ar(buf):
+                    t = torch.from_numpy(buf)
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+                y = combine(h, out.weights, slot_exchange(slots, ar))
+                ref = OM.moe_forward(h, out, [m.expert(layer, e) for e in out.experts])
+                results.append(bool(np.array_equal(y, ref)))
+        q.put((rank, all(results), len(results)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_slot_exchange_is_exact_world2():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r for r, _, _ in out) == [0, 1]
+    assert all(ok for _, ok, _ in out), out
+    assert all(n == 10 for _, _, n in out)

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <cstdint>
 #include <cmath>
@@ -29,6 +30,23 @@ __global__ void k_subnormal(const uint32_t* codes, const float* xs, float* out, 
   float2 r = __ffma2_rn(a, b, c);
   out[2 * i] = r.x;
   out[2 * i + 1] = fmaf(xs[i], m, 0.f);
+}
+
+// ---------------------------------------------------------------- zero-copy pull
+// GPU-initiated H2D: CTAs read a mapped pinned host buffer over PCIe and store
+// into HBM (the alternative to DMA copies issued by a host thread).
+template <int UNR>
+__global__ void k_pull(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t n) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (; i + (UNR - 1) * stride < n; i += UNR * stride) {
+    uint4 v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) v[u] = src[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) dst[i + u * stride] = v[u];
+  }
+  for (; i < n; i += stride) dst[i] = src[i];
 }
 
 // ---------------------------------------------------------------- proto GEMV
@@ -254,6 +272,34 @@ int main() {
     cudaEventRecord(e1, s1); cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     printf("D2D copy %.1f MB: %.3f ms = %.1f GB/s (r+w)\n", 4 * sz / 1e6, ms, 2 * 4 * sz / ms / 1e6);
+    // zero-copy pull kernel from mapped pinned memory
+    {
+      char* hm; CK(cudaHostAlloc(&hm, sz, cudaHostAllocMapped));
+      memset(hm, 1, sz);
+      char* hd; CK(cudaHostGetDevicePointer((void**)&hd, hm, 0));
+      for (int nb : {2, 4, 8, 16, 32, 64, 148, 296}) {
+        for (int thr : {256, 1024}) {
+          float bestp = 1e9;
+          for (int it = 0; it < 5; ++it) {
+            cudaEventRecord(e0, s1);
+            k_pull<8><<<nb, thr, 0, s1>>>((const uint4*)hd, (uint4*)dev, sz / 16);
+            cudaEventRecord(e1, s1); CK(cudaEventSynchronize(e1));
+            float m2; cudaEventElapsedTime(&m2, e0, e1); bestp = std::min(bestp, m2);
+          }
+          printf("zero-copy pull %3d CTAs x %4d thr: %.3f ms = %.1f GB/s\n", nb, thr, bestp, sz / bestp / 1e6);
+        }
+      }
+      // DMA copy concurrent with a pull on another stream (two engines on one link)
+      cudaEventRecord(e0, s1);
+      cudaStreamWaitEvent(s2, e0, 0);
+      CK(cudaMemcpyAsync(dev + sz, host, sz, cudaMemcpyHostToDevice, s2));
+      k_pull<8><<<16, 1024, 0, s1>>>((const uint4*)hd, (uint4*)dev, sz / 16);
+      cudaEvent_t e3; cudaEventCreate(&e3); cudaEventRecord(e3, s2); cudaStreamWaitEvent(s1, e3, 0);
+      cudaEventRecord(e1, s1); CK(cudaEventSynchronize(e1));
+      float m3; cudaEventElapsedTime(&m3, e0, e1);
+      printf("DMA + pull concurrently (2 x %.1f MB): %.3f ms = %.1f GB/s\n", sz / 1e6, m3, 2 * sz / m3 / 1e6);
+      cudaFreeHost(hm);
+    }
     // ---- 4. stream write value
     CUdeviceptr flag; cuMemAlloc(&flag, 4); cuMemsetD32(flag, 0, 1);
     CUresult r = cuStreamWriteValue32((CUstream)s1, flag, 42, CU_STREAM_WRITE_VALUE_DEFAULT);
