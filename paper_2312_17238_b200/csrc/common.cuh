@@ -60,25 +60,38 @@ MOE_DEV double block_sum_d(double v, double* sh) {
 }
 
 // ---------------------------------------------------------------- layout
-// Tiled device layout of one K x N matrix (x[K] @ W[K,N]).  A "chunk" is WC
-// consecutive outputs of one row; a "quad" is 4 consecutive rows; 32 chunks form
-// a column block (cb).  Record (quad, chunk) = the chunk's bytes for the 4 rows,
-// R bytes = 16*NV uint4; records are stored [cb][quad][v][lane] so each warp
-// load instruction is one contiguous 512 B segment.
-//   quant (bits 2/3/4): the record bytes are the reference bitstream bytes of
-//     the chunk (quant.py:105-113 packing), zeros [quad][G] u32 (4 rows' u8
-//     zero codes), scales [quad][S] uint2 (4 rows' f16), zmeta [run] half2.
-//   dense f16 / f32: the record holds the raw row values.
+// Tiled device layout of one K x N matrix (x[K] @ W[K,N]), built for a
+// bulk-copy (cp.async.bulk) pipeline through shared memory.
+//   chunk  = WC consecutive outputs of one row (one lane's outputs)
+//   quad   = 4 consecutive rows
+//   column block (cb) = 32 chunks (the 32 lanes of a warp); the last cb of a
+//            matrix may be narrower (wcb < 32 chunks)
+// Record (cb, quad) holds everything one warp needs for 4 rows of its cb,
+// contiguously:
+//   codes   [NV][wcb] uint4   the chunk's bytes for the 4 rows: reference
+//                             bitstream bytes (quant.py:105-113) for bits
+//                             2/3/4, raw row values for dense f16 / f32
+//   zeros   [ZPR] u32         4 rows' u8 zero codes per zero group (quant only)
+//   scales  [SPR] uint2       4 rows' f16 scales per scale group (quant only)
+// ZPR = wcb*WC/g zero groups and SPR = wcb*WC/sg scale groups per row of the
+// cb.  Records are stored [cb][quad], so the records of one cb over a range
+// of quads are one contiguous byte range = one bulk copy.  The zero-point
+// metadata (one (zscale, zoffset) f16 pair per run of sg groups, flat over
+// the whole matrix, quant.py:147-178) follows all records.  The layout is a
+// pure byte permutation of the reference block: total bytes == payload_nbytes
+// (quant.py:332-343), so an expert buffer is exactly expert_bytes.
 struct MatDev {
-  const uint4* rec;
-  const uint32_t* zeros;
-  const uint2* scales;
-  const __half2* zmeta;
-  int K, N;      // rows (reduction dim), cols (outputs)
-  int G, S;      // zero groups / scale groups per row
-  int g_log2;    // zero group size (weights)
-  int sg_log2;   // scale group size (weights) = zmeta run length (groups)
-  int bits;      // 2,3,4 quant; 16, 32 dense
+  const uint8_t* base;   // records (absolute, or byte offset when relative)
+  const __half2* zmeta;  // [nruns] (absolute, or byte offset when relative)
+  int K, N;              // rows (reduction dim), cols (outputs)
+  int nquads, nchunks, ncb;
+  int nqp;               // quads per cb in storage: nquads rounded up to a multiple
+                         // of 8 (padding records are zero; only when K % 32 != 0)
+  int rb_full;           // record bytes of a full (32-chunk) cb
+  int G;                 // zero groups per row (N / g)
+  int g_log2;            // zero group size (weights)
+  int sg_log2;           // scale group size (weights) = zmeta run length (groups)
+  int bits;              // 2,3,4 quant; 16, 32 dense
 };
 
 template <int BITS> struct Fmt;
@@ -93,9 +106,15 @@ __host__ __device__ inline int fmt_wc(int bits) {
 }
 __host__ __device__ inline int fmt_nv(int bits) { return bits == 3 ? 3 : (bits >= 16 ? 4 : 1); }
 
-// record (cb, quad, v, lane) -> uint4 index
-__host__ __device__ inline int64_t rec_index(int cb, int quad, int v, int lane, int nquads,
-                                             int nchunks, int nv) {
-  const int wcb = min(32, nchunks - cb * 32);
-  return (int64_t)cb * 32 * nquads * nv + ((int64_t)quad * nv + v) * wcb + lane;
+// bytes of one (cb, quad) record for a cb of `wcb` chunks
+__host__ __device__ inline int rec_bytes(int bits, int wcb, int g_log2, int sg_log2) {
+  int b = 16 * fmt_nv(bits) * wcb;
+  if (bits <= 4) {
+    const int outs = wcb * fmt_wc(bits);
+    b += 4 * (outs >> g_log2) + 8 * (outs >> sg_log2);
+  }
+  return b;
+}
+__host__ __device__ inline int64_t cb_offset(const MatDev& M, int cb) {
+  return (int64_t)cb * M.nqp * M.rb_full;
 }

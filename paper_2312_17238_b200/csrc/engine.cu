@@ -47,8 +47,19 @@ struct DevMat {  // one tiled matrix in device memory
   void* mem = nullptr;
   size_t bytes = 0;
   int bits = 0;
-  int ncb = 0, nchunks = 0, nquads = 0;
 };
+
+// split the quad range of every job so one launch is ~2 CTAs per SM
+// (MOE_GEMV_THREADS threads, ~100 KB smem each); QPS is a multiple of the
+// pipeline stage so every bulk copy stays 16-byte aligned
+int plan_qps(int total_cb, int nquads) {
+  const int target = 2 * 148;
+  int S = std::max(1, (target + total_cb - 1) / total_cb);
+  int qps = (nquads + S - 1) / S;
+  qps = (qps + MOE_GEMV_QS - 1) / MOE_GEMV_QS * MOE_GEMV_QS;
+  while (qps * 4 > MOE_XS_MAX) qps -= MOE_GEMV_QS;
+  return std::max(qps, MOE_GEMV_QS);
+}
 
 struct Layout {  // byte sections of one tiled matrix
   int bits = 0, K = 0, N = 0, g = 0, sg = 0;
@@ -56,6 +67,16 @@ struct Layout {  // byte sections of one tiled matrix
   int64_t nruns = 0;
   size_t total() const { return rec + scales + zeros + zmeta; }
 };
+
+// record bytes of a laid-out matrix, including zero pad quads (K % 32 != 0)
+size_t layout_rec_bytes(const Layout& L) {
+  const int wc = fmt_wc(L.bits), nchunks = L.N / wc, ncb = (nchunks + 31) / 32;
+  const int nqp = ((L.K / 4) + 7) / 8 * 8;
+  const int gl = L.bits <= 4 ? ilog2(L.g) : 0, sl = L.bits <= 4 ? ilog2(L.sg) : 0;
+  const int last = nchunks - (ncb - 1) * 32;
+  return (size_t)nqp * ((size_t)(ncb - 1) * rec_bytes(L.bits, 32, gl, sl) +
+                        rec_bytes(L.bits, last, gl, sl));
+}
 
 int make_layout(const moe_matrix* m, Layout* L, const char* what) {
   const int bits = m->bits;
@@ -74,14 +95,14 @@ int make_layout(const moe_matrix* m, Layout* L, const char* what) {
   if (bits >= 16) {
     const int64_t need = (int64_t)K * N * (bits / 8);
     if (m->codes_len != need) return fail(MOE_ERR_FORMAT, std::string(what) + ": payload size mismatch");
-    L->rec = need;
+    L->rec = layout_rec_bytes(*L);
     return MOE_OK;
   }
   const int g = m->group_size, sg = m->scale_group_size;
   if (m->meta_bits != 8) return fail(MOE_ERR_VALUE, std::string(what) + ": meta_bits must be 8");
   if (m->pad_count != 0 || N % g)
     return fail(MOE_ERR_VALUE, std::string(what) + ": cols must be a multiple of group_size");
-  if (ilog2(g) < 0 || ilog2(sg) < 0 || g % wc || sg % g || N % sg)
+  if (ilog2(g) < 0 || ilog2(sg) < 0 || g % wc || sg % g || N % sg || (32 * wc) % sg)
     return fail(MOE_ERR_VALUE, std::string(what) + ": unsupported grouping for the device layout");
   if (((int64_t)g * bits) % 32) return fail(MOE_ERR_VALUE, std::string(what) + ": group not word aligned");
   const int64_t ng = (int64_t)K * N / g;
@@ -92,9 +113,9 @@ int make_layout(const moe_matrix* m, Layout* L, const char* what) {
     return fail(MOE_ERR_FORMAT, std::string(what) + ": block arrays inconsistent with shape");
   L->g = g;
   L->sg = sg;
-  L->rec = (size_t)K * N * bits / 8;
-  L->scales = (size_t)nsg * 2;
-  L->zeros = (size_t)ng;
+  // records = codes + zeros (1 B per group) + scales (f16 per scale group);
+  // equal to the reference byte count whenever K % 32 == 0 (no pad quads)
+  L->rec = layout_rec_bytes(*L);
   L->zmeta = (size_t)nruns * 4;
   L->nruns = nruns;
   return MOE_OK;
@@ -102,27 +123,28 @@ int make_layout(const moe_matrix* m, Layout* L, const char* what) {
 
 MatDev matdev_from(const Layout& L, const uint8_t* base) {
   MatDev M{};
-  M.rec = reinterpret_cast<const uint4*>(base);
-  M.scales = reinterpret_cast<const uint2*>(base + L.rec);
-  M.zeros = reinterpret_cast<const uint32_t*>(base + L.rec + L.scales);
-  M.zmeta = reinterpret_cast<const __half2*>(base + L.rec + L.scales + L.zeros);
+  M.base = base;
+  M.zmeta = reinterpret_cast<const __half2*>(base + L.rec);
   M.K = L.K;
   M.N = L.N;
   M.bits = L.bits;
+  M.nquads = L.K / 4;
+  M.nqp = (M.nquads + 7) / 8 * 8;
+  M.nchunks = L.N / fmt_wc(L.bits);
+  M.ncb = (M.nchunks + 31) / 32;
   if (L.bits <= 4) {
     M.G = L.N / L.g;
-    M.S = L.N / L.sg;
     M.g_log2 = ilog2(L.g);
     M.sg_log2 = ilog2(L.sg);
   }
+  M.rb_full = rec_bytes(L.bits, 32, M.g_log2, M.sg_log2);
   return M;
 }
 
 // tile a reference-layout matrix already resident on device into `dst`
 int tile_device(const RefMat& R, const Layout& L, uint8_t* dst, cudaStream_t s) {
-  launch_tile(R, dst, reinterpret_cast<uint32_t*>(dst + L.rec + L.scales),
-              reinterpret_cast<uint2*>(dst + L.rec),
-              reinterpret_cast<__half2*>(dst + L.rec + L.scales + L.zeros), s);
+  if ((L.K / 4) % 8) CU(cudaMemsetAsync(dst, 0, L.rec, s));  // zero pad quads
+  launch_tile(R, matdev_from(L, dst), dst, reinterpret_cast<__half2*>(dst + L.rec), s);
   CU(cudaGetLastError());
   return MOE_OK;
 }
@@ -227,7 +249,8 @@ struct moe_engine {
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
   float *qkv_part = nullptr, *wo_part = nullptr, *up_part = nullptr, *dn_part = nullptr,
         *lm_part = nullptr;
-  int S_qkv = 1, S_wo = 1, S_up = 1, S_dn = 1, S_lm = 1;
+  int S_qkv = 1, S_wo = 1, S_up = 1, S_dn = 1, S_lm = 1;   // splits of the quad range
+  int Q_qkv = 8, Q_wo = 8, Q_up = 8, Q_dn = 8, Q_lm = 8;   // quads per split
   float *kc = nullptr, *vc = nullptr;
   RouteRec* route = nullptr;
   TraceRecDev* trace = nullptr;
@@ -265,6 +288,9 @@ struct moe_engine {
   double last_ms = 0;
   unsigned long long wait_ns = 60000000000ull;
   bool debug = false;
+  bool serial_copies = false;  // MOE_SERIAL_COPIES=1
+  bool pdl = true;             // programmatic dependent launch (MOE_PDL=0 disables)
+  std::atomic<uint64_t> copier_tail{0};
   // run-ahead bound: the host may enqueue at most `ahead` units (one layer of
   // one position) beyond the oldest unfinished one, so the launch queue never
   // fills while a kernel waits for the copy engine.
@@ -323,8 +349,7 @@ struct moe_engine {
   int enq_experts(int p);
   int enq_logits(int p, float* out);
   int finish_call();
-  int choose_splits(int njobs, int ncb, int nquads) const;
-  GJob dense_job(const DevMat& D, const float* x, float* out, int S) const;
+  GJob dense_job(const DevMat& D, const float* x, float* out, int qps) const;
 };
 
 moe_engine::~moe_engine() {
@@ -410,31 +435,21 @@ int moe_engine::run_copier() {
         copies.push_back({a, b, (int64_t)xbytes});
       }
       ++tail;
+      copier_tail.store(tail, std::memory_order_release);
     }
   }
   return MOE_OK;
 }
 
-int moe_engine::choose_splits(int njobs, int ncb, int nquads) const {
-  const int target = 4 * 148;
-  int S = (target + njobs * ncb - 1) / (njobs * ncb);
-  S = std::max(1, std::min(S, std::max(1, nquads / MOE_GEMV_WARPS)));
-  while ((nquads + S - 1) / S * 4 > MOE_XS_MAX) ++S;
-  return S;
-}
-
-GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* out, int S) const {
+GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* out, int qps) const {
   GJob j{};
   j.M = D.M;
   j.rel_slot = -1;
   j.xmode = X_PLAIN;
   j.x = xin;
   j.out = out;
-  j.S = S;
-  j.QPS = (D.nquads + S - 1) / S;
-  j.ncb = D.ncb;
-  j.nchunks = D.nchunks;
-  j.nquads = D.nquads;
+  j.QPS = qps;
+  j.S = (D.M.nqp + qps - 1) / qps;
   return j;
 }
 
@@ -442,7 +457,7 @@ static int finalize_launch(GLaunch& P) {
   int blk = 0;
   for (int i = 0; i < P.nj; ++i) {
     P.j[i].blk0 = blk;
-    blk += P.j[i].ncb * P.j[i].S;
+    blk += P.j[i].M.ncb * P.j[i].S;
   }
   return blk;
 }
@@ -455,11 +470,11 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   dbg("ln1", l, p);
   GLaunch q{};
   q.nj = 3;
-  q.j[0] = dense_job(wq[l], xn, qkv_part, S_qkv);
-  q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, S_qkv);
-  q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, S_qkv);
+  q.j[0] = dense_job(wq[l], xn, qkv_part, Q_qkv);
+  q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, Q_qkv);
+  q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, Q_qkv);
   prof_begin(K_QKV);
-  launch_gemv(attn_bits, q, finalize_launch(q), s_comp);
+  launch_gemv(attn_bits, q, finalize_launch(q), s_comp, pdl && !prof);
   prof_end(K_QKV);
   dbg("qkv", l, p);
   AttnParams a{};
@@ -476,9 +491,9 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   dbg("attn", l, p);
   GLaunch o{};
   o.nj = 1;
-  o.j[0] = dense_job(wo[l], ctx, wo_part, S_wo);
+  o.j[0] = dense_job(wo[l], ctx, wo_part, Q_wo);
   prof_begin(K_WO);
-  launch_gemv(attn_bits, o, finalize_launch(o), s_comp);
+  launch_gemv(attn_bits, o, finalize_launch(o), s_comp, pdl && !prof);
   prof_end(K_WO);
   dbg("wo", l, p);
   TailParams t{};
@@ -518,30 +533,26 @@ int moe_engine::enq_experts(int p) {
   u.route = route + p;
   u.pool = pool;
   u.slot_stride = slot_stride;
+  u.flags = flags;
+  u.err = err;
+  u.wait_ns = wait_ns;
   GLaunch dn = u;
   for (int j = 0; j < topk; ++j) {
     for (int m = 0; m < 2; ++m) {
       GJob& J = u.j[2 * j + m];
       J = GJob{};
       J.M = matdev_from(xl[m], reinterpret_cast<const uint8_t*>(xoff[m][0]));
-      J.M.scales = reinterpret_cast<const uint2*>(xoff[m][1]);
-      J.M.zeros = reinterpret_cast<const uint32_t*>(xoff[m][2]);
       J.M.zmeta = reinterpret_cast<const __half2*>(xoff[m][3]);
       J.rel_slot = j;
       J.xmode = X_PLAIN;
       J.x = h + (size_t)p * d;
       J.out = up_part + ((size_t)(2 * j + m) * S_up) * f;
+      J.QPS = Q_up;
       J.S = S_up;
-      J.nquads = d / 4;
-      J.QPS = (J.nquads + S_up - 1) / S_up;
-      J.nchunks = f / fmt_wc(expert_bits);
-      J.ncb = (J.nchunks + 31) / 32;
     }
     GJob& J = dn.j[j];
     J = GJob{};
     J.M = matdev_from(xl[2], reinterpret_cast<const uint8_t*>(xoff[2][0]));
-    J.M.scales = reinterpret_cast<const uint2*>(xoff[2][1]);
-    J.M.zeros = reinterpret_cast<const uint32_t*>(xoff[2][2]);
     J.M.zmeta = reinterpret_cast<const __half2*>(xoff[2][3]);
     J.rel_slot = j;
     J.xmode = X_SWIGLU;
@@ -549,22 +560,24 @@ int moe_engine::enq_experts(int p) {
     J.up3 = up_part + ((size_t)(2 * j + 1) * S_up) * f;
     J.S_up = S_up;
     J.out = dn_part + ((size_t)j * S_dn) * d;
+    J.QPS = Q_dn;
     J.S = S_dn;
-    J.nquads = f / 4;
-    J.QPS = (J.nquads + S_dn - 1) / S_dn;
-    J.nchunks = d / fmt_wc(expert_bits);
-    J.ncb = (J.nchunks + 31) / 32;
   }
   u.nj = 2 * topk;
   dn.nj = topk;
-  launch_wait_ready(route + p, topk, flags, err, wait_ns, s_comp);
-  dbg("wait", -1, p);
+  if (serial_copies) {  // ncu / debugging: the host drains the mailbox before the GEMV
+    CU(cudaStreamSynchronize(s_comp));
+    while (copier_tail.load(std::memory_order_acquire) <
+           __atomic_load_n(&mb_host->head, __ATOMIC_ACQUIRE))
+      std::this_thread::yield();
+    CU(cudaStreamSynchronize(s_copy));
+  }
   prof_begin(K_UP);
-  launch_gemv(expert_bits, u, finalize_launch(u), s_comp);
+  launch_gemv(expert_bits, u, finalize_launch(u), s_comp, pdl && !prof);
   prof_end(K_UP);
   dbg("up", -1, p);
   prof_begin(K_DOWN);
-  launch_gemv(expert_bits, dn, finalize_launch(dn), s_comp);
+  launch_gemv(expert_bits, dn, finalize_launch(dn), s_comp, pdl && !prof);
   prof_end(K_DOWN);
   dbg("down", -1, p);
   CombineParams c{};
@@ -586,9 +599,9 @@ int moe_engine::enq_logits(int p, float* out) {
   launch_layernorm(x + (size_t)p * d, lnfg, lnfb, xn, d, s_comp);
   GLaunch g{};
   g.nj = 1;
-  g.j[0] = dense_job(lm_head, xn, lm_part, S_lm);
+  g.j[0] = dense_job(lm_head, xn, lm_part, Q_lm);
   prof_begin(K_LM);
-  launch_gemv(lm_bits, g, finalize_launch(g), s_comp);
+  launch_gemv(lm_bits, g, finalize_launch(g), s_comp, pdl && !prof);
   prof_end(K_LM);
   LogitsParams lp{};
   lp.part = lm_part;
@@ -695,6 +708,8 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   e->dev = device;
   e->rec_hidden = record_hidden != 0;
   if (const char* dbgv = getenv("MOE_DEBUG")) e->debug = atoi(dbgv) != 0;
+  if (const char* sv = getenv("MOE_SERIAL_COPIES")) e->serial_copies = atoi(sv) != 0;
+  if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* w = getenv("MOE_WAIT_TIMEOUT_MS")) e->wait_ns = 1000000ull * atoll(w);
   if (const char* a = getenv("MOE_AHEAD")) e->ahead = std::max(1, atoi(a));
   e->ring.resize(64);
@@ -749,9 +764,6 @@ static int load_dense_mat(moe_engine* e, const moe_matrix* m, DevMat* D, const c
   if (rc) return rc;
   D->M = matdev_from(Lo, static_cast<uint8_t*>(D->mem));
   D->bits = Lo.bits;
-  D->nchunks = Lo.N / fmt_wc(Lo.bits);
-  D->ncb = (D->nchunks + 31) / 32;
-  D->nquads = Lo.K / 4;
   return MOE_OK;
 }
 
@@ -944,11 +956,16 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->ctx, d))) return rc;
   if ((rc = e->dalloc(&e->logits, (size_t)T * V))) return rc;
   const int wca = fmt_wc(e->attn_bits), wcx = fmt_wc(e->expert_bits);
-  e->S_qkv = e->choose_splits(3, (d / wca + 31) / 32, d / 4);
-  e->S_wo = e->choose_splits(1, (d / wca + 31) / 32, d / 4);
-  e->S_up = e->choose_splits(2 * e->topk, (f / wcx + 31) / 32, d / 4);
-  e->S_dn = e->choose_splits(e->topk, (d / wcx + 31) / 32, f / 4);
-  e->S_lm = e->choose_splits(1, e->lm_head.ncb, d / 4);
+  auto plan = [](int total_cb, int nquads, int* Q, int* S) {
+    nquads = (nquads + 7) / 8 * 8;  // storage quads (MatDev.nqp)
+    *Q = plan_qps(total_cb, nquads);
+    *S = (nquads + *Q - 1) / *Q;
+  };
+  plan(3 * ((d / wca + 31) / 32), d / 4, &e->Q_qkv, &e->S_qkv);
+  plan((d / wca + 31) / 32, d / 4, &e->Q_wo, &e->S_wo);
+  plan(2 * e->topk * ((f / wcx + 31) / 32), d / 4, &e->Q_up, &e->S_up);
+  plan(e->topk * ((d / wcx + 31) / 32), f / 4, &e->Q_dn, &e->S_dn);
+  plan(e->lm_head.M.ncb, d / 4, &e->Q_lm, &e->S_lm);
   if ((rc = e->dalloc(&e->qkv_part, (size_t)3 * e->S_qkv * d))) return rc;
   if ((rc = e->dalloc(&e->wo_part, (size_t)e->S_wo * d))) return rc;
   if ((rc = e->dalloc(&e->up_part, (size_t)2 * e->topk * e->S_up * f))) return rc;
@@ -1450,9 +1467,6 @@ int moe_synth_model(moe_engine* e, uint64_t seed, int32_t attn_bits, int32_t exp
       CU(cudaMemcpyAsync(D.mem, Q.tiled, lo.total(), cudaMemcpyDeviceToDevice, s));
       D.M = matdev_from(lo, static_cast<uint8_t*>(D.mem));
       D.bits = lo.bits;
-      D.nchunks = lo.N / fmt_wc(lo.bits);
-      D.ncb = (D.nchunks + 31) / 32;
-      D.nquads = lo.K / 4;
       e->attn_bits = lo.bits;
     }
     if (rc) break;
@@ -1559,9 +1573,8 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
     cudaFree(mem);
     return rc;
   }
-  const int nquads = L.K / 4, nchunks = L.N / fmt_wc(L.bits), ncb = (nchunks + 31) / 32;
-  int S = std::max(1, std::min((592 + ncb - 1) / ncb, std::max(1, nquads / MOE_GEMV_WARPS)));
-  while ((nquads + S - 1) / S * 4 > MOE_XS_MAX) ++S;
+  const MatDev M = matdev_from(L, mem);
+  const int qps = plan_qps(M.ncb, M.nqp), S = (M.nqp + qps - 1) / qps;
   float *dx, *part;
   CU(cudaMalloc(&dx, (size_t)L.K * 4));
   CU(cudaMalloc(&part, (size_t)S * L.N * 4));
@@ -1569,18 +1582,15 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
   GLaunch P{};
   P.nj = 1;
   GJob& J = P.j[0];
-  J.M = matdev_from(L, mem);
+  J.M = M;
   J.rel_slot = -1;
   J.xmode = X_PLAIN;
   J.x = dx;
   J.out = part;
   J.S = S;
-  J.QPS = (nquads + S - 1) / S;
-  J.ncb = ncb;
-  J.nchunks = nchunks;
-  J.nquads = nquads;
+  J.QPS = qps;
   J.blk0 = 0;
-  launch_gemv(L.bits, P, ncb * S, 0);
+  launch_gemv(L.bits, P, M.ncb * S, 0, false);
   CU(cudaGetLastError());
   CU(cudaDeviceSynchronize());
   std::vector<float> h((size_t)S * L.N);

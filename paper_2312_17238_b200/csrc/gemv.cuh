@@ -84,103 +84,109 @@ MOE_DEV void fma_codes3(float (&acc)[32], float xs, uint32_t w0, uint32_t w1, ui
   for (int k = 0; k < 32; k += 2) ffma_pair(acc[k], acc[k + 1], xs, m[k], m[k + 1]);
 }
 
-template <int BITS, int U>
-struct Batch {
-  uint4 r[U][Fmt<BITS>::NV];
-  uint32_t z[U];
-  uint2 s[U];
-};
+// ------------------------------------------------------------ async pipeline
+MOE_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// Where this thread's data lives for the current job.
-struct Lane {
-  const uint4* rec;       // already offset to (cb, lane): index(quad, v) = rec[(quad*NV + v)*wcb]
-  const uint32_t* zeros;  // offset to group column: zeros[quad*G]
-  const uint2* scales;    // offset to scale column: scales[quad*S]
-  const __half2* zmeta;
-  int wcb, G, S, grp, sg_log2;
-};
+MOE_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+MOE_DEV void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+MOE_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+MOE_DEV void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+MOE_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// one bulk global -> shared copy completing on `bar` (16-byte aligned, size % 16 == 0)
+MOE_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+MOE_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+MOE_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-template <int BITS, int U>
-MOE_DEV void load_batch(Batch<BITS, U>& b, const Lane& L, int q, int qend) {
+// Accumulate one record (4 rows of one lane's chunk) from shared memory.
+//   rec: the record in smem; wcb: chunks in this cb; xs: smem x slice,
+//   row = first row of the quad relative to the slice, grow = absolute row.
+template <int BITS>
+MOE_DEV void quad_fma(float (&acc)[Fmt<BITS>::WC], float& zacc, const uint8_t* rec, int wcb,
+                      int lane, const float* xs, int row, int grow, const MatDev& M, int grp) {
   constexpr int NV = Fmt<BITS>::NV;
-  constexpr bool QUANT = BITS <= 4;
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int qq = q + u;
-    if (qq < qend) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) b.r[u][v] = ld_nc_v4(L.rec + (int64_t)(qq * NV + v) * L.wcb);
-      if (QUANT) {
-        b.z[u] = ld_nc_u32(L.zeros + (int64_t)qq * L.G);
-        b.s[u] = ld_nc_v2(L.scales + (int64_t)qq * L.S);
-      }
-    }
-  }
-}
-
-// Accumulate one batch.  xs: smem x slice (prescaled for quant), row0 = its first row.
-template <int BITS, int U>
-MOE_DEV void compute_batch(float (&acc)[Fmt<BITS>::WC], float& zacc, const Batch<BITS, U>& b,
-                           const Lane& L, const float* xs, int row0, int q, int qend) {
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int qq = q + u;
-    if (qq >= qend) break;
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(&b.r[u][0]);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int row = qq * 4 + r;
-      const float x = xs[row - row0];
-      if constexpr (BITS <= 4) {
-        const uint32_t sh = (r & 1) ? (((r >> 1) ? b.s[u].y : b.s[u].x) >> 16)
-                                    : (((r >> 1) ? b.s[u].y : b.s[u].x) & 0xffffu);
-        const float xsv = x * h2f_bits(sh);
-        const uint32_t zc = (b.z[u] >> (8 * r)) & 0xffu;
-        const int run = (row * L.G + L.grp) >> L.sg_log2;
-        const __half2 zm = __ldg(L.zmeta + run);
-        const float zh = fmaf((float)zc, __low2float(zm), __high2float(zm));
-        zacc = fmaf(x, zh, zacc);
-        if constexpr (BITS == 2) fma_codes2(acc, xsv, w[r]);
-        if constexpr (BITS == 4) fma_codes4(acc, xsv, w[r]);
-        if constexpr (BITS == 3) fma_codes3(acc, xsv, w[3 * r], w[3 * r + 1], w[3 * r + 2]);
-      } else if constexpr (BITS == 16) {
-        const uint32_t* h = w + 4 * r;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[k]));
-          ffma_pair(acc[2 * k], acc[2 * k + 1], x, f.x, f.y);
-        }
-      } else {
-        const float* f = reinterpret_cast<const float*>(w + 4 * r);
-        ffma_pair(acc[0], acc[1], x, f[0], f[1]);
-        ffma_pair(acc[2], acc[3], x, f[2], f[3]);
-      }
-    }
-  }
-}
-
-// Runs this thread's quads [qbeg, qend) and returns per-output sums (unscaled).
-template <int BITS, int U>
-MOE_DEV void run_lane(float (&y)[Fmt<BITS>::WC], const Lane& L, const float* xs, int row0, int qbeg,
-                      int qend) {
   constexpr int WC = Fmt<BITS>::WC;
-  float acc[WC];
+  const uint4* cw = reinterpret_cast<const uint4*>(rec);
+  uint4 r[NV];
 #pragma unroll
-  for (int k = 0; k < WC; ++k) acc[k] = 0.f;
-  float zacc = 0.f;
-  if (qbeg < qend) {
-    Batch<BITS, U> cur, nxt;
-    load_batch<BITS, U>(cur, L, qbeg, qend);
-    for (int q = qbeg; q < qend; q += U) {
-      if (q + U < qend) load_batch<BITS, U>(nxt, L, q + U, qend);
-      compute_batch<BITS, U>(acc, zacc, cur, L, xs, row0, q, qend);
-      cur = nxt;
+  for (int v = 0; v < NV; ++v) r[v] = cw[v * wcb + lane];
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&r[0]);
+  if constexpr (BITS <= 4) {
+    const int outs = wcb * WC;
+    const uint8_t* meta = rec + 16 * NV * wcb;
+    const uint32_t z4 = reinterpret_cast<const uint32_t*>(meta)[(lane * WC) >> M.g_log2];
+    const uint2 s4 = reinterpret_cast<const uint2*>(meta + 4 * (outs >> M.g_log2))
+        [(lane * WC) >> M.sg_log2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float x = xs[row + q];
+      const uint32_t sh = (q & 1) ? (((q >> 1) ? s4.y : s4.x) >> 16)
+                                  : (((q >> 1) ? s4.y : s4.x) & 0xffffu);
+      const float xsv = x * h2f_bits(sh);
+      const uint32_t zc = (z4 >> (8 * q)) & 0xffu;
+      const int run = ((grow + q) * M.G + grp) >> M.sg_log2;
+      const __half2 zm = __ldg(M.zmeta + run);
+      const float zh = fmaf((float)zc, __low2float(zm), __high2float(zm));
+      zacc = fmaf(x, zh, zacc);
+      if constexpr (BITS == 2) fma_codes2(acc, xsv, w[q]);
+      if constexpr (BITS == 4) fma_codes4(acc, xsv, w[q]);
+      if constexpr (BITS == 3) fma_codes3(acc, xsv, w[3 * q], w[3 * q + 1], w[3 * q + 2]);
+    }
+  } else if constexpr (BITS == 16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float x = xs[row + q];
+      const uint32_t* h = w + 4 * q;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[k]));
+        ffma_pair(acc[2 * k], acc[2 * k + 1], x, f.x, f.y);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float x = xs[row + q];
+      const float* f = reinterpret_cast<const float*>(w + 4 * q);
+      ffma_pair(acc[0], acc[1], x, f[0], f[1]);
+      ffma_pair(acc[2], acc[3], x, f[2], f[3]);
     }
   }
+}
+
+// final per-output value of one lane: exact power-of-two rescale of the
+// masked-code accumulators plus the zero-point term
+template <int BITS>
+MOE_DEV void finish_lane(float (&y)[Fmt<BITS>::WC], const float (&acc)[Fmt<BITS>::WC], float zacc) {
+  constexpr int WC = Fmt<BITS>::WC;
   if constexpr (BITS <= 4) {
     const float z = zacc * kZUnscale;
 #pragma unroll
-    for (int k = 0; k < WC; ++k) y[k] = fmaf(acc[k], __uint_as_float(pow2_bits(49 - posq<BITS>(k))), z);
+    for (int k = 0; k < WC; ++k)
+      y[k] = fmaf(acc[k], __uint_as_float(pow2_bits(49 - posq<BITS>(k))), z);
   } else {
 #pragma unroll
     for (int k = 0; k < WC; ++k) y[k] = acc[k];

@@ -25,15 +25,40 @@ MOE_DEV float sigmoid_ref(float x) {  // model.py:229-235 branch-stable logistic
 }
 
 // ------------------------------------------------------------------ GEMV
+// One launch computes up to MOE_GEMV_MAXJOBS independent x@W products (e.g.
+// W1 and W3 of both routed experts).  CTA = one (job, column block, split):
+// a contiguous byte range of records, streamed through a ring of shared-memory
+// stages by one producer thread with cp.async.bulk + mbarriers, consumed by 8
+// warps (one quad per warp per stage).  Bytes in flight are bounded by the
+// ring (80 KB per CTA, 2 CTAs per SM), not by registers.
+// Expert matrices (rel_slot >= 0) live in pool buffers named by the route the
+// tail kernel wrote; the producer waits for the buffer's copy generation
+// (copy engine -> cuStreamWriteValue32) before streaming it.  Dense weights
+// are prefetched before griddepcontrol.wait, overlapping the previous kernel
+// (programmatic dependent launch).
+MOE_DEV bool wait_flag(const uint32_t* f, uint32_t gen, int* err, unsigned long long wait_ns) {
+  if ((int)(ld_acquire_u32(f) - gen) >= 0) return true;
+  const unsigned long long t0 = globaltimer();
+  while ((int)(ld_acquire_u32(f) - gen) < 0) {
+    __nanosleep(256);
+    if (globaltimer() - t0 > wait_ns) {
+      atomicOr(err, MOE_ERRF_TIMEOUT);
+      return false;
+    }
+  }
+  return true;
+}
+
 template <int BITS>
-__global__ void __launch_bounds__(MOE_GEMV_WARPS * 32)
-    k_gemv(const __grid_constant__ GLaunch P, int xs_cap) {
-  constexpr int WC = Fmt<BITS>::WC, NV = Fmt<BITS>::NV;
-  constexpr int U = (BITS == 2 || BITS == 4) ? 4 : 2;
-  constexpr int W = MOE_GEMV_WARPS;
-  extern __shared__ float smem[];
-  float* xs = smem;
-  float* red = smem + xs_cap;
+__global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
+    k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int nst, int stage_bytes) {
+  constexpr int WC = Fmt<BITS>::WC;
+  constexpr int W = MOE_GEMV_WARPS, QS = MOE_GEMV_QS;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 16;
+  float* xs = reinterpret_cast<float*>(smem + 256);
+  uint8_t* ring = smem + 256 + (((size_t)xs_cap * 4 + 127) & ~(size_t)127);
 
   int ji = 0;
   for (int i = 1; i < P.nj; ++i)
@@ -42,22 +67,59 @@ __global__ void __launch_bounds__(MOE_GEMV_WARPS * 32)
   const int local = blockIdx.x - J.blk0;
   const int cb = local / J.S, s = local % J.S;
   MatDev M = J.M;
+  const int qs = s * J.QPS, qe = min(M.nqp, qs + J.QPS);  // storage quads (pads are zero)
+  const int wcb = min(32, M.nchunks - cb * 32);
+  const int rb = rec_bytes(BITS, wcb, M.g_log2, M.sg_log2);
+  const int nit = (max(qe - qs, 0) + QS - 1) / QS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      gemv::mbar_init(full + i, 1);
+      gemv::mbar_init(empty + i, W);
+    }
+    gemv::mbar_fence_init();
+  }
+  __syncthreads();
+  gemv::pdl_trigger();
+
+  if (warp == W) {  // ---------------------------------------------- producer
+    if (lane == 0) {
+      if (J.rel_slot >= 0) {
+        gemv::pdl_wait();  // the route is written by the previous kernel
+        const int buf = P.route->buf[J.rel_slot];
+        wait_flag(P.flags + buf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
+        M.base = P.pool + (long long)buf * P.slot_stride + reinterpret_cast<size_t>(M.base);
+      }
+      const uint8_t* src = M.base + cb_offset(M, cb) + (int64_t)qs * rb;
+      for (int it = 0; it < nit; ++it) {
+        const int st = it % nst;
+        if (it >= nst) gemv::mbar_wait(empty + st, ((it / nst) & 1) ^ 1);
+        const int nq = min(QS, qe - (qs + it * QS));
+        const uint32_t bytes = (uint32_t)(nq * rb);
+        gemv::mbar_arrive_tx(full + st, bytes);
+        gemv::bulk_g2s(ring + (size_t)st * stage_bytes, src + (int64_t)it * QS * rb, bytes,
+                       full + st);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  gemv::pdl_wait();
   if (J.rel_slot >= 0) {
     const int buf = P.route->buf[J.rel_slot];
-    const uint8_t* base = P.pool + (long long)buf * P.slot_stride;
-    M.rec = reinterpret_cast<const uint4*>(base + reinterpret_cast<size_t>(M.rec));
-    M.zeros = reinterpret_cast<const uint32_t*>(base + reinterpret_cast<size_t>(M.zeros));
-    M.scales = reinterpret_cast<const uint2*>(base + reinterpret_cast<size_t>(M.scales));
-    M.zmeta = reinterpret_cast<const __half2*>(base + reinterpret_cast<size_t>(M.zmeta));
+    M.zmeta = reinterpret_cast<const __half2*>(P.pool + (long long)buf * P.slot_stride +
+                                               reinterpret_cast<size_t>(M.zmeta));
   }
-  const int qs = s * J.QPS, qe = min(J.nquads, qs + J.QPS);
-  const int row0 = qs * 4, nrows = max(qe - qs, 0) * 4;
+  const int row0 = qs * 4, nrows = max(min(qe, M.nquads) - qs, 0) * 4;
   const float xscale = BITS <= 4 ? gemv::kXScale : 1.f;
+  const int nthr = W * 32;
   if (J.xmode == X_PLAIN) {
-    for (int i = threadIdx.x; i < nrows; i += blockDim.x) xs[i] = J.x[row0 + i] * xscale;
+    for (int i = threadIdx.x; i < nrows; i += nthr) xs[i] = J.x[row0 + i] * xscale;
   } else {  // SwiGLU of the up-projection partials (model.py:223-226)
     const int K = M.K;
-    for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nrows; i += nthr) {
       const int r = row0 + i;
       float a = 0.f, b = 0.f;
       for (int t = 0; t < J.S_up; ++t) {
@@ -67,42 +129,39 @@ __global__ void __launch_bounds__(MOE_GEMV_WARPS * 32)
       xs[i] = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b) * xscale;
     }
   }
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qpw = (qe - qs + W - 1) / W;
-  const int qb = qs + warp * qpw, qend = min(qe, qb + qpw);
-  const int chunk = cb * 32 + lane;
-  float y[WC];
-  if (chunk < J.nchunks) {
-    gemv::Lane L;
-    L.wcb = min(32, J.nchunks - cb * 32);
-    L.rec = M.rec + (int64_t)cb * 32 * J.nquads * NV + lane;
-    L.G = M.G;
-    L.S = M.S;
-    L.sg_log2 = M.sg_log2;
-    if (BITS <= 4) {
-      L.grp = (chunk * WC) >> M.g_log2;
-      L.zeros = M.zeros + L.grp;
-      L.scales = M.scales + ((chunk * WC) >> M.sg_log2);
-      L.zmeta = M.zmeta;
-    }
-    gemv::run_lane<BITS, U>(y, L, xs, row0, qb, qend);
-  } else {
+  float acc[WC];
 #pragma unroll
-    for (int k = 0; k < WC; ++k) y[k] = 0.f;
+  for (int k = 0; k < WC; ++k) acc[k] = 0.f;
+  float zacc = 0.f;
+  const int grp = ((cb * 32 + lane) * WC) >> M.g_log2;
+  const bool active = lane < wcb;
+  for (int it = 0; it < nit; ++it) {
+    const int st = it % nst;
+    gemv::mbar_wait(full + st, (it / nst) & 1);
+    const int q = qs + it * QS + warp;
+    if (active && q < qe && q < M.nquads)
+      gemv::quad_fma<BITS>(acc, zacc, ring + (size_t)st * stage_bytes + (size_t)warp * rb, wcb,
+                           lane, xs, (q - qs) * 4, q * 4, M, grp);
+    __syncwarp();
+    if (lane == 0) gemv::mbar_arrive(empty + st);
   }
+  float y[WC];
+  gemv::finish_lane<BITS>(y, acc, zacc);
+  // cross-warp reduction through the (now idle) ring, fixed order
+  float* red = reinterpret_cast<float*>(ring);
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
 #pragma unroll
   for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
-  __syncthreads();
-  for (int t = threadIdx.x; t < 32 * WC; t += blockDim.x) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  for (int t = threadIdx.x; t < 32 * WC; t += nthr) {
     const int l = t / WC, k = t % WC;
-    const int c = cb * 32 + l;
-    if (c < J.nchunks) {
-      float acc = 0.f;
+    if (l < wcb) {
+      float a = 0.f;
 #pragma unroll
-      for (int w = 0; w < W; ++w) acc += red[(w * 32 + l) * (WC + 1) + k];
-      J.out[(size_t)s * M.N + (size_t)c * WC + k] = acc;
+      for (int w = 0; w < W; ++w) a += red[(w * 32 + l) * (WC + 1) + k];
+      J.out[(size_t)s * M.N + (size_t)(cb * 32 + l) * WC + k] = a;
     }
   }
 }
@@ -498,23 +557,50 @@ cudaError_t preload_kernels() {
                               200 * 1024);
 }
 
-template <int BITS>
-static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s) {
-  constexpr int WC = Fmt<BITS>::WC;
-  int xs_cap = 0;
-  for (int i = 0; i < P.nj; ++i) xs_cap = max(xs_cap, P.j[i].QPS * 4);
-  xs_cap = (xs_cap + 3) & ~3;
-  const size_t smem = (size_t)(xs_cap + MOE_GEMV_WARPS * 32 * (WC + 1)) * sizeof(float);
-  k_gemv<BITS><<<nblocks, MOE_GEMV_WARPS * 32, smem, s>>>(P, xs_cap);
+// shared memory of one GEMV CTA: barriers, x slice, stage ring (which also
+// holds the cross-warp reduction scratch at the end)
+int gemv_smem_bytes(int bits, int xs_rows, int rb_full, int* nstages, int* stage_bytes) {
+  const int WC = fmt_wc(bits);
+  const int stage = MOE_GEMV_QS * rb_full;
+  int nst = MOE_GEMV_RING / stage;
+  nst = nst < 2 ? 2 : (nst > 16 ? 16 : nst);
+  int ring = nst * stage;
+  const int red = MOE_GEMV_WARPS * 32 * (WC + 1) * 4;
+  if (ring < red) ring = red;
+  if (nstages) *nstages = nst;
+  if (stage_bytes) *stage_bytes = stage;
+  return 256 + ((xs_rows * 4 + 127) & ~127) + ring;
 }
 
-void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s) {
+template <int BITS>
+static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
+  int xs_cap = 0, rbf = 0;
+  for (int i = 0; i < P.nj; ++i) {
+    xs_cap = max(xs_cap, P.j[i].QPS * 4);
+    rbf = max(rbf, P.j[i].M.rb_full);
+  }
+  int nst = 0, stage = 0;
+  const int smem = gemv_smem_bytes(BITS, xs_cap, rbf, &nst, &stage);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nblocks);
+  cfg.blockDim = dim3(MOE_GEMV_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, nst, stage);
+}
+
+void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
   switch (bits) {
-    case 2: launch_gemv_t<2>(P, nblocks, s); break;
-    case 3: launch_gemv_t<3>(P, nblocks, s); break;
-    case 4: launch_gemv_t<4>(P, nblocks, s); break;
-    case 16: launch_gemv_t<16>(P, nblocks, s); break;
-    default: launch_gemv_t<32>(P, nblocks, s); break;
+    case 2: launch_gemv_t<2>(P, nblocks, s, pdl); break;
+    case 3: launch_gemv_t<3>(P, nblocks, s, pdl); break;
+    case 4: launch_gemv_t<4>(P, nblocks, s, pdl); break;
+    case 16: launch_gemv_t<16>(P, nblocks, s, pdl); break;
+    default: launch_gemv_t<32>(P, nblocks, s, pdl); break;
   }
 }
 

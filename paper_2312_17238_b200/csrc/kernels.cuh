@@ -3,9 +3,12 @@
 #include "common.cuh"
 #include "store_dev.cuh"
 
-#define MOE_GEMV_WARPS 8
+#define MOE_GEMV_WARPS 8     // consumer warps per CTA (+1 producer warp)
+#define MOE_GEMV_THREADS (MOE_GEMV_WARPS * 32 + 32)
+#define MOE_GEMV_QS 8        // quads per pipeline stage (one per consumer warp)
 #define MOE_GEMV_MAXJOBS 8
-#define MOE_XS_MAX 4096  // rows of x kept in smem per CTA
+#define MOE_GEMV_RING (80 * 1024)  // bytes of stage ring per CTA (2 CTAs / SM)
+#define MOE_XS_MAX 4096            // rows of x kept in smem per CTA
 
 enum XMode { X_PLAIN = 0, X_SWIGLU = 1 };
 
@@ -18,7 +21,7 @@ struct GJob {
   const float* up3;    //           partial sums of x@W3 [S_up][K]
   int S_up;
   float* out;          // partial outputs [S][N]
-  int S, QPS, ncb, nchunks, nquads, blk0;
+  int S, QPS, blk0;    // splits of the quad range, quads per split (multiple of QS)
 };
 
 struct GLaunch {
@@ -27,6 +30,9 @@ struct GLaunch {
   const RouteRec* route;
   const uint8_t* pool;
   long long slot_stride;
+  const uint32_t* flags;        // buffer ready generations (copy engine)
+  int* err;
+  unsigned long long wait_ns;
 };
 
 struct AttnParams {
@@ -94,7 +100,8 @@ struct EmbedParams {
 };
 
 // launchers (kernels.cu)
-void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s);
+void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
+int gemv_smem_bytes(int bits, int xs_rows, int rb_full, int* nstages, int* stage_bytes);
 void launch_embed(const EmbedParams& P, cudaStream_t s);
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
                       cudaStream_t s);
@@ -119,7 +126,7 @@ struct RefMat {  // reference-layout matrix resident on device
   const uint16_t* scales;
   int64_t nruns;
 };
-void launch_tile(const RefMat& R, uint8_t* rec, uint32_t* zeros, uint2* scales, __half2* zmeta,
+void launch_tile(const RefMat& R, const MatDev& M, uint8_t* rec, __half2* zmeta,
                  cudaStream_t s);
 void launch_quantize(const float* w, int K, int N, int bits, int g, int sg, uint8_t* codes,
                      uint8_t* zeros, uint16_t* zs, uint16_t* zo, uint16_t* scales, float* gmin_ws,

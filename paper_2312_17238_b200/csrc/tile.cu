@@ -11,16 +11,18 @@
 namespace {
 
 // ------------------------------------------------------------------ tiling
-__global__ void k_tile_rec(RefMat R, uint4* rec) {
+// codes: one thread per (quad, chunk)
+__global__ void k_tile_rec(RefMat R, MatDev M, uint8_t* dst) {
   const int WC = fmt_wc(R.bits), NV = fmt_nv(R.bits);
-  const int nchunks = R.N / WC, nquads = R.K / 4;
+  const int nchunks = M.nchunks, nquads = M.nquads;
   const int64_t n = (int64_t)nquads * nchunks;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(R.codes);
+  const int wpr = R.bits == 3 ? 3 : (R.bits <= 4 ? 1 : 4);  // words per row-chunk
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int q = (int)(idx / nchunks), c = (int)(idx % nchunks);
+    const int cb = c / 32, lane = c % 32, wcb = min(32, nchunks - cb * 32);
     uint32_t w[16];
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(R.codes);
-    const int words_per_row = R.bits == 3 ? 3 : (R.bits <= 4 ? 1 : 4);
     for (int r = 0; r < 4; ++r) {
       const int64_t row = 4 * q + r;
       int64_t wbase;
@@ -30,32 +32,46 @@ __global__ void k_tile_rec(RefMat R, uint4* rec) {
         wbase = (row * R.N + (int64_t)c * 8) >> 1;
       else
         wbase = row * R.N + (int64_t)c * 4;
-      for (int t = 0; t < words_per_row; ++t) w[r * words_per_row + t] = src[wbase + t];
+      for (int t = 0; t < wpr; ++t) w[r * wpr + t] = src[wbase + t];
     }
-    const int cb = c / 32, lane = c % 32;
+    uint4* rec = reinterpret_cast<uint4*>(
+        dst + cb_offset(M, cb) + (int64_t)q * rec_bytes(R.bits, wcb, M.g_log2, M.sg_log2));
     for (int v = 0; v < NV; ++v)
-      rec[rec_index(cb, q, v, lane, nquads, nchunks, NV)] =
-          make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+      rec[v * wcb + lane] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
   }
 }
 
-__global__ void k_tile_meta(RefMat R, uint32_t* zeros, uint2* scales, __half2* zmeta) {
-  const int G = R.N / R.g, S = R.N / R.sg, nquads = R.K / 4;
+// zeros / scales into each record's metadata, zero-point runs into zmeta
+__global__ void k_tile_meta(RefMat R, MatDev M, uint8_t* dst, __half2* zmeta) {
+  const int WC = fmt_wc(R.bits), NV = fmt_nv(R.bits);
+  const int G = R.N / R.g, S = R.N / R.sg, nquads = M.nquads;
+  const int cbw = 32 * WC;  // outputs per full cb
   const int64_t nz = (int64_t)nquads * G, ns = (int64_t)nquads * S;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nz; i += stride) {
-    const int64_t q = i / G, g = i % G;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < nz; i += stride) {
+    const int q = (int)(i / G), gz = (int)(i % G);
+    const int cb = (gz * R.g) / cbw, j = gz - cb * (cbw / R.g);
+    const int wcb = min(32, M.nchunks - cb * 32);
+    uint8_t* meta = dst + cb_offset(M, cb) +
+                    (int64_t)q * rec_bytes(R.bits, wcb, M.g_log2, M.sg_log2) + 16 * NV * wcb;
     uint32_t v = 0;
-    for (int r = 0; r < 4; ++r) v |= (uint32_t)R.zeros[(4 * q + r) * G + g] << (8 * r);
-    zeros[i] = v;
+    for (int r = 0; r < 4; ++r) v |= (uint32_t)R.zeros[(int64_t)(4 * q + r) * G + gz] << (8 * r);
+    reinterpret_cast<uint32_t*>(meta)[j] = v;
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += stride) {
-    const int64_t q = i / S, s = i % S;
-    const uint32_t a = R.scales[(4 * q) * S + s], b = R.scales[(4 * q + 1) * S + s];
-    const uint32_t c = R.scales[(4 * q + 2) * S + s], d = R.scales[(4 * q + 3) * S + s];
-    scales[i] = make_uint2(a | (b << 16), c | (d << 16));
+  for (int64_t i = t0; i < ns; i += stride) {
+    const int q = (int)(i / S), gs = (int)(i % S);
+    const int cb = (gs * R.sg) / cbw, j = gs - cb * (cbw / R.sg);
+    const int wcb = min(32, M.nchunks - cb * 32);
+    const int zpr = (wcb * WC) >> M.g_log2;
+    uint8_t* meta = dst + cb_offset(M, cb) +
+                    (int64_t)q * rec_bytes(R.bits, wcb, M.g_log2, M.sg_log2) + 16 * NV * wcb +
+                    4 * zpr;
+    uint32_t h[4];
+    for (int r = 0; r < 4; ++r) h[r] = R.scales[(int64_t)(4 * q + r) * S + gs];
+    reinterpret_cast<uint2*>(meta)[j] = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R.nruns; i += stride)
+  for (int64_t i = t0; i < R.nruns; i += stride)
     zmeta[i] = __halves2half2(__ushort_as_half(R.zs[i]), __ushort_as_half(R.zo[i]));
 }
 
@@ -166,13 +182,13 @@ int grid_for(int64_t n) {
 
 }  // namespace
 
-void launch_tile(const RefMat& R, uint8_t* rec, uint32_t* zeros, uint2* scales, __half2* zmeta,
+void launch_tile(const RefMat& R, const MatDev& M, uint8_t* rec, __half2* zmeta,
                  cudaStream_t s) {
-  const int64_t nrec = (int64_t)(R.K / 4) * (R.N / fmt_wc(R.bits));
-  k_tile_rec<<<grid_for(nrec), 256, 0, s>>>(R, reinterpret_cast<uint4*>(rec));
+  const int64_t nrec = (int64_t)M.nquads * M.nchunks;
+  k_tile_rec<<<grid_for(nrec), 256, 0, s>>>(R, M, rec);
   if (R.bits <= 4) {
-    const int64_t n = (int64_t)(R.K / 4) * (R.N / R.g);
-    k_tile_meta<<<grid_for(n), 256, 0, s>>>(R, zeros, scales, zmeta);
+    const int64_t n = (int64_t)M.nquads * (R.N / R.g);
+    k_tile_meta<<<grid_for(n), 256, 0, s>>>(R, M, rec, zmeta);
   }
 }
 
