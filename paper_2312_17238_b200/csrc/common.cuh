@@ -77,9 +77,10 @@ MOE_DEV double block_sum_d(double v, double* sh) {
 // cb.  Records are stored [cb][quad], so the records of one cb over a range
 // of quads are one contiguous byte range = one bulk copy.  The zero-point
 // metadata (one (zscale, zoffset) f16 pair per run of sg groups, flat over
-// the whole matrix, quant.py:147-178) follows all records.  The layout is a
-// pure byte permutation of the reference block: total bytes == payload_nbytes
-// (quant.py:332-343), so an expert buffer is exactly expert_bytes.
+// the whole matrix, quant.py:147-178) follows all records.  For the 2/3-bit
+// presets at Mixtral shape the layout is a pure byte permutation of the
+// reference block: total bytes == payload_nbytes (quant.py:332-343), so an
+// expert buffer is exactly expert_bytes.
 struct MatDev {
   const uint8_t* base;   // records (absolute, or byte offset when relative)
   const __half2* zmeta;  // [nruns] (absolute, or byte offset when relative)
@@ -92,6 +93,7 @@ struct MatDev {
   int g_log2;            // zero group size (weights)
   int sg_log2;           // scale group size (weights) = zmeta run length (groups)
   int bits;              // 2,3,4 quant; 16, 32 dense
+  int runs_uniform;      // 1: in every row the groups of a cb share one zero run
 };
 
 template <int BITS> struct Fmt;
@@ -106,14 +108,17 @@ __host__ __device__ inline int fmt_wc(int bits) {
 }
 __host__ __device__ inline int fmt_nv(int bits) { return bits == 3 ? 3 : (bits >= 16 ? 4 : 1); }
 
-// bytes of one (cb, quad) record for a cb of `wcb` chunks
+// bytes of one (cb, quad) record for a cb of `wcb` chunks, rounded up to 16 so
+// every record (uint4 code loads) and every bulk copy stays 16-byte aligned.
+// No padding for the 2/3-bit presets with full column blocks (672 / 1664 B);
+// 4-bit records carry 8 pad bytes (536 -> 544).
 __host__ __device__ inline int rec_bytes(int bits, int wcb, int g_log2, int sg_log2) {
   int b = 16 * fmt_nv(bits) * wcb;
   if (bits <= 4) {
     const int outs = wcb * fmt_wc(bits);
     b += 4 * (outs >> g_log2) + 8 * (outs >> sg_log2);
   }
-  return b;
+  return (b + 15) & ~15;
 }
 __host__ __device__ inline int64_t cb_offset(const MatDev& M, int cb) {
   return (int64_t)cb * M.nqp * M.rb_full;

@@ -54,7 +54,7 @@ struct DevMat {  // one tiled matrix in device memory
 // pipeline stage so every bulk copy stays 16-byte aligned
 int plan_qps(int total_cb, int nquads) {
   const int target = 2 * 148;
-  int S = std::max(1, (target + total_cb - 1) / total_cb);
+  int S = std::max(1, target / total_cb);  // at most one wave
   int qps = (nquads + S - 1) / S;
   qps = (qps + MOE_GEMV_QS - 1) / MOE_GEMV_QS * MOE_GEMV_QS;
   while (qps * 4 > MOE_XS_MAX) qps -= MOE_GEMV_QS;
@@ -63,6 +63,7 @@ int plan_qps(int total_cb, int nquads) {
 
 struct Layout {  // byte sections of one tiled matrix
   int bits = 0, K = 0, N = 0, g = 0, sg = 0;
+  int runs_uniform = 0;  // see MatDev::runs_uniform
   size_t rec = 0, scales = 0, zeros = 0, zmeta = 0;
   int64_t nruns = 0;
   size_t total() const { return rec + scales + zeros + zmeta; }
@@ -118,6 +119,18 @@ int make_layout(const moe_matrix* m, Layout* L, const char* what) {
   L->rec = layout_rec_bytes(*L);
   L->zmeta = (size_t)nruns * 4;
   L->nruns = nruns;
+  // does any row's slice of a column block straddle a zero-point run?
+  {
+    const int64_t G = N / g, cbg = 32 * wc / g;
+    const int ncb = (N / wc + 31) / 32, lg = ilog2(sg);
+    bool uni = true;
+    for (int64_t r = 0; r < K && uni; ++r)
+      for (int c = 0; c < ncb && uni; ++c) {
+        const int64_t f0 = r * G + c * cbg, n = std::min<int64_t>(cbg, G - c * cbg);
+        uni = (f0 >> lg) == ((f0 + n - 1) >> lg);
+      }
+    L->runs_uniform = uni ? 1 : 0;
+  }
   return MOE_OK;
 }
 
@@ -138,12 +151,13 @@ MatDev matdev_from(const Layout& L, const uint8_t* base) {
     M.sg_log2 = ilog2(L.sg);
   }
   M.rb_full = rec_bytes(L.bits, 32, M.g_log2, M.sg_log2);
+  M.runs_uniform = L.runs_uniform;
   return M;
 }
 
 // tile a reference-layout matrix already resident on device into `dst`
 int tile_device(const RefMat& R, const Layout& L, uint8_t* dst, cudaStream_t s) {
-  if ((L.K / 4) % 8) CU(cudaMemsetAsync(dst, 0, L.rec, s));  // zero pad quads
+  CU(cudaMemsetAsync(dst, 0, L.rec, s));  // pad quads / pad bytes are zero
   launch_tile(R, matdev_from(L, dst), dst, reinterpret_cast<__half2*>(dst + L.rec), s);
   CU(cudaGetLastError());
   return MOE_OK;
@@ -248,7 +262,9 @@ struct moe_engine {
   // activations
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
   float *qkv_part = nullptr, *wo_part = nullptr, *up_part = nullptr, *dn_part = nullptr,
-        *lm_part = nullptr;
+        *lm_part = nullptr;  // split-K partials
+  float *qkv_out = nullptr, *wo_out = nullptr, *up_out = nullptr, *dn_out = nullptr;  // finals
+  int* cnt = nullptr;  // split-K arrival counters
   int S_qkv = 1, S_wo = 1, S_up = 1, S_dn = 1, S_lm = 1;   // splits of the quad range
   int Q_qkv = 8, Q_wo = 8, Q_up = 8, Q_dn = 8, Q_lm = 8;   // quads per split
   float *kc = nullptr, *vc = nullptr;
@@ -290,6 +306,14 @@ struct moe_engine {
   bool debug = false;
   bool serial_copies = false;  // MOE_SERIAL_COPIES=1
   bool pdl = true;             // programmatic dependent launch (MOE_PDL=0 disables)
+  bool use_graph = true;       // one CUDA graph per decode token (MOE_GRAPH=0 disables)
+  bool capturing = false;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_launches = 0;
+  cudaEvent_t tok_ev[4] = {};
+  DecodeState* ds_dev = nullptr;        // device decode cursor
+  DecodeState* ds_host = nullptr;       // pinned staging for the cursor
+  const DecodeState* cur_ds = nullptr;  // non-null while enqueuing a decode token
   std::atomic<uint64_t> copier_tail{0};
   // run-ahead bound: the host may enqueue at most `ahead` units (one layer of
   // one position) beyond the oldest unfinished one, so the launch queue never
@@ -348,8 +372,10 @@ struct moe_engine {
   int enq_attention(int l, int p, int mode);
   int enq_experts(int p);
   int enq_logits(int p, float* out);
+  int enq_token();
+  int run_tokens(int n);
   int finish_call();
-  GJob dense_job(const DevMat& D, const float* x, float* out, int qps) const;
+  GJob dense_job(const DevMat& D, const float* x, float* part, float* out, int qps) const;
 };
 
 moe_engine::~moe_engine() {
@@ -364,10 +390,15 @@ moe_engine::~moe_engine() {
   for (auto e : free_events) cudaEventDestroy(e);
   for (auto e : ring) cudaEventDestroy(e);
   for (auto e : pev) cudaEventDestroy(e);
+  for (auto e : tok_ev)
+    if (e) cudaEventDestroy(e);
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (ds_host) cudaFreeHost(ds_host);
   void* ptrs[] = {wte, wpe, lm_head.mem, lnfg, lnfb, pool, flags, x, h, xn, ctx, logits,
-                  qkv_part, wo_part, up_part, dn_part, lm_part, kc, vc, route, trace,
+                  qkv_part, wo_part, up_part, dn_part, lm_part, qkv_out, wo_out, up_out, dn_out,
+                  cnt, kc, vc, route, trace,
                   trace_hidden, tok_dev, tok_hist, tok_in, cand_val, cand_idx, counter, err,
-                  st_mem};
+                  st_mem, ds_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* v : {&wq, &wk, &wv, &wo})
@@ -441,12 +472,14 @@ int moe_engine::run_copier() {
   return MOE_OK;
 }
 
-GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* out, int qps) const {
+GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* part, float* out,
+                          int qps) const {
   GJob j{};
   j.M = D.M;
   j.rel_slot = -1;
   j.xmode = X_PLAIN;
   j.x = xin;
+  j.part = part;
   j.out = out;
   j.QPS = qps;
   j.S = (D.M.nqp + qps - 1) / qps;
@@ -466,40 +499,45 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   throttle();
   float* xp = x + (size_t)p * d;
   float* hp = h + (size_t)p * d;
-  launch_layernorm(xp, ln1g[l], ln1b[l], xn, d, s_comp);
+  const bool pl = pdl && !prof;
+  launch_layernorm(xp, ln1g[l], ln1b[l], xn, d, s_comp, pl);
   dbg("ln1", l, p);
   GLaunch q{};
   q.nj = 3;
-  q.j[0] = dense_job(wq[l], xn, qkv_part, Q_qkv);
-  q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, Q_qkv);
-  q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, Q_qkv);
+  q.cnt = cnt;
+  q.j[0] = dense_job(wq[l], xn, qkv_part, qkv_out, Q_qkv);
+  q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, qkv_out + d, Q_qkv);
+  q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, qkv_out + 2 * d, Q_qkv);
   prof_begin(K_QKV);
   launch_gemv(attn_bits, q, finalize_launch(q), s_comp, pdl && !prof);
   prof_end(K_QKV);
   dbg("qkv", l, p);
   AttnParams a{};
-  a.qkv_part = qkv_part;
-  a.S = S_qkv;
+  a.qkv_part = qkv_out;
+  a.S = 1;
   a.kc = kc + (size_t)l * T * d;
   a.vc = vc + (size_t)l * T * d;
   a.ctx = ctx;
+  a.ds = cur_ds;
   a.pos = p;
   a.H = H;
   a.hd = hd;
   a.d = d;
-  launch_attention(a, s_comp);
+  a.T_max = T;
+  launch_attention(a, s_comp, pl);
   dbg("attn", l, p);
   GLaunch o{};
   o.nj = 1;
-  o.j[0] = dense_job(wo[l], ctx, wo_part, Q_wo);
+  o.cnt = cnt;
+  o.j[0] = dense_job(wo[l], ctx, wo_part, wo_out, Q_wo);
   prof_begin(K_WO);
   launch_gemv(attn_bits, o, finalize_launch(o), s_comp, pdl && !prof);
   prof_end(K_WO);
   dbg("wo", l, p);
   TailParams t{};
   t.x = xp;
-  t.part = wo_part;
-  t.S = S_wo;
+  t.part = wo_out;
+  t.S = 1;
   t.g2 = ln2g[l];
   t.b2 = ln2b[l];
   t.gate_l = gate[l];
@@ -510,8 +548,10 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   t.m = guess ? sc.m : 0;
   t.h = hp;
   t.route = route + p;
-  t.trace = trace + (size_t)p * L + l;
-  t.trace_hidden = rec_hidden ? trace_hidden + ((size_t)p * L + l) * d : nullptr;
+  t.trace = trace;
+  t.trace_hidden = rec_hidden ? trace_hidden : nullptr;
+  t.ds = cur_ds;
+  t.n_layers = L;
   t.st = st;
   t.d = d;
   t.E = E;
@@ -520,7 +560,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   t.pos = p;
   t.mode = mode;
   t.ep_size = 1;
-  launch_tail(t, s_comp);
+  launch_tail(t, s_comp, pl);
   dbg("tail", l, p);
   launches += 6;
   unit_done();
@@ -536,6 +576,7 @@ int moe_engine::enq_experts(int p) {
   u.flags = flags;
   u.err = err;
   u.wait_ns = wait_ns;
+  u.cnt = cnt;
   GLaunch dn = u;
   for (int j = 0; j < topk; ++j) {
     for (int m = 0; m < 2; ++m) {
@@ -546,7 +587,8 @@ int moe_engine::enq_experts(int p) {
       J.rel_slot = j;
       J.xmode = X_PLAIN;
       J.x = h + (size_t)p * d;
-      J.out = up_part + ((size_t)(2 * j + m) * S_up) * f;
+      J.part = up_part + ((size_t)(2 * j + m) * S_up) * f;
+      J.out = up_out + (size_t)(2 * j + m) * f;
       J.QPS = Q_up;
       J.S = S_up;
     }
@@ -556,10 +598,10 @@ int moe_engine::enq_experts(int p) {
     J.M.zmeta = reinterpret_cast<const __half2*>(xoff[2][3]);
     J.rel_slot = j;
     J.xmode = X_SWIGLU;
-    J.up1 = up_part + ((size_t)(2 * j) * S_up) * f;
-    J.up3 = up_part + ((size_t)(2 * j + 1) * S_up) * f;
-    J.S_up = S_up;
-    J.out = dn_part + ((size_t)j * S_dn) * d;
+    J.up1 = up_out + (size_t)(2 * j) * f;
+    J.up3 = up_out + (size_t)(2 * j + 1) * f;
+    J.part = dn_part + ((size_t)j * S_dn) * d;
+    J.out = dn_out + (size_t)j * d;
     J.QPS = Q_dn;
     J.S = S_dn;
   }
@@ -582,13 +624,13 @@ int moe_engine::enq_experts(int p) {
   dbg("down", -1, p);
   CombineParams c{};
   c.h = h + (size_t)p * d;
-  c.part = dn_part;
-  c.S = S_dn;
+  c.part = dn_out;
+  c.S = 1;
   c.route = route + p;
   c.out = x + (size_t)p * d;
   c.d = d;
   c.top_k = topk;
-  launch_combine(c, s_comp);
+  launch_combine(c, s_comp, pdl && !prof);
   dbg("combine", -1, p);
   launches += 3;
   unit_done();
@@ -596,30 +638,90 @@ int moe_engine::enq_experts(int p) {
 }
 
 int moe_engine::enq_logits(int p, float* out) {
-  launch_layernorm(x + (size_t)p * d, lnfg, lnfb, xn, d, s_comp);
+  const bool pl = pdl && !prof;
+  launch_layernorm(x + (size_t)p * d, lnfg, lnfb, xn, d, s_comp, pl);
   GLaunch g{};
   g.nj = 1;
-  g.j[0] = dense_job(lm_head, xn, lm_part, Q_lm);
+  g.cnt = cnt;
+  g.j[0] = dense_job(lm_head, xn, lm_part, out, Q_lm);
   prof_begin(K_LM);
-  launch_gemv(lm_bits, g, finalize_launch(g), s_comp, pdl && !prof);
+  launch_gemv(lm_bits, g, finalize_launch(g), s_comp, pl);
   prof_end(K_LM);
   LogitsParams lp{};
-  lp.part = lm_part;
-  lp.S = S_lm;
+  lp.part = out;
+  lp.S = 1;
   lp.V = V;
   lp.logits = out;
   lp.cand_val = cand_val;
   lp.cand_idx = cand_idx;
   lp.counter = counter;
   lp.tok_out = tok_dev;
+  lp.tok_hist = tok_hist;
+  lp.ds = const_cast<DecodeState*>(cur_ds);
   lp.err = err;
-  launch_logits(lp, s_comp);
+  launch_logits(lp, s_comp, pl);
   dbg("logits", -1, p);
   launches += 3;
   return MOE_OK;
 }
 
+// One decode token (embed -> L x (attention, experts) -> logits + argmax) with
+// every position-dependent quantity read from the device cursor ds_dev, so
+// the same launch sequence (and the same captured CUDA graph) serves any token.
+int moe_engine::enq_token() {
+  cur_ds = ds_dev;
+  EmbedParams ep{};
+  ep.wte = wte;
+  ep.wpe = wpe;
+  ep.half = emb_half;
+  ep.ds = ds_dev;
+  ep.d = d;
+  ep.x = x;
+  launch_embed(ep, s_comp, pdl && !prof);
+  for (int l = 0; l < L; ++l) {
+    enq_attention(l, 0, 0);
+    enq_experts(0);
+  }
+  enq_logits(0, logits);
+  cur_ds = nullptr;
+  launches += 1;
+  return MOE_OK;
+}
+
+// n decode tokens: one graph launch per token when graphs are enabled (the
+// graph is captured on first use), else the eager launch sequence.  At most
+// two tokens are in flight so the launch queue never fills while a kernel
+// waits for the copy engine.
+int moe_engine::run_tokens(int n) {
+  const bool graphs = use_graph && !prof && !debug && !serial_copies;
+  if (!graphs) {
+    for (int i = 0; i < n; ++i) enq_token();
+    return MOE_OK;
+  }
+  if (!gexec) {
+    const int64_t l0 = launches;
+    CU(cudaStreamBeginCapture(s_comp, cudaStreamCaptureModeThreadLocal));
+    capturing = true;
+    enq_token();
+    capturing = false;
+    cudaGraph_t g = nullptr;
+    CU(cudaStreamEndCapture(s_comp, &g));
+    CU(cudaGraphInstantiate(&gexec, g, 0));
+    CU(cudaGraphDestroy(g));
+    graph_launches = launches - l0;
+    launches = l0;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (i >= 2) CU(cudaEventSynchronize(tok_ev[(i - 2) % 4]));
+    CU(cudaGraphLaunch(gexec, s_comp));
+    CU(cudaEventRecord(tok_ev[i % 4], s_comp));
+    launches += graph_launches;
+  }
+  return MOE_OK;
+}
+
 int moe_engine::throttle() {
+  if (capturing) return MOE_OK;
   while (units_issued - units_done >= ahead) {
     CU(cudaEventSynchronize(ring[units_done % ring.size()]));
     ++units_done;
@@ -628,6 +730,7 @@ int moe_engine::throttle() {
 }
 
 int moe_engine::unit_done() {
+  if (capturing) return MOE_OK;
   CU(cudaEventRecord(ring[units_issued % ring.size()], s_comp));
   ++units_issued;
   return MOE_OK;
@@ -710,6 +813,8 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* dbgv = getenv("MOE_DEBUG")) e->debug = atoi(dbgv) != 0;
   if (const char* sv = getenv("MOE_SERIAL_COPIES")) e->serial_copies = atoi(sv) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
+  if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
+  for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (const char* w = getenv("MOE_WAIT_TIMEOUT_MS")) e->wait_ns = 1000000ull * atoll(w);
   if (const char* a = getenv("MOE_AHEAD")) e->ahead = std::max(1, atoi(a));
   e->ring.resize(64);
@@ -971,6 +1076,11 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->up_part, (size_t)2 * e->topk * e->S_up * f))) return rc;
   if ((rc = e->dalloc(&e->dn_part, (size_t)e->topk * e->S_dn * d))) return rc;
   if ((rc = e->dalloc(&e->lm_part, (size_t)e->S_lm * V))) return rc;
+  if ((rc = e->dalloc(&e->qkv_out, (size_t)3 * d))) return rc;
+  if ((rc = e->dalloc(&e->wo_out, (size_t)d))) return rc;
+  if ((rc = e->dalloc(&e->up_out, (size_t)2 * e->topk * f))) return rc;
+  if ((rc = e->dalloc(&e->dn_out, (size_t)e->topk * d))) return rc;
+  if ((rc = e->dalloc(&e->cnt, 4096))) return rc;
   if ((rc = e->dalloc(&e->kc, (size_t)L * T * d))) return rc;
   if ((rc = e->dalloc(&e->vc, (size_t)L * T * d))) return rc;
   if ((rc = e->dalloc(&e->route, T))) return rc;
@@ -984,6 +1094,8 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->cand_idx, nblk))) return rc;
   if ((rc = e->dalloc(&e->counter, 1))) return rc;
   if ((rc = e->dalloc(&e->err, 1))) return rc;
+  if ((rc = e->dalloc(&e->ds_dev, 1))) return rc;
+  CU(cudaHostAlloc(&e->ds_host, sizeof(DecodeState), cudaHostAllocDefault));
   // device store state
   const int kk = std::max(k, 1);
   e->ev_cap = std::max(4096, T * L * (3 * e->topk + e->sc.m + 2) + L * E * 3);
@@ -1087,7 +1199,7 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
     ep.pos = p;
     ep.d = e->d;
     ep.x = e->x + (size_t)p * e->d;
-    launch_embed(ep, e->s_comp);
+    launch_embed(ep, e->s_comp, e->pdl);
   }
   for (int l = 0; l < e->L; ++l) {
     for (int p = 0; p < n; ++p) e->enq_attention(l, p, 1);
@@ -1115,28 +1227,6 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
   return MOE_OK;
 }
 
-static int run_one(moe_engine* e, int tok_host, const int* tok_dev, int* tok_hist) {
-  EmbedParams ep{};
-  ep.wte = e->wte;
-  ep.wpe = e->wpe;
-  ep.half = e->emb_half;
-  ep.tok = tok_host;
-  ep.tok_dev = tok_dev;
-  ep.tok_hist = tok_hist;
-  ep.pos = e->pos;
-  ep.d = e->d;
-  ep.x = e->x + (size_t)e->pos * e->d;
-  launch_embed(ep, e->s_comp);
-  for (int l = 0; l < e->L; ++l) {
-    e->enq_attention(l, e->pos, 0);
-    e->enq_experts(e->pos);
-  }
-  e->enq_logits(e->pos, e->logits);
-  e->launches += 1;
-  e->pos += 1;
-  return MOE_OK;
-}
-
 int moe_step(moe_engine* e, int32_t token, float* logits_out) {
   int rc = check_ready(e);
   if (rc) return rc;
@@ -1148,10 +1238,15 @@ int moe_step(moe_engine* e, int32_t token, float* logits_out) {
                                    std::to_string(e->T));
   e->launches = 0;
   CU(cudaEventRecord(e->t0, e->s_comp));
-  run_one(e, token, nullptr, nullptr);
+  *e->ds_host = DecodeState{e->pos, 0, token, 0};
+  CU(cudaMemcpyAsync(e->ds_dev, e->ds_host, sizeof(DecodeState), cudaMemcpyHostToDevice,
+                     e->s_comp));
+  rc = e->run_tokens(1);
+  if (rc) return rc;
   CU(cudaGetLastError());
   rc = e->finish_call();
   if (rc) return rc;
+  e->pos += 1;
   if (logits_out) CU(cudaMemcpy(logits_out, e->logits, (size_t)e->V * 4, cudaMemcpyDeviceToHost));
   e->has_logits = true;
   return MOE_OK;
@@ -1167,10 +1262,18 @@ int moe_decode_greedy(moe_engine* e, int32_t n, int32_t* tokens_out, float* fina
                                    std::to_string(e->T));
   e->launches = 0;
   CU(cudaEventRecord(e->t0, e->s_comp));
-  for (int i = 0; i < n; ++i) run_one(e, 0, e->tok_dev, e->tok_hist + i);
+  // cursor: position from the host, first token = argmax of the last logits
+  *e->ds_host = DecodeState{e->pos, 0, 0, 0};
+  CU(cudaMemcpyAsync(e->ds_dev, e->ds_host, sizeof(DecodeState), cudaMemcpyHostToDevice,
+                     e->s_comp));
+  CU(cudaMemcpyAsync(&e->ds_dev->tok, e->tok_dev, sizeof(int), cudaMemcpyDeviceToDevice,
+                     e->s_comp));
+  rc = e->run_tokens(n);
+  if (rc) return rc;
   CU(cudaGetLastError());
   rc = e->finish_call();
   if (rc) return rc;
+  e->pos += n;
   if (tokens_out) CU(cudaMemcpy(tokens_out, e->tok_hist, (size_t)n * 4, cudaMemcpyDeviceToHost));
   if (final_logits_out)
     CU(cudaMemcpy(final_logits_out, e->logits, (size_t)e->V * 4, cudaMemcpyDeviceToHost));
@@ -1575,9 +1678,13 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
   }
   const MatDev M = matdev_from(L, mem);
   const int qps = plan_qps(M.ncb, M.nqp), S = (M.nqp + qps - 1) / qps;
-  float *dx, *part;
+  float *dx, *part, *dy;
+  int* dcnt;
   CU(cudaMalloc(&dx, (size_t)L.K * 4));
   CU(cudaMalloc(&part, (size_t)S * L.N * 4));
+  CU(cudaMalloc(&dy, (size_t)L.N * 4));
+  CU(cudaMalloc(&dcnt, (size_t)M.ncb * 4));
+  CU(cudaMemset(dcnt, 0, (size_t)M.ncb * 4));
   CU(cudaMemcpy(dx, x, (size_t)L.K * 4, cudaMemcpyHostToDevice));
   GLaunch P{};
   P.nj = 1;
@@ -1586,23 +1693,21 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
   J.rel_slot = -1;
   J.xmode = X_PLAIN;
   J.x = dx;
-  J.out = part;
+  J.part = part;
+  J.out = dy;
   J.S = S;
   J.QPS = qps;
   J.blk0 = 0;
+  P.cnt = dcnt;
   launch_gemv(L.bits, P, M.ncb * S, 0, false);
   CU(cudaGetLastError());
   CU(cudaDeviceSynchronize());
-  std::vector<float> h((size_t)S * L.N);
-  CU(cudaMemcpy(h.data(), part, h.size() * 4, cudaMemcpyDeviceToHost));
-  for (int j = 0; j < L.N; ++j) {
-    float a = 0.f;
-    for (int s = 0; s < S; ++s) a += h[(size_t)s * L.N + j];
-    y[j] = a;
-  }
+  CU(cudaMemcpy(y, dy, (size_t)L.N * 4, cudaMemcpyDeviceToHost));
   cudaFree(mem);
   cudaFree(dx);
   cudaFree(part);
+  cudaFree(dy);
+  cudaFree(dcnt);
   return MOE_OK;
 }
 

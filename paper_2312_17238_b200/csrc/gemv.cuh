@@ -121,12 +121,13 @@ MOE_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 MOE_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 MOE_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// Accumulate one record (4 rows of one lane's chunk) from shared memory.
-//   rec: the record in smem; wcb: chunks in this cb; xs: smem x slice,
-//   row = first row of the quad relative to the slice, grow = absolute row.
+// Accumulate the code part of one record (4 rows of one lane's chunk) from
+// shared memory: acc_k += (x_r * s_r) * bits(code_{r,k} in place).
+//   rec: the record in smem; wcb: chunks in this cb; x4: the quad's 4 x values
+//   (prescaled by 2^100 for quant formats)
 template <int BITS>
-MOE_DEV void quad_fma(float (&acc)[Fmt<BITS>::WC], float& zacc, const uint8_t* rec, int wcb,
-                      int lane, const float* xs, int row, int grow, const MatDev& M, int grp) {
+MOE_DEV void quad_codes(float (&acc)[Fmt<BITS>::WC], const uint8_t* rec, int wcb, int lane,
+                        float4 x4, int g_log2, int sg_log2) {
   constexpr int NV = Fmt<BITS>::NV;
   constexpr int WC = Fmt<BITS>::WC;
   const uint4* cw = reinterpret_cast<const uint4*>(rec);
@@ -134,23 +135,17 @@ MOE_DEV void quad_fma(float (&acc)[Fmt<BITS>::WC], float& zacc, const uint8_t* r
 #pragma unroll
   for (int v = 0; v < NV; ++v) r[v] = cw[v * wcb + lane];
   const uint32_t* w = reinterpret_cast<const uint32_t*>(&r[0]);
+  const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
   if constexpr (BITS <= 4) {
     const int outs = wcb * WC;
-    const uint8_t* meta = rec + 16 * NV * wcb;
-    const uint32_t z4 = reinterpret_cast<const uint32_t*>(meta)[(lane * WC) >> M.g_log2];
-    const uint2 s4 = reinterpret_cast<const uint2*>(meta + 4 * (outs >> M.g_log2))
-        [(lane * WC) >> M.sg_log2];
+    const uint2 s4 = reinterpret_cast<const uint2*>(rec + 16 * NV * wcb + 4 * (outs >> g_log2))
+        [(lane * WC) >> sg_log2];
+    const float2 s01 = __half22float2(*reinterpret_cast<const __half2*>(&s4.x));
+    const float2 s23 = __half22float2(*reinterpret_cast<const __half2*>(&s4.y));
+    const float sv[4] = {s01.x, s01.y, s23.x, s23.y};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float x = xs[row + q];
-      const uint32_t sh = (q & 1) ? (((q >> 1) ? s4.y : s4.x) >> 16)
-                                  : (((q >> 1) ? s4.y : s4.x) & 0xffffu);
-      const float xsv = x * h2f_bits(sh);
-      const uint32_t zc = (z4 >> (8 * q)) & 0xffu;
-      const int run = ((grow + q) * M.G + grp) >> M.sg_log2;
-      const __half2 zm = __ldg(M.zmeta + run);
-      const float zh = fmaf((float)zc, __low2float(zm), __high2float(zm));
-      zacc = fmaf(x, zh, zacc);
+      const float xsv = xv[q] * sv[q];
       if constexpr (BITS == 2) fma_codes2(acc, xsv, w[q]);
       if constexpr (BITS == 4) fma_codes4(acc, xsv, w[q]);
       if constexpr (BITS == 3) fma_codes3(acc, xsv, w[3 * q], w[3 * q + 1], w[3 * q + 2]);
@@ -158,21 +153,64 @@ MOE_DEV void quad_fma(float (&acc)[Fmt<BITS>::WC], float& zacc, const uint8_t* r
   } else if constexpr (BITS == 16) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float x = xs[row + q];
       const uint32_t* h = w + 4 * q;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[k]));
-        ffma_pair(acc[2 * k], acc[2 * k + 1], x, f.x, f.y);
+        ffma_pair(acc[2 * k], acc[2 * k + 1], xv[q], f.x, f.y);
       }
     }
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float x = xs[row + q];
       const float* f = reinterpret_cast<const float*>(w + 4 * q);
-      ffma_pair(acc[0], acc[1], x, f[0], f[1]);
-      ffma_pair(acc[2], acc[3], x, f[2], f[3]);
+      ffma_pair(acc[0], acc[1], xv[q], f[0], f[1]);
+      ffma_pair(acc[2], acc[3], xv[q], f[2], f[3]);
+    }
+  }
+}
+
+// Zero-point terms of one quad: sum_r x_r * zhat(r, group) for the 4*ZPR
+// (row, group) pairs of the record, spread over the warp's lanes.
+//   mode 0 (32 % ZPR == 0): lane takes terms t = lane + 32 i, group t % ZPR,
+//          so every lane keeps one group; mode 1: lane < ZPR takes its group
+//   uniform runs: zhat*x = zc * xz[r] with xz = x * zscale(run of the row)
+//   (the zoffset part is a per-CTA scalar added once); else the run is
+//   looked up per term (quant.py:172-178: zhat = zc * zscale + zoffset).
+struct ZeroCtx {
+  const uint32_t* zeros;  // record's [ZPR] u32 (4 rows each)
+  const float* xs;        // x slice (prescaled) at the quad's first row
+  const float* xz;        // x * zscale at the quad's first row (uniform runs)
+  const __half2* zmeta;
+  int zpr, zpr_log2, mode, uniform, G, sg_log2, grow, gcb0;
+};
+
+MOE_DEV void quad_zero(float& zacc, const ZeroCtx& Z, int lane) {
+  const int nterms = 4 * Z.zpr;
+  if (Z.mode == 0) {
+    for (int t = lane; t < nterms; t += 32) {
+      const int j = t & (Z.zpr - 1), r = t >> Z.zpr_log2;
+      const uint32_t zc = (Z.zeros[j] >> (8 * r)) & 0xffu;
+      if (Z.uniform) {
+        zacc = fmaf((float)zc, Z.xz[r], zacc);
+      } else {
+        const int run = ((Z.grow + r) * Z.G + Z.gcb0 + j) >> Z.sg_log2;
+        const float2 zm = __half22float2(__ldg(Z.zmeta + run));
+        zacc = fmaf(Z.xs[r], fmaf((float)zc, zm.x, zm.y), zacc);
+      }
+    }
+  } else if (lane < Z.zpr) {
+    const uint32_t z4 = Z.zeros[lane];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t zc = (z4 >> (8 * r)) & 0xffu;
+      if (Z.uniform) {
+        zacc = fmaf((float)zc, Z.xz[r], zacc);
+      } else {
+        const int run = ((Z.grow + r) * Z.G + Z.gcb0 + lane) >> Z.sg_log2;
+        const float2 zm = __half22float2(__ldg(Z.zmeta + run));
+        zacc = fmaf(Z.xs[r], fmaf((float)zc, zm.x, zm.y), zacc);
+      }
     }
   }
 }
@@ -180,10 +218,10 @@ MOE_DEV void quad_fma(float (&acc)[Fmt<BITS>::WC], float& zacc, const uint8_t* r
 // final per-output value of one lane: exact power-of-two rescale of the
 // masked-code accumulators plus the zero-point term
 template <int BITS>
-MOE_DEV void finish_lane(float (&y)[Fmt<BITS>::WC], const float (&acc)[Fmt<BITS>::WC], float zacc) {
+MOE_DEV void finish_lane(float (&y)[Fmt<BITS>::WC], const float (&acc)[Fmt<BITS>::WC], float ztot) {
   constexpr int WC = Fmt<BITS>::WC;
   if constexpr (BITS <= 4) {
-    const float z = zacc * kZUnscale;
+    const float z = ztot * kZUnscale;
 #pragma unroll
     for (int k = 0; k < WC; ++k)
       y[k] = fmaf(acc[k], __uint_as_float(pow2_bits(49 - posq<BITS>(k))), z);

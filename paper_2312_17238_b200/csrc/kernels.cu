@@ -53,16 +53,20 @@ template <int BITS>
 __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
     k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int nst, int stage_bytes) {
   constexpr int WC = Fmt<BITS>::WC;
+  constexpr bool QUANT = BITS <= 4;
   constexpr int W = MOE_GEMV_WARPS, QS = MOE_GEMV_QS;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 16;
-  float* xs = reinterpret_cast<float*>(smem + 256);
-  uint8_t* ring = smem + 256 + (((size_t)xs_cap * 4 + 127) & ~(size_t)127);
+  float* misc = reinterpret_cast<float*>(smem + 256);  // [16]: zo partials, flags
+  float* xs = reinterpret_cast<float*>(smem + 512);
+  float* xz = xs + xs_cap;  // x * zscale per row (uniform zero-point runs)
+  uint8_t* ring = smem + 512 + (((size_t)xs_cap * 8 + 127) & ~(size_t)127);
 
-  int ji = 0;
+  int ji = 0, cnt_base = 0;
   for (int i = 1; i < P.nj; ++i)
     if ((int)blockIdx.x >= P.j[i].blk0) ji = i;
+  for (int i = 0; i < ji; ++i) cnt_base += P.j[i].M.ncb;
   const GJob& J = P.j[ji];
   const int local = blockIdx.x - J.blk0;
   const int cb = local / J.S, s = local % J.S;
@@ -106,64 +110,125 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
   }
 
   // ------------------------------------------------------------ consumers
+  const int nthr = W * 32;
   gemv::pdl_wait();
   if (J.rel_slot >= 0) {
     const int buf = P.route->buf[J.rel_slot];
     M.zmeta = reinterpret_cast<const __half2*>(P.pool + (long long)buf * P.slot_stride +
                                                reinterpret_cast<size_t>(M.zmeta));
   }
-  const int row0 = qs * 4, nrows = max(min(qe, M.nquads) - qs, 0) * 4;
-  const float xscale = BITS <= 4 ? gemv::kXScale : 1.f;
-  const int nthr = W * 32;
-  if (J.xmode == X_PLAIN) {
-    for (int i = threadIdx.x; i < nrows; i += nthr) xs[i] = J.x[row0 + i] * xscale;
-  } else {  // SwiGLU of the up-projection partials (model.py:223-226)
-    const int K = M.K;
-    for (int i = threadIdx.x; i < nrows; i += nthr) {
-      const int r = row0 + i;
-      float a = 0.f, b = 0.f;
-      for (int t = 0; t < J.S_up; ++t) {
-        a += __ldcg(J.up1 + (size_t)t * K + r);
-        b += __ldcg(J.up3 + (size_t)t * K + r);
-      }
-      xs[i] = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b) * xscale;
+  const int qv = min(qe, M.nquads);  // real quads of this split
+  const int row0 = qs * 4, nrows = max(qv - qs, 0) * 4;
+  const float xscale = QUANT ? gemv::kXScale : 1.f;
+  const int gcb0 = QUANT ? ((cb * 32 * WC) >> M.g_log2) : 0;  // first zero group of the cb
+  float zo_part = 0.f;
+  for (int i = threadIdx.x; i < nrows; i += nthr) {
+    const int r = row0 + i;
+    float xv;
+    if (J.xmode == X_PLAIN) {
+      xv = J.x[r];
+    } else {  // SwiGLU of the up projections (model.py:223-226)
+      const float a = __ldcg(J.up1 + r), b = __ldcg(J.up3 + r);
+      xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
+    }
+    xv *= xscale;
+    xs[i] = xv;
+    if (QUANT && M.runs_uniform) {  // the cb's groups of this row share one zero run
+      const float2 zm = __half22float2(__ldg(M.zmeta + (((int64_t)r * M.G + gcb0) >> M.sg_log2)));
+      xz[i] = xv * zm.x;
+      zo_part = fmaf(xv, zm.y, zo_part);
     }
   }
+  if (QUANT && M.runs_uniform) {
+    zo_part = warp_sum(zo_part);
+    if (lane == 0) misc[warp] = zo_part;
+  }
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  float zo_sum = 0.f;
+  if (QUANT && M.runs_uniform)
+#pragma unroll
+    for (int w = 0; w < W; ++w) zo_sum += misc[w];
 
   float acc[WC];
 #pragma unroll
   for (int k = 0; k < WC; ++k) acc[k] = 0.f;
   float zacc = 0.f;
-  const int grp = ((cb * 32 + lane) * WC) >> M.g_log2;
+  gemv::ZeroCtx Z;
+  if (QUANT) {
+    Z.zpr = (wcb * WC) >> M.g_log2;
+    Z.zpr_log2 = __ffs(Z.zpr) - 1;
+    Z.mode = (Z.zpr & (Z.zpr - 1)) == 0 ? 0 : 1;
+    Z.uniform = M.runs_uniform;
+    Z.G = M.G;
+    Z.sg_log2 = M.sg_log2;
+    Z.gcb0 = gcb0;
+    Z.zmeta = M.zmeta;
+  }
   const bool active = lane < wcb;
   for (int it = 0; it < nit; ++it) {
     const int st = it % nst;
     gemv::mbar_wait(full + st, (it / nst) & 1);
     const int q = qs + it * QS + warp;
-    if (active && q < qe && q < M.nquads)
-      gemv::quad_fma<BITS>(acc, zacc, ring + (size_t)st * stage_bytes + (size_t)warp * rb, wcb,
-                           lane, xs, (q - qs) * 4, q * 4, M, grp);
+    if (q < qv) {
+      const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)warp * rb;
+      const int lr = (q - qs) * 4;
+      const float4 x4 = *reinterpret_cast<const float4*>(xs + lr);
+      if (active) gemv::quad_codes<BITS>(acc, rec, wcb, lane, x4, M.g_log2, M.sg_log2);
+      if (QUANT) {
+        Z.zeros = reinterpret_cast<const uint32_t*>(rec + 16 * Fmt<BITS>::NV * wcb);
+        Z.xs = xs + lr;
+        Z.xz = xz + lr;
+        Z.grow = q * 4;
+        gemv::quad_zero(zacc, Z, lane);
+      }
+    }
     __syncwarp();
     if (lane == 0) gemv::mbar_arrive(empty + st);
   }
+  float ztot = 0.f;
+  if (QUANT) {  // per-group totals, then the lane's own group
+    if (Z.mode == 0)
+      for (int o = Z.zpr; o < 32; o <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, o);
+    ztot = __shfl_sync(0xffffffffu, zacc, (lane * WC) >> M.g_log2);
+  }
   float y[WC];
-  gemv::finish_lane<BITS>(y, acc, zacc);
+  gemv::finish_lane<BITS>(y, acc, ztot);
   // cross-warp reduction through the (now idle) ring, fixed order
   float* red = reinterpret_cast<float*>(ring);
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
 #pragma unroll
   for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  const float zo_out = zo_sum * gemv::kZUnscale;
+  float* dst = J.S == 1 ? J.out : J.part + (size_t)s * M.N;
   for (int t = threadIdx.x; t < 32 * WC; t += nthr) {
     const int l = t / WC, k = t % WC;
     if (l < wcb) {
       float a = 0.f;
 #pragma unroll
       for (int w = 0; w < W; ++w) a += red[(w * 32 + l) * (WC + 1) + k];
-      J.out[(size_t)s * M.N + (size_t)(cb * 32 + l) * WC + k] = a;
+      dst[(size_t)(cb * 32 + l) * WC + k] = a + zo_out;
     }
   }
+  if (J.S == 1) return;
+  // split-K: the last CTA of this column block sums the S partials in order
+  __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  int* flag = reinterpret_cast<int*>(misc + 8);
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(P.cnt + cnt_base + cb, 1);
+    *flag = old == J.S - 1;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  if (!*flag) return;
+  __threadfence();
+  for (int t = threadIdx.x; t < wcb * WC; t += nthr) {
+    const size_t o = (size_t)cb * 32 * WC + t;
+    float a = 0.f;
+    for (int ss = 0; ss < J.S; ++ss) a += __ldcg(J.part + (size_t)ss * M.N + o);
+    J.out[o] = a;
+  }
+  if (threadIdx.x == 0) P.cnt[cnt_base + cb] = 0;
 }
 
 // ------------------------------------------------------------------ wait
@@ -191,17 +256,19 @@ __global__ void k_wait_ready(const RouteRec* route, int n, const uint32_t* flags
 
 // ------------------------------------------------------------------ embed
 __global__ void k_embed(EmbedParams P) {
-  const int tok = P.tok_dev ? *P.tok_dev : P.tok;
-  if (P.tok_hist && blockIdx.x == 0 && threadIdx.x == 0) *P.tok_hist = tok;
+  gemv::pdl_trigger();
+  gemv::pdl_wait();
+  const int tok = P.ds ? P.ds->tok : P.tok;
+  const int pos = P.ds ? P.ds->pos : P.pos;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.d) return;
   float a, b;
   if (P.half) {
     a = __half2float(reinterpret_cast<const __half*>(P.wte)[(size_t)tok * P.d + i]);
-    b = __half2float(reinterpret_cast<const __half*>(P.wpe)[(size_t)P.pos * P.d + i]);
+    b = __half2float(reinterpret_cast<const __half*>(P.wpe)[(size_t)pos * P.d + i]);
   } else {
     a = reinterpret_cast<const float*>(P.wte)[(size_t)tok * P.d + i];
-    b = reinterpret_cast<const float*>(P.wpe)[(size_t)P.pos * P.d + i];
+    b = reinterpret_cast<const float*>(P.wpe)[(size_t)pos * P.d + i];
   }
   P.x[i] = __fadd_rn(a, b);  // model.py:319
 }
@@ -231,6 +298,8 @@ MOE_DEV void layernorm_block(const float* x, const float* g, const float* b, flo
 __global__ void __launch_bounds__(1024) k_layernorm(const float* x, const float* g, const float* b,
                                                     float* y, int d) {
   __shared__ double red[32];
+  gemv::pdl_trigger();
+  gemv::pdl_wait();
   layernorm_block(x, g, b, y, nullptr, d, red);
 }
 
@@ -244,7 +313,10 @@ __global__ void __launch_bounds__(256) k_attention(AttnParams P) {
   float* sc = sh + hd;
   __shared__ float red[32];
   __shared__ float bval;
-  const size_t kvrow = (size_t)P.pos * P.H * hd + (size_t)h * hd;
+  gemv::pdl_trigger();
+  gemv::pdl_wait();
+  const int pos = P.ds ? P.ds->pos : P.pos;
+  const size_t kvrow = (size_t)pos * P.H * hd + (size_t)h * hd;
   for (int i = threadIdx.x; i < hd; i += blockDim.x) {
     const int o = h * hd + i;
     float a = 0.f, bk = 0.f, bv = 0.f;
@@ -258,7 +330,7 @@ __global__ void __launch_bounds__(256) k_attention(AttnParams P) {
     P.vc[kvrow + i] = bv;
   }
   __syncthreads();
-  const int T = P.pos + 1;
+  const int T = pos + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const float rs = sqrtf((float)hd);
   for (int t = warp; t < T; t += nw) {
@@ -322,6 +394,11 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   __shared__ float lg[64];
   const int d = P.d, E = P.E;
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  gemv::pdl_trigger();
+  gemv::pdl_wait();
+  const int pos = P.ds ? P.ds->pos : P.pos;
+  const size_t slot = (size_t)pos * P.n_layers + P.layer;
+  float* th = P.trace_hidden ? P.trace_hidden + slot * d : nullptr;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     float a = 0.f;
     for (int s = 0; s < P.S; ++s) a += __ldcg(P.part + (size_t)s * d + i);
@@ -333,7 +410,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   int bad = 0;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     if (!isfinite(hs[i])) bad = 1;
-    if (P.trace_hidden) P.trace_hidden[i] = hs[i];
+    if (th) th[i] = hs[i];
   }
   bad = __syncthreads_or(bad);
   const int nlog = P.gate_g ? 2 * E : E;  // E <= 16
@@ -390,13 +467,13 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     R.gen[j] = 0;
   }
   TraceRecDev tr;
-  tr.pos = P.pos;
+  tr.pos = pos;
   tr.layer = P.layer;
   for (int j = 0; j < 8; ++j) {
     tr.experts[j] = j < k ? sel[j] : -1;
     tr.weights[j] = j < k ? R.w[j] : 0.f;
   }
-  *P.trace = tr;
+  P.trace[slot] = tr;
   if (bad) {
     atomicOr(P.st.err, MOE_ERRF_NONFINITE_GATE);
     *P.route = R;
@@ -418,7 +495,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
       }
       m = P.m;
     }
-    store::resolve_token(S, P.layer, sel, k, g, m, m ? P.guess_layer : -1, P.pos, R.buf, R.gen);
+    store::resolve_token(S, P.layer, sel, k, g, m, m ? P.guess_layer : -1, pos, R.buf, R.gen);
   }
   *P.route = R;
 }
@@ -426,6 +503,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
 // prefill: each distinct expert of the layer acquired once, first-use order
 // over (position, descending weight), no speculation (engine.py:233-240).
 __global__ void k_prefill_bk(PrefillBKParams P) {
+  gemv::pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   StoreDev S = P.st;
   RouteRec* R = P.route;
@@ -443,6 +521,8 @@ __global__ void k_begin_call(StoreDev S) {
 
 // out = h + w0*y0 + w1*y1 in descending-weight order (model.py:251-254)
 __global__ void k_combine(CombineParams P) {
+  gemv::pdl_trigger();
+  gemv::pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.d) return;
   float out = P.h[i];
@@ -460,6 +540,8 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
   __shared__ float bv[256];
   __shared__ int bi[256];
   __shared__ bool last;
+  gemv::pdl_trigger();
+  gemv::pdl_wait();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   float val = -INFINITY;
   int idx = 0x7fffffff;
@@ -522,7 +604,13 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
   if (threadIdx.x == 0) {
     const int t = bi[0] == 0x7fffffff ? 0 : bi[0];
     *P.tok_out = t;
-    if (P.tok_hist) *P.tok_hist = t;
+    if (P.ds) {  // decode: record the greedy token and advance the cursor
+      DecodeState* ds = P.ds;
+      P.tok_hist[ds->step] = t;
+      ds->tok = t;
+      ds->step += 1;
+      ds->pos += 1;
+    }
     *P.counter = 0u;
   }
 }
@@ -569,7 +657,7 @@ int gemv_smem_bytes(int bits, int xs_rows, int rb_full, int* nstages, int* stage
   if (ring < red) ring = red;
   if (nstages) *nstages = nst;
   if (stage_bytes) *stage_bytes = stage;
-  return 256 + ((xs_rows * 4 + 127) & ~127) + ring;
+  return 512 + ((xs_rows * 8 + 127) & ~127) + ring;
 }
 
 template <int BITS>
@@ -604,22 +692,41 @@ void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool p
   }
 }
 
-void launch_embed(const EmbedParams& P, cudaStream_t s) {
-  k_embed<<<(P.d + 255) / 256, 256, 0, s>>>(P);
+// small kernels: optionally launched with programmatic stream serialization so
+// the next kernel (usually a GEMV streaming weights that do not depend on this
+// kernel) is scheduled while this one runs
+template <class... Params, class... Args>
+static void launch_small(void (*kern)(Params...), dim3 grid, dim3 block, size_t smem,
+                         cudaStream_t s, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl) {
+  launch_small(k_embed, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
 }
 
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
-                      cudaStream_t s) {
-  k_layernorm<<<1, 1024, 0, s>>>(x, g, b, y, d);
+                      cudaStream_t s, bool pdl) {
+  launch_small(k_layernorm, dim3(1), dim3(1024), 0, s, pdl, x, g, b, y, d);
 }
 
-void launch_attention(const AttnParams& P, cudaStream_t s) {
-  const size_t smem = (size_t)(P.hd + P.pos + 1) * sizeof(float);
-  k_attention<<<P.H, 256, smem, s>>>(P);
+void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl) {
+  const size_t smem = (size_t)(P.hd + P.T_max) * sizeof(float);
+  launch_small(k_attention, dim3(P.H), dim3(256), smem, s, pdl, P);
 }
 
-void launch_tail(const TailParams& P, cudaStream_t s) {
-  k_tail<<<1, 1024, (size_t)P.d * sizeof(float), s>>>(P);
+void launch_tail(const TailParams& P, cudaStream_t s, bool pdl) {
+  launch_small(k_tail, dim3(1), dim3(1024), (size_t)P.d * sizeof(float), s, pdl, P);
 }
 
 void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s) { k_prefill_bk<<<1, 32, 0, s>>>(P); }
@@ -630,10 +737,10 @@ void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int*
   k_wait_ready<<<1, 32, 0, s>>>(route, n, flags, err, wait_ns);
 }
 
-void launch_combine(const CombineParams& P, cudaStream_t s) {
-  k_combine<<<(P.d + 255) / 256, 256, 0, s>>>(P);
+void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl) {
+  launch_small(k_combine, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
 }
 
-void launch_logits(const LogitsParams& P, cudaStream_t s) {
-  k_logits<<<(P.V + 255) / 256, 256, 0, s>>>(P);
+void launch_logits(const LogitsParams& P, cudaStream_t s, bool pdl) {
+  launch_small(k_logits, dim3((P.V + 255) / 256), dim3(256), 0, s, pdl, P);
 }

@@ -17,10 +17,10 @@ struct GJob {
   int rel_slot;        // >= 0: expert matrix, base = pool + route.buf[rel_slot]*stride
   int xmode;
   const float* x;      // X_PLAIN input (length K)
-  const float* up1;    // X_SWIGLU: partial sums of x@W1 [S_up][K]
-  const float* up3;    //           partial sums of x@W3 [S_up][K]
-  int S_up;
-  float* out;          // partial outputs [S][N]
+  const float* up1;    // X_SWIGLU: x@W1 [K]
+  const float* up3;    //           x@W3 [K]
+  float* part;         // split-K partial outputs [S][N] (S > 1)
+  float* out;          // final outputs [N] (the last CTA of a cb reduces the partials)
   int S, QPS, blk0;    // splits of the quad range, quads per split (multiple of QS)
 };
 
@@ -31,8 +31,19 @@ struct GLaunch {
   const uint8_t* pool;
   long long slot_stride;
   const uint32_t* flags;        // buffer ready generations (copy engine)
+  int* cnt;                     // split-K arrival counters [sum of ncb] (zero between launches)
   int* err;
   unsigned long long wait_ns;
+};
+
+// Device-resident decode cursor: the kernels of one decode token read the
+// position and input token from here, and k_logits advances it, so one
+// captured CUDA graph serves every token (no per-token parameters).
+struct DecodeState {
+  int pos;   // position of the token being decoded
+  int step;  // index of this token within the current decode call
+  int tok;   // token to embed
+  int pad;
 };
 
 struct AttnParams {
@@ -41,7 +52,8 @@ struct AttnParams {
   float* kc;              // this layer's K cache [max_seq][H][hd]
   float* vc;
   float* ctx;             // [d]
-  int pos, H, hd, d;
+  const DecodeState* ds;  // decode: position from here (else `pos`)
+  int pos, H, hd, d, T_max;
 };
 
 struct TailParams {
@@ -54,8 +66,10 @@ struct TailParams {
   const float* gate_g;    // [d][E] gate of the guessed layer (or null)
   float* h;               // pre-MoE hidden out [d]
   RouteRec* route;        // route of this position
-  TraceRecDev* trace;     // record slot for (pos, layer)
-  float* trace_hidden;    // [d] or null
+  TraceRecDev* trace;     // trace records [T][L]; slot pos*L + layer
+  float* trace_hidden;    // [T][L][d] or null
+  const DecodeState* ds;  // decode: position from here (else `pos`)
+  int n_layers;
   StoreDev st;
   int d, E, top_k, m, layer, guess_layer, pos, mode;  // mode 0 decode, 1 prefill (no store)
   int ep_rank, ep_size;   // expert parallel (ep_size 1 = off)
@@ -84,34 +98,33 @@ struct LogitsParams {
   int* cand_idx;
   unsigned int* counter;
   int* tok_out;       // argmax
-  int* tok_hist;      // optional history slot
+  int* tok_hist;      // decode: argmax history, slot ds->step
+  DecodeState* ds;    // decode: advanced (tok, step, pos) by the last block
   int* err;
 };
 
 struct EmbedParams {
   const void* wte;
   const void* wpe;
-  int half;           // 1: fp16 tables
-  const int* tok_dev; // token from device (greedy) or null
-  int tok;            // host token
-  int* tok_hist;      // write the consumed token here (or null)
-  int pos, d;
+  int half;               // 1: fp16 tables
+  const DecodeState* ds;  // decode: token and position from here
+  int tok, pos, d;        // prefill
   float* x;
 };
 
 // launchers (kernels.cu)
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
 int gemv_smem_bytes(int bits, int xs_rows, int rb_full, int* nstages, int* stage_bytes);
-void launch_embed(const EmbedParams& P, cudaStream_t s);
+void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl = false);
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
-                      cudaStream_t s);
-void launch_attention(const AttnParams& P, cudaStream_t s);
-void launch_tail(const TailParams& P, cudaStream_t s);
+                      cudaStream_t s, bool pdl = false);
+void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl = false);
+void launch_tail(const TailParams& P, cudaStream_t s, bool pdl = false);
 void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s);
-void launch_combine(const CombineParams& P, cudaStream_t s);
+void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl = false);
 void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int* err,
                        unsigned long long wait_ns, cudaStream_t s);
-void launch_logits(const LogitsParams& P, cudaStream_t s);
+void launch_logits(const LogitsParams& P, cudaStream_t s, bool pdl = false);
 void launch_begin_call(StoreDev st, cudaStream_t s);
 cudaError_t preload_kernels();
 cudaError_t preload_tile_kernels();
