@@ -370,7 +370,7 @@ struct moe_engine {
   }
   int run_copier();
   int enq_attention(int l, int p, int mode);
-  int enq_experts(int p);
+  int enq_experts(int l, int p);
   int enq_logits(int p, float* out);
   int enq_token();
   int run_tokens(int n);
@@ -500,7 +500,8 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   float* xp = x + (size_t)p * d;
   float* hp = h + (size_t)p * d;
   const bool pl = pdl && !prof;
-  launch_layernorm(xp, ln1g[l], ln1b[l], xn, d, s_comp, pl);
+  if (!cur_ds)  // decode: LN1 is fused into the embed / previous combine kernel
+    launch_layernorm(xp, ln1g[l], ln1b[l], xn, d, s_comp, pl);
   dbg("ln1", l, p);
   GLaunch q{};
   q.nj = 3;
@@ -562,12 +563,11 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   t.ep_size = 1;
   launch_tail(t, s_comp, pl);
   dbg("tail", l, p);
-  launches += 6;
   unit_done();
   return MOE_OK;
 }
 
-int moe_engine::enq_experts(int p) {
+int moe_engine::enq_experts(int l, int p) {
   throttle();
   GLaunch u{};
   u.route = route + p;
@@ -614,6 +614,8 @@ int moe_engine::enq_experts(int p) {
       std::this_thread::yield();
     CU(cudaStreamSynchronize(s_copy));
   }
+  if (prof)  // keep copy waits out of the GEMV's event-timed span
+    launch_wait_ready(route + p, topk, flags, err, wait_ns, s_comp);
   prof_begin(K_UP);
   launch_gemv(expert_bits, u, finalize_launch(u), s_comp, pdl && !prof);
   prof_end(K_UP);
@@ -630,16 +632,21 @@ int moe_engine::enq_experts(int p) {
   c.out = x + (size_t)p * d;
   c.d = d;
   c.top_k = topk;
+  if (cur_ds) {  // decode: fuse the next LayerNorm (LN1 of l+1, or LN_f)
+    c.ln_g = l + 1 < L ? ln1g[l + 1] : lnfg;
+    c.ln_b = l + 1 < L ? ln1b[l + 1] : lnfb;
+    c.xn = xn;
+  }
   launch_combine(c, s_comp, pdl && !prof);
   dbg("combine", -1, p);
-  launches += 3;
   unit_done();
   return MOE_OK;
 }
 
 int moe_engine::enq_logits(int p, float* out) {
   const bool pl = pdl && !prof;
-  launch_layernorm(x + (size_t)p * d, lnfg, lnfb, xn, d, s_comp, pl);
+  if (!cur_ds)  // decode: LN_f is fused into the last combine kernel
+    launch_layernorm(x + (size_t)p * d, lnfg, lnfb, xn, d, s_comp, pl);
   GLaunch g{};
   g.nj = 1;
   g.cnt = cnt;
@@ -661,7 +668,6 @@ int moe_engine::enq_logits(int p, float* out) {
   lp.err = err;
   launch_logits(lp, s_comp, pl);
   dbg("logits", -1, p);
-  launches += 3;
   return MOE_OK;
 }
 
@@ -677,14 +683,16 @@ int moe_engine::enq_token() {
   ep.ds = ds_dev;
   ep.d = d;
   ep.x = x;
+  ep.ln_g = ln1g[0];
+  ep.ln_b = ln1b[0];
+  ep.xn = xn;
   launch_embed(ep, s_comp, pdl && !prof);
   for (int l = 0; l < L; ++l) {
     enq_attention(l, 0, 0);
-    enq_experts(0);
+    enq_experts(l, 0);
   }
   enq_logits(0, logits);
   cur_ds = nullptr;
-  launches += 1;
   return MOE_OK;
 }
 
@@ -695,11 +703,13 @@ int moe_engine::enq_token() {
 int moe_engine::run_tokens(int n) {
   const bool graphs = use_graph && !prof && !debug && !serial_copies;
   if (!graphs) {
+    const long long c0 = launch_count();
     for (int i = 0; i < n; ++i) enq_token();
+    launches += launch_count() - c0;
     return MOE_OK;
   }
   if (!gexec) {
-    const int64_t l0 = launches;
+    const long long c0 = launch_count();
     CU(cudaStreamBeginCapture(s_comp, cudaStreamCaptureModeThreadLocal));
     capturing = true;
     enq_token();
@@ -708,8 +718,7 @@ int moe_engine::run_tokens(int n) {
     CU(cudaStreamEndCapture(s_comp, &g));
     CU(cudaGraphInstantiate(&gexec, g, 0));
     CU(cudaGraphDestroy(g));
-    graph_launches = launches - l0;
-    launches = l0;
+    graph_launches = launch_count() - c0;
   }
   for (int i = 0; i < n; ++i) {
     if (i >= 2) CU(cudaEventSynchronize(tok_ev[(i - 2) % 4]));
@@ -1190,6 +1199,7 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
                                      std::to_string(e->T));
   }
   CU(cudaEventRecord(e->t0, e->s_comp));
+  const long long c0 = launch_count();
   for (int p = 0; p < n; ++p) {
     EmbedParams ep{};
     ep.wte = e->wte;
@@ -1211,9 +1221,10 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
     pb.top_k = e->topk;
     launch_prefill_bk(pb, e->s_comp);
     e->dbg("prefill_bk", l, n);
-    for (int p = 0; p < n; ++p) e->enq_experts(p);
+    for (int p = 0; p < n; ++p) e->enq_experts(l, p);
   }
   for (int p = 0; p < n; ++p) e->enq_logits(p, e->logits + (size_t)p * e->V);
+  e->launches = launch_count() - c0;
   CU(cudaGetLastError());
   rc = e->finish_call();
   if (rc) return rc;

@@ -7,6 +7,8 @@
 //   | combine (h + w0*y0 + w1*y1, reference order)
 // then layernorm(ln_f) | gemv<f16>(lm_head) | logits (+ argmax on device).
 // All reductions are in a fixed order, so results are run-to-run deterministic.
+#include <atomic>
+
 #include "kernels.cuh"
 #include "gemv.cuh"
 
@@ -254,25 +256,6 @@ __global__ void k_wait_ready(const RouteRec* route, int n, const uint32_t* flags
   }
 }
 
-// ------------------------------------------------------------------ embed
-__global__ void k_embed(EmbedParams P) {
-  gemv::pdl_trigger();
-  gemv::pdl_wait();
-  const int tok = P.ds ? P.ds->tok : P.tok;
-  const int pos = P.ds ? P.ds->pos : P.pos;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P.d) return;
-  float a, b;
-  if (P.half) {
-    a = __half2float(reinterpret_cast<const __half*>(P.wte)[(size_t)tok * P.d + i]);
-    b = __half2float(reinterpret_cast<const __half*>(P.wpe)[(size_t)pos * P.d + i]);
-  } else {
-    a = reinterpret_cast<const float*>(P.wte)[(size_t)tok * P.d + i];
-    b = reinterpret_cast<const float*>(P.wpe)[(size_t)pos * P.d + i];
-  }
-  P.x[i] = __fadd_rn(a, b);  // model.py:319
-}
-
 // LayerNorm with the reference's float32 rounding structure (model.py:186-189):
 // mu, var rounded to float32 (sums taken in double), then
 // ((x - mu) / sqrt(var + eps)) * gamma + beta with separately rounded ops.
@@ -292,6 +275,34 @@ MOE_DEV void layernorm_block(const float* x, const float* g, const float* b, flo
     const float v = __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(x[i], mu), den), g[i]), b[i]);
     if (y) y[i] = v;
     if (ysh) ysh[i] = v;
+  }
+}
+
+// ------------------------------------------------------------------ embed
+__global__ void k_embed(EmbedParams P) {
+  __shared__ double red[32];
+  extern __shared__ float xsh[];
+  gemv::pdl_trigger();
+  gemv::pdl_wait();
+  const int tok = P.ds ? P.ds->tok : P.tok;
+  const int pos = P.ds ? P.ds->pos : P.pos;
+  const int step = P.xn ? blockDim.x : gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.d; i += step) {
+    float a, b;
+    if (P.half) {
+      a = __half2float(reinterpret_cast<const __half*>(P.wte)[(size_t)tok * P.d + i]);
+      b = __half2float(reinterpret_cast<const __half*>(P.wpe)[(size_t)pos * P.d + i]);
+    } else {
+      a = reinterpret_cast<const float*>(P.wte)[(size_t)tok * P.d + i];
+      b = reinterpret_cast<const float*>(P.wpe)[(size_t)pos * P.d + i];
+    }
+    const float v = __fadd_rn(a, b);  // model.py:319
+    P.x[i] = v;
+    if (P.xn) xsh[i] = v;
+  }
+  if (P.xn) {  // fused LN1 of layer 0
+    __syncthreads();
+    layernorm_block(xsh, P.ln_g, P.ln_b, P.xn, nullptr, P.d, red);
   }
 }
 
@@ -388,116 +399,118 @@ __global__ void __launch_bounds__(256) k_attention(AttnParams P) {
 // expert in descending-weight order and speculative_load the guesses
 // (engine.py:222-231).
 __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
-  extern __shared__ float hs[];
-  __shared__ double red[32];
-  __shared__ double gred[32][33];
-  __shared__ float lg[64];
+  extern __shared__ __align__(16) unsigned char tsm[];
   const int d = P.d, E = P.E;
-  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* hs = reinterpret_cast<float*>(tsm);                                  // [d]
+  double* gpart = reinterpret_cast<double*>(tsm + (((size_t)d * 4 + 15) & ~(size_t)15));
+  int* sst = reinterpret_cast<int*>(gpart + 2 * blockDim.x);                  // store state
+  __shared__ double red[32];
+  __shared__ float lg[64];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   gemv::pdl_trigger();
+  // gate matrices are immutable: pull them toward L2 while the Wo GEMV finishes
+  for (int i = tid * 32; i < d * E; i += blockDim.x * 32) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(P.gate_l + i));
+    if (P.gate_g) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.gate_g + i));
+  }
   gemv::pdl_wait();
   const int pos = P.ds ? P.ds->pos : P.pos;
   const size_t slot = (size_t)pos * P.n_layers + P.layer;
   float* th = P.trace_hidden ? P.trace_hidden + slot * d : nullptr;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float a = 0.f;
-    for (int s = 0; s < P.S; ++s) a += __ldcg(P.part + (size_t)s * d + i);
-    hs[i] = __fadd_rn(P.x[i], a);
-  }
+  StoreDev S = P.st;
+  if (P.mode == 0) S = store::stage_in(P.st, sst);
+  for (int i = tid; i < d; i += blockDim.x) hs[i] = __fadd_rn(P.x[i], __ldcg(P.part + i));
   __syncthreads();
   layernorm_block(hs, P.g2, P.b2, P.h, hs, d, red);
   __syncthreads();
   int bad = 0;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+  for (int i = tid; i < d; i += blockDim.x) {
     if (!isfinite(hs[i])) bad = 1;
     if (th) th[i] = hs[i];
   }
   bad = __syncthreads_or(bad);
-  const int nlog = P.gate_g ? 2 * E : E;  // E <= 16
-  double acc[32];
-#pragma unroll
-  for (int e = 0; e < 32; ++e) acc[e] = 0.0;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const double hv = hs[i];
-#pragma unroll
-    for (int e = 0; e < 16; ++e)
-      if (e < E) acc[e] += hv * P.gate_l[(size_t)i * E + e];
-    if (P.gate_g) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if (e < E) acc[16 + e] += hv * P.gate_g[(size_t)i * E + e];
+  // gate logits of this layer and the guessed layer on the same h (model.py:210,
+  // engine.py:60-68): thread t owns expert t % E over rows t/E, t/E + nt/E, ...
+  const int nt = (blockDim.x / E) * E;
+  if (tid < nt) {
+    const int e = tid % E;
+    double a = 0.0, ag = 0.0;
+    for (int i = tid; i < d * E; i += nt) {
+      const double hv = hs[i / E];
+      a += hv * (double)P.gate_l[i];
+      if (P.gate_g) ag += hv * (double)P.gate_g[i];
     }
-  }
-#pragma unroll
-  for (int e = 0; e < 32; ++e) {
-    const double v = warp_sum_d(acc[e]);
-    if (lane == 0) gred[warp][e] = v;
+    (void)e;
+    gpart[tid] = a;
+    gpart[blockDim.x + tid] = ag;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    const int e = threadIdx.x;
+  const int nlog = P.gate_g ? 2 * E : E;
+  if (warp < nlog) {  // warp w reduces logit w in a fixed order
+    const int e = warp % E;
+    const double* gp = gpart + (warp >= E ? blockDim.x : 0);
     double t = 0.0;
-    for (int w = 0; w < nw; ++w) t += gred[w][e];
-    const int idx = e < 16 ? e : E + (e - 16);
-    if ((e < 16 && e < E) || (e >= 16 && e - 16 < E && P.gate_g)) lg[idx] = (float)t;
+    for (int i = e + E * lane; i < nt; i += 32 * E) t += gp[i];
+    t = warp_sum_d(t);
+    if (lane == 0) lg[warp] = (float)t;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  (void)nlog;
-  RouteRec R;
-  const int k = P.top_k;
-  int sel[MOE_MAX_TOPK];
-  unsigned long long used = 0ull;
-  for (int j = 0; j < k; ++j) {  // stable descending (ties -> lower index)
-    int best = -1;
-    for (int e = 0; e < E; ++e)
-      if (!((used >> e) & 1ull) && (best < 0 || lg[e] > lg[best])) best = e;
-    sel[j] = best;
-    used |= 1ull << best;
-  }
-  float ez[MOE_MAX_TOPK], sum = 0.f;
-  for (int j = 0; j < k; ++j) {
-    ez[j] = expf(__fsub_rn(lg[sel[j]], lg[sel[0]]));
-    sum = __fadd_rn(sum, ez[j]);
-  }
-  for (int j = 0; j < MOE_MAX_TOPK; ++j) {
-    R.e[j] = j < k ? sel[j] : -1;
-    R.w[j] = j < k ? __fdiv_rn(ez[j], sum) : 0.f;
-    R.buf[j] = -1;
-    R.gen[j] = 0;
-  }
-  TraceRecDev tr;
-  tr.pos = pos;
-  tr.layer = P.layer;
-  for (int j = 0; j < 8; ++j) {
-    tr.experts[j] = j < k ? sel[j] : -1;
-    tr.weights[j] = j < k ? R.w[j] : 0.f;
-  }
-  P.trace[slot] = tr;
-  if (bad) {
-    atomicOr(P.st.err, MOE_ERRF_NONFINITE_GATE);
+  if (tid == 0) {
+    RouteRec R;
+    const int k = P.top_k;
+    int sel[MOE_MAX_TOPK];
+    unsigned long long used = 0ull;
+    for (int j = 0; j < k; ++j) {  // stable descending (ties -> lower index)
+      int best = -1;
+      for (int e = 0; e < E; ++e)
+        if (!((used >> e) & 1ull) && (best < 0 || lg[e] > lg[best])) best = e;
+      sel[j] = best;
+      used |= 1ull << best;
+    }
+    float ez[MOE_MAX_TOPK], sum = 0.f;
+    for (int j = 0; j < k; ++j) {
+      ez[j] = expf(__fsub_rn(lg[sel[j]], lg[sel[0]]));
+      sum = __fadd_rn(sum, ez[j]);
+    }
+    for (int j = 0; j < MOE_MAX_TOPK; ++j) {
+      R.e[j] = j < k ? sel[j] : -1;
+      R.w[j] = j < k ? __fdiv_rn(ez[j], sum) : 0.f;
+      R.buf[j] = -1;
+      R.gen[j] = 0;
+    }
+    TraceRecDev tr;
+    tr.pos = pos;
+    tr.layer = P.layer;
+    for (int j = 0; j < 8; ++j) {
+      tr.experts[j] = j < k ? sel[j] : -1;
+      tr.weights[j] = j < k ? R.w[j] : 0.f;
+    }
+    P.trace[slot] = tr;
+    if (bad) {
+      atomicOr(P.st.err, MOE_ERRF_NONFINITE_GATE);
+    } else if (P.mode == 0) {
+      int g[16];
+      int m = 0;
+      if (P.gate_g && P.m > 0) {
+        unsigned long long gu = 0ull;
+        const float* lgg = lg + E;
+        for (int j = 0; j < P.m; ++j) {  // top-m, ties -> lower index (engine.py:60-68)
+          int best = -1;
+          for (int e = 0; e < E; ++e)
+            if (!((gu >> e) & 1ull) && (best < 0 || lgg[e] > lgg[best])) best = e;
+          g[j] = best;
+          gu |= 1ull << best;
+        }
+        m = P.m;
+      }
+      store::resolve_token(S, P.layer, sel, k, g, m, m ? P.guess_layer : -1, pos, R.buf, R.gen);
+    }
     *P.route = R;
-    return;
   }
   if (P.mode == 0) {
-    StoreDev S = P.st;
-    int g[16];
-    int m = 0;
-    if (P.gate_g && P.m > 0) {
-      unsigned long long gu = 0ull;
-      const float* lgg = lg + E;
-      for (int j = 0; j < P.m; ++j) {  // top-m, ties -> lower index (engine.py:60-68)
-        int best = -1;
-        for (int e = 0; e < E; ++e)
-          if (!((gu >> e) & 1ull) && (best < 0 || lgg[e] > lgg[best])) best = e;
-        g[j] = best;
-        gu |= 1ull << best;
-      }
-      m = P.m;
-    }
-    store::resolve_token(S, P.layer, sel, k, g, m, m ? P.guess_layer : -1, pos, R.buf, R.gen);
+    __syncthreads();
+    store::stage_out(P.st, S);
   }
-  *P.route = R;
 }
 
 // prefill: each distinct expert of the layer acquired once, first-use order
@@ -521,17 +534,25 @@ __global__ void k_begin_call(StoreDev S) {
 
 // out = h + w0*y0 + w1*y1 in descending-weight order (model.py:251-254)
 __global__ void k_combine(CombineParams P) {
+  __shared__ double red[32];
+  extern __shared__ float osh[];
   gemv::pdl_trigger();
   gemv::pdl_wait();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P.d) return;
-  float out = P.h[i];
-  for (int j = 0; j < P.top_k; ++j) {
-    float y = 0.f;
-    for (int s = 0; s < P.S; ++s) y += __ldcg(P.part + ((size_t)j * P.S + s) * P.d + i);
-    out = __fadd_rn(out, __fmul_rn(P.route->w[j], y));
+  const int step = P.xn ? blockDim.x : gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.d; i += step) {
+    float out = P.h[i];
+    for (int j = 0; j < P.top_k; ++j) {
+      float y = 0.f;
+      for (int s = 0; s < P.S; ++s) y += __ldcg(P.part + ((size_t)j * P.S + s) * P.d + i);
+      out = __fadd_rn(out, __fmul_rn(P.route->w[j], y));
+    }
+    P.out[i] = out;
+    if (P.xn) osh[i] = out;
   }
-  P.out[i] = out;
+  if (P.xn) {  // fused LayerNorm of the residual stream (next LN1 or LN_f)
+    __syncthreads();
+    layernorm_block(osh, P.ln_g, P.ln_b, P.xn, nullptr, P.d, red);
+  }
 }
 
 // logits = sum of lm_head partials; non-finite check (model.py:308-309);
@@ -604,9 +625,9 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
   if (threadIdx.x == 0) {
     const int t = bi[0] == 0x7fffffff ? 0 : bi[0];
     *P.tok_out = t;
-    if (P.ds) {  // decode: record the greedy token and advance the cursor
+    if (P.ds) {  // decode: record the consumed token, feed the argmax, advance
       DecodeState* ds = P.ds;
-      P.tok_hist[ds->step] = t;
+      P.tok_hist[ds->step] = ds->tok;
       ds->tok = t;
       ds->step += 1;
       ds->pos += 1;
@@ -618,6 +639,9 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+static std::atomic<long long> g_launches{0};
+long long launch_count() { return g_launches.load(); }
+
 // Loads every kernel and sets its shared-memory limit while the GPU is idle.
 // With lazy module loading, the first launch of a kernel while another kernel
 // spin-waits on the copy engine can block the runtime (and so the copy
@@ -637,6 +661,11 @@ cudaError_t preload_kernels() {
     cudaError_t e = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          200 * 1024);
     if (e != cudaSuccess) return e;
+  }
+  for (const void* f : {(const void*)k_embed, (const void*)k_combine}) {
+    cudaError_t e2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          200 * 1024);
+    if (e2 != cudaSuccess) return e2;
   }
   cudaError_t e = cudaFuncSetAttribute((const void*)k_attention,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -680,6 +709,7 @@ static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pd
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, nst, stage);
+  g_launches.fetch_add(1);
 }
 
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
@@ -709,10 +739,14 @@ static void launch_small(void (*kern)(Params...), dim3 grid, dim3 block, size_t 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kern, args...);
+  g_launches.fetch_add(1);
 }
 
 void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl) {
-  launch_small(k_embed, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
+  if (P.xn)
+    launch_small(k_embed, dim3(1), dim3(1024), (size_t)P.d * 4, s, pdl, P);
+  else
+    launch_small(k_embed, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
 }
 
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
@@ -725,20 +759,32 @@ void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl) {
   launch_small(k_attention, dim3(P.H), dim3(256), smem, s, pdl, P);
 }
 
-void launch_tail(const TailParams& P, cudaStream_t s, bool pdl) {
-  launch_small(k_tail, dim3(1), dim3(1024), (size_t)P.d * sizeof(float), s, pdl, P);
+int tail_smem_bytes(const TailParams& P) {
+  return (int)((((size_t)P.d * 4 + 15) & ~(size_t)15) + 2 * 1024 * sizeof(double) +
+               ((size_t)store::stage_ints(P.st) + 2) * 4);
 }
 
-void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s) { k_prefill_bk<<<1, 32, 0, s>>>(P); }
+void launch_tail(const TailParams& P, cudaStream_t s, bool pdl) {
+  launch_small(k_tail, dim3(1), dim3(1024), (size_t)tail_smem_bytes(P), s, pdl, P);
+}
+
+void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s) {
+  k_prefill_bk<<<1, 32, 0, s>>>(P);
+  g_launches.fetch_add(1);
+}
 void launch_begin_call(StoreDev st, cudaStream_t s) { k_begin_call<<<1, 32, 0, s>>>(st); }
 
 void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int* err,
                        unsigned long long wait_ns, cudaStream_t s) {
   k_wait_ready<<<1, 32, 0, s>>>(route, n, flags, err, wait_ns);
+  g_launches.fetch_add(1);
 }
 
 void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl) {
-  launch_small(k_combine, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
+  if (P.xn)
+    launch_small(k_combine, dim3(1), dim3(1024), (size_t)P.d * 4, s, pdl, P);
+  else
+    launch_small(k_combine, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
 }
 
 void launch_logits(const LogitsParams& P, cudaStream_t s, bool pdl) {

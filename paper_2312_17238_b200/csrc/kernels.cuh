@@ -88,6 +88,11 @@ struct CombineParams {
   const RouteRec* route;
   float* out;         // [d]
   int d, top_k;
+  // optional fused LayerNorm of `out` (next layer's LN1, or LN_f after the
+  // last layer): one CTA, xn = LN(out)
+  const float* ln_g;
+  const float* ln_b;
+  float* xn;
 };
 
 struct LogitsParams {
@@ -110,6 +115,9 @@ struct EmbedParams {
   const DecodeState* ds;  // decode: token and position from here
   int tok, pos, d;        // prefill
   float* x;
+  const float* ln_g;      // optional fused LN1 of layer 0 (one CTA): xn = LN(x)
+  const float* ln_b;
+  float* xn;
 };
 
 // launchers (kernels.cu)
@@ -127,6 +135,7 @@ void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int*
 void launch_logits(const LogitsParams& P, cudaStream_t s, bool pdl = false);
 void launch_begin_call(StoreDev st, cudaStream_t s);
 cudaError_t preload_kernels();
+long long launch_count();  // kernels launched (or captured) by this process
 cudaError_t preload_tile_kernels();
 
 // tiling + quantization + synthesis (tile.cu)

@@ -265,6 +265,61 @@ MOE_HD void speculative_load(StoreDev& S, int tl, const int* es, int m, int pos,
   }
 }
 
+// ---- shared-memory staging of the store state for the bookkeeping kernels:
+// the single bookkeeping thread does a few hundred dependent accesses per
+// layer; on shared memory they cost ~30 cycles instead of an L2 round trip.
+MOE_HD int stage_ints(const StoreDev& S) {
+  const int kk = S.k > 1 ? S.k : 1, bb = S.b > 1 ? S.b : 1;
+  return 2 + 4 + S.L * kk + S.L + S.L * S.E + 4 * bb + 3 * S.nbuf;
+}
+
+#ifdef __CUDACC__
+// all threads: view V of global store G backed by `sm` (stage_ints ints, 8-aligned)
+__device__ __forceinline__ StoreDev stage_in(const StoreDev& G, int* sm) {
+  StoreDev V = G;
+  const int kk = G.k > 1 ? G.k : 1, bb = G.b > 1 ? G.b : 1;
+  int* p = sm;
+  V.seq = reinterpret_cast<long long*>(p); p += 2;
+  V.scalars = p; p += 4;
+  V.lru = p; p += G.L * kk;
+  V.lru_len = p; p += G.L;
+  V.res_buf = p; p += G.L * G.E;
+  V.stg_layer = p; p += bb;
+  V.stg_exp = p; p += bb;
+  V.stg_stamp = p; p += bb;
+  V.stg_buf = p; p += bb;
+  V.free_stack = p; p += G.nbuf;
+  V.pending = p; p += G.nbuf;
+  V.gen = reinterpret_cast<uint32_t*>(p);
+  const int* src[11] = {G.scalars, G.lru, G.lru_len, G.res_buf, G.stg_layer, G.stg_exp,
+                        G.stg_stamp, G.stg_buf, G.free_stack, G.pending,
+                        reinterpret_cast<const int*>(G.gen)};
+  int* dst[11] = {V.scalars, V.lru, V.lru_len, V.res_buf, V.stg_layer, V.stg_exp,
+                  V.stg_stamp, V.stg_buf, V.free_stack, V.pending,
+                  reinterpret_cast<int*>(V.gen)};
+  const int n[11] = {4, G.L * kk, G.L, G.L * G.E, bb, bb, bb, bb, G.nbuf, G.nbuf, G.nbuf};
+  for (int a = 0; a < 11; ++a)
+    for (int i = threadIdx.x; i < n[a]; i += blockDim.x) dst[a][i] = src[a][i];
+  if (threadIdx.x == 0) V.seq[0] = G.seq[0];
+  return V;
+}
+
+// all threads: write the staged state back
+__device__ __forceinline__ void stage_out(const StoreDev& G, const StoreDev& V) {
+  const int kk = G.k > 1 ? G.k : 1, bb = G.b > 1 ? G.b : 1;
+  const int* src[11] = {V.scalars, V.lru, V.lru_len, V.res_buf, V.stg_layer, V.stg_exp,
+                        V.stg_stamp, V.stg_buf, V.free_stack, V.pending,
+                        reinterpret_cast<const int*>(V.gen)};
+  int* dst[11] = {G.scalars, G.lru, G.lru_len, G.res_buf, G.stg_layer, G.stg_exp,
+                  G.stg_stamp, G.stg_buf, G.free_stack, G.pending,
+                  reinterpret_cast<int*>(G.gen)};
+  const int n[11] = {4, G.L * kk, G.L, G.L * G.E, bb, bb, bb, bb, G.nbuf, G.nbuf, G.nbuf};
+  for (int a = 0; a < 11; ++a)
+    for (int i = threadIdx.x; i < n[a]; i += blockDim.x) dst[a][i] = src[a][i];
+  if (threadIdx.x == 0) G.seq[0] = V.seq[0];
+}
+#endif
+
 // One decode layer's bookkeeping, in the order of OffloadEngine._resolve_token
 // (engine.py:222-231): acquire the selected experts in descending-weight
 // order, then speculative_load the top-m guesses for layer + lookahead.
