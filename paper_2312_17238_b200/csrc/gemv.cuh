@@ -215,6 +215,47 @@ MOE_DEV void quad_zero(float& zacc, const ZeroCtx& Z, int lane) {
   }
 }
 
+// Fast zero-point path for the reference presets with full column blocks
+// and uniform runs (2-bit g=16: ZPR=32; 3/4-bit g=64: ZPR=16 / 4): the
+// lane -> (group, rows) split is a compile-time function of the lane.
+//   zeros: the record's [ZPR] u32; xz: x * zscale for the quad's 4 rows
+template <int BITS>
+MOE_DEV void quad_zero_fast(float& zacc, const uint32_t* zeros, const float* xz, int lane) {
+  if constexpr (BITS == 2) {  // lane = group, all 4 rows
+    const uint32_t z4 = zeros[lane];
+    const float4 x4 = *reinterpret_cast<const float4*>(xz);
+    zacc = fmaf((float)(z4 & 0xffu), x4.x, zacc);
+    zacc = fmaf((float)((z4 >> 8) & 0xffu), x4.y, zacc);
+    zacc = fmaf((float)((z4 >> 16) & 0xffu), x4.z, zacc);
+    zacc = fmaf((float)(z4 >> 24), x4.w, zacc);
+  } else if constexpr (BITS == 3) {  // group lane & 15, rows (lane >> 4) and +2
+    const uint32_t z4 = zeros[lane & 15];
+    const int r = lane >> 4;
+    zacc = fmaf((float)((z4 >> (8 * r)) & 0xffu), xz[r], zacc);
+    zacc = fmaf((float)((z4 >> (8 * r + 16)) & 0xffu), xz[r + 2], zacc);
+  } else {  // 4-bit: lanes < 16, group lane & 3, row lane >> 2
+    if (lane < 16) {
+      const uint32_t z4 = zeros[lane & 3];
+      const int r = lane >> 2;
+      zacc = fmaf((float)((z4 >> (8 * r)) & 0xffu), xz[r], zacc);
+    }
+  }
+}
+
+// lanes -> per-group totals for the fast path (then the lane's own group)
+template <int BITS>
+MOE_DEV float zero_total_fast(float zacc, int lane) {
+  if constexpr (BITS == 2) return zacc;
+  if constexpr (BITS == 3) {
+    zacc += __shfl_xor_sync(0xffffffffu, zacc, 16);
+    return __shfl_sync(0xffffffffu, zacc, lane >> 1);
+  }
+  zacc += __shfl_xor_sync(0xffffffffu, zacc, 4);
+  zacc += __shfl_xor_sync(0xffffffffu, zacc, 8);
+  zacc += __shfl_xor_sync(0xffffffffu, zacc, 16);
+  return __shfl_sync(0xffffffffu, zacc, lane >> 3);
+}
+
 // final per-output value of one lane: exact power-of-two rescale of the
 // masked-code accumulators plus the zero-point term
 template <int BITS>

@@ -167,28 +167,51 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
     Z.zmeta = M.zmeta;
   }
   const bool active = lane < wcb;
-  for (int it = 0; it < nit; ++it) {
-    const int st = it % nst;
-    gemv::mbar_wait(full + st, (it / nst) & 1);
-    const int q = qs + it * QS + warp;
-    if (q < qv) {
-      const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)warp * rb;
-      const int lr = (q - qs) * 4;
-      const float4 x4 = *reinterpret_cast<const float4*>(xs + lr);
-      if (active) gemv::quad_codes<BITS>(acc, rec, wcb, lane, x4, M.g_log2, M.sg_log2);
-      if (QUANT) {
+  // fast path: reference preset grouping, full column block, uniform runs
+  const bool fast = QUANT && wcb == 32 && M.runs_uniform &&
+                    M.g_log2 == (BITS == 2 ? 4 : 6);
+  float ztot = 0.f;
+  if (fast || !QUANT) {
+    for (int it = 0; it < nit; ++it) {
+      const int st = it % nst;
+      gemv::mbar_wait(full + st, (it / nst) & 1);
+      const int q = qs + it * QS + warp;
+      if (q < qv) {
+        const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)warp * rb;
+        const int lr = (q - qs) * 4;
+        const float4 x4 = *reinterpret_cast<const float4*>(xs + lr);
+        if (QUANT) {
+          gemv::quad_codes<BITS>(acc, rec, 32, lane, x4, M.g_log2, M.sg_log2);
+          gemv::quad_zero_fast<BITS>(
+              zacc, reinterpret_cast<const uint32_t*>(rec + 16 * Fmt<BITS>::NV * 32), xz + lr,
+              lane);
+        } else if (active) {
+          gemv::quad_codes<BITS>(acc, rec, wcb, lane, x4, 0, 0);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) gemv::mbar_arrive(empty + st);
+    }
+    if (QUANT) ztot = gemv::zero_total_fast<BITS>(zacc, lane);
+  } else {
+    for (int it = 0; it < nit; ++it) {
+      const int st = it % nst;
+      gemv::mbar_wait(full + st, (it / nst) & 1);
+      const int q = qs + it * QS + warp;
+      if (q < qv) {
+        const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)warp * rb;
+        const int lr = (q - qs) * 4;
+        const float4 x4 = *reinterpret_cast<const float4*>(xs + lr);
+        if (active) gemv::quad_codes<BITS>(acc, rec, wcb, lane, x4, M.g_log2, M.sg_log2);
         Z.zeros = reinterpret_cast<const uint32_t*>(rec + 16 * Fmt<BITS>::NV * wcb);
         Z.xs = xs + lr;
         Z.xz = xz + lr;
         Z.grow = q * 4;
         gemv::quad_zero(zacc, Z, lane);
       }
+      __syncwarp();
+      if (lane == 0) gemv::mbar_arrive(empty + st);
     }
-    __syncwarp();
-    if (lane == 0) gemv::mbar_arrive(empty + st);
-  }
-  float ztot = 0.f;
-  if (QUANT) {  // per-group totals, then the lane's own group
     if (Z.mode == 0)
       for (int o = Z.zpr; o < 32; o <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, o);
     ztot = __shfl_sync(0xffffffffu, zacc, (lane * WC) >> M.g_log2);
@@ -388,6 +411,81 @@ __global__ void __launch_bounds__(256) k_attention(AttnParams P) {
     for (int t = 0; t < T; ++t)
       a = fmaf(sc[t], __ldcg(P.vc + (size_t)t * P.H * hd + (size_t)h * hd + i), a);
     P.ctx[h * hd + i] = a;
+  }
+}
+
+// Fast path for head_dim % 128 == 0: 4 warps per head, float4 lanes; the
+// current k/v row is appended first, then scores, softmax, alpha @ V.
+__global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
+  extern __shared__ float sc[];  // [T_max]
+  __shared__ float red[4];
+  __shared__ float bval;
+  const int HD = P.hd, h = blockIdx.x, d = P.d, nc = P.hd / 128;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  gemv::pdl_trigger();
+  gemv::pdl_wait();
+  const int pos = P.ds ? P.ds->pos : P.pos;
+  const int T = pos + 1;
+  const size_t rstride = (size_t)P.H * HD;
+  const float* qg = P.qkv_part + (size_t)h * HD;
+  const float* kg = qg + d;
+  const float* vg = qg + 2 * d;
+  float* krow = P.kc + (size_t)pos * rstride + (size_t)h * HD;
+  float* vrow = P.vc + (size_t)pos * rstride + (size_t)h * HD;
+  for (int i = tid; i < HD; i += 128) {  // KV append (model.py:293, KVCache.append)
+    krow[i] = __ldcg(kg + i);
+    vrow[i] = __ldcg(vg + i);
+  }
+  __syncthreads();
+  const float rs = sqrtf((float)HD);
+  for (int t = warp; t < T; t += 4) {
+    const float* kr = P.kc + (size_t)t * rstride + (size_t)h * HD;
+    float a = 0.f;
+    for (int c = 0; c < nc; ++c) {
+      const float4 qv = __ldcg(reinterpret_cast<const float4*>(qg + 128 * c) + lane);
+      const float4 kv = __ldcg(reinterpret_cast<const float4*>(kr + 128 * c) + lane);
+      a = fmaf(qv.x, kv.x, a);
+      a = fmaf(qv.y, kv.y, a);
+      a = fmaf(qv.z, kv.z, a);
+      a = fmaf(qv.w, kv.w, a);
+    }
+    a = warp_sum(a);
+    if (lane == 0) sc[t] = __fdiv_rn(a, rs);
+  }
+  __syncthreads();
+  float mx = -INFINITY;
+  for (int t = tid; t < T; t += 128) mx = fmaxf(mx, sc[t]);
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) bval = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  mx = bval;
+  float su = 0.f;
+  for (int t = tid; t < T; t += 128) {
+    const float e = expf(__fsub_rn(sc[t], mx));
+    sc[t] = e;
+    su += e;
+  }
+  su = warp_sum(su);
+  __syncthreads();
+  if (lane == 0) red[warp] = su;
+  __syncthreads();
+  if (tid == 0) bval = ((red[0] + red[1]) + red[2]) + red[3];
+  __syncthreads();
+  su = bval;
+  for (int t = tid; t < T; t += 128) sc[t] = __fdiv_rn(sc[t], su);
+  __syncthreads();
+  for (int i = tid; i < HD; i += 128) {
+    const float* vcol = P.vc + (size_t)h * HD + i;
+    float a0 = 0.f, a1 = 0.f;
+    int t = 0;
+    for (; t + 1 < T; t += 2) {
+      a0 = fmaf(sc[t], __ldcg(vcol + (size_t)t * rstride), a0);
+      a1 = fmaf(sc[t + 1], __ldcg(vcol + (size_t)(t + 1) * rstride), a1);
+    }
+    if (t < T) a0 = fmaf(sc[t], __ldcg(vcol + (size_t)t * rstride), a0);
+    P.ctx[h * HD + i] = a0 + a1;
   }
 }
 
@@ -662,7 +760,8 @@ cudaError_t preload_kernels() {
                                          200 * 1024);
     if (e != cudaSuccess) return e;
   }
-  for (const void* f : {(const void*)k_embed, (const void*)k_combine}) {
+  for (const void* f : {(const void*)k_embed, (const void*)k_combine,
+                        (const void*)k_attention128}) {
     cudaError_t e2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           200 * 1024);
     if (e2 != cudaSuccess) return e2;
@@ -755,6 +854,11 @@ void launch_layernorm(const float* x, const float* g, const float* b, float* y, 
 }
 
 void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl) {
+  if (P.hd % 128 == 0 && P.S == 1) {
+    launch_small(k_attention128, dim3(P.H), dim3(128), (size_t)P.T_max * sizeof(float), s, pdl,
+                 P);
+    return;
+  }
   const size_t smem = (size_t)(P.hd + P.T_max) * sizeof(float);
   launch_small(k_attention, dim3(P.H), dim3(256), smem, s, pdl, P);
 }
