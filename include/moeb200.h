@@ -182,6 +182,12 @@ int moe_quantize_device(const float* w, int32_t rows, int32_t cols, int32_t bits
 /* y = x @ dequantize(m) through the engine's GEMV kernel (fp32 accumulate). */
 int moe_gemv_device(const moe_matrix* m, const float* x, float* y);
 
+/* GEMV microbenchmark (profiling aid): njobs K x N synthetic matrices of
+ * `bits` per launch, weight sets rotated beyond L2; average us per launch and
+ * algorithmic GB/s (reference payload bytes / time). */
+int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t iters, int32_t pdl,
+                   double* us_out, double* gbs_out);
+
 /* synthetic tensor (oracle/model.py synth_tensor) generated on device */
 int moe_synth_tensor_device(uint64_t seed, uint64_t tensor_id, int64_t count, float scale,
                             float* out);

@@ -9,7 +9,9 @@
 #include <cuda_profiler_api.h>
 #include <atomic>
 #include <chrono>
+#include <algorithm>
 #include <cmath>
+#include <deque>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -314,7 +316,8 @@ struct moe_engine {
   DecodeState* ds_dev = nullptr;        // device decode cursor
   DecodeState* ds_host = nullptr;       // pinned staging for the cursor
   const DecodeState* cur_ds = nullptr;  // non-null while enqueuing a decode token
-  std::atomic<uint64_t> copier_tail{0};
+  std::atomic<uint64_t> copier_tail{0};   // mailbox entries fully copied (serial mode)
+  size_t copy_chunk = 16u << 20;          // H2D chunk: demand copies preempt speculation
   // run-ahead bound: the host may enqueue at most `ahead` units (one layer of
   // one position) beyond the oldest unfinished one, so the launch queue never
   // fills while a kernel waits for the copy engine.
@@ -421,52 +424,117 @@ moe_engine::~moe_engine() {
 // buffer's generation into its ready flag.
 int moe_engine::run_copier() {
   cudaSetDevice(dev);
+  struct Job {
+    int buf, layer, expert;
+    uint32_t gen;
+    size_t off;
+  };
+  struct Chunk {
+    cudaEvent_t a, b;
+    int64_t bytes;
+  };
+  std::deque<Job> demand;   // MISS_LOAD (and promoted staging hits), FIFO
+  std::vector<Job> spec;    // SPECULATIVE_LOAD, newest first (LIFO)
+  std::vector<uint32_t> latest(nbuf, 0);  // newest requested generation per buffer
+  std::deque<Chunk> inflight;
   uint64_t tail = 0;
   int idle = 0;
+  auto stale = [&](const Job& j) { return j.gen != latest[j.buf]; };
+  auto get_events = [&](cudaEvent_t& a, cudaEvent_t& b) {
+    std::lock_guard<std::mutex> g(cmu);
+    if (free_events.size() < 2) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+    } else {
+      a = free_events.back();
+      free_events.pop_back();
+      b = free_events.back();
+      free_events.pop_back();
+    }
+  };
   while (!stop.load(std::memory_order_acquire)) {
+    bool work = false;
+    // 1. drain the device mailbox
     const uint64_t head = __atomic_load_n(&mb_host->head, __ATOMIC_ACQUIRE);
-    if (head == tail) {
+    while (tail < head) {
+      const CopyReq r = const_cast<const CopyReq&>(mb_host->ring[tail % MOE_MAILBOX_CAP]);
+      const int kind = (r.layer >> 24) & 0xff, layer = r.layer & 0xffffff;
+      if (debug) {
+        fprintf(stderr, "[moe-copy] req %llu kind %d buf %d key (%d,%d) gen %u\n",
+                (unsigned long long)tail, kind, r.buf, layer, r.expert, r.gen);
+        fflush(stderr);
+      }
+      if (kind == MOE_COPY_PROMOTE) {
+        for (size_t i = 0; i < spec.size(); ++i)
+          if (spec[i].buf == r.buf && spec[i].gen == r.gen) {
+            demand.push_back(spec[i]);
+            spec.erase(spec.begin() + i);
+            break;
+          }
+      } else {
+        latest[r.buf] = r.gen;
+        const Job j{r.buf, layer, r.expert, r.gen, 0};
+        if (kind == MOE_COPY_DEMAND)
+          demand.push_back(j);
+        else
+          spec.push_back(j);
+      }
+      ++tail;
+      work = true;
+    }
+    // 2. retire finished chunks
+    while (!inflight.empty() && cudaEventQuery(inflight.front().b) == cudaSuccess) {
+      std::lock_guard<std::mutex> g(cmu);
+      const Chunk& c = inflight.front();
+      copies.push_back({c.a, c.b, c.bytes});
+      inflight.pop_front();
+      work = true;
+    }
+    // 3. keep <= 2 chunks queued on the copy stream; demand before speculation;
+    //    a job whose buffer was reassigned (newer generation) is dropped
+    while (inflight.size() < 2) {
+      Job* j = nullptr;
+      bool from_demand = false;
+      while (!demand.empty() && stale(demand.front())) demand.pop_front();
+      while (!spec.empty() && stale(spec.back())) spec.pop_back();
+      if (!demand.empty()) {
+        j = &demand.front();
+        from_demand = true;
+      } else if (!spec.empty()) {
+        j = &spec.back();
+      }
+      if (!j) break;
+      const size_t bytes = std::min(copy_chunk, xbytes - j->off);
+      const uint8_t* src = arena + ((size_t)j->layer * E + j->expert) * xbytes + j->off;
+      uint8_t* dst = pool + (size_t)j->buf * slot_stride + j->off;
+      Chunk c;
+      get_events(c.a, c.b);
+      c.bytes = (int64_t)bytes;
+      cudaEventRecord(c.a, s_copy);
+      cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s_copy);
+      cudaEventRecord(c.b, s_copy);
+      j->off += bytes;
+      if (j->off == xbytes) {  // whole expert landed: publish its generation
+        write_value32()(reinterpret_cast<CUstream>(s_copy),
+                        reinterpret_cast<CUdeviceptr>(flags + j->buf), j->gen,
+                        CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (from_demand)
+          demand.pop_front();
+        else
+          spec.pop_back();
+      }
+      inflight.push_back(c);
+      work = true;
+    }
+    if (inflight.empty() && demand.empty() && spec.empty())
+      copier_tail.store(tail, std::memory_order_release);
+    if (!work) {
       if (++idle > 20000) std::this_thread::yield();
 #if defined(__x86_64__)
       __builtin_ia32_pause();
 #endif
-      continue;
-    }
-    idle = 0;
-    while (tail < head) {
-      const CopyReq r = const_cast<const CopyReq&>(mb_host->ring[tail % MOE_MAILBOX_CAP]);
-      if (debug) {
-        fprintf(stderr, "[moe-copy] req %llu buf %d key (%d,%d) gen %u\n",
-                (unsigned long long)tail, r.buf, r.layer, r.expert, r.gen);
-        fflush(stderr);
-      }
-      const uint8_t* src = arena + ((size_t)r.layer * E + r.expert) * xbytes;
-      uint8_t* dst = pool + (size_t)r.buf * slot_stride;
-      cudaEvent_t a, b;
-      {
-        std::lock_guard<std::mutex> g(cmu);
-        if (free_events.size() < 2) {
-          cudaEventCreate(&a);
-          cudaEventCreate(&b);
-        } else {
-          a = free_events.back();
-          free_events.pop_back();
-          b = free_events.back();
-          free_events.pop_back();
-        }
-      }
-      cudaEventRecord(a, s_copy);
-      cudaMemcpyAsync(dst, src, xbytes, cudaMemcpyHostToDevice, s_copy);
-      cudaEventRecord(b, s_copy);
-      write_value32()(reinterpret_cast<CUstream>(s_copy),
-                      reinterpret_cast<CUdeviceptr>(flags + r.buf), r.gen,
-                      CU_STREAM_WRITE_VALUE_DEFAULT);
-      {
-        std::lock_guard<std::mutex> g(cmu);
-        copies.push_back({a, b, (int64_t)xbytes});
-      }
-      ++tail;
-      copier_tail.store(tail, std::memory_order_release);
+    } else {
+      idle = 0;
     }
   }
   return MOE_OK;
@@ -1162,6 +1230,9 @@ int moe_finalize(moe_engine* e) {
   memset(e->mb_host, 0, sizeof(Mailbox));
   CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->mb_dev), e->mb_host, 0));
   S.mb = e->mb_dev;
+  S.flags = e->flags;
+  if (!e->sc.enabled) e->copy_chunk = e->xbytes;  // nothing to preempt: whole experts
+  if (const char* cm = getenv("MOE_COPY_CHUNK_MB")) e->copy_chunk = (size_t)atoll(cm) << 20;
   CU(cudaDeviceSynchronize());
   e->copier = std::thread([e] { e->run_copier(); });
   e->finalized = true;
@@ -1731,6 +1802,95 @@ int moe_synth_tensor_device(uint64_t seed, uint64_t tensor_id, int64_t count, fl
   CU(cudaMemcpy(out, d, count * 4, cudaMemcpyDeviceToHost));
   cudaFree(d);
   return MOE_OK;
+}
+
+// GEMV microbenchmark: `njobs` independent K x N matrices of `bits` in one
+// launch (like the expert up-projection), synthetic weights, weight sets
+// rotated so the working set exceeds L2.  Returns the average device time per
+// launch (back-to-back, PDL as requested) and the algorithmic GB/s.
+int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t iters, int32_t pdl,
+                   double* us_out, double* gbs_out) {
+  if (njobs < 1 || njobs > MOE_GEMV_MAXJOBS || iters < 1) return fail(MOE_ERR_VALUE, "bad args");
+  const Layout L = synth_layout(K, N, bits);
+  if (L.bits == 0) return fail(MOE_ERR_VALUE, "unsupported shape");
+  const size_t mbytes = L.total();
+  const size_t set_bytes = mbytes * njobs;
+  const int nsets = (int)std::max<size_t>(2, (400ull << 20) / set_bytes + 1);
+  QScratch Q;
+  int rc = qscratch_alloc(Q, (size_t)K * N);
+  if (rc) {
+    Q.release();
+    return rc;
+  }
+  std::vector<uint8_t*> mats((size_t)nsets * njobs, nullptr);
+  cudaStream_t s;
+  CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  for (size_t i = 0; i < mats.size(); ++i) {
+    Layout lo;
+    rc = synth_matrix(Q, 7, 100 + i % 8, K, N, 0.01, bits, 0, &lo, s);
+    if (rc) break;
+    CU(cudaMalloc(&mats[i], mbytes));
+    CU(cudaMemcpyAsync(mats[i], Q.tiled, mbytes, cudaMemcpyDeviceToDevice, s));
+  }
+  float *x, *part, *out;
+  int* cnt;
+  const MatDev M0 = matdev_from(L, nullptr);
+  const int qps = plan_qps(M0.ncb * njobs, M0.nqp), S = (M0.nqp + qps - 1) / qps;
+  CU(cudaMalloc(&x, (size_t)K * 4));
+  CU(cudaMalloc(&part, (size_t)njobs * S * N * 4));
+  CU(cudaMalloc(&out, (size_t)njobs * N * 4));
+  CU(cudaMalloc(&cnt, 4096 * 4));
+  CU(cudaMemset(cnt, 0, 4096 * 4));
+  launch_synth(9, 9, K, 1e-5f, 0, x, s);
+  std::vector<GLaunch> P(nsets);
+  int nblk = 0;
+  for (int t = 0; t < nsets; ++t) {
+    P[t] = GLaunch{};
+    P[t].nj = njobs;
+    P[t].cnt = cnt;
+    for (int j = 0; j < njobs; ++j) {
+      GJob& J = P[t].j[j];
+      J.M = matdev_from(L, mats[(size_t)t * njobs + j]);
+      J.rel_slot = -1;
+      J.xmode = X_PLAIN;
+      J.x = x;
+      J.part = part + (size_t)j * S * N;
+      J.out = out + (size_t)j * N;
+      J.QPS = qps;
+      J.S = S;
+    }
+    nblk = finalize_launch(P[t]);
+  }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int w = 0; w < 3; ++w) launch_gemv(bits, P[w % nsets], nblk, s, pdl != 0);
+  CU(cudaEventRecord(a, s));
+  for (int i = 0; i < iters; ++i) launch_gemv(bits, P[i % nsets], nblk, s, pdl != 0);
+  CU(cudaEventRecord(b, s));
+  CU(cudaEventSynchronize(b));
+  CU(cudaGetLastError());
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const double us = 1e3 * ms / iters;
+  // algorithmic bytes = reference payload bytes of the matrices
+  const double alg = (double)njobs * ((double)K * N * bits / 8 +
+                                      (bits <= 4 ? (double)K * N / L.g + 2.0 * K * N / L.sg +
+                                                       4.0 * L.nruns
+                                                 : 0.0));
+  if (us_out) *us_out = us;
+  if (gbs_out) *gbs_out = alg / (us * 1e-6) / 1e9;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  for (auto p : mats)
+    if (p) cudaFree(p);
+  cudaFree(x);
+  cudaFree(part);
+  cudaFree(out);
+  cudaFree(cnt);
+  Q.release();
+  cudaStreamDestroy(s);
+  return rc;
 }
 
 }  // extern "C"

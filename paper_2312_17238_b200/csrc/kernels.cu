@@ -98,14 +98,19 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
         M.base = P.pool + (long long)buf * P.slot_stride + reinterpret_cast<size_t>(M.base);
       }
       const uint8_t* src = M.base + cb_offset(M, cb) + (int64_t)qs * rb;
+      int st = 0;
+      uint32_t ph = 0;
       for (int it = 0; it < nit; ++it) {
-        const int st = it % nst;
-        if (it >= nst) gemv::mbar_wait(empty + st, ((it / nst) & 1) ^ 1);
+        if (it >= nst) gemv::mbar_wait(empty + st, ph ^ 1);
         const int nq = min(QS, qe - (qs + it * QS));
         const uint32_t bytes = (uint32_t)(nq * rb);
         gemv::mbar_arrive_tx(full + st, bytes);
         gemv::bulk_g2s(ring + (size_t)st * stage_bytes, src + (int64_t)it * QS * rb, bytes,
                        full + st);
+        if (++st == nst) {
+          st = 0;
+          ph ^= 1;
+        }
       }
     }
     return;
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
     const int r = row0 + i;
     float xv;
     if (J.xmode == X_PLAIN) {
-      xv = J.x[r];
+      xv = __ldcg(J.x + r);
     } else {  // SwiGLU of the up projections (model.py:223-226)
       const float a = __ldcg(J.up1 + r), b = __ldcg(J.up3 + r);
       xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
@@ -172,9 +177,10 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
                     M.g_log2 == (BITS == 2 ? 4 : 6);
   float ztot = 0.f;
   if (fast || !QUANT) {
+    int st = 0;
+    uint32_t ph = 0;
     for (int it = 0; it < nit; ++it) {
-      const int st = it % nst;
-      gemv::mbar_wait(full + st, (it / nst) & 1);
+      gemv::mbar_wait(full + st, ph);
       const int q = qs + it * QS + warp;
       if (q < qv) {
         const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)warp * rb;
@@ -191,12 +197,17 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
       }
       __syncwarp();
       if (lane == 0) gemv::mbar_arrive(empty + st);
+      if (++st == nst) {
+        st = 0;
+        ph ^= 1;
+      }
     }
     if (QUANT) ztot = gemv::zero_total_fast<BITS>(zacc, lane);
   } else {
+    int st = 0;
+    uint32_t ph = 0;
     for (int it = 0; it < nit; ++it) {
-      const int st = it % nst;
-      gemv::mbar_wait(full + st, (it / nst) & 1);
+      gemv::mbar_wait(full + st, ph);
       const int q = qs + it * QS + warp;
       if (q < qv) {
         const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)warp * rb;
@@ -211,6 +222,10 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
       }
       __syncwarp();
       if (lane == 0) gemv::mbar_arrive(empty + st);
+      if (++st == nst) {
+        st = 0;
+        ph ^= 1;
+      }
     }
     if (Z.mode == 0)
       for (int o = Z.zpr; o < 32; o <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, o);

@@ -31,8 +31,13 @@ struct DevEvent {  // layout identical to moe_event
   long long bytes;
 };
 
+// copy request kinds (packed into CopyReq::layer bits 24..31)
+#define MOE_COPY_DEMAND 0   // MISS_LOAD: the current layer waits for it
+#define MOE_COPY_SPEC 1     // SPECULATIVE_LOAD: best effort, lowest priority
+#define MOE_COPY_PROMOTE 2  // STAGING_HIT on a staged buffer whose copy may be pending
+
 struct CopyReq {
-  int buf, layer, expert;
+  int buf, layer, expert;  // layer: bits 0..23 layer, 24..31 kind
   uint32_t gen;
 };
 
@@ -75,6 +80,7 @@ struct StoreDev {
   Mailbox* mb;    // device-mapped pointer
   const unsigned char* owned;  // [L][E] or null (expert parallel subset)
   int* err;
+  const volatile uint32_t* flags;  // buffer ready generations (null: host simulator)
 };
 
 // Every store operation is __host__ __device__: the engine runs it on one GPU
@@ -138,13 +144,12 @@ MOE_HD int alloc_buf(StoreDev& S) {
 
 MOE_HD void release(StoreDev& S, int buf) { S.pending[S.scalars[2]++] = buf; }
 
-MOE_HD void issue_copy(StoreDev& S, int buf, int l, int e) {
-  const uint32_t g = ++S.gen[buf];
+MOE_HD void post(StoreDev& S, int buf, int l, int e, uint32_t g, int kind) {
   Mailbox* mb = S.mb;
   const unsigned long long h = mb->head;
   CopyReq r;
   r.buf = buf;
-  r.layer = l;
+  r.layer = l | (kind << 24);
   r.expert = e;
   r.gen = g;
   volatile int* dst = reinterpret_cast<volatile int*>(&mb->ring[h % MOE_MAILBOX_CAP]);
@@ -155,6 +160,10 @@ MOE_HD void issue_copy(StoreDev& S, int buf, int l, int e) {
   fence_system();
   mb->head = h + 1;
   fence_system();
+}
+
+MOE_HD void issue_copy(StoreDev& S, int buf, int l, int e, int kind) {
+  post(S, buf, l, e, ++S.gen[buf], kind);
 }
 
 MOE_HD int lru_find(const StoreDev& S, int l, int e) {
@@ -213,6 +222,9 @@ MOE_HD int acquire(StoreDev& S, int l, int e, int pos) {
   if (s >= 0) {
     emit(S, MOE_EV_STAGING_HIT, l, e, pos, false);
     const int buf = S.stg_buf[s];
+    // the speculative copy may still be queued behind demand copies: promote it
+    if (S.flags == nullptr || (int)(S.flags[buf] - S.gen[buf]) < 0)
+      post(S, buf, l, e, S.gen[buf], MOE_COPY_PROMOTE);
     S.stg_layer[s] = -1;
     S.stg_exp[s] = -1;
     if (S.k > 0) {
@@ -225,7 +237,7 @@ MOE_HD int acquire(StoreDev& S, int l, int e, int pos) {
   }
   emit(S, MOE_EV_MISS_LOAD, l, e, pos, true);
   const int buf = alloc_buf(S);
-  issue_copy(S, buf, l, e);
+  issue_copy(S, buf, l, e, MOE_COPY_DEMAND);
   if (S.k > 0)
     make_resident(S, l, e, buf, pos);
   else
@@ -256,7 +268,7 @@ MOE_HD void speculative_load(StoreDev& S, int tl, const int* es, int m, int pos,
       release(S, S.stg_buf[slot]);
     }
     const int buf = alloc_buf(S);
-    issue_copy(S, buf, tl, e);
+    issue_copy(S, buf, tl, e, MOE_COPY_SPEC);
     S.stg_layer[slot] = tl;
     S.stg_exp[slot] = e;
     S.stg_stamp[slot] = S.scalars[0]++;

@@ -25,8 +25,11 @@ struct moe_store_sim {
   void drain() {
     while (tail < mb->head) {
       const CopyReq& r = mb->ring[tail % MOE_MAILBOX_CAP];
-      content[r.buf] = r.layer * S.E + r.expert;
-      ++copies;
+      const int kind = (r.layer >> 24) & 0xff, layer = r.layer & 0xffffff;
+      if (kind != MOE_COPY_PROMOTE) {
+        content[r.buf] = layer * S.E + r.expert;
+        ++copies;
+      }
       ++tail;
     }
   }
