@@ -1748,6 +1748,7 @@ int moe_quantize_device(const float* w, int32_t rows, int32_t cols, int32_t bits
 }
 
 int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
+  CU(preload_kernels());
   Layout L;
   int rc = make_layout(m, &L, "gemv");
   if (rc) return rc;
@@ -1811,6 +1812,8 @@ int moe_synth_tensor_device(uint64_t seed, uint64_t tensor_id, int64_t count, fl
 int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t iters, int32_t pdl,
                    double* us_out, double* gbs_out) {
   if (njobs < 1 || njobs > MOE_GEMV_MAXJOBS || iters < 1) return fail(MOE_ERR_VALUE, "bad args");
+  CU(preload_kernels());
+  CU(preload_tile_kernels());
   const Layout L = synth_layout(K, N, bits);
   if (L.bits == 0) return fail(MOE_ERR_VALUE, "unsupported shape");
   const size_t mbytes = L.total();

@@ -123,6 +123,9 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
     const int buf = P.route->buf[J.rel_slot];
     M.zmeta = reinterpret_cast<const __half2*>(P.pool + (long long)buf * P.slot_stride +
                                                reinterpret_cast<size_t>(M.zmeta));
+    // the prologue reads this buffer's zero-point metadata: wait for the copy too
+    if (threadIdx.x == 0) wait_flag(P.flags + buf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   }
   const int qv = min(qe, M.nquads);  // real quads of this split
   const int row0 = qs * 4, nrows = max(qv - qs, 0) * 4;
