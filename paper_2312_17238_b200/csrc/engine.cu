@@ -1835,6 +1835,9 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
     CU(cudaMalloc(&mats[i], mbytes));
     CU(cudaMemcpyAsync(mats[i], Q.tiled, mbytes, cudaMemcpyDeviceToDevice, s));
   }
+  CU(cudaStreamSynchronize(s));
+  CU(cudaGetLastError());
+  if (rc) return rc;
   float *x, *part, *out;
   int* cnt;
   const MatDev M0 = matdev_from(L, nullptr);
@@ -1867,6 +1870,17 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
+  CU(cudaStreamSynchronize(s));
+  CU(cudaGetLastError());
+  launch_gemv(bits, P[0], nblk, s, pdl != 0);
+  {
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess)
+      return fail(MOE_ERR_CUDA, std::string("gemv launch (grid ") + std::to_string(nblk) +
+                                    ", smem " + std::to_string(gemv_smem_bytes(
+                                        bits, qps * 4, M0.rb_full, nullptr, nullptr)) +
+                                    "): " + cudaGetErrorString(le));
+  }
   for (int w = 0; w < 3; ++w) launch_gemv(bits, P[w % nsets], nblk, s, pdl != 0);
   CU(cudaEventRecord(a, s));
   for (int i = 0; i < iters; ++i) launch_gemv(bits, P[i % nsets], nblk, s, pdl != 0);

@@ -41,8 +41,12 @@ MOE_DEV void ffma_pair(float& a0, float& a1, float x, float m0, float m1) {
 }
 
 // 16 two-bit codes of one row-chunk word
+// Right shifts as IMAD.HI: they issue on the FMA pipe, leaving the ALU pipe
+// (rt 2 cycles / warp instruction, like the FMA pipe) to the code masks.
+MOE_DEV uint32_t shr_fma(uint32_t v, int s) { return __umulhi(v, 1u << (32 - s)); }
+
 MOE_DEV void fma_codes2(float (&acc)[16], float xs, uint32_t w) {
-  const uint32_t wh = w >> 16;
+  const uint32_t wh = shr_fma(w, 16);
   float m[16];
 #pragma unroll
   for (int k = 0; k < 12; ++k) m[k] = fbits(w & (3u << (2 * k)));
@@ -54,7 +58,7 @@ MOE_DEV void fma_codes2(float (&acc)[16], float xs, uint32_t w) {
 
 // 8 four-bit codes
 MOE_DEV void fma_codes4(float (&acc)[8], float xs, uint32_t w) {
-  const uint32_t wh = w >> 16;
+  const uint32_t wh = shr_fma(w, 16);
   float m[8];
 #pragma unroll
   for (int k = 0; k < 6; ++k) m[k] = fbits(w & (15u << (4 * k)));
@@ -67,12 +71,13 @@ MOE_DEV void fma_codes4(float (&acc)[8], float xs, uint32_t w) {
 // 32 three-bit codes = 96 bits = 3 words of the reference LE bitstream.
 // Funnel shifts realign codes 10..19 and 20..29 to 3k positions.
 MOE_DEV void fma_codes3(float (&acc)[32], float xs, uint32_t w0, uint32_t w1, uint32_t w2) {
-  const uint32_t v[3] = {w0, __funnelshift_r(w0, w1, 30), __funnelshift_r(w1, w2, 28)};
-  const uint32_t v3 = w2 >> 26;
+  // funnel shifts as (lo >> s) + hi * 2^(32-s), all on the FMA pipe
+  const uint32_t v[3] = {w0, shr_fma(w0, 30) + w1 * 4u, shr_fma(w1, 28) + w2 * 16u};
+  const uint32_t v3 = shr_fma(w2, 26);
   float m[32];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const uint32_t u = v[i] >> 12;
+    const uint32_t u = shr_fma(v[i], 12);
 #pragma unroll
     for (int k = 0; k < 8; ++k) m[10 * i + k] = fbits(v[i] & (7u << (3 * k)));
     m[10 * i + 8] = fbits(u & (7u << 12));
