@@ -218,6 +218,13 @@ int moe_store_sim_state(moe_store_sim* s, int32_t* lru_out, int32_t* staged_out,
                         int32_t* content_out, int32_t* res_buf_out, int32_t* stg_buf_out,
                         int32_t* nbuf_out);
 int64_t moe_store_sim_copies(moe_store_sim* s);
+/* simulate the engine's copy-engine policy (copy_sched.h): expert jobs of
+ * job_bytes in chunks of chunk_bytes (0 = whole), `progress` chunks executed
+ * after each bookkeeping call before the GEMVs pull their buffers; a routed
+ * buffer that can never be published returns MOE_ERR_TIMEOUT (deadlock) */
+int moe_store_sim_copy_policy(moe_store_sim* s, int64_t job_bytes, int64_t chunk_bytes,
+                              int32_t progress);
+int64_t moe_store_sim_chunks(moe_store_sim* s);
 const char* moe_store_sim_last_error(void);
 int moe_store_sim_destroy(moe_store_sim* s);
 

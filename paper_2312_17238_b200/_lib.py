@@ -99,6 +99,8 @@ SIGNATURES = {
     "moe_store_sim_events": (I32, [P, C.POINTER(Event), I64]),
     "moe_store_sim_state": (I32, [P, IP, IP, IP, IP, IP, IP]),
     "moe_store_sim_copies": (I64, [P]),
+    "moe_store_sim_copy_policy": (I32, [P, I64, I64, I32]),
+    "moe_store_sim_chunks": (I64, [P]),
     "moe_store_sim_last_error": (C.c_char_p, []),
     "moe_store_sim_destroy": (I32, [P]),
 }

@@ -1,0 +1,91 @@
+// Copy-engine scheduling policy (host side), shared by the engine's copier
+// thread and the CPU store simulator so the policy is unit-testable.
+//
+// Requests come from the device store through the mailbox (store_dev.cuh):
+//   DEMAND  (MISS_LOAD)         the current layer's GEMVs wait for it
+//   SPEC    (SPECULATIVE_LOAD)  best effort
+//   PROMOTE (STAGING_HIT)       a staged buffer is needed now
+// Policy: demand jobs first (FIFO), then speculative jobs newest-first; a
+// promoted speculative job joins the demand queue.  Jobs are split into
+// chunks so a demand copy waits at most one chunk behind speculation.  A job
+// whose buffer has since been re-requested with a newer generation is stale
+// (its staging entry was replaced and the buffer reassigned) and is dropped.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <deque>
+#include <vector>
+
+struct CopySched {
+  struct Job {
+    int buf, layer, expert;
+    uint32_t gen;
+    size_t off;
+  };
+  struct Chunk {
+    int buf, layer, expert;
+    uint32_t gen;
+    size_t off, bytes;
+    bool last;  // the job is complete after this chunk: publish `gen`
+  };
+  std::deque<Job> demand;
+  std::vector<Job> spec;
+  std::vector<uint32_t> latest;
+  size_t xbytes = 0, chunk = 0;
+
+  void init(int nbuf, size_t job_bytes, size_t chunk_bytes) {
+    latest.assign(nbuf, 0u);
+    xbytes = job_bytes;
+    chunk = chunk_bytes ? chunk_bytes : job_bytes;
+    demand.clear();
+    spec.clear();
+  }
+
+  // kind: 0 demand, 1 speculative, 2 promote (store_dev.cuh MOE_COPY_*)
+  void on_request(int kind, int buf, int layer, int expert, uint32_t gen) {
+    if (kind == 2) {
+      for (size_t i = 0; i < spec.size(); ++i)
+        if (spec[i].buf == buf && spec[i].gen == gen) {
+          demand.push_back(spec[i]);
+          spec.erase(spec.begin() + (long)i);
+          break;
+        }
+      return;
+    }
+    latest[buf] = gen;
+    const Job j{buf, layer, expert, gen, 0};
+    if (kind == 0)
+      demand.push_back(j);
+    else
+      spec.push_back(j);
+  }
+
+  bool stale(const Job& j) const { return j.gen != latest[j.buf]; }
+
+  bool empty() const { return demand.empty() && spec.empty(); }
+
+  // next chunk to issue, or false when idle
+  bool next(Chunk* c) {
+    while (!demand.empty() && stale(demand.front())) demand.pop_front();
+    while (!spec.empty() && stale(spec.back())) spec.pop_back();
+    Job* j = nullptr;
+    bool from_demand = false;
+    if (!demand.empty()) {
+      j = &demand.front();
+      from_demand = true;
+    } else if (!spec.empty()) {
+      j = &spec.back();
+    }
+    if (!j) return false;
+    const size_t n = chunk < xbytes - j->off ? chunk : xbytes - j->off;
+    *c = Chunk{j->buf, j->layer, j->expert, j->gen, j->off, n, j->off + n == xbytes};
+    j->off += n;
+    if (c->last) {
+      if (from_demand)
+        demand.pop_front();
+      else
+        spec.pop_back();
+    }
+    return true;
+  }
+};

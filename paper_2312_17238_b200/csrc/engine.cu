@@ -20,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include "copy_sched.h"
 #include "kernels.cuh"
 
 namespace {
@@ -424,22 +425,15 @@ moe_engine::~moe_engine() {
 // buffer's generation into its ready flag.
 int moe_engine::run_copier() {
   cudaSetDevice(dev);
-  struct Job {
-    int buf, layer, expert;
-    uint32_t gen;
-    size_t off;
-  };
-  struct Chunk {
+  struct Inflight {
     cudaEvent_t a, b;
     int64_t bytes;
   };
-  std::deque<Job> demand;   // MISS_LOAD (and promoted staging hits), FIFO
-  std::vector<Job> spec;    // SPECULATIVE_LOAD, newest first (LIFO)
-  std::vector<uint32_t> latest(nbuf, 0);  // newest requested generation per buffer
-  std::deque<Chunk> inflight;
+  CopySched sched;
+  sched.init(nbuf, xbytes, copy_chunk);
+  std::deque<Inflight> inflight;
   uint64_t tail = 0;
   int idle = 0;
-  auto stale = [&](const Job& j) { return j.gen != latest[j.buf]; };
   auto get_events = [&](cudaEvent_t& a, cudaEvent_t& b) {
     std::lock_guard<std::mutex> g(cmu);
     if (free_events.size() < 2) {
@@ -454,7 +448,7 @@ int moe_engine::run_copier() {
   };
   while (!stop.load(std::memory_order_acquire)) {
     bool work = false;
-    // 1. drain the device mailbox
+    // 1. drain the device mailbox into the scheduler (copy_sched.h)
     const uint64_t head = __atomic_load_n(&mb_host->head, __ATOMIC_ACQUIRE);
     while (tail < head) {
       const CopyReq r = const_cast<const CopyReq&>(mb_host->ring[tail % MOE_MAILBOX_CAP]);
@@ -464,70 +458,42 @@ int moe_engine::run_copier() {
                 (unsigned long long)tail, kind, r.buf, layer, r.expert, r.gen);
         fflush(stderr);
       }
-      if (kind == MOE_COPY_PROMOTE) {
-        for (size_t i = 0; i < spec.size(); ++i)
-          if (spec[i].buf == r.buf && spec[i].gen == r.gen) {
-            demand.push_back(spec[i]);
-            spec.erase(spec.begin() + i);
-            break;
-          }
-      } else {
-        latest[r.buf] = r.gen;
-        const Job j{r.buf, layer, r.expert, r.gen, 0};
-        if (kind == MOE_COPY_DEMAND)
-          demand.push_back(j);
-        else
-          spec.push_back(j);
-      }
+      sched.on_request(kind, r.buf, layer, r.expert, r.gen);
       ++tail;
       work = true;
     }
     // 2. retire finished chunks
     while (!inflight.empty() && cudaEventQuery(inflight.front().b) == cudaSuccess) {
       std::lock_guard<std::mutex> g(cmu);
-      const Chunk& c = inflight.front();
+      const Inflight& c = inflight.front();
       copies.push_back({c.a, c.b, c.bytes});
       inflight.pop_front();
       work = true;
     }
-    // 3. keep <= 2 chunks queued on the copy stream; demand before speculation;
-    //    a job whose buffer was reassigned (newer generation) is dropped
-    while (inflight.size() < 2) {
-      Job* j = nullptr;
-      bool from_demand = false;
-      while (!demand.empty() && stale(demand.front())) demand.pop_front();
-      while (!spec.empty() && stale(spec.back())) spec.pop_back();
-      if (!demand.empty()) {
-        j = &demand.front();
-        from_demand = true;
-      } else if (!spec.empty()) {
-        j = &spec.back();
-      }
-      if (!j) break;
-      const size_t bytes = std::min(copy_chunk, xbytes - j->off);
-      const uint8_t* src = arena + ((size_t)j->layer * E + j->expert) * xbytes + j->off;
-      uint8_t* dst = pool + (size_t)j->buf * slot_stride + j->off;
-      Chunk c;
-      get_events(c.a, c.b);
-      c.bytes = (int64_t)bytes;
-      cudaEventRecord(c.a, s_copy);
-      cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s_copy);
-      cudaEventRecord(c.b, s_copy);
-      j->off += bytes;
-      if (j->off == xbytes) {  // whole expert landed: publish its generation
+    // 3. keep <= 2 chunks queued on the copy stream
+    CopySched::Chunk c;
+    while (inflight.size() < 2 && sched.next(&c)) {
+      const uint8_t* src = arena + ((size_t)c.layer * E + c.expert) * xbytes + c.off;
+      uint8_t* dst = pool + (size_t)c.buf * slot_stride + c.off;
+      Inflight f;
+      get_events(f.a, f.b);
+      f.bytes = (int64_t)c.bytes;
+      cudaEventRecord(f.a, s_copy);
+      cudaMemcpyAsync(dst, src, c.bytes, cudaMemcpyHostToDevice, s_copy);
+      cudaEventRecord(f.b, s_copy);
+      if (c.last)  // whole expert landed: publish its generation
         write_value32()(reinterpret_cast<CUstream>(s_copy),
-                        reinterpret_cast<CUdeviceptr>(flags + j->buf), j->gen,
+                        reinterpret_cast<CUdeviceptr>(flags + c.buf), c.gen,
                         CU_STREAM_WRITE_VALUE_DEFAULT);
-        if (from_demand)
-          demand.pop_front();
-        else
-          spec.pop_back();
+      if (debug) {
+        fprintf(stderr, "[moe-copy] chunk buf %d gen %u off %zu bytes %zu last %d\n", c.buf,
+                c.gen, c.off, c.bytes, (int)c.last);
+        fflush(stderr);
       }
-      inflight.push_back(c);
+      inflight.push_back(f);
       work = true;
     }
-    if (inflight.empty() && demand.empty() && spec.empty())
-      copier_tail.store(tail, std::memory_order_release);
+    if (inflight.empty() && sched.empty()) copier_tail.store(tail, std::memory_order_release);
     if (!work) {
       if (++idle > 20000) std::this_thread::yield();
 #if defined(__x86_64__)

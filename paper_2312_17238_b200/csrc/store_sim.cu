@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "copy_sched.h"
 #include "kernels.cuh"
 
 struct moe_store_sim {
@@ -18,20 +19,44 @@ struct moe_store_sim {
   std::vector<DevEvent> ev;
   std::vector<unsigned char> owned;
   std::vector<int> content;  // buffer -> layer*E + expert last copied into it
+  std::vector<uint32_t> flag;  // buffer -> last published generation (ready flag)
   Mailbox* mb = nullptr;
   unsigned long long tail = 0;
   int err = 0;
-  int64_t copies = 0;
+  int64_t copies = 0, chunks = 0;
+  // copy-engine simulation: the engine's CopySched policy; `progress` chunks
+  // run after every bookkeeping call, then the consumer (the GEMVs) pulls
+  // chunks until its buffers are ready.  A consumer that can never be
+  // satisfied is a copy-engine deadlock.
+  CopySched sched;
+  int progress = 1 << 30;  // default: every request completes immediately
   void drain() {
     while (tail < mb->head) {
       const CopyReq& r = mb->ring[tail % MOE_MAILBOX_CAP];
       const int kind = (r.layer >> 24) & 0xff, layer = r.layer & 0xffffff;
-      if (kind != MOE_COPY_PROMOTE) {
-        content[r.buf] = layer * S.E + r.expert;
-        ++copies;
-      }
+      sched.on_request(kind, r.buf, layer, r.expert, r.gen);
+      if (kind != MOE_COPY_PROMOTE) ++copies;
       ++tail;
     }
+  }
+  bool step() {  // execute one chunk
+    CopySched::Chunk c;
+    if (!sched.next(&c)) return false;
+    ++chunks;
+    if (c.last) {
+      content[c.buf] = c.layer * S.E + c.expert;
+      flag[c.buf] = c.gen;
+    }
+    return true;
+  }
+  void run(int n) {
+    for (int i = 0; i < n && step(); ++i) {
+    }
+  }
+  bool consume(int buf, uint32_t gen) {  // GEMV wait on (buf, gen)
+    while ((int)(flag[buf] - gen) < 0)
+      if (!step()) return false;
+    return true;
   }
   ~moe_store_sim() { delete mb; }
 };
@@ -79,6 +104,8 @@ int moe_store_sim_create(int32_t n_layers, int32_t n_experts, int32_t k, int32_t
   s->seq.assign(1, 0);
   s->gen.assign(nbuf, 0);
   s->content.assign(nbuf, -1);
+  s->flag.assign(nbuf, 0u);
+  s->sched.init(nbuf, 1, 1);
   s->ev.resize(1 << 20);
   if (owned) s->owned.assign(owned, owned + (size_t)L * E);
   s->mb = new Mailbox();
@@ -108,6 +135,7 @@ int moe_store_sim_create(int32_t n_layers, int32_t n_experts, int32_t k, int32_t
   S.mb = s->mb;
   S.owned = owned ? s->owned.data() : nullptr;
   S.err = &s->err;
+  S.flags = s->flag.data();
   *out = s;
   return MOE_OK;
 }
@@ -123,6 +151,10 @@ int moe_store_sim_token(moe_store_sim* s, int32_t layer, int32_t pos, const int3
   uint32_t gens[MOE_MAX_TOPK];
   store::resolve_token(s->S, layer, experts, k, guesses, m, guess_layer, pos, bufs, gens);
   s->drain();
+  s->run(s->progress);
+  for (int j = 0; j < k; ++j)
+    if (bufs[j] >= 0 && !s->consume(bufs[j], gens[j]))
+      return sfail(MOE_ERR_TIMEOUT, "copy engine deadlock: routed buffer never published");
   if (bufs_out)
     for (int j = 0; j < k; ++j) bufs_out[j] = bufs[j];
   return err_status(s);
@@ -131,12 +163,21 @@ int moe_store_sim_token(moe_store_sim* s, int32_t layer, int32_t pos, const int3
 int moe_store_sim_prefill(moe_store_sim* s, int32_t layer, const int32_t* experts, int32_t n,
                           int32_t k, int32_t* bufs_out) {
   if (!s || n < 1 || k < 1 || k > MOE_MAX_TOPK) return sfail(MOE_ERR_VALUE, "bad arguments");
+  std::vector<int> bb((size_t)n * k);
+  std::vector<uint32_t> gg((size_t)n * k);
   store::resolve_prefill(
       s->S, layer, n, k, [&](int p, int j) { return (int)experts[p * k + j]; },
-      [&](int p, int j, int b, uint32_t) {
-        if (bufs_out) bufs_out[p * k + j] = b;
+      [&](int p, int j, int b, uint32_t g) {
+        bb[p * k + j] = b;
+        gg[p * k + j] = g;
       });
   s->drain();
+  s->run(s->progress);
+  for (size_t i = 0; i < bb.size(); ++i)
+    if (bb[i] >= 0 && !s->consume(bb[i], gg[i]))
+      return sfail(MOE_ERR_TIMEOUT, "copy engine deadlock: routed buffer never published");
+  if (bufs_out)
+    for (size_t i = 0; i < bb.size(); ++i) bufs_out[i] = bb[i];
   return err_status(s);
 }
 
@@ -181,6 +222,17 @@ int moe_store_sim_state(moe_store_sim* s, int32_t* lru_out, int32_t* staged_out,
 }
 
 int64_t moe_store_sim_copies(moe_store_sim* s) { return s ? s->copies : 0; }
+
+int moe_store_sim_copy_policy(moe_store_sim* s, int64_t job_bytes, int64_t chunk_bytes,
+                              int32_t progress) {
+  if (!s || job_bytes < 1 || chunk_bytes < 0 || progress < 0)
+    return sfail(MOE_ERR_VALUE, "bad copy policy");
+  s->sched.init(s->S.nbuf, (size_t)job_bytes, (size_t)chunk_bytes);
+  s->progress = progress;
+  return MOE_OK;
+}
+
+int64_t moe_store_sim_chunks(moe_store_sim* s) { return s ? s->chunks : 0; }
 
 const char* moe_store_sim_last_error(void) { return s_err.c_str(); }
 

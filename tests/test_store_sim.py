@@ -145,3 +145,37 @@ def test_ep_rank_store_equals_oracle_on_owned_subset():
         assert rows(sim.events) == orows(ref.events)
         sim.audit()
     assert len(resolved) == len(ops) * 2 and set(resolved.values()) == {1}
+
+
+@pytest.mark.parametrize("k,b,m", [(0, 4, 2), (1, 2, 1), (2, 4, 2), (4, 4, 2), (2, 2, 2)])
+@pytest.mark.parametrize("progress", [0, 1, 3])
+def test_copy_engine_policy_never_deadlocks(k, b, m, progress):
+    """The engine's copy scheduling (copy_sched.h: demand first, speculation
+    newest-first, promotion on staging hits, stale-job dropping, chunked jobs)
+    driven by the device store's real request stream: every routed buffer is
+    eventually published with the right contents, whatever the copy progress
+    between bookkeeping calls."""
+    import ctypes as C
+
+    from paper_2312_17238_b200 import _lib
+    L, E, T = 4, 8, 30
+    rng = np.random.default_rng(17 * k + 5 * b + m + progress)
+    sim = DeviceStoreSim(L, E, CacheConfig(k, b, 4096), top_k=2, m=m)
+    assert _lib.lib().moe_store_sim_copy_policy(sim._h, 4096, 1024, progress) == 0
+    ref = ExpertStore(L, E, OCache(k, b, 4096))
+    for pos in range(T):
+        for l in range(L):
+            ex = [int(x) for x in rng.choice(E, 2, replace=False)]
+            g = [int(x) for x in rng.choice(E, m, replace=False)]
+            gl = l + 1 if l + 1 < L else -1
+            bufs = sim.resolve_token(l, pos, ex, g if gl >= 0 else [], gl)
+            for e in ex:
+                ref.acquire(l, e, pos)
+            if gl >= 0:
+                ref.speculative_load([(gl, x) for x in g], pos, current_layer=l)
+            content = sim.buffers()["content"]
+            for e, bf in zip(ex, bufs):
+                assert content[bf] == l * E + e
+    assert rows(sim.events) == orows(ref.events)
+    chunks = _lib.lib().moe_store_sim_chunks(sim._h)
+    assert chunks <= 4 * sim.copies  # stale speculative jobs may be dropped, never duplicated
