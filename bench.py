@@ -182,6 +182,45 @@ def run_b200(args, rank, world):
     _lib.check(L.moe_set_profiling(eng._h, 0))
     prof_ms_step = eng.stats()["last_call_ms"] / kp
 
+    # ---- device timeline of one token (%globaltimer spans per kernel, PDL on)
+    timeline = None
+    try:
+        eng.prefill(prompt)
+        eng.decode(2)
+        _lib.check(L.moe_timeline(eng._h, 1))
+        eng.decode(1)
+        n = C.c_int32()
+        _lib.check(L.moe_read_timeline(eng._h, None, 0, C.byref(n)))
+        buf = (C.c_uint64 * (2 * n.value))()
+        _lib.check(L.moe_read_timeline(eng._h, buf, n.value, C.byref(n)))
+        _lib.check(L.moe_timeline(eng._h, 0))
+        st = np.array(buf[0::2], dtype=np.float64)
+        en = np.array(buf[1::2], dtype=np.float64)
+        ok = (en > 0) & (st < 2 ** 63)
+        t0 = st[ok].min()
+        names = ["qkv", "attention", "wo", "tail", "expert_up", "expert_down", "combine_ln"]
+        nl = cfg["n_layers"]
+        kinds = {}
+        for i, nm in enumerate(names):
+            idx = [1 + 8 * l + i for l in range(nl)]
+            d = [(en[j] - st[j]) / 1e3 for j in idx if ok[j]]
+            if d:
+                kinds[nm] = {"avg_us": round(float(np.mean(d)), 2),
+                             "sum_us": round(float(np.sum(d)), 1)}
+        for nm, j in (("embed", 0), ("lm_head", 1 + 8 * nl), ("logits", 2 + 8 * nl)):
+            if ok[j]:
+                kinds[nm] = {"avg_us": round((en[j] - st[j]) / 1e3, 2),
+                             "sum_us": round((en[j] - st[j]) / 1e3, 1)}
+        span = (en[ok].max() - t0) / 1e3
+        timeline = {"token_span_us": round(float(span), 1),
+                    "busy_sum_us": round(float(sum(v["sum_us"] for v in kinds.values())), 1),
+                    "kernels": kinds,
+                    "how": "one decode token after the timed region, graph + PDL; per kernel "
+                           "earliest CTA start (after griddepcontrol.wait) to latest CTA end, "
+                           "%globaltimer"}
+    except Exception as ex:  # profiling aid only
+        timeline = {"error": str(ex)}
+
     # ---- e2e through the public API: host sampler, per-step H2D token + D2H logits
     e2e = None
     if not args.no_e2e:
@@ -260,7 +299,7 @@ def run_b200(args, rank, world):
         "h2d_gbs_wall": round(win["h2d_bytes"] / (ms_tot / 1e3) / 1e9, 2),
         "miss_loads_per_token": win["miss_loads"] / args.steps,
         "spec_loads_per_token": win["speculative_loads"] / args.steps,
-        "roofline": roofline, "roofline_e2e": rl_e2e, "e2e": e2e,
+        "roofline": roofline, "roofline_e2e": rl_e2e, "e2e": e2e, "timeline": timeline,
         "gpu_launches": launches, "gpu_launches_per_step": round(launches / args.steps, 1),
         "clocks": clk.summary(), "build_s": round(t_build, 1),
         "tokens": res.tokens[:8],

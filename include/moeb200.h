@@ -165,6 +165,14 @@ int moe_get_stats(moe_engine* eng, moe_stats* out);
  * counts per class [qkv, wo, expert_up, expert_down, lm_head] (5 entries). */
 int moe_set_profiling(moe_engine* eng, int32_t on);
 int moe_kernel_times(moe_engine* eng, double* ms_out, int64_t* count_out);
+/* Kernel timeline (profiling aid): on = reset the table and make every kernel
+ * record its earliest CTA start (after its programmatic-launch wait) and
+ * latest CTA end (%globaltimer ns) into slot: 0 embed, 1+8l+{0 qkv, 1 attn,
+ * 2 wo, 3 tail, 4 up, 5 down, 6 combine}, 1+8L lm_head, 2+8L logits.
+ * moe_read_timeline: out[2*i] = start, out[2*i+1] = end (cap slots). */
+int moe_timeline(moe_engine* eng, int32_t on);
+int moe_read_timeline(moe_engine* eng, uint64_t* out, int32_t cap, int32_t* n_out);
+
 /* cudaProfilerStart/Stop, so `ncu --profile-from-start off` captures only the
  * bench's timed decode region. */
 int moe_profiler_range(int32_t on);

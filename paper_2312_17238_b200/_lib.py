@@ -85,6 +85,8 @@ SIGNATURES = {
     "moe_set_profiling": (I32, [P, I32]),
     "moe_kernel_times": (I32, [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "moe_profiler_range": (I32, [I32]),
+    "moe_timeline": (I32, [P, I32]),
+    "moe_read_timeline": (I32, [P, C.POINTER(C.c_uint64), I32, C.POINTER(C.c_int32)]),
     "moe_last_error": (C.c_char_p, []),
     "moe_destroy": (I32, [P]),
     "moe_quantize_device": (I32, [FP, I32, I32, I32, I32, I32, P, P, P, P, P]),

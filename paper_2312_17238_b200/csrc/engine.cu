@@ -380,6 +380,8 @@ struct moe_engine {
   int run_tokens(int n);
   int finish_call();
   GJob dense_job(const DevMat& D, const float* x, float* part, float* out, int qps) const;
+  int site_of(int l, int kind) const { return 1 + 8 * l + kind; }  // timeline slots
+  TimelineSlot* timeline = nullptr;
 };
 
 moe_engine::~moe_engine() {
@@ -397,6 +399,10 @@ moe_engine::~moe_engine() {
   for (auto e : tok_ev)
     if (e) cudaEventDestroy(e);
   if (gexec) cudaGraphExecDestroy(gexec);
+  if (timeline) {
+    set_timeline(nullptr);
+    cudaFree(timeline);
+  }
   if (ds_host) cudaFreeHost(ds_host);
   void* ptrs[] = {wte, wpe, lm_head.mem, lnfg, lnfb, pool, flags, x, h, xn, ctx, logits,
                   qkv_part, wo_part, up_part, dn_part, lm_part, qkv_out, wo_out, up_out, dn_out,
@@ -540,6 +546,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   GLaunch q{};
   q.nj = 3;
   q.cnt = cnt;
+  q.site = site_of(l, 0);
   q.j[0] = dense_job(wq[l], xn, qkv_part, qkv_out, Q_qkv);
   q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, qkv_out + d, Q_qkv);
   q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, qkv_out + 2 * d, Q_qkv);
@@ -554,6 +561,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   a.vc = vc + (size_t)l * T * d;
   a.ctx = ctx;
   a.ds = cur_ds;
+  a.site = site_of(l, 1);
   a.pos = p;
   a.H = H;
   a.hd = hd;
@@ -564,6 +572,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   GLaunch o{};
   o.nj = 1;
   o.cnt = cnt;
+  o.site = site_of(l, 2);
   o.j[0] = dense_job(wo[l], ctx, wo_part, wo_out, Q_wo);
   prof_begin(K_WO);
   launch_gemv(attn_bits, o, finalize_launch(o), s_comp, pdl && !prof);
@@ -587,6 +596,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   t.trace_hidden = rec_hidden ? trace_hidden : nullptr;
   t.ds = cur_ds;
   t.n_layers = L;
+  t.site = site_of(l, 3);
   t.st = st;
   t.d = d;
   t.E = E;
@@ -611,7 +621,9 @@ int moe_engine::enq_experts(int l, int p) {
   u.err = err;
   u.wait_ns = wait_ns;
   u.cnt = cnt;
+  u.site = site_of(l, 4);
   GLaunch dn = u;
+  dn.site = site_of(l, 5);
   for (int j = 0; j < topk; ++j) {
     for (int m = 0; m < 2; ++m) {
       GJob& J = u.j[2 * j + m];
@@ -666,6 +678,7 @@ int moe_engine::enq_experts(int l, int p) {
   c.out = x + (size_t)p * d;
   c.d = d;
   c.top_k = topk;
+  c.site = site_of(l, 6);
   if (cur_ds) {  // decode: fuse the next LayerNorm (LN1 of l+1, or LN_f)
     c.ln_g = l + 1 < L ? ln1g[l + 1] : lnfg;
     c.ln_b = l + 1 < L ? ln1b[l + 1] : lnfb;
@@ -684,6 +697,7 @@ int moe_engine::enq_logits(int p, float* out) {
   GLaunch g{};
   g.nj = 1;
   g.cnt = cnt;
+  g.site = 1 + 8 * L;
   g.j[0] = dense_job(lm_head, xn, lm_part, out, Q_lm);
   prof_begin(K_LM);
   launch_gemv(lm_bits, g, finalize_launch(g), s_comp, pl);
@@ -699,6 +713,7 @@ int moe_engine::enq_logits(int p, float* out) {
   lp.tok_out = tok_dev;
   lp.tok_hist = tok_hist;
   lp.ds = const_cast<DecodeState*>(cur_ds);
+  lp.site = 2 + 8 * L;
   lp.err = err;
   launch_logits(lp, s_comp, pl);
   dbg("logits", -1, p);
@@ -720,6 +735,7 @@ int moe_engine::enq_token() {
   ep.ln_g = ln1g[0];
   ep.ln_b = ln1b[0];
   ep.xn = xn;
+  ep.site = 0;
   launch_embed(ep, s_comp, pdl && !prof);
   for (int l = 0; l < L; ++l) {
     enq_attention(l, 0, 0);
@@ -731,9 +747,9 @@ int moe_engine::enq_token() {
 }
 
 // n decode tokens: one graph launch per token when graphs are enabled (the
-// graph is captured on first use), else the eager launch sequence.  At most
-// two tokens are in flight so the launch queue never fills while a kernel
-// waits for the copy engine.
+// graph is captured on first use), else the eager launch sequence.  One token
+// is in flight at a time so the launch queue never fills while a kernel waits
+// for the copy engine (the copier thread must always be able to submit).
 int moe_engine::run_tokens(int n) {
   const bool graphs = use_graph && !prof && !debug && !serial_copies;
   if (!graphs) {
@@ -755,7 +771,9 @@ int moe_engine::run_tokens(int n) {
     graph_launches = launch_count() - c0;
   }
   for (int i = 0; i < n; ++i) {
-    if (i >= 2) CU(cudaEventSynchronize(tok_ev[(i - 2) % 4]));
+    // one token in flight: a graph launch never waits for queue space while a
+    // GEMV spins on a copy the copier thread still has to submit
+    if (i >= 1) CU(cudaEventSynchronize(tok_ev[(i - 1) % 4]));
     CU(cudaGraphLaunch(gexec, s_comp));
     CU(cudaEventRecord(tok_ev[i % 4], s_comp));
     launches += graph_launches;
@@ -1246,6 +1264,7 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
     ep.pos = p;
     ep.d = e->d;
     ep.x = e->x + (size_t)p * e->d;
+    ep.site = 0;
     launch_embed(ep, e->s_comp, e->pdl);
   }
   for (int l = 0; l < e->L; ++l) {
@@ -1423,6 +1442,31 @@ int moe_kernel_times(moe_engine* e, double* ms_out, int64_t* count_out) {
     if (ms_out) ms_out[i] = e->prof_ms[i];
     if (count_out) count_out[i] = e->prof_cnt[i];
   }
+  return MOE_OK;
+}
+
+int moe_timeline(moe_engine* e, int32_t on) {
+  if (!e) return fail(MOE_ERR_VALUE, "null engine");
+  cudaSetDevice(e->dev);
+  const int n = 3 + 8 * e->L;
+  if (on) {
+    if (!e->timeline) CU(cudaMalloc(&e->timeline, n * sizeof(TimelineSlot)));
+    std::vector<TimelineSlot> init(n, TimelineSlot{~0ull, 0ull});
+    CU(cudaMemcpy(e->timeline, init.data(), n * sizeof(TimelineSlot), cudaMemcpyHostToDevice));
+    CU(set_timeline(e->timeline));
+  } else {
+    CU(set_timeline(nullptr));
+  }
+  return MOE_OK;
+}
+
+int moe_read_timeline(moe_engine* e, uint64_t* out, int32_t cap, int32_t* n_out) {
+  if (!e || !e->timeline) return fail(MOE_ERR_VALUE, "timeline not enabled");
+  const int n = 3 + 8 * e->L;
+  if (n_out) *n_out = n;
+  if (out && cap > 0)
+    CU(cudaMemcpy(out, e->timeline, std::min(cap, n) * sizeof(TimelineSlot),
+                  cudaMemcpyDeviceToHost));
   return MOE_OK;
 }
 
@@ -1748,6 +1792,7 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
   J.QPS = qps;
   J.blk0 = 0;
   P.cnt = dcnt;
+  P.site = -1;
   launch_gemv(L.bits, P, M.ncb * S, 0, false);
   CU(cudaGetLastError());
   CU(cudaDeviceSynchronize());
@@ -1820,6 +1865,7 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
     P[t] = GLaunch{};
     P[t].nj = njobs;
     P[t].cnt = cnt;
+    P[t].site = -1;
     for (int j = 0; j < njobs; ++j) {
       GJob& J = P[t].j[j];
       J.M = matdev_from(L, mats[(size_t)t * njobs + j]);

@@ -12,12 +12,24 @@
 #include "kernels.cuh"
 #include "gemv.cuh"
 
+__device__ TimelineSlot* g_timeline = nullptr;
+
 namespace {
 
 MOE_DEV unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// per-CTA timeline marks (thread 0 of the CTA)
+MOE_DEV void tl_begin(int site) {
+  TimelineSlot* t = g_timeline;
+  if (t && site >= 0 && threadIdx.x == 0) atomicMin(&t[site].start, globaltimer());
+}
+MOE_DEV void tl_end(int site) {
+  TimelineSlot* t = g_timeline;
+  if (t && site >= 0 && threadIdx.x == 0) atomicMax(&t[site].end, globaltimer());
 }
 
 MOE_DEV float sigmoid_ref(float x) {  // model.py:229-235 branch-stable logistic
@@ -119,6 +131,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
   // ------------------------------------------------------------ consumers
   const int nthr = W * 32;
   gemv::pdl_wait();
+  tl_begin(P.site);
   if (J.rel_slot >= 0) {
     const int buf = P.route->buf[J.rel_slot];
     M.zmeta = reinterpret_cast<const __half2*>(P.pool + (long long)buf * P.slot_stride +
@@ -253,7 +266,10 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
       dst[(size_t)(cb * 32 + l) * WC + k] = a + zo_out;
     }
   }
-  if (J.S == 1) return;
+  if (J.S == 1) {
+    tl_end(P.site);
+    return;
+  }
   // split-K: the last CTA of this column block sums the S partials in order
   __threadfence();
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
@@ -263,7 +279,10 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
     *flag = old == J.S - 1;
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
-  if (!*flag) return;
+  if (!*flag) {
+    tl_end(P.site);
+    return;
+  }
   __threadfence();
   for (int t = threadIdx.x; t < wcb * WC; t += nthr) {
     const size_t o = (size_t)cb * 32 * WC + t;
@@ -272,6 +291,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
     J.out[o] = a;
   }
   if (threadIdx.x == 0) P.cnt[cnt_base + cb] = 0;
+  tl_end(P.site);
 }
 
 // ------------------------------------------------------------------ wait
@@ -325,6 +345,7 @@ __global__ void k_embed(EmbedParams P) {
   extern __shared__ float xsh[];
   gemv::pdl_trigger();
   gemv::pdl_wait();
+  tl_begin(P.site);
   const int tok = P.ds ? P.ds->tok : P.tok;
   const int pos = P.ds ? P.ds->pos : P.pos;
   const int step = P.xn ? blockDim.x : gridDim.x * blockDim.x;
@@ -345,6 +366,7 @@ __global__ void k_embed(EmbedParams P) {
     __syncthreads();
     layernorm_block(xsh, P.ln_g, P.ln_b, P.xn, nullptr, P.d, red);
   }
+  tl_end(P.site);
 }
 
 __global__ void __launch_bounds__(1024) k_layernorm(const float* x, const float* g, const float* b,
@@ -442,6 +464,7 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   gemv::pdl_trigger();
   gemv::pdl_wait();
+  tl_begin(P.site);
   const int pos = P.ds ? P.ds->pos : P.pos;
   const int T = pos + 1;
   const size_t rstride = (size_t)P.H * HD;
@@ -505,6 +528,7 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
     if (t < T) a0 = fmaf(sc[t], __ldcg(vcol + (size_t)t * rstride), a0);
     P.ctx[h * HD + i] = a0 + a1;
   }
+  tl_end(P.site);
 }
 
 // ------------------------------------------------------------------ tail
@@ -530,6 +554,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     if (P.gate_g) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.gate_g + i));
   }
   gemv::pdl_wait();
+  tl_begin(P.site);
   const int pos = P.ds ? P.ds->pos : P.pos;
   const size_t slot = (size_t)pos * P.n_layers + P.layer;
   float* th = P.trace_hidden ? P.trace_hidden + slot * d : nullptr;
@@ -627,6 +652,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     __syncthreads();
     store::stage_out(P.st, S);
   }
+  tl_end(P.site);
 }
 
 // prefill: each distinct expert of the layer acquired once, first-use order
@@ -654,6 +680,7 @@ __global__ void k_combine(CombineParams P) {
   extern __shared__ float osh[];
   gemv::pdl_trigger();
   gemv::pdl_wait();
+  tl_begin(P.site);
   const int step = P.xn ? blockDim.x : gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.d; i += step) {
     float out = P.h[i];
@@ -669,6 +696,7 @@ __global__ void k_combine(CombineParams P) {
     __syncthreads();
     layernorm_block(osh, P.ln_g, P.ln_b, P.xn, nullptr, P.d, red);
   }
+  tl_end(P.site);
 }
 
 // logits = sum of lm_head partials; non-finite check (model.py:308-309);
@@ -679,6 +707,7 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
   __shared__ bool last;
   gemv::pdl_trigger();
   gemv::pdl_wait();
+  tl_begin(P.site);
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   float val = -INFINITY;
   int idx = 0x7fffffff;
@@ -712,7 +741,10 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
     last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!last) return;
+  if (!last) {
+    tl_end(P.site);
+    return;
+  }
   __threadfence();
   float best = -INFINITY;
   int besti = 0x7fffffff;
@@ -750,12 +782,17 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
     }
     *P.counter = 0u;
   }
+  tl_end(P.site);
 }
 
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
 static std::atomic<long long> g_launches{0};
+
+cudaError_t set_timeline(TimelineSlot* table) {
+  return cudaMemcpyToSymbol(g_timeline, &table, sizeof(table));
+}
 long long launch_count() { return g_launches.load(); }
 
 // Loads every kernel and sets its shared-memory limit while the GPU is idle.

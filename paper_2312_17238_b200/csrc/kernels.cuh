@@ -34,6 +34,7 @@ struct GLaunch {
   int* cnt;                     // split-K arrival counters [sum of ncb] (zero between launches)
   int* err;
   unsigned long long wait_ns;
+  int site;  // timeline slot of this launch (profiling), -1 none
 };
 
 // Device-resident decode cursor: the kernels of one decode token read the
@@ -54,6 +55,7 @@ struct AttnParams {
   float* ctx;             // [d]
   const DecodeState* ds;  // decode: position from here (else `pos`)
   int pos, H, hd, d, T_max;
+  int site;  // timeline slot of this launch (profiling), -1 none
 };
 
 struct TailParams {
@@ -73,6 +75,7 @@ struct TailParams {
   StoreDev st;
   int d, E, top_k, m, layer, guess_layer, pos, mode;  // mode 0 decode, 1 prefill (no store)
   int ep_rank, ep_size;   // expert parallel (ep_size 1 = off)
+  int site;  // timeline slot of this launch (profiling), -1 none
 };
 
 struct PrefillBKParams {
@@ -93,6 +96,7 @@ struct CombineParams {
   const float* ln_g;
   const float* ln_b;
   float* xn;
+  int site;  // timeline slot of this launch (profiling), -1 none
 };
 
 struct LogitsParams {
@@ -106,6 +110,7 @@ struct LogitsParams {
   int* tok_hist;      // decode: argmax history, slot ds->step
   DecodeState* ds;    // decode: advanced (tok, step, pos) by the last block
   int* err;
+  int site;  // timeline slot of this launch (profiling), -1 none
 };
 
 struct EmbedParams {
@@ -118,7 +123,16 @@ struct EmbedParams {
   const float* ln_g;      // optional fused LN1 of layer 0 (one CTA): xn = LN(x)
   const float* ln_b;
   float* xn;
+  int site;  // timeline slot of this launch (profiling), -1 none
 };
+
+// Kernel timeline (profiling): when enabled, every kernel records the
+// earliest CTA start and the latest CTA end (%globaltimer, ns) into slot
+// `site` of a device table; with PDL the spans overlap like the real run.
+struct TimelineSlot {
+  unsigned long long start, end;
+};
+cudaError_t set_timeline(TimelineSlot* table);  // null disables
 
 // launchers (kernels.cu)
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
