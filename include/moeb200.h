@@ -160,6 +160,17 @@ int moe_device_state(moe_engine* eng, int32_t* lru_out, int32_t* staged_out);
 
 int moe_get_stats(moe_engine* eng, moe_stats* out);
 
+/* Expert parallel over N GPUs; no reference counterpart (the
+ * reference is single-process).  configure: before any expert is loaded; this
+ * rank then owns experts e with e*world/E == rank in every layer (its arena,
+ * cache and store, store.py restricted to the owned keys).  After finalize,
+ * exchange every rank's 64-byte handle (moe_ep_handle) and moe_ep_connect
+ * with all of them, in rank order: the per-layer slot exchange then runs
+ * over peer memory (NVLink P2P / CUDA IPC) inside the decode graph. */
+int moe_ep_configure(moe_engine* eng, int32_t rank, int32_t world);
+int moe_ep_handle(moe_engine* eng, void* out64);
+int moe_ep_connect(moe_engine* eng, const void* handles);
+
 /* Profiling: when on, every GEMV launch is bracketed by CUDA events on the
  * compute stream; moe_kernel_times returns summed milliseconds and launch
  * counts per class [qkv, wo, expert_up, expert_down, lm_head] (5 entries). */

@@ -82,6 +82,9 @@ SIGNATURES = {
     "moe_reset_session": (I32, [P]),
     "moe_device_state": (I32, [P, IP, IP]),
     "moe_get_stats": (I32, [P, C.POINTER(Stats)]),
+    "moe_ep_configure": (I32, [P, I32, I32]),
+    "moe_ep_handle": (I32, [P, C.c_void_p]),
+    "moe_ep_connect": (I32, [P, C.c_void_p]),
     "moe_set_profiling": (I32, [P, I32]),
     "moe_kernel_times": (I32, [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "moe_profiler_range": (I32, [I32]),

@@ -257,6 +257,21 @@ struct moe_engine {
   size_t xoff[3][4] = {};  // per matrix: rec, scales, zeros, zmeta offsets in a buffer
   size_t xbytes = 0, slot_stride = 0;
   uint8_t* arena = nullptr;
+  // expert parallel (moe_ep_configure): this rank owns experts e with
+  // e * world / E == rank in every layer; the arena holds only those
+  int ep_rank = 0, ep_world = 1;
+  std::vector<int> arena_idx;          // layer*E + expert -> arena slot, -1 not owned
+  int n_owned = 0;
+  uint8_t* owned_dev = nullptr;        // [L][E] mask for the device store
+  uint8_t* xch = nullptr;              // exchange block: recv [2][topk][N][d] f32, flags [N], seq
+  float* xrecv = nullptr;
+  unsigned long long *xflag = nullptr, *xseq = nullptr;
+  float* peer_recv[MOE_EP_MAX] = {};
+  unsigned long long* peer_flag[MOE_EP_MAX] = {};
+  std::vector<void*> ipc_opened;
+  bool ep_connected = false;
+  size_t arena_off(int l, int x) const { return (size_t)arena_idx[(size_t)l * E + x] * xbytes; }
+  bool owns(int l, int x) const { return arena_idx[(size_t)l * E + x] >= 0; }
   std::vector<bool> loaded;
   uint8_t* pool = nullptr;
   uint32_t* flags = nullptr;
@@ -308,6 +323,7 @@ struct moe_engine {
   unsigned long long wait_ns = 60000000000ull;
   bool debug = false;
   bool serial_copies = false;  // MOE_SERIAL_COPIES=1
+  bool trace_copies = false;   // MOE_COPY_TRACE=1: copier log on stderr
   bool pdl = true;             // programmatic dependent launch (MOE_PDL=0 disables)
   bool use_graph = true;       // one CUDA graph per decode token (MOE_GRAPH=0 disables)
   bool capturing = false;
@@ -418,6 +434,9 @@ moe_engine::~moe_engine() {
     for (auto p : *v)
       if (p) cudaFree(p);
   if (arena) cudaFreeHost(arena);
+  for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+  if (owned_dev) cudaFree(owned_dev);
+  if (xch) cudaFree(xch);
   if (mb_host) cudaFreeHost(mb_host);
   if (t0) cudaEventDestroy(t0);
   if (t1) cudaEventDestroy(t1);
@@ -459,7 +478,7 @@ int moe_engine::run_copier() {
     while (tail < head) {
       const CopyReq r = const_cast<const CopyReq&>(mb_host->ring[tail % MOE_MAILBOX_CAP]);
       const int kind = (r.layer >> 24) & 0xff, layer = r.layer & 0xffffff;
-      if (debug) {
+      if (debug || trace_copies) {
         fprintf(stderr, "[moe-copy] req %llu kind %d buf %d key (%d,%d) gen %u\n",
                 (unsigned long long)tail, kind, r.buf, layer, r.expert, r.gen);
         fflush(stderr);
@@ -479,7 +498,7 @@ int moe_engine::run_copier() {
     // 3. keep <= 2 chunks queued on the copy stream
     CopySched::Chunk c;
     while (inflight.size() < 2 && sched.next(&c)) {
-      const uint8_t* src = arena + ((size_t)c.layer * E + c.expert) * xbytes + c.off;
+      const uint8_t* src = arena + arena_off(c.layer, c.expert) + c.off;
       uint8_t* dst = pool + (size_t)c.buf * slot_stride + c.off;
       Inflight f;
       get_events(f.a, f.b);
@@ -491,7 +510,7 @@ int moe_engine::run_copier() {
         write_value32()(reinterpret_cast<CUstream>(s_copy),
                         reinterpret_cast<CUdeviceptr>(flags + c.buf), c.gen,
                         CU_STREAM_WRITE_VALUE_DEFAULT);
-      if (debug) {
+      if (debug || trace_copies) {
         fprintf(stderr, "[moe-copy] chunk buf %d gen %u off %zu bytes %zu last %d\n", c.buf,
                 c.gen, c.off, c.bytes, (int)c.last);
         fflush(stderr);
@@ -674,6 +693,28 @@ int moe_engine::enq_experts(int l, int p) {
   c.h = h + (size_t)p * d;
   c.part = dn_out;
   c.S = 1;
+  if (ep_world > 1) {  // sum-exchange of the slot buffers over peer memory
+    ExchangeParams xp{};
+    xp.src = dn_out;
+    for (int r = 0; r < ep_world; ++r) {
+      xp.recv[r] = peer_recv[r];
+      xp.flag[r] = peer_flag[r];
+    }
+    xp.seq = xseq;
+    xp.my_flag = xflag;
+    xp.rank = ep_rank;
+    xp.N = ep_world;
+    xp.top_k = topk;
+    xp.d = d;
+    xp.err = err;
+    xp.wait_ns = wait_ns;
+    xp.site = site_of(l, 7);
+    launch_exchange(xp, s_comp, pdl && !prof);
+    c.part = xrecv;
+    c.S = ep_world;
+    c.ep_seq = xseq;
+    c.ep_slab = (long long)topk * ep_world * d;
+  }
   c.route = route + p;
   c.out = x + (size_t)p * d;
   c.d = d;
@@ -830,7 +871,16 @@ int moe_engine::finish_call() {
     CU(cudaMemcpy(events.data() + old, st.ev, nev * sizeof(moe_event), cudaMemcpyDeviceToHost));
     CU(cudaMemset(st.scalars + 3, 0, sizeof(int)));
   }
-  if (e & MOE_ERRF_TIMEOUT) return fail(MOE_ERR_TIMEOUT, "expert buffer never became ready");
+  if (e & MOE_ERRF_TIMEOUT) {
+    int diag[8] = {0};
+    cudaMemcpy(diag, err, sizeof(diag), cudaMemcpyDeviceToHost);
+    const int buf = (int)(((uintptr_t)diag[4] - ((uintptr_t)flags & 0x7fffffff)) / 4);
+    cudaMemset(err, 0, sizeof(diag));
+    return fail(MOE_ERR_TIMEOUT, "expert buffer never became ready (buffer " +
+                                     std::to_string(buf) + " waiting for generation " +
+                                     std::to_string(diag[2]) + ", flag " +
+                                     std::to_string(diag[3]) + ")");
+  }
   if (e & (MOE_ERRF_ALLOC | MOE_ERRF_EVENTS))
     return fail(MOE_ERR_RUNTIME, "device store overflow (buffers or event log)");
   if (e & MOE_ERRF_UNKNOWN) return fail(MOE_ERR_UNKNOWN_EXPERT, "no such expert");
@@ -873,6 +923,7 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   e->rec_hidden = record_hidden != 0;
   if (const char* dbgv = getenv("MOE_DEBUG")) e->debug = atoi(dbgv) != 0;
   if (const char* sv = getenv("MOE_SERIAL_COPIES")) e->serial_copies = atoi(sv) != 0;
+  if (const char* tv = getenv("MOE_COPY_TRACE")) e->trace_copies = atoi(tv) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
   for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
@@ -915,6 +966,9 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   e->ln2b.assign(L, nullptr);
   e->gate.assign(L, nullptr);
   e->loaded.assign((size_t)L * e->E, false);
+  e->arena_idx.resize((size_t)L * e->E);
+  for (size_t i = 0; i < e->arena_idx.size(); ++i) e->arena_idx[i] = (int)i;
+  e->n_owned = L * e->E;
   *out = e;
   return MOE_OK;
 }
@@ -1052,7 +1106,7 @@ static int set_expert_layout(moe_engine* e, const moe_matrix* ms[3]) {
   e->slot_stride = (off + 255) & ~size_t(255);
   e->expert_bits = lo[0].bits;
   e->xl_set = true;
-  const size_t arena = e->xbytes * (size_t)e->L * e->E;
+  const size_t arena = e->xbytes * (size_t)e->n_owned;
   CU(cudaHostAlloc(&e->arena, arena, cudaHostAllocPortable));
   return MOE_OK;
 }
@@ -1066,6 +1120,7 @@ int moe_load_expert(moe_engine* e, int32_t layer, int32_t expert, const moe_matr
   const moe_matrix* ms[3] = {w1, w3, w2};
   int rc = set_expert_layout(e, ms);
   if (rc) return rc;
+  if (!e->owns(layer, expert)) return MOE_OK;  // expert parallel: another rank's expert
   uint8_t* tmp = nullptr;
   CU(cudaMalloc(&tmp, e->xbytes + 256));
   for (int i = 0; i < 3; ++i) {
@@ -1088,7 +1143,7 @@ int moe_load_expert(moe_engine* e, int32_t layer, int32_t expert, const moe_matr
     if (rc) break;
   }
   if (!rc) {
-    CU(cudaMemcpy(e->arena + ((size_t)layer * e->E + expert) * e->xbytes, tmp, e->xbytes,
+    CU(cudaMemcpy(e->arena + e->arena_off(layer, expert), tmp, e->xbytes,
                   cudaMemcpyDeviceToHost));
     e->loaded[(size_t)layer * e->E + expert] = true;
   }
@@ -1108,7 +1163,8 @@ int moe_finalize(moe_engine* e) {
         !e->ln1b[l] || !e->ln2g[l] || !e->ln2b[l] || !e->gate[l])
       return fail(MOE_ERR_VALUE, "missing tensors of layer " + std::to_string(l));
   for (size_t i = 0; i < e->loaded.size(); ++i)
-    if (!e->loaded[i]) return fail(MOE_ERR_UNKNOWN_EXPERT, "expert payload missing");
+    if (!e->loaded[i] && e->arena_idx[i] >= 0)
+      return fail(MOE_ERR_UNKNOWN_EXPERT, "expert payload missing");
   const int k = e->cc.k, b = e->cc.b;
   e->nbuf = L * k + b + E + k + e->sc.m + 2;
   CU(cudaMalloc(&e->pool, e->slot_stride * (size_t)e->nbuf));
@@ -1154,7 +1210,7 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->cand_val, nblk))) return rc;
   if ((rc = e->dalloc(&e->cand_idx, nblk))) return rc;
   if ((rc = e->dalloc(&e->counter, 1))) return rc;
-  if ((rc = e->dalloc(&e->err, 1))) return rc;
+  if ((rc = e->dalloc(&e->err, 8))) return rc;
   if ((rc = e->dalloc(&e->ds_dev, 1))) return rc;
   CU(cudaHostAlloc(&e->ds_host, sizeof(DecodeState), cudaHostAllocDefault));
   // device store state
@@ -1209,6 +1265,21 @@ int moe_finalize(moe_engine* e) {
     const int sc4[4] = {0, e->nbuf, 0, 0};
     CU(cudaMemcpy(S.scalars, sc4, 16, cudaMemcpyHostToDevice));
   }
+  if (e->ep_world > 1) {  // expert parallel: owned mask + exchange block
+    std::vector<uint8_t> own((size_t)L * E);
+    for (size_t i = 0; i < own.size(); ++i) own[i] = e->arena_idx[i] >= 0;
+    CU(cudaMalloc(&e->owned_dev, own.size()));
+    CU(cudaMemcpy(e->owned_dev, own.data(), own.size(), cudaMemcpyHostToDevice));
+    S.owned = e->owned_dev;
+    const size_t recv_bytes = (size_t)2 * e->topk * e->ep_world * d * sizeof(float);
+    const size_t xbytes_all = recv_bytes + (size_t)(e->ep_world + 1) * 8;
+    CU(cudaMalloc(&e->xch, xbytes_all));
+    CU(cudaMemset(e->xch, 0, xbytes_all));
+    e->dev_bytes += xbytes_all;
+    e->xrecv = reinterpret_cast<float*>(e->xch);
+    e->xflag = reinterpret_cast<unsigned long long*>(e->xch + recv_bytes);
+    e->xseq = e->xflag + e->ep_world;
+  }
   if (!write_value32()) return fail(MOE_ERR_CUDA, "cuStreamWriteValue32 unavailable");
   CU(cudaHostAlloc(&e->mb_host, sizeof(Mailbox), cudaHostAllocMapped));
   memset(e->mb_host, 0, sizeof(Mailbox));
@@ -1223,9 +1294,11 @@ int moe_finalize(moe_engine* e) {
   return MOE_OK;
 }
 
-static int check_ready(moe_engine* e) {
+static int check_ready(moe_engine* e, bool need_peers = false) {
   if (!e) return fail(MOE_ERR_VALUE, "null engine");
   if (!e->finalized) return fail(MOE_ERR_RUNTIME, "engine not finalized (weights not loaded)");
+  if (need_peers && e->ep_world > 1 && !e->ep_connected)
+    return fail(MOE_ERR_RUNTIME, "expert parallel engine not connected to its peers");
   cudaSetDevice(e->dev);
   return MOE_OK;
 }
@@ -1239,7 +1312,7 @@ int moe_reset_session(moe_engine* e) {
 }
 
 int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_out) {
-  int rc = check_ready(e);
+  int rc = check_ready(e, true);
   if (rc) return rc;
   e->pos = 0;  // reset_session (engine.py:149): KV and trace, not the store
   e->has_logits = false;
@@ -1295,7 +1368,7 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
 }
 
 int moe_step(moe_engine* e, int32_t token, float* logits_out) {
-  int rc = check_ready(e);
+  int rc = check_ready(e, true);
   if (rc) return rc;
   if (token < 0 || token >= e->V)
     return fail(MOE_ERR_VALUE, "token id " + std::to_string(token) + " outside vocabulary of " +
@@ -1320,7 +1393,7 @@ int moe_step(moe_engine* e, int32_t token, float* logits_out) {
 }
 
 int moe_decode_greedy(moe_engine* e, int32_t n, int32_t* tokens_out, float* final_logits_out) {
-  int rc = check_ready(e);
+  int rc = check_ready(e, true);
   if (rc) return rc;
   if (n < 1) return fail(MOE_ERR_VALUE, "n_tokens must be >= 1");
   if (!e->has_logits) return fail(MOE_ERR_RUNTIME, "prefill must run before decoding");
@@ -1420,7 +1493,7 @@ int moe_get_stats(moe_engine* e, moe_stats* out) {
   out->n_buffers = e->nbuf;
   out->slot_bytes = (int64_t)e->slot_stride;
   out->device_bytes = (int64_t)e->dev_bytes;
-  out->arena_bytes = (int64_t)(e->xbytes * (size_t)e->L * e->E);
+  out->arena_bytes = (int64_t)(e->xbytes * (size_t)e->n_owned);
   out->kernel_launches = e->launches;
   out->last_call_ms = e->last_ms;
   return MOE_OK;
@@ -1442,6 +1515,53 @@ int moe_kernel_times(moe_engine* e, double* ms_out, int64_t* count_out) {
     if (ms_out) ms_out[i] = e->prof_ms[i];
     if (count_out) count_out[i] = e->prof_cnt[i];
   }
+  return MOE_OK;
+}
+
+int moe_ep_configure(moe_engine* e, int32_t rank, int32_t world) {
+  if (!e) return fail(MOE_ERR_VALUE, "null engine");
+  if (e->finalized || e->xl_set)
+    return fail(MOE_ERR_RUNTIME, "moe_ep_configure must precede expert loading");
+  if (world < 1 || world > MOE_EP_MAX || rank < 0 || rank >= world || world > e->E)
+    return fail(MOE_ERR_VALUE, "expert parallel: need 0 <= rank < world <= min(8, E)");
+  e->ep_rank = rank;
+  e->ep_world = world;
+  e->n_owned = 0;
+  for (int l = 0; l < e->L; ++l)
+    for (int x = 0; x < e->E; ++x)  // expert_parallel.owner_of
+      e->arena_idx[(size_t)l * e->E + x] = (x * world) / e->E == rank ? e->n_owned++ : -1;
+  return MOE_OK;
+}
+
+int moe_ep_handle(moe_engine* e, void* out64) {
+  if (!e || !out64) return fail(MOE_ERR_VALUE, "null argument");
+  if (!e->xch) return fail(MOE_ERR_RUNTIME, "expert parallel not configured / not finalized");
+  cudaSetDevice(e->dev);
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, e->xch));
+  memcpy(out64, &h, sizeof(h));
+  return MOE_OK;
+}
+
+int moe_ep_connect(moe_engine* e, const void* handles) {
+  if (!e || !handles) return fail(MOE_ERR_VALUE, "null argument");
+  if (!e->xch) return fail(MOE_ERR_RUNTIME, "expert parallel not configured / not finalized");
+  cudaSetDevice(e->dev);
+  const size_t recv_bytes = (size_t)2 * e->topk * e->ep_world * e->d * sizeof(float);
+  for (int r = 0; r < e->ep_world; ++r) {
+    uint8_t* base = e->xch;
+    if (r != e->ep_rank) {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, static_cast<const uint8_t*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+      void* p = nullptr;
+      CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      e->ipc_opened.push_back(p);
+      base = static_cast<uint8_t*>(p);
+    }
+    e->peer_recv[r] = reinterpret_cast<float*>(base);
+    e->peer_flag[r] = reinterpret_cast<unsigned long long*>(base + recv_bytes);
+  }
+  e->ep_connected = true;
   return MOE_OK;
 }
 
@@ -1691,9 +1811,10 @@ int moe_synth_model(moe_engine* e, uint64_t seed, int32_t attn_bits, int32_t exp
         e->slot_stride = (off + 255) & ~size_t(255);
         e->expert_bits = xl3[0].bits;
         e->xl_set = true;
-        CU(cudaHostAlloc(&e->arena, e->xbytes * (size_t)L * E, cudaHostAllocPortable));
+        CU(cudaHostAlloc(&e->arena, e->xbytes * (size_t)e->n_owned, cudaHostAllocPortable));
         CU(cudaMalloc(&xtmp, e->slot_stride));
       }
+      if (!e->owns(l, x)) continue;  // expert parallel: another rank's expert
       const int K3[3] = {d, d, f}, N3[3] = {f, f, d};
       const double sd3[3] = {sd, sd, sf};
       for (int i = 0; i < 3 && !rc; ++i) {
@@ -1710,7 +1831,7 @@ int moe_synth_model(moe_engine* e, uint64_t seed, int32_t attn_bits, int32_t exp
         }
       }
       if (rc) break;
-      CU(cudaMemcpyAsync(e->arena + ((size_t)l * E + x) * e->xbytes, xtmp, e->xbytes,
+      CU(cudaMemcpyAsync(e->arena + e->arena_off(l, x), xtmp, e->xbytes,
                          cudaMemcpyDeviceToHost, s));
       CU(cudaStreamSynchronize(s));
       e->loaded[(size_t)l * E + x] = true;

@@ -56,7 +56,11 @@ MOE_DEV bool wait_flag(const uint32_t* f, uint32_t gen, int* err, unsigned long 
   while ((int)(ld_acquire_u32(f) - gen) < 0) {
     __nanosleep(256);
     if (globaltimer() - t0 > wait_ns) {
-      atomicOr(err, MOE_ERRF_TIMEOUT);
+      if ((atomicOr(err, MOE_ERRF_TIMEOUT) & MOE_ERRF_TIMEOUT) == 0) {
+        err[2] = (int)gen;  // diagnostics: generation waited for, flag value seen
+        err[3] = (int)ld_acquire_u32(f);
+        err[4] = (int)(reinterpret_cast<uintptr_t>(f) & 0x7fffffff);
+      }
       return false;
     }
   }
@@ -106,6 +110,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
       if (J.rel_slot >= 0) {
         gemv::pdl_wait();  // the route is written by the previous kernel
         const int buf = P.route->buf[J.rel_slot];
+        if (buf < 0) return;  // expert parallel: another rank owns this expert
         wait_flag(P.flags + buf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
         M.base = P.pool + (long long)buf * P.slot_stride + reinterpret_cast<size_t>(M.base);
       }
@@ -134,6 +139,12 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
   tl_begin(P.site);
   if (J.rel_slot >= 0) {
     const int buf = P.route->buf[J.rel_slot];
+    if (buf < 0) {  // expert parallel: not ours; contribute zeros to the exchange
+      if (s == 0)
+        for (int t = threadIdx.x; t < wcb * WC; t += nthr) J.out[(size_t)cb * 32 * WC + t] = 0.f;
+      tl_end(P.site);
+      return;
+    }
     M.zmeta = reinterpret_cast<const __half2*>(P.pool + (long long)buf * P.slot_stride +
                                                reinterpret_cast<size_t>(M.zmeta));
     // the prologue reads this buffer's zero-point metadata: wait for the copy too
@@ -681,12 +692,14 @@ __global__ void k_combine(CombineParams P) {
   gemv::pdl_trigger();
   gemv::pdl_wait();
   tl_begin(P.site);
+  const float* part = P.part;
+  if (P.ep_seq) part += (size_t)(*P.ep_seq & 1ull) * P.ep_slab;
   const int step = P.xn ? blockDim.x : gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.d; i += step) {
     float out = P.h[i];
     for (int j = 0; j < P.top_k; ++j) {
       float y = 0.f;
-      for (int s = 0; s < P.S; ++s) y += __ldcg(P.part + ((size_t)j * P.S + s) * P.d + i);
+      for (int s = 0; s < P.S; ++s) y += __ldcg(part + ((size_t)j * P.S + s) * P.d + i);
       out = __fadd_rn(out, __fmul_rn(P.route->w[j], y));
     }
     P.out[i] = out;
@@ -696,6 +709,52 @@ __global__ void k_combine(CombineParams P) {
     __syncthreads();
     layernorm_block(osh, P.ln_g, P.ln_b, P.xn, nullptr, P.d, red);
   }
+  tl_end(P.site);
+}
+
+MOE_DEV unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+MOE_DEV void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(1024) k_exchange(ExchangeParams P) {
+  __shared__ unsigned long long sq;
+  gemv::pdl_trigger();
+  gemv::pdl_wait();
+  tl_begin(P.site);
+  if (threadIdx.x == 0) {
+    sq = *P.seq + 1;
+    *P.seq = sq;
+  }
+  __syncthreads();
+  const size_t slab = (size_t)P.top_k * P.N * P.d;
+  const int n = P.top_k * P.d;
+  for (int r = 0; r < P.N; ++r) {  // P2P stores into every rank's receive buffer
+    float* dst = P.recv[r] + (size_t)(sq & 1ull) * slab;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int j = i / P.d, c = i - j * P.d;
+      dst[((size_t)j * P.N + P.rank) * P.d + c] = __ldcg(P.src + i);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int r = 0; r < P.N; ++r) st_release_sys_u64(P.flag[r] + P.rank, sq);
+    const unsigned long long t0 = globaltimer();
+    for (int r = 0; r < P.N; ++r)
+      while (ld_acquire_sys_u64(P.my_flag + r) < sq) {
+        __nanosleep(128);
+        if (globaltimer() - t0 > P.wait_ns) {
+          atomicOr(P.err, MOE_ERRF_TIMEOUT);
+          break;
+        }
+      }
+  }
+  __syncthreads();
   tl_end(P.site);
 }
 
@@ -805,7 +864,8 @@ cudaError_t preload_kernels() {
                        (const void*)k_gemv<16>,  (const void*)k_gemv<32>, (const void*)k_embed,
                        (const void*)k_layernorm, (const void*)k_attention, (const void*)k_tail,
                        (const void*)k_prefill_bk, (const void*)k_begin_call,
-                       (const void*)k_combine,   (const void*)k_logits, (const void*)k_wait_ready};
+                       (const void*)k_combine,   (const void*)k_logits, (const void*)k_wait_ready,
+                       (const void*)k_exchange};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -944,6 +1004,10 @@ void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl) {
     launch_small(k_combine, dim3(1), dim3(1024), (size_t)P.d * 4, s, pdl, P);
   else
     launch_small(k_combine, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
+}
+
+void launch_exchange(const ExchangeParams& P, cudaStream_t s, bool pdl) {
+  launch_small(k_exchange, dim3(1), dim3(1024), 0, s, pdl, P);
 }
 
 void launch_logits(const LogitsParams& P, cudaStream_t s, bool pdl) {

@@ -91,12 +91,35 @@ struct CombineParams {
   const RouteRec* route;
   float* out;         // [d]
   int d, top_k;
+  // expert parallel: `part` is the local receive buffer [2][top_k][S=N][d];
+  // the half in use is picked by the exchange counter's parity
+  const unsigned long long* ep_seq;
+  long long ep_slab;
   // optional fused LayerNorm of `out` (next layer's LN1, or LN_f after the
   // last layer): one CTA, xn = LN(out)
   const float* ln_g;
   const float* ln_b;
   float* xn;
   int site;  // timeline slot of this launch (profiling), -1 none
+};
+
+// Expert-parallel slot exchange (one per layer and position): every rank
+// stores its (top_k x d) slot buffer -- the outputs of the routed experts it
+// owns, zeros elsewhere -- into the receive buffer of every rank over peer
+// memory (NVLink P2P / CUDA IPC), then raises its flag on every rank and
+// waits for all flags.  Receive buffers are double-buffered by the exchange
+// sequence number (a rank can be at most one exchange ahead of any other).
+#define MOE_EP_MAX 8
+struct ExchangeParams {
+  const float* src;                      // [top_k][d]
+  float* recv[MOE_EP_MAX];               // per rank: its receive buffer [2][top_k][N][d]
+  unsigned long long* flag[MOE_EP_MAX];  // per rank: its flag array [N]
+  unsigned long long* seq;               // local exchange counter
+  const unsigned long long* my_flag;     // local flags [N]
+  int rank, N, top_k, d;
+  int* err;
+  unsigned long long wait_ns;
+  int site;
 };
 
 struct LogitsParams {
@@ -144,6 +167,7 @@ void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl = false);
 void launch_tail(const TailParams& P, cudaStream_t s, bool pdl = false);
 void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s);
 void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl = false);
+void launch_exchange(const ExchangeParams& P, cudaStream_t s, bool pdl = false);
 void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int* err,
                        unsigned long long wait_ns, cudaStream_t s);
 void launch_logits(const LogitsParams& P, cudaStream_t s, bool pdl = false);

@@ -187,12 +187,17 @@ class OffloadEngine:
       device      : CUDA device ordinal.
       synth       : (seed, attn_bits, expert_bits) -> skip host weights and build
                     the counter-hash synthetic model on device (bench path).
+      ep_rank / ep_world : expert parallel (expert_parallel.py); after
+                    construction call ``ep_connect`` with every rank's
+                    ``ep_handle()`` (expert_parallel.connect does it over
+                    torch.distributed).
     """
 
     def __init__(self, model, cache: CacheConfig | None = None,
                  speculation: SpeculationConfig = SpeculationConfig(), payloads=None,
                  record_hidden: bool = True, attn_blocks: dict | None = None, device: int = 0,
-                 synth: tuple | None = None, expert_bytes: int | None = None):
+                 synth: tuple | None = None, expert_bytes: int | None = None,
+                 ep_rank: int = 0, ep_world: int = 1):
         self.model = model
         self.record_hidden = record_hidden
         self._h = None
@@ -223,6 +228,9 @@ class OffloadEngine:
         check(L.moe_create(C.byref(_model_desc(cfg)), C.byref(cc), C.byref(sc), device,
                            int(record_hidden), C.byref(h)))
         self._h = h
+        self.ep_rank, self.ep_world = ep_rank, ep_world
+        if ep_world > 1:
+            check(L.moe_ep_configure(h, ep_rank, ep_world))
         if synth is not None:
             check(L.moe_synth_model(h, int(synth[0]), int(synth[1]), int(synth[2])))
         else:
@@ -252,11 +260,28 @@ class OffloadEngine:
             for nm in ("wq", "wk", "wv", "wo"):
                 key = f"{pre}.attn.{nm}"
                 put(key, attn_blocks.get(key, p[key]))
+        from .expert_parallel import owner_of
         for key, payload in payloads.items():
             k = ExpertKey(*key)
+            if owner_of(k.expert, cfg.n_experts, self.ep_world) != self.ep_rank:
+                continue  # another rank's expert
             mk = _Marshal()
             ms = [mk.any(w) for w in expert_triple(payload)]
             check(L.moe_load_expert(self._h, k.layer, k.expert, *[C.byref(m) for m in ms]))
+
+    # ------------------------------------------------------------ expert parallel
+    def ep_handle(self) -> bytes:
+        """This rank's 64-byte exchange-buffer handle (CUDA IPC)."""
+        buf = C.create_string_buffer(64)
+        check(lib().moe_ep_handle(self._h, buf))
+        return buf.raw
+
+    def ep_connect(self, handles) -> None:
+        """Open every rank's exchange buffer (handles in rank order)."""
+        blob = b"".join(handles)
+        if len(blob) != 64 * self.ep_world:
+            raise ValueError("need one 64-byte handle per rank")
+        check(lib().moe_ep_connect(self._h, C.c_char_p(blob)))
 
     def close(self):
         if self._h is not None:

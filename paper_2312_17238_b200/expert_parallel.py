@@ -56,3 +56,12 @@ def combine(h: np.ndarray, weights, slots: np.ndarray) -> np.ndarray:
     for w, y in zip(weights, slots):
         out = out + np.float32(w) * y
     return out
+
+
+def connect(engine, group=None) -> None:
+    """Exchange the engines' IPC handles over torch.distributed and connect
+    every rank's engine to its peers (all ranks call this collectively)."""
+    import torch.distributed as dist
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, engine.ep_handle(), group=group)
+    engine.ep_connect(handles)
