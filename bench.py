@@ -146,6 +146,11 @@ def window_stats(events, cfg, xb):
             "miss_loads": miss, "speculative_loads": spec, "h2d_bytes": moved}
 
 
+def _progress(msg):
+    if os.environ.get("MOE_BENCH_VERBOSE"):
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def run_b200(args, rank, world):
     import ctypes as C
 
@@ -155,10 +160,13 @@ def run_b200(args, rank, world):
     t_build = time.perf_counter()
     eng = build_engine(cfg, args.config, args.seed, device=args.device, rank=rank, world=world)
     t_build = time.perf_counter() - t_build
+    _progress(f"engine built in {t_build:.1f}s")
     V = cfg["vocab_size"]
     prompt = [int(t) for t in np.random.default_rng(0).integers(0, V, 16)]
     eng.prefill(prompt)
+    _progress("prefill done")
     eng.decode(args.warmup)
+    _progress("warmup done")
     n0 = len(eng.events)
     s0 = eng.stats()
     L = _lib.lib()
@@ -362,6 +370,9 @@ def cpu_reference(args, steps, sample_layers=2):
 
 
 def main():
+    if os.environ.get("MOE_FAULTHANDLER"):
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["MOE_FAULTHANDLER"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=32)

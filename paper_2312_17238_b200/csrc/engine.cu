@@ -479,7 +479,9 @@ int moe_engine::run_copier() {
       const CopyReq r = const_cast<const CopyReq&>(mb_host->ring[tail % MOE_MAILBOX_CAP]);
       const int kind = (r.layer >> 24) & 0xff, layer = r.layer & 0xffffff;
       if (debug || trace_copies) {
-        fprintf(stderr, "[moe-copy] req %llu kind %d buf %d key (%d,%d) gen %u\n",
+        fprintf(stderr, "[moe-copy %.3f] req %llu kind %d buf %d key (%d,%d) gen %u\n",
+                std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+                    .count(),
                 (unsigned long long)tail, kind, r.buf, layer, r.expert, r.gen);
         fflush(stderr);
       }
@@ -511,8 +513,10 @@ int moe_engine::run_copier() {
                         reinterpret_cast<CUdeviceptr>(flags + c.buf), c.gen,
                         CU_STREAM_WRITE_VALUE_DEFAULT);
       if (debug || trace_copies) {
-        fprintf(stderr, "[moe-copy] chunk buf %d gen %u off %zu bytes %zu last %d\n", c.buf,
-                c.gen, c.off, c.bytes, (int)c.last);
+        fprintf(stderr, "[moe-copy %.3f] chunk buf %d gen %u off %zu bytes %zu last %d\n",
+                std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+                    .count(),
+                c.buf, c.gen, c.off, c.bytes, (int)c.last);
         fflush(stderr);
       }
       inflight.push_back(f);
