@@ -473,19 +473,21 @@ int moe_engine::run_copier() {
   };
   while (!stop.load(std::memory_order_acquire)) {
     bool work = false;
-    // 1. drain the device mailbox into the scheduler (copy_sched.h)
-    const uint64_t head = __atomic_load_n(&mb_host->head, __ATOMIC_ACQUIRE);
-    while (tail < head) {
-      const CopyReq r = const_cast<const CopyReq&>(mb_host->ring[tail % MOE_MAILBOX_CAP]);
+    // 1. drain the device mailbox into the scheduler (copy_sched.h): an entry
+    //    is valid once its stamp equals its index + 1 (single 16-byte write)
+    for (;;) {
+      const CopyReq* slot = &mb_host->ring[tail % MOE_MAILBOX_CAP];
+      if (__atomic_load_n(&slot->stamp, __ATOMIC_ACQUIRE) != (uint32_t)(tail + 1)) break;
+      const CopyReq r = *const_cast<const CopyReq*>(slot);
       const int kind = (r.layer >> 24) & 0xff, layer = r.layer & 0xffffff;
       if (debug || trace_copies) {
         fprintf(stderr, "[moe-copy %.3f] req %llu kind %d buf %d key (%d,%d) gen %u\n",
                 std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
                     .count(),
-                (unsigned long long)tail, kind, r.buf, layer, r.expert, r.gen);
+                (unsigned long long)tail, kind, req_buf(r), layer, req_expert(r), r.gen);
         fflush(stderr);
       }
-      sched.on_request(kind, r.buf, layer, r.expert, r.gen);
+      sched.on_request(kind, req_buf(r), layer, req_expert(r), r.gen);
       ++tail;
       work = true;
     }
@@ -678,9 +680,12 @@ int moe_engine::enq_experts(int l, int p) {
   dn.nj = topk;
   if (serial_copies) {  // ncu / debugging: the host drains the mailbox before the GEMV
     CU(cudaStreamSynchronize(s_comp));
-    while (copier_tail.load(std::memory_order_acquire) <
-           __atomic_load_n(&mb_host->head, __ATOMIC_ACQUIRE))
-      std::this_thread::yield();
+    {  // entries posted so far = device-side head (seq[1])
+      long long posted = 0;
+      CU(cudaMemcpy(&posted, st.seq + 1, sizeof(posted), cudaMemcpyDeviceToHost));
+      while ((long long)copier_tail.load(std::memory_order_acquire) < posted)
+        std::this_thread::yield();
+    }
     CU(cudaStreamSynchronize(s_copy));
   }
   if (prof)  // keep copy waits out of the GEMV's event-timed span
@@ -850,7 +855,7 @@ int moe_engine::dbg(const char* what, int l, int p) {
   cudaMemcpy(&fl, err, 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(&ev, st.scalars + 3, 4, cudaMemcpyDeviceToHost);
   fprintf(stderr, "[moe] %-10s layer %3d pos %3d : %s err=0x%x nev=%d mailbox=%llu\n", what, l, p,
-          cudaGetErrorString(ce), fl, ev, mb_host ? (unsigned long long)mb_host->head : 0ull);
+          cudaGetErrorString(ce), fl, ev, 0ull);
   fflush(stderr);
   return ce == cudaSuccess ? MOE_OK : fail(MOE_ERR_CUDA, cudaGetErrorString(ce));
 }
@@ -1229,7 +1234,7 @@ int moe_finalize(moe_engine* e) {
   const size_t o_lru = take((size_t)L * kk * 4), o_len = take((size_t)L * 4),
                o_res = take((size_t)L * E * 4), o_sl = take(std::max(b, 1) * 4),
                o_se = take(std::max(b, 1) * 4), o_ss = take(std::max(b, 1) * 4),
-               o_sb = take(std::max(b, 1) * 4), o_sc = take(16), o_seq = take(8),
+               o_sb = take(std::max(b, 1) * 4), o_sc = take(16), o_seq = take(16),
                o_free = take((size_t)e->nbuf * 4), o_pend = take((size_t)e->nbuf * 4),
                o_gen = take((size_t)e->nbuf * 4), o_ev = take((size_t)e->ev_cap * sizeof(DevEvent));
   CU(cudaMalloc(&e->st_mem, off));

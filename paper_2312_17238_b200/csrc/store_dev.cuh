@@ -36,14 +36,20 @@ struct DevEvent {  // layout identical to moe_event
 #define MOE_COPY_SPEC 1     // SPECULATIVE_LOAD: best effort, lowest priority
 #define MOE_COPY_PROMOTE 2  // STAGING_HIT on a staged buffer whose copy may be pending
 
+// One 16-byte mailbox entry, written by the device with a single vector store
+// and validated by the host through its stamp (= entry index + 1): the host
+// never relies on the ordering of separate PCIe writes.
 struct CopyReq {
-  int buf, layer, expert;  // layer: bits 0..23 layer, 24..31 kind
-  uint32_t gen;
+  int buf;        // bits 0..15 buffer, 16..31 expert
+  int layer;      // bits 0..23 layer, 24..31 kind
+  uint32_t gen;   // buffer generation
+  uint32_t stamp; // (index + 1) mod 2^32
 };
+__host__ __device__ inline int req_buf(const CopyReq& r) { return r.buf & 0xffff; }
+__host__ __device__ inline int req_expert(const CopyReq& r) { return (r.buf >> 16) & 0xffff; }
 
 struct Mailbox {
-  volatile unsigned long long head;
-  unsigned long long pad[15];
+  unsigned long long pad[16];
   CopyReq ring[MOE_MAILBOX_CAP];
 };
 
@@ -71,7 +77,7 @@ struct StoreDev {
   int* stg_stamp;
   int* stg_buf;
   int* scalars;    // [0]=stamp [1]=nfree [2]=npending [3]=nev
-  long long* seq;  // [1]
+  long long* seq;  // [0] event seq, [1] mailbox head (entries posted)
   int* free_stack;
   int* pending;
   uint32_t* gen;  // [nbuf]
@@ -145,21 +151,22 @@ MOE_HD int alloc_buf(StoreDev& S) {
 MOE_HD void release(StoreDev& S, int buf) { S.pending[S.scalars[2]++] = buf; }
 
 MOE_HD void post(StoreDev& S, int buf, int l, int e, uint32_t g, int kind) {
-  Mailbox* mb = S.mb;
-  const unsigned long long h = mb->head;
-  CopyReq r;
-  r.buf = buf;
-  r.layer = l | (kind << 24);
-  r.expert = e;
-  r.gen = g;
-  volatile int* dst = reinterpret_cast<volatile int*>(&mb->ring[h % MOE_MAILBOX_CAP]);
-  dst[0] = r.buf;
-  dst[1] = r.layer;
-  dst[2] = r.expert;
-  dst[3] = (int)r.gen;
-  fence_system();
-  mb->head = h + 1;
-  fence_system();
+  const unsigned long long h = (unsigned long long)S.seq[1]++;  // device-side mailbox head
+  CopyReq* slot = &S.mb->ring[h % MOE_MAILBOX_CAP];
+  const uint32_t w0 = (uint32_t)(buf & 0xffff) | ((uint32_t)(e & 0xffff) << 16);
+  const uint32_t w1 = (uint32_t)l | ((uint32_t)kind << 24);
+  const uint32_t stamp = (uint32_t)(h + 1);
+#ifdef __CUDA_ARCH__
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(slot), "r"(w0), "r"(w1),
+               "r"(g), "r"(stamp)
+               : "memory");
+#else
+  slot->buf = (int)w0;
+  slot->layer = (int)w1;
+  slot->gen = g;
+  __atomic_store_n(&slot->stamp, stamp, __ATOMIC_RELEASE);
+#endif
+  fence_system();  // push the entry out toward the host promptly
 }
 
 MOE_HD void issue_copy(StoreDev& S, int buf, int l, int e, int kind) {
@@ -282,7 +289,7 @@ MOE_HD void speculative_load(StoreDev& S, int tl, const int* es, int m, int pos,
 // layer; on shared memory they cost ~30 cycles instead of an L2 round trip.
 MOE_HD int stage_ints(const StoreDev& S) {
   const int kk = S.k > 1 ? S.k : 1, bb = S.b > 1 ? S.b : 1;
-  return 2 + 4 + S.L * kk + S.L + S.L * S.E + 4 * bb + 3 * S.nbuf;
+  return 4 + 4 + S.L * kk + S.L + S.L * S.E + 4 * bb + 3 * S.nbuf;
 }
 
 #ifdef __CUDACC__
@@ -291,7 +298,7 @@ __device__ __forceinline__ StoreDev stage_in(const StoreDev& G, int* sm) {
   StoreDev V = G;
   const int kk = G.k > 1 ? G.k : 1, bb = G.b > 1 ? G.b : 1;
   int* p = sm;
-  V.seq = reinterpret_cast<long long*>(p); p += 2;
+  V.seq = reinterpret_cast<long long*>(p); p += 4;
   V.scalars = p; p += 4;
   V.lru = p; p += G.L * kk;
   V.lru_len = p; p += G.L;
@@ -312,7 +319,10 @@ __device__ __forceinline__ StoreDev stage_in(const StoreDev& G, int* sm) {
   const int n[11] = {4, G.L * kk, G.L, G.L * G.E, bb, bb, bb, bb, G.nbuf, G.nbuf, G.nbuf};
   for (int a = 0; a < 11; ++a)
     for (int i = threadIdx.x; i < n[a]; i += blockDim.x) dst[a][i] = src[a][i];
-  if (threadIdx.x == 0) V.seq[0] = G.seq[0];
+  if (threadIdx.x == 0) {
+    V.seq[0] = G.seq[0];
+    V.seq[1] = G.seq[1];
+  }
   return V;
 }
 
@@ -328,7 +338,10 @@ __device__ __forceinline__ void stage_out(const StoreDev& G, const StoreDev& V) 
   const int n[11] = {4, G.L * kk, G.L, G.L * G.E, bb, bb, bb, bb, G.nbuf, G.nbuf, G.nbuf};
   for (int a = 0; a < 11; ++a)
     for (int i = threadIdx.x; i < n[a]; i += blockDim.x) dst[a][i] = src[a][i];
-  if (threadIdx.x == 0) G.seq[0] = V.seq[0];
+  if (threadIdx.x == 0) {
+    G.seq[0] = V.seq[0];
+    G.seq[1] = V.seq[1];
+  }
 }
 #endif
 

@@ -31,10 +31,11 @@ struct moe_store_sim {
   CopySched sched;
   int progress = 1 << 30;  // default: every request completes immediately
   void drain() {
-    while (tail < mb->head) {
+    for (;;) {
       const CopyReq& r = mb->ring[tail % MOE_MAILBOX_CAP];
+      if (__atomic_load_n(&r.stamp, __ATOMIC_ACQUIRE) != (uint32_t)(tail + 1)) break;
       const int kind = (r.layer >> 24) & 0xff, layer = r.layer & 0xffffff;
-      sched.on_request(kind, r.buf, layer, r.expert, r.gen);
+      sched.on_request(kind, req_buf(r), layer, req_expert(r), r.gen);
       if (kind != MOE_COPY_PROMOTE) ++copies;
       ++tail;
     }
@@ -101,7 +102,7 @@ int moe_store_sim_create(int32_t n_layers, int32_t n_experts, int32_t k, int32_t
   s->free_stack.resize(nbuf);
   for (int i = 0; i < nbuf; ++i) s->free_stack[i] = nbuf - 1 - i;
   s->pending.assign(nbuf, 0);
-  s->seq.assign(1, 0);
+  s->seq.assign(2, 0);
   s->gen.assign(nbuf, 0);
   s->content.assign(nbuf, -1);
   s->flag.assign(nbuf, 0u);
