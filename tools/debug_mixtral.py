@@ -52,6 +52,26 @@ def main(ebits=3, k=4, m=0, ntok=3, nprompt=3):
     rt, rl = ref.decode(ntok)
     res = eng.decode(ntok)
     print("decode tokens ref", rt, "got", res.tokens)
+    rrec = {(r.token_pos, r.layer): r for r in ref.sorted_records()}
+    for b in res.trace.records:
+        a = rrec.get((b.token_pos, b.layer))
+        if a is None or b.token_pos < nprompt:
+            continue
+        nl = b.layer + 1
+        if nl < cfg2.n_layers:
+            G = model.params[f"layers.{nl}.gate"]
+            la, lb = a.hidden @ G, b.hidden @ G
+            ta, tb = OM.top_k(la, 3), OM.top_k(lb, 3)
+            print(f"pos {b.token_pos} layer {b.layer}: guess ref {ta.tolist()} {np.sort(la)[::-1][:3]} "
+                  f"got {tb.tolist()} {np.sort(lb)[::-1][:3]} |dh| {np.abs(a.hidden-b.hidden).max():.2e}")
+    ev_r = ref.events
+    ev_g = [(e.seq, e.kind, e.key.layer, e.key.expert, e.token_pos, e.bytes_moved) for e in eng.events]
+    for i, (x, y) in enumerate(zip(ev_r, ev_g)):
+        if x != y:
+            print("first event diff at", i, "ref", x, "got", y)
+            print("ref around:", ev_r[max(0, i - 4):i + 3])
+            print("got around:", ev_g[max(0, i - 4):i + 3])
+            break
     ref.pool.shutdown()
 
 
