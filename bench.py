@@ -140,10 +140,16 @@ def window_stats(events, cfg, xb):
     from paper_2312_17238_b200 import recall
     miss = sum(1 for e in events if e.kind == "miss_load")
     spec = sum(1 for e in events if e.kind == "speculative_load")
+    shit = sum(1 for e in events if e.kind == "staging_hit")
     moved = sum(e.bytes_moved for e in events if e.kind in ("miss_load", "speculative_load"))
+    eb = max((e.bytes_moved for e in events), default=0)
     return {"hit_rate": recall(events) if events else None,
             "hit_rate_device_only": recall(events, "device_only") if events else None,
-            "miss_loads": miss, "speculative_loads": spec, "h2d_bytes": moved}
+            "miss_loads": miss, "speculative_loads": spec, "staging_hits": shit,
+            "h2d_bytes": moved,
+            # bytes any engine must move for these decisions: every miss, and
+            # the speculative copy behind every staging hit
+            "h2d_bytes_needed": (miss + shit) * eb}
 
 
 def _progress(msg):
@@ -282,7 +288,8 @@ def run_b200(args, rank, world):
     # north-star end-to-end roofline: max(hit bytes / HBM, miss bytes / H2D)
     hit_bytes_tok = (cfg["n_layers"] * (4 * attn_block + 2 * cfg["d_model"] * cfg["n_experts"]
                                         + 2 * expert_bytes(cfg, xb)) + cfg["d_model"] * V * 2)
-    miss_bytes_tok = win["h2d_bytes"] / args.steps
+    miss_bytes_tok = win["h2d_bytes_needed"] / args.steps
+    logical_bytes_tok = win["h2d_bytes"] / args.steps
     copies = s1["h2d_copies"] - s0["h2d_copies"]
     cbytes = s1["h2d_bytes"] - s0["h2d_bytes"]
     cbusy = s1["h2d_busy_ms"] - s0["h2d_busy_ms"]
@@ -290,6 +297,10 @@ def run_b200(args, rank, world):
     h2d_peak = float(peaks.get("h2d_gbs", 55.4))
     t_floor = max(hit_bytes_tok / (hbm * 1e9), miss_bytes_tok / (h2d_peak * 1e9))
     rl_e2e = {"hit_bytes_per_token": hit_bytes_tok, "miss_bytes_per_token": miss_bytes_tok,
+              "miss_bytes_def": "(MISS_LOAD + STAGING_HIT) x expert_bytes: the copies the "
+                                "reference's decisions require",
+              "event_log_load_bytes_per_token": logical_bytes_tok,
+              "physical_h2d_bytes_per_token": round(cbytes / args.steps),
               "hbm_floor_ms": round(hit_bytes_tok / (hbm * 1e9) * 1e3, 4),
               "h2d_floor_ms": round(miss_bytes_tok / (h2d_peak * 1e9) * 1e3, 4),
               "h2d_peak_gbs": h2d_peak, "frac": round(t_floor / (ms_tot / 1e3 / args.steps), 4),

@@ -37,6 +37,11 @@ class ParallelOffloadEngine(OE.OffloadEngine):
         pos = out.token_pos
         for e in out.experts:
             self.store.acquire(layer, e, pos)
+        sp = self.speculation  # engine.py:226-229, as OE.OffloadEngine._resolve_token
+        if sp.enabled and sp.m > 0:
+            g = OE.guess_experts(self.model, h, layer + sp.lookahead, sp.m)
+            if g:
+                self.store.speculative_load(g, pos, current_layer=layer)
         if self.pool is None:
             return [OE.materialize(self.payloads[(layer, e)]) for e in out.experts]
         blocks = [w for e in out.experts for w in self.payloads[(layer, e)]]

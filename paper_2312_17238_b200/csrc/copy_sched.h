@@ -6,10 +6,12 @@
 //   SPEC    (SPECULATIVE_LOAD)  best effort
 //   PROMOTE (STAGING_HIT)       a staged buffer is needed now
 // Policy: demand jobs first (FIFO), then speculative jobs newest-first; a
-// promoted speculative job joins the demand queue.  Jobs are split into
-// chunks so a demand copy waits at most one chunk behind speculation.  A job
-// whose buffer has since been re-requested with a newer generation is stale
-// (its staging entry was replaced and the buffer reassigned) and is dropped.
+// promoted speculative job joins the demand queue.  Speculative jobs are
+// issued in small chunks so a demand copy waits at most one small chunk
+// behind speculation; demand jobs go out whole (nothing may preempt them).
+// A job whose buffer has since been re-requested with a newer generation is
+// stale (its staging entry was replaced and the buffer reassigned) and is
+// dropped.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -77,7 +79,8 @@ struct CopySched {
       j = &spec.back();
     }
     if (!j) return false;
-    const size_t n = chunk < xbytes - j->off ? chunk : xbytes - j->off;
+    const size_t left = xbytes - j->off;
+    const size_t n = from_demand ? left : (chunk < left ? chunk : left);
     *c = Chunk{j->buf, j->layer, j->expert, j->gen, j->off, n, j->off + n == xbytes};
     j->off += n;
     if (c->last) {

@@ -334,7 +334,7 @@ struct moe_engine {
   DecodeState* ds_host = nullptr;       // pinned staging for the cursor
   const DecodeState* cur_ds = nullptr;  // non-null while enqueuing a decode token
   std::atomic<uint64_t> copier_tail{0};   // mailbox entries fully copied (serial mode)
-  size_t copy_chunk = 16u << 20;          // H2D chunk: demand copies preempt speculation
+  size_t copy_chunk = 2u << 20;           // speculative H2D chunk (demand copies go whole)
   // run-ahead bound: the host may enqueue at most `ahead` units (one layer of
   // one position) beyond the oldest unfinished one, so the launch queue never
   // fills while a kernel waits for the copy engine.
