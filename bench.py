@@ -213,11 +213,13 @@ def run_b200(args, rank, world):
         eng.decode(1)
         n = C.c_int32()
         _lib.check(L.moe_read_timeline(eng._h, None, 0, C.byref(n)))
-        buf = (C.c_uint64 * (2 * n.value))()
-        _lib.check(L.moe_read_timeline(eng._h, buf, n.value, C.byref(n)))
+        buf = (C.c_uint64 * (10 * n.value))()
+        _lib.check(L.moe_read_timeline(eng._h, buf, 5 * n.value, C.byref(n)))
         _lib.check(L.moe_timeline(eng._h, 0))
-        st = np.array(buf[0::2], dtype=np.float64)
-        en = np.array(buf[1::2], dtype=np.float64)
+        raw = np.array(buf[:], dtype=np.float64)
+        st = raw[0:2 * n.value:2]
+        en = raw[1:2 * n.value:2]
+        marks = raw[2 * n.value:].reshape(n.value, 8)
         ok = (en > 0) & (st < 2 ** 63)
         t0 = st[ok].min()
         names = ["qkv", "attention", "wo", "tail", "expert_up", "expert_down", "combine_ln"]
@@ -233,10 +235,18 @@ def run_b200(args, rank, world):
             if ok[j]:
                 kinds[nm] = {"avg_us": round((en[j] - st[j]) / 1e3, 2),
                              "sum_us": round((en[j] - st[j]) / 1e3, 1)}
+        phases = {}
+        for nm, kind, nph in (("tail", 3, 7), ("combine_ln", 6, 3)):
+            rows = [marks[1 + 8 * l + kind] for l in range(nl) if ok[1 + 8 * l + kind]]
+            starts = [st[1 + 8 * l + kind] for l in range(nl) if ok[1 + 8 * l + kind]]
+            if rows:
+                m = np.array(rows)[:, :nph]
+                prev = np.concatenate([np.array(starts)[:, None], m[:, :-1]], axis=1)
+                phases[nm] = [round(float(x), 2) for x in ((m - prev) / 1e3).mean(axis=0)]
         span = (en[ok].max() - t0) / 1e3
         timeline = {"token_span_us": round(float(span), 1),
                     "busy_sum_us": round(float(sum(v["sum_us"] for v in kinds.values())), 1),
-                    "kernels": kinds,
+                    "kernels": kinds, "phases_us": phases,
                     "how": "one decode token after the timed region, graph + PDL; per kernel "
                            "earliest CTA start (after griddepcontrol.wait) to latest CTA end, "
                            "%globaltimer"}

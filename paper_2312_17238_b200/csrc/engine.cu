@@ -56,7 +56,7 @@ struct DevMat {  // one tiled matrix in device memory
 // (MOE_GEMV_THREADS threads, ~100 KB smem each); QPS is a multiple of the
 // pipeline stage so every bulk copy stays 16-byte aligned
 int plan_qps(int total_cb, int nquads) {
-  const int target = 2 * 148;
+  const int target = MOE_GEMV_MINB * 148;
   int S = std::max(1, target / total_cb);  // at most one wave
   int qps = (nquads + S - 1) / S;
   qps = (qps + MOE_GEMV_QS - 1) / MOE_GEMV_QS * MOE_GEMV_QS;
@@ -416,7 +416,7 @@ moe_engine::~moe_engine() {
     if (e) cudaEventDestroy(e);
   if (gexec) cudaGraphExecDestroy(gexec);
   if (timeline) {
-    set_timeline(nullptr);
+    set_timeline(nullptr, 0);
     cudaFree(timeline);
   }
   if (ds_host) cudaFreeHost(ds_host);
@@ -1578,13 +1578,15 @@ int moe_timeline(moe_engine* e, int32_t on) {
   if (!e) return fail(MOE_ERR_VALUE, "null engine");
   cudaSetDevice(e->dev);
   const int n = 3 + 8 * e->L;
+  const size_t bytes = n * sizeof(TimelineSlot) + (size_t)n * 8 * 8;  // spans + phase marks
   if (on) {
-    if (!e->timeline) CU(cudaMalloc(&e->timeline, n * sizeof(TimelineSlot)));
+    if (!e->timeline) CU(cudaMalloc(&e->timeline, bytes));
     std::vector<TimelineSlot> init(n, TimelineSlot{~0ull, 0ull});
+    CU(cudaMemset(e->timeline, 0, bytes));
     CU(cudaMemcpy(e->timeline, init.data(), n * sizeof(TimelineSlot), cudaMemcpyHostToDevice));
-    CU(set_timeline(e->timeline));
+    CU(set_timeline(e->timeline, n));
   } else {
-    CU(set_timeline(nullptr));
+    CU(set_timeline(nullptr, 0));
   }
   return MOE_OK;
 }
@@ -1593,8 +1595,10 @@ int moe_read_timeline(moe_engine* e, uint64_t* out, int32_t cap, int32_t* n_out)
   if (!e || !e->timeline) return fail(MOE_ERR_VALUE, "timeline not enabled");
   const int n = 3 + 8 * e->L;
   if (n_out) *n_out = n;
+  // out: 2*n span words, then 8*n phase marks (cap counts 64-bit words / 2)
   if (out && cap > 0)
-    CU(cudaMemcpy(out, e->timeline, std::min(cap, n) * sizeof(TimelineSlot),
+    CU(cudaMemcpy(out, e->timeline,
+                  std::min<size_t>((size_t)cap * 2, (size_t)n * 10) * sizeof(uint64_t),
                   cudaMemcpyDeviceToHost));
   return MOE_OK;
 }

@@ -13,6 +13,7 @@
 #include "gemv.cuh"
 
 __device__ TimelineSlot* g_timeline = nullptr;
+__device__ int g_timeline_n = 0;  // span slots; phase marks follow
 
 namespace {
 
@@ -26,6 +27,13 @@ MOE_DEV unsigned long long globaltimer() {
 MOE_DEV void tl_begin(int site) {
   TimelineSlot* t = g_timeline;
   if (t && site >= 0 && threadIdx.x == 0) atomicMin(&t[site].start, globaltimer());
+}
+// intra-kernel phase marks (block 0, thread 0): slot site*8 + phase of the
+// mark table that follows the span table (profiling)
+MOE_DEV void tl_mark(int site, int phase) {
+  TimelineSlot* t = g_timeline;
+  if (t && site >= 0 && threadIdx.x == 0 && blockIdx.x == 0)
+    reinterpret_cast<unsigned long long*>(t + g_timeline_n)[site * 8 + phase] = globaltimer();
 }
 MOE_DEV void tl_end(int site) {
   TimelineSlot* t = g_timeline;
@@ -68,7 +76,7 @@ MOE_DEV bool wait_flag(const uint32_t* f, uint32_t gen, int* err, unsigned long 
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(MOE_GEMV_THREADS, 2)
+__global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int nst, int stage_bytes) {
   constexpr int WC = Fmt<BITS>::WC;
   constexpr bool QUANT = BITS <= 4;
@@ -571,10 +579,13 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   float* th = P.trace_hidden ? P.trace_hidden + slot * d : nullptr;
   StoreDev S = P.st;
   if (P.mode == 0) S = store::stage_in(P.st, sst);
+  tl_mark(P.site, 0);
   for (int i = tid; i < d; i += blockDim.x) hs[i] = __fadd_rn(P.x[i], __ldcg(P.part + i));
   __syncthreads();
+  tl_mark(P.site, 1);
   layernorm_block(hs, P.g2, P.b2, P.h, hs, d, red);
   __syncthreads();
+  tl_mark(P.site, 2);
   int bad = 0;
   for (int i = tid; i < d; i += blockDim.x) {
     if (!isfinite(hs[i])) bad = 1;
@@ -597,6 +608,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     gpart[blockDim.x + tid] = ag;
   }
   __syncthreads();
+  tl_mark(P.site, 3);
   const int nlog = P.gate_g ? 2 * E : E;
   if (warp < nlog) {  // warp w reduces logit w in a fixed order
     const int e = warp % E;
@@ -607,6 +619,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     if (lane == 0) lg[warp] = (float)t;
   }
   __syncthreads();
+  tl_mark(P.site, 4);
   if (tid == 0) {
     RouteRec R;
     const int k = P.top_k;
@@ -659,10 +672,12 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     }
     *P.route = R;
   }
+  tl_mark(P.site, 5);
   if (P.mode == 0) {
     __syncthreads();
     store::stage_out(P.st, S);
   }
+  tl_mark(P.site, 6);
   tl_end(P.site);
 }
 
@@ -705,10 +720,13 @@ __global__ void k_combine(CombineParams P) {
     P.out[i] = out;
     if (P.xn) osh[i] = out;
   }
+  tl_mark(P.site, 0);
   if (P.xn) {  // fused LayerNorm of the residual stream (next LN1 or LN_f)
     __syncthreads();
+    tl_mark(P.site, 1);
     layernorm_block(osh, P.ln_g, P.ln_b, P.xn, nullptr, P.d, red);
   }
+  tl_mark(P.site, 2);
   tl_end(P.site);
 }
 
@@ -849,7 +867,9 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
 // ------------------------------------------------------------------ launchers
 static std::atomic<long long> g_launches{0};
 
-cudaError_t set_timeline(TimelineSlot* table) {
+cudaError_t set_timeline(TimelineSlot* table, int nslots) {
+  cudaError_t e = cudaMemcpyToSymbol(g_timeline_n, &nslots, sizeof(nslots));
+  if (e != cudaSuccess) return e;
   return cudaMemcpyToSymbol(g_timeline, &table, sizeof(table));
 }
 long long launch_count() { return g_launches.load(); }

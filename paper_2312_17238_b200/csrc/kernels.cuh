@@ -7,7 +7,8 @@
 #define MOE_GEMV_THREADS (MOE_GEMV_WARPS * 32 + 32)
 #define MOE_GEMV_QS 8        // quads per pipeline stage (one per consumer warp)
 #define MOE_GEMV_MAXJOBS 8
-#define MOE_GEMV_RING (80 * 1024)  // bytes of stage ring per CTA (2 CTAs / SM)
+#define MOE_GEMV_MINB 3            // CTAs per SM the kernel is register-limited for
+#define MOE_GEMV_RING (52 * 1024)  // bytes of stage ring per CTA (3 CTAs / SM)
 #define MOE_XS_MAX 4096            // rows of x kept in smem per CTA
 
 enum XMode { X_PLAIN = 0, X_SWIGLU = 1 };
@@ -155,7 +156,7 @@ struct EmbedParams {
 struct TimelineSlot {
   unsigned long long start, end;
 };
-cudaError_t set_timeline(TimelineSlot* table);  // null disables
+cudaError_t set_timeline(TimelineSlot* table, int nslots);  // null disables
 
 // launchers (kernels.cu)
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
