@@ -248,6 +248,7 @@ struct moe_engine {
   DevMat lm_head;
   std::vector<DevMat> wq, wk, wv, wo;
   std::vector<float*> ln1g, ln1b, ln2g, ln2b, gate;
+  std::vector<__half*> gate_h;  // exact fp16 copies of the gates (null if not exact)
   float *lnfg = nullptr, *lnfb = nullptr;
   std::vector<bool> have;  // named tensor presence
 
@@ -433,6 +434,8 @@ moe_engine::~moe_engine() {
   for (auto* v : {&ln1g, &ln1b, &ln2g, &ln2b, &gate})
     for (auto p : *v)
       if (p) cudaFree(p);
+  for (auto p : gate_h)
+    if (p) cudaFree(p);
   if (arena) cudaFreeHost(arena);
   for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
   if (owned_dev) cudaFree(owned_dev);
@@ -613,6 +616,8 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   const int gl = l + sc.lookahead;
   const bool guess = mode == 0 && sc.enabled && sc.m > 0 && gl < L;
   t.gate_g = guess ? gate[gl] : nullptr;
+  t.gh_l = gate_h[l];
+  t.gh_g = guess ? gate_h[gl] : nullptr;
   t.guess_layer = guess ? gl : -1;
   t.m = guess ? sc.m : 0;
   t.h = hp;
@@ -630,6 +635,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   t.pos = p;
   t.mode = mode;
   t.ep_size = 1;
+  if (tail_smem_bytes(t) > 227 * 1024) t.gh_l = t.gh_g = nullptr;  // gates too big to stage
   launch_tail(t, s_comp, pl);
   dbg("tail", l, p);
   unit_done();
@@ -974,6 +980,7 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   e->ln2g.assign(L, nullptr);
   e->ln2b.assign(L, nullptr);
   e->gate.assign(L, nullptr);
+  e->gate_h.assign(L, nullptr);
   e->loaded.assign((size_t)L * e->E, false);
   e->arena_idx.resize((size_t)L * e->E);
   for (size_t i = 0; i < e->arena_idx.size(); ++i) e->arena_idx[i] = (int)i;
@@ -1059,7 +1066,26 @@ int moe_load_tensor(moe_engine* e, const char* name, const moe_matrix* m) {
     if (r == "ln2.beta") return load_vec(e, m, &e->ln2b[l], d, name);
     if (r == "gate") {
       if (m->rows != d || m->cols != e->E) return fail(MOE_ERR_VALUE, nm + ": wrong shape");
-      return load_vec(e, m, &e->gate[l], (int64_t)d * e->E, name);
+      const int64_t n = (int64_t)d * e->E;
+      int rc = load_vec(e, m, &e->gate[l], n, name);
+      if (rc) return rc;
+      // fp16-passthrough role (quant.py:428): keep an exact fp16 copy for TMA staging
+      std::vector<float> f(n);
+      CU(cudaMemcpy(f.data(), e->gate[l], n * 4, cudaMemcpyDeviceToHost));
+      std::vector<__half> hv(n);
+      bool exact = true;
+      for (int64_t i = 0; i < n && exact; ++i) {
+        hv[i] = __float2half_rn(f[i]);
+        exact = __half2float(hv[i]) == f[i];
+      }
+      if (e->gate_h[l]) cudaFree(e->gate_h[l]);
+      e->gate_h[l] = nullptr;
+      if (exact) {
+        CU(cudaMalloc(&e->gate_h[l], n * 2));
+        CU(cudaMemcpy(e->gate_h[l], hv.data(), n * 2, cudaMemcpyHostToDevice));
+        e->dev_bytes += n * 2;
+      }
+      return MOE_OK;
     }
     DevMat* D = r == "attn.wq" ? &e->wq[l] : r == "attn.wk" ? &e->wk[l]
               : r == "attn.wv" ? &e->wv[l] : r == "attn.wo" ? &e->wo[l] : nullptr;

@@ -336,20 +336,38 @@ __global__ void k_wait_ready(const RouteRec* route, int n, const uint32_t* flags
   }
 }
 
-// LayerNorm with the reference's float32 rounding structure (model.py:186-189):
-// mu, var rounded to float32 (sums taken in double), then
-// ((x - mu) / sqrt(var + eps)) * gamma + beta with separately rounded ops.
+// Block-wide fp32 sum in a fixed order (per-thread, warp tree, warp 0 over
+// the warp sums): deterministic.  `red` needs 33 floats.
+MOE_DEV float block_sum_f(float v, float* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    float t = lane < nw ? red[lane] : 0.f;
+    t = warp_sum(t);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  const float r = red[32];
+  __syncthreads();
+  return r;
+}
+
+// LayerNorm with the reference's rounding structure (model.py:186-189):
+// population mean / variance, then ((x - mu) / sqrt(var + eps)) * gamma + beta
+// with separately rounded float32 ops.  x, g, b may live in shared memory.
 MOE_DEV void layernorm_block(const float* x, const float* g, const float* b, float* y, float* ysh,
-                             int d, double* red) {
-  double s = 0.0;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) s += (double)x[i];
-  const float mu = (float)(block_sum_d(s, red) / d);
-  double q = 0.0;
+                             int d, float* red) {
+  float s = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) s += x[i];
+  const float mu = __fdiv_rn(block_sum_f(s, red), (float)d);
+  float q = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float t = __fsub_rn(x[i], mu);
-    q += (double)__fmul_rn(t, t);
+    q = fmaf(t, t, q);
   }
-  const float var = (float)(block_sum_d(q, red) / d);
+  const float var = __fdiv_rn(block_sum_f(q, red), (float)d);
   const float den = sqrtf(__fadd_rn(var, 1e-5f));
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float v = __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(x[i], mu), den), g[i]), b[i]);
@@ -360,9 +378,16 @@ MOE_DEV void layernorm_block(const float* x, const float* g, const float* b, flo
 
 // ------------------------------------------------------------------ embed
 __global__ void k_embed(EmbedParams P) {
-  __shared__ double red[32];
-  extern __shared__ float xsh[];
+  __shared__ float red[33];
+  extern __shared__ float xsh[];  // x [d], then LN gamma / beta [d] each
+  float* gs = xsh + P.d;
+  float* bs = gs + P.d;
   gemv::pdl_trigger();
+  if (P.xn)
+    for (int i = threadIdx.x; i < P.d; i += blockDim.x) {
+      gs[i] = __ldg(P.ln_g + i);
+      bs[i] = __ldg(P.ln_b + i);
+    }
   gemv::pdl_wait();
   tl_begin(P.site);
   const int tok = P.ds ? P.ds->tok : P.tok;
@@ -383,14 +408,14 @@ __global__ void k_embed(EmbedParams P) {
   }
   if (P.xn) {  // fused LN1 of layer 0
     __syncthreads();
-    layernorm_block(xsh, P.ln_g, P.ln_b, P.xn, nullptr, P.d, red);
+    layernorm_block(xsh, gs, bs, P.xn, nullptr, P.d, red);
   }
   tl_end(P.site);
 }
 
 __global__ void __launch_bounds__(1024) k_layernorm(const float* x, const float* g, const float* b,
                                                     float* y, int d) {
-  __shared__ double red[32];
+  __shared__ float red[33];
   gemv::pdl_trigger();
   gemv::pdl_wait();
   layernorm_block(x, g, b, y, nullptr, d, red);
@@ -473,14 +498,17 @@ __global__ void __launch_bounds__(256) k_attention(AttnParams P) {
   }
 }
 
-// Fast path for head_dim % 128 == 0: 4 warps per head, float4 lanes; the
-// current k/v row is appended first, then scores, softmax, alpha @ V.
+// Fast path for head_dim % 128 == 0: one CTA of 128 threads per head.  The
+// current k/v row is appended first; scores use one thread per position
+// (a whole K row per thread, 4 independent accumulators), then softmax and
+// alpha @ V with one thread per head dimension.
 __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
-  extern __shared__ float sc[];  // [T_max]
-  __shared__ float red[4];
-  __shared__ float bval;
-  const int HD = P.hd, h = blockIdx.x, d = P.d, nc = P.hd / 128;
+  extern __shared__ float asm_[];  // q [HD], scores [T_max]
+  __shared__ float red[33];
+  const int HD = P.hd, h = blockIdx.x, d = P.d;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* q = asm_;
+  float* sc = asm_ + HD;
   gemv::pdl_trigger();
   gemv::pdl_wait();
   tl_begin(P.site);
@@ -493,24 +521,27 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
   float* krow = P.kc + (size_t)pos * rstride + (size_t)h * HD;
   float* vrow = P.vc + (size_t)pos * rstride + (size_t)h * HD;
   for (int i = tid; i < HD; i += 128) {  // KV append (model.py:293, KVCache.append)
+    q[i] = __ldcg(qg + i);
     krow[i] = __ldcg(kg + i);
     vrow[i] = __ldcg(vg + i);
   }
   __syncthreads();
   const float rs = sqrtf((float)HD);
-  for (int t = warp; t < T; t += 4) {
-    const float* kr = P.kc + (size_t)t * rstride + (size_t)h * HD;
-    float a = 0.f;
-    for (int c = 0; c < nc; ++c) {
-      const float4 qv = __ldcg(reinterpret_cast<const float4*>(qg + 128 * c) + lane);
-      const float4 kv = __ldcg(reinterpret_cast<const float4*>(kr + 128 * c) + lane);
-      a = fmaf(qv.x, kv.x, a);
-      a = fmaf(qv.y, kv.y, a);
-      a = fmaf(qv.z, kv.z, a);
-      a = fmaf(qv.w, kv.w, a);
+  const float4* q4 = reinterpret_cast<const float4*>(q);
+  for (int t = tid; t < T; t += 128) {
+    const float4* kr = reinterpret_cast<const float4*>(P.kc + (size_t)t * rstride + (size_t)h * HD);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < HD / 4; c += 4) {
+      const float4 k0 = __ldcg(kr + c), k1 = __ldcg(kr + c + 1), k2 = __ldcg(kr + c + 2),
+                   k3 = __ldcg(kr + c + 3);
+      const float4 x0 = q4[c], x1 = q4[c + 1], x2 = q4[c + 2], x3 = q4[c + 3];
+      a0 = fmaf(x0.x, k0.x, fmaf(x0.y, k0.y, fmaf(x0.z, k0.z, fmaf(x0.w, k0.w, a0))));
+      a1 = fmaf(x1.x, k1.x, fmaf(x1.y, k1.y, fmaf(x1.z, k1.z, fmaf(x1.w, k1.w, a1))));
+      a2 = fmaf(x2.x, k2.x, fmaf(x2.y, k2.y, fmaf(x2.z, k2.z, fmaf(x2.w, k2.w, a2))));
+      a3 = fmaf(x3.x, k3.x, fmaf(x3.y, k3.y, fmaf(x3.z, k3.z, fmaf(x3.w, k3.w, a3))));
     }
-    a = warp_sum(a);
-    if (lane == 0) sc[t] = __fdiv_rn(a, rs);
+    sc[t] = __fdiv_rn((a0 + a1) + (a2 + a3), rs);
   }
   __syncthreads();
   float mx = -INFINITY;
@@ -518,34 +549,32 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
   mx = warp_max(mx);
   if (lane == 0) red[warp] = mx;
   __syncthreads();
-  if (tid == 0) bval = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
   __syncthreads();
-  mx = bval;
   float su = 0.f;
   for (int t = tid; t < T; t += 128) {
     const float e = expf(__fsub_rn(sc[t], mx));
     sc[t] = e;
     su += e;
   }
-  su = warp_sum(su);
-  __syncthreads();
-  if (lane == 0) red[warp] = su;
-  __syncthreads();
-  if (tid == 0) bval = ((red[0] + red[1]) + red[2]) + red[3];
-  __syncthreads();
-  su = bval;
+  su = block_sum_f(su, red);
   for (int t = tid; t < T; t += 128) sc[t] = __fdiv_rn(sc[t], su);
   __syncthreads();
   for (int i = tid; i < HD; i += 128) {
     const float* vcol = P.vc + (size_t)h * HD + i;
-    float a0 = 0.f, a1 = 0.f;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     int t = 0;
-    for (; t + 1 < T; t += 2) {
-      a0 = fmaf(sc[t], __ldcg(vcol + (size_t)t * rstride), a0);
-      a1 = fmaf(sc[t + 1], __ldcg(vcol + (size_t)(t + 1) * rstride), a1);
+    for (; t + 3 < T; t += 4) {
+      const float v0 = __ldcg(vcol + (size_t)t * rstride), v1 = __ldcg(vcol + (size_t)(t + 1) * rstride),
+                  v2 = __ldcg(vcol + (size_t)(t + 2) * rstride),
+                  v3 = __ldcg(vcol + (size_t)(t + 3) * rstride);
+      a0 = fmaf(sc[t], v0, a0);
+      a1 = fmaf(sc[t + 1], v1, a1);
+      a2 = fmaf(sc[t + 2], v2, a2);
+      a3 = fmaf(sc[t + 3], v3, a3);
     }
-    if (t < T) a0 = fmaf(sc[t], __ldcg(vcol + (size_t)t * rstride), a0);
-    P.ctx[h * HD + i] = a0 + a1;
+    for (; t < T; ++t) a0 = fmaf(sc[t], __ldcg(vcol + (size_t)t * rstride), a0);
+    P.ctx[h * HD + i] = (a0 + a1) + (a2 + a3);
   }
   tl_end(P.site);
 }
@@ -558,19 +587,42 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
 // expert in descending-weight order and speculative_load the guesses
 // (engine.py:222-231).
 __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
-  extern __shared__ __align__(16) unsigned char tsm[];
+  extern __shared__ __align__(128) unsigned char tsm[];
   const int d = P.d, E = P.E;
-  float* hs = reinterpret_cast<float*>(tsm);                                  // [d]
-  double* gpart = reinterpret_cast<double*>(tsm + (((size_t)d * 4 + 15) & ~(size_t)15));
-  int* sst = reinterpret_cast<int*>(gpart + 2 * blockDim.x);                  // store state
-  __shared__ double red[32];
+  const bool guess = P.gate_g != nullptr;
+  const bool hg = P.gh_l != nullptr && (!guess || P.gh_g != nullptr);
+  // smem: hs[d] | g2[d] | b2[d] | gates (fp16, 1 or 2) | gpart[2*1024] dbl | store
+  float* hs = reinterpret_cast<float*>(tsm);
+  float* g2s = hs + d;
+  float* b2s = g2s + d;
+  __half* gls = reinterpret_cast<__half*>(b2s + d);
+  __half* ggs = gls + (size_t)d * E;
+  double* gpart = reinterpret_cast<double*>(
+      tsm + ((3 * (size_t)d * 4 + (hg ? (guess ? 2 : 1) * (size_t)d * E * 2 : 0) + 15) & ~15));
+  int* sst = reinterpret_cast<int*>(gpart + 2 * blockDim.x);
+  __shared__ float red[33];
   __shared__ float lg[64];
+  __shared__ __align__(8) uint64_t wbar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   gemv::pdl_trigger();
-  // gate matrices are immutable: pull them toward L2 while the Wo GEMV finishes
-  for (int i = tid * 32; i < d * E; i += blockDim.x * 32) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(P.gate_l + i));
-    if (P.gate_g) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.gate_g + i));
+  // immutable weights (LN2 affine, gate matrices) stream into shared memory
+  // with one bulk copy each while the Wo GEMV finishes
+  if (tid == 0) {
+    gemv::mbar_init(&wbar, 1);
+    gemv::mbar_fence_init();
+    const uint32_t vb = (uint32_t)d * 4, gb = (uint32_t)d * E * 2;
+    gemv::mbar_arrive_tx(&wbar, 2 * vb + (hg ? (guess ? 2 : 1) * gb : 0));
+    gemv::bulk_g2s(g2s, P.g2, vb, &wbar);
+    gemv::bulk_g2s(b2s, P.b2, vb, &wbar);
+    if (hg) {
+      gemv::bulk_g2s(gls, P.gh_l, gb, &wbar);
+      if (guess) gemv::bulk_g2s(ggs, P.gh_g, gb, &wbar);
+    }
+  } else if (!hg) {  // fp32 gates: pull them toward L2 instead
+    for (int i = tid * 32; i < d * E; i += blockDim.x * 32) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(P.gate_l + i));
+      if (guess) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.gate_g + i));
+    }
   }
   gemv::pdl_wait();
   tl_begin(P.site);
@@ -578,12 +630,13 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   const size_t slot = (size_t)pos * P.n_layers + P.layer;
   float* th = P.trace_hidden ? P.trace_hidden + slot * d : nullptr;
   StoreDev S = P.st;
-  if (P.mode == 0) S = store::stage_in(P.st, sst);
+  if (P.mode == 0) S = store::stage_in(P.st, sst);  // overlaps the residual loads
+  for (int i = tid; i < d; i += blockDim.x) hs[i] = __fadd_rn(__ldcg(P.x + i), __ldcg(P.part + i));
   tl_mark(P.site, 0);
-  for (int i = tid; i < d; i += blockDim.x) hs[i] = __fadd_rn(P.x[i], __ldcg(P.part + i));
+  gemv::mbar_wait(&wbar, 0);
   __syncthreads();
   tl_mark(P.site, 1);
-  layernorm_block(hs, P.g2, P.b2, P.h, hs, d, red);
+  layernorm_block(hs, g2s, b2s, P.h, hs, d, red);
   __syncthreads();
   tl_mark(P.site, 2);
   int bad = 0;
@@ -596,20 +649,26 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   // engine.py:60-68): thread t owns expert t % E over rows t/E, t/E + nt/E, ...
   const int nt = (blockDim.x / E) * E;
   if (tid < nt) {
-    const int e = tid % E;
     double a = 0.0, ag = 0.0;
-    for (int i = tid; i < d * E; i += nt) {
-      const double hv = hs[i / E];
-      a += hv * (double)P.gate_l[i];
-      if (P.gate_g) ag += hv * (double)P.gate_g[i];
+    if (hg) {
+      for (int i = tid; i < d * E; i += nt) {
+        const double hv = hs[i / E];
+        a += hv * (double)__half2float(gls[i]);
+        if (guess) ag += hv * (double)__half2float(ggs[i]);
+      }
+    } else {
+      for (int i = tid; i < d * E; i += nt) {
+        const double hv = hs[i / E];
+        a += hv * (double)__ldg(P.gate_l + i);
+        if (guess) ag += hv * (double)__ldg(P.gate_g + i);
+      }
     }
-    (void)e;
     gpart[tid] = a;
     gpart[blockDim.x + tid] = ag;
   }
   __syncthreads();
   tl_mark(P.site, 3);
-  const int nlog = P.gate_g ? 2 * E : E;
+  const int nlog = guess ? 2 * E : E;
   if (warp < nlog) {  // warp w reduces logit w in a fixed order
     const int e = warp % E;
     const double* gp = gpart + (warp >= E ? blockDim.x : 0);
@@ -656,7 +715,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     } else if (P.mode == 0) {
       int g[16];
       int m = 0;
-      if (P.gate_g && P.m > 0) {
+      if (guess && P.m > 0) {
         unsigned long long gu = 0ull;
         const float* lgg = lg + E;
         for (int j = 0; j < P.m; ++j) {  // top-m, ties -> lower index (engine.py:60-68)
@@ -702,20 +761,29 @@ __global__ void k_begin_call(StoreDev S) {
 
 // out = h + w0*y0 + w1*y1 in descending-weight order (model.py:251-254)
 __global__ void k_combine(CombineParams P) {
-  __shared__ double red[32];
-  extern __shared__ float osh[];
+  __shared__ float red[33];
+  extern __shared__ float osh[];  // out [d], then LN gamma / beta [d] each
+  float* gs = osh + P.d;
+  float* bs = gs + P.d;
   gemv::pdl_trigger();
+  if (P.xn)  // immutable LN affine: fetched before waiting for the down GEMV
+    for (int i = threadIdx.x; i < P.d; i += blockDim.x) {
+      gs[i] = __ldg(P.ln_g + i);
+      bs[i] = __ldg(P.ln_b + i);
+    }
   gemv::pdl_wait();
   tl_begin(P.site);
   const float* part = P.part;
   if (P.ep_seq) part += (size_t)(*P.ep_seq & 1ull) * P.ep_slab;
+  float w[MOE_MAX_TOPK];
+  for (int j = 0; j < P.top_k; ++j) w[j] = P.route->w[j];
   const int step = P.xn ? blockDim.x : gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.d; i += step) {
-    float out = P.h[i];
+    float out = __ldcg(P.h + i);
     for (int j = 0; j < P.top_k; ++j) {
       float y = 0.f;
       for (int s = 0; s < P.S; ++s) y += __ldcg(part + ((size_t)j * P.S + s) * P.d + i);
-      out = __fadd_rn(out, __fmul_rn(P.route->w[j], y));
+      out = __fadd_rn(out, __fmul_rn(w[j], y));  // model.py:251-254, reference order
     }
     P.out[i] = out;
     if (P.xn) osh[i] = out;
@@ -724,7 +792,7 @@ __global__ void k_combine(CombineParams P) {
   if (P.xn) {  // fused LayerNorm of the residual stream (next LN1 or LN_f)
     __syncthreads();
     tl_mark(P.site, 1);
-    layernorm_block(osh, P.ln_g, P.ln_b, P.xn, nullptr, P.d, red);
+    layernorm_block(osh, gs, bs, P.xn, nullptr, P.d, red);
   }
   tl_mark(P.site, 2);
   tl_end(P.site);
@@ -905,7 +973,7 @@ cudaError_t preload_kernels() {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute((const void*)k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              200 * 1024);
+                              227 * 1024);
 }
 
 // shared memory of one GEMV CTA: barriers, x slice, stage ring (which also
@@ -978,7 +1046,7 @@ static void launch_small(void (*kern)(Params...), dim3 grid, dim3 block, size_t 
 
 void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl) {
   if (P.xn)
-    launch_small(k_embed, dim3(1), dim3(1024), (size_t)P.d * 4, s, pdl, P);
+    launch_small(k_embed, dim3(1), dim3(1024), (size_t)P.d * 12, s, pdl, P);
   else
     launch_small(k_embed, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
 }
@@ -990,8 +1058,8 @@ void launch_layernorm(const float* x, const float* g, const float* b, float* y, 
 
 void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl) {
   if (P.hd % 128 == 0 && P.S == 1) {
-    launch_small(k_attention128, dim3(P.H), dim3(128), (size_t)P.T_max * sizeof(float), s, pdl,
-                 P);
+    launch_small(k_attention128, dim3(P.H), dim3(128), (size_t)(P.hd + P.T_max) * sizeof(float),
+                 s, pdl, P);
     return;
   }
   const size_t smem = (size_t)(P.hd + P.T_max) * sizeof(float);
@@ -999,8 +1067,11 @@ void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl) {
 }
 
 int tail_smem_bytes(const TailParams& P) {
-  return (int)((((size_t)P.d * 4 + 15) & ~(size_t)15) + 2 * 1024 * sizeof(double) +
-               ((size_t)store::stage_ints(P.st) + 2) * 4);
+  const bool guess = P.gate_g != nullptr;
+  const bool hg = P.gh_l != nullptr && (!guess || P.gh_g != nullptr);
+  const size_t head = (3 * (size_t)P.d * 4 +
+                       (hg ? (guess ? 2 : 1) * (size_t)P.d * P.E * 2 : 0) + 15) & ~(size_t)15;
+  return (int)(head + 2 * 1024 * sizeof(double) + ((size_t)store::stage_ints(P.st) + 2) * 4);
 }
 
 void launch_tail(const TailParams& P, cudaStream_t s, bool pdl) {
@@ -1021,7 +1092,7 @@ void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int*
 
 void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl) {
   if (P.xn)
-    launch_small(k_combine, dim3(1), dim3(1024), (size_t)P.d * 4, s, pdl, P);
+    launch_small(k_combine, dim3(1), dim3(1024), (size_t)P.d * 12, s, pdl, P);
   else
     launch_small(k_combine, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
 }

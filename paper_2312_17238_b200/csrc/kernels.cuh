@@ -7,8 +7,8 @@
 #define MOE_GEMV_THREADS (MOE_GEMV_WARPS * 32 + 32)
 #define MOE_GEMV_QS 8        // quads per pipeline stage (one per consumer warp)
 #define MOE_GEMV_MAXJOBS 8
-#define MOE_GEMV_MINB 3            // CTAs per SM the kernel is register-limited for
-#define MOE_GEMV_RING (52 * 1024)  // bytes of stage ring per CTA (3 CTAs / SM)
+#define MOE_GEMV_MINB 2            // CTAs per SM the kernel is register-limited for
+#define MOE_GEMV_RING (80 * 1024)  // bytes of stage ring per CTA (2 CTAs / SM)
 #define MOE_XS_MAX 4096            // rows of x kept in smem per CTA
 
 enum XMode { X_PLAIN = 0, X_SWIGLU = 1 };
@@ -67,6 +67,8 @@ struct TailParams {
   const float* b2;
   const float* gate_l;    // [d][E] gate of this layer
   const float* gate_g;    // [d][E] gate of the guessed layer (or null)
+  const __half* gh_l;     // the same gates as exact fp16 copies (fp16-passthrough
+  const __half* gh_g;     //   roles, quant.py:428), or null: staged in smem by TMA
   float* h;               // pre-MoE hidden out [d]
   RouteRec* route;        // route of this position
   TraceRecDev* trace;     // trace records [T][L]; slot pos*L + layer
@@ -166,6 +168,7 @@ void launch_layernorm(const float* x, const float* g, const float* b, float* y, 
                       cudaStream_t s, bool pdl = false);
 void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl = false);
 void launch_tail(const TailParams& P, cudaStream_t s, bool pdl = false);
+int tail_smem_bytes(const TailParams& P);
 void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s);
 void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl = false);
 void launch_exchange(const ExchangeParams& P, cudaStream_t s, bool pdl = false);
