@@ -973,7 +973,7 @@ cudaError_t preload_kernels() {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute((const void*)k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              227 * 1024);
+                              226 * 1024);  // + static shared memory <= 227 KB
 }
 
 // shared memory of one GEMV CTA: barriers, x slice, stage ring (which also
