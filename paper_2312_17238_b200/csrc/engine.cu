@@ -55,13 +55,13 @@ struct DevMat {  // one tiled matrix in device memory
 // split the quad range of every job so one launch is ~2 CTAs per SM
 // (MOE_GEMV_THREADS threads, ~100 KB smem each); QPS is a multiple of the
 // pipeline stage so every bulk copy stays 16-byte aligned
-int plan_qps(int total_cb, int nquads) {
+int plan_qps(int total_cb, int nquads, int qs) {
   const int target = MOE_GEMV_MINB * 148;
   int S = std::max(1, target / total_cb);  // at most one wave
   int qps = (nquads + S - 1) / S;
-  qps = (qps + MOE_GEMV_QS - 1) / MOE_GEMV_QS * MOE_GEMV_QS;
-  while (qps * 4 > MOE_XS_MAX) qps -= MOE_GEMV_QS;
-  return std::max(qps, MOE_GEMV_QS);
+  qps = (qps + qs - 1) / qs * qs;
+  while (qps * 4 > MOE_XS_MAX) qps -= qs;
+  return std::max(qps, qs);
 }
 
 struct Layout {  // byte sections of one tiled matrix
@@ -1213,16 +1213,16 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->ctx, d))) return rc;
   if ((rc = e->dalloc(&e->logits, (size_t)T * V))) return rc;
   const int wca = fmt_wc(e->attn_bits), wcx = fmt_wc(e->expert_bits);
-  auto plan = [](int total_cb, int nquads, int* Q, int* S) {
+  auto plan = [](int total_cb, int nquads, int bits, int* Q, int* S) {
     nquads = (nquads + 7) / 8 * 8;  // storage quads (MatDev.nqp)
-    *Q = plan_qps(total_cb, nquads);
+    *Q = plan_qps(total_cb, nquads, gemv_qs(bits));
     *S = (nquads + *Q - 1) / *Q;
   };
-  plan(3 * ((d / wca + 31) / 32), d / 4, &e->Q_qkv, &e->S_qkv);
-  plan((d / wca + 31) / 32, d / 4, &e->Q_wo, &e->S_wo);
-  plan(2 * e->topk * ((f / wcx + 31) / 32), d / 4, &e->Q_up, &e->S_up);
-  plan(e->topk * ((d / wcx + 31) / 32), f / 4, &e->Q_dn, &e->S_dn);
-  plan(e->lm_head.M.ncb, d / 4, &e->Q_lm, &e->S_lm);
+  plan(3 * ((d / wca + 31) / 32), d / 4, e->attn_bits, &e->Q_qkv, &e->S_qkv);
+  plan((d / wca + 31) / 32, d / 4, e->attn_bits, &e->Q_wo, &e->S_wo);
+  plan(2 * e->topk * ((f / wcx + 31) / 32), d / 4, e->expert_bits, &e->Q_up, &e->S_up);
+  plan(e->topk * ((d / wcx + 31) / 32), f / 4, e->expert_bits, &e->Q_dn, &e->S_dn);
+  plan(e->lm_head.M.ncb, d / 4, e->lm_bits, &e->Q_lm, &e->S_lm);
   if ((rc = e->dalloc(&e->qkv_part, (size_t)3 * e->S_qkv * d))) return rc;
   if ((rc = e->dalloc(&e->wo_part, (size_t)e->S_wo * d))) return rc;
   if ((rc = e->dalloc(&e->up_part, (size_t)2 * e->topk * e->S_up * f))) return rc;
@@ -1288,6 +1288,8 @@ int moe_finalize(moe_engine* e) {
   S.pending = reinterpret_cast<int*>(sm + o_pend);
   S.gen = reinterpret_cast<uint32_t*>(sm + o_gen);
   S.ev = reinterpret_cast<DevEvent*>(sm + o_ev);
+  S.state_base = reinterpret_cast<int*>(sm);  // everything before the event log
+  S.state_ints = (int)(o_ev / 4);
   S.ev_cap = e->ev_cap;
   S.owned = nullptr;
   S.err = e->err;
@@ -1930,7 +1932,7 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
     return rc;
   }
   const MatDev M = matdev_from(L, mem);
-  const int qps = plan_qps(M.ncb, M.nqp), S = (M.nqp + qps - 1) / qps;
+  const int qps = plan_qps(M.ncb, M.nqp, gemv_qs(L.bits)), S = (M.nqp + qps - 1) / qps;
   float *dx, *part, *dy;
   int* dcnt;
   CU(cudaMalloc(&dx, (size_t)L.K * 4));
@@ -2012,7 +2014,7 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
   float *x, *part, *out;
   int* cnt;
   const MatDev M0 = matdev_from(L, nullptr);
-  const int qps = plan_qps(M0.ncb * njobs, M0.nqp), S = (M0.nqp + qps - 1) / qps;
+  const int qps = plan_qps(M0.ncb * njobs, M0.nqp, gemv_qs(bits)), S = (M0.nqp + qps - 1) / qps;
   CU(cudaMalloc(&x, (size_t)K * 4));
   CU(cudaMalloc(&part, (size_t)njobs * S * N * 4));
   CU(cudaMalloc(&out, (size_t)njobs * N * 4));

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int nst, int stage_bytes) {
   constexpr int WC = Fmt<BITS>::WC;
   constexpr bool QUANT = BITS <= 4;
-  constexpr int W = MOE_GEMV_WARPS, QS = MOE_GEMV_QS;
+  constexpr int W = MOE_GEMV_WARPS, QPW = gemv_qpw(BITS), QS = gemv_qs(BITS);
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 16;
@@ -216,18 +216,21 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     uint32_t ph = 0;
     for (int it = 0; it < nit; ++it) {
       gemv::mbar_wait(full + st, ph);
-      const int q = qs + it * QS + warp;
-      if (q < qv) {
-        const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)warp * rb;
-        const int lr = (q - qs) * 4;
-        const float4 x4 = *reinterpret_cast<const float4*>(xs + lr);
-        if (QUANT) {
-          gemv::quad_codes<BITS>(acc, rec, 32, lane, x4, M.g_log2, M.sg_log2);
-          gemv::quad_zero_fast<BITS>(
-              zacc, reinterpret_cast<const uint32_t*>(rec + 16 * Fmt<BITS>::NV * 32), xz + lr,
-              lane);
-        } else if (active) {
-          gemv::quad_codes<BITS>(acc, rec, wcb, lane, x4, 0, 0);
+#pragma unroll
+      for (int u = 0; u < QPW; ++u) {
+        const int q = qs + it * QS + u * W + warp;
+        if (q < qv) {
+          const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)(u * W + warp) * rb;
+          const int lr = (q - qs) * 4;
+          const float4 x4 = *reinterpret_cast<const float4*>(xs + lr);
+          if (QUANT) {
+            gemv::quad_codes<BITS>(acc, rec, 32, lane, x4, M.g_log2, M.sg_log2);
+            gemv::quad_zero_fast<BITS>(
+                zacc, reinterpret_cast<const uint32_t*>(rec + 16 * Fmt<BITS>::NV * 32), xz + lr,
+                lane);
+          } else if (active) {
+            gemv::quad_codes<BITS>(acc, rec, wcb, lane, x4, 0, 0);
+          }
         }
       }
       __syncwarp();
@@ -243,17 +246,19 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     uint32_t ph = 0;
     for (int it = 0; it < nit; ++it) {
       gemv::mbar_wait(full + st, ph);
-      const int q = qs + it * QS + warp;
-      if (q < qv) {
-        const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)warp * rb;
-        const int lr = (q - qs) * 4;
-        const float4 x4 = *reinterpret_cast<const float4*>(xs + lr);
-        if (active) gemv::quad_codes<BITS>(acc, rec, wcb, lane, x4, M.g_log2, M.sg_log2);
-        Z.zeros = reinterpret_cast<const uint32_t*>(rec + 16 * Fmt<BITS>::NV * wcb);
-        Z.xs = xs + lr;
-        Z.xz = xz + lr;
-        Z.grow = q * 4;
-        gemv::quad_zero(zacc, Z, lane);
+      for (int u = 0; u < QPW; ++u) {
+        const int q = qs + it * QS + u * W + warp;
+        if (q < qv) {
+          const uint8_t* rec = ring + (size_t)st * stage_bytes + (size_t)(u * W + warp) * rb;
+          const int lr = (q - qs) * 4;
+          const float4 x4 = *reinterpret_cast<const float4*>(xs + lr);
+          if (active) gemv::quad_codes<BITS>(acc, rec, wcb, lane, x4, M.g_log2, M.sg_log2);
+          Z.zeros = reinterpret_cast<const uint32_t*>(rec + 16 * Fmt<BITS>::NV * wcb);
+          Z.xs = xs + lr;
+          Z.xz = xz + lr;
+          Z.grow = q * 4;
+          gemv::quad_zero(zacc, Z, lane);
+        }
       }
       __syncwarp();
       if (lane == 0) gemv::mbar_arrive(empty + st);
@@ -526,6 +531,7 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
     vrow[i] = __ldcg(vg + i);
   }
   __syncthreads();
+  tl_mark(P.site, 0);
   const float rs = sqrtf((float)HD);
   const float4* q4 = reinterpret_cast<const float4*>(q);
   for (int t = tid; t < T; t += 128) {
@@ -544,6 +550,7 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
     sc[t] = __fdiv_rn((a0 + a1) + (a2 + a3), rs);
   }
   __syncthreads();
+  tl_mark(P.site, 1);
   float mx = -INFINITY;
   for (int t = tid; t < T; t += 128) mx = fmaxf(mx, sc[t]);
   mx = warp_max(mx);
@@ -560,6 +567,7 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
   su = block_sum_f(su, red);
   for (int t = tid; t < T; t += 128) sc[t] = __fdiv_rn(sc[t], su);
   __syncthreads();
+  tl_mark(P.site, 2);
   for (int i = tid; i < HD; i += 128) {
     const float* vcol = P.vc + (size_t)h * HD + i;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
@@ -631,7 +639,21 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   float* th = P.trace_hidden ? P.trace_hidden + slot * d : nullptr;
   StoreDev S = P.st;
   if (P.mode == 0) S = store::stage_in(P.st, sst);  // overlaps the residual loads
-  for (int i = tid; i < d; i += blockDim.x) hs[i] = __fadd_rn(__ldcg(P.x + i), __ldcg(P.part + i));
+  {  // residual: all loads first, then the stores (no load waits behind a store)
+    constexpr int MAXV = 8;  // d <= 8192 with 1024 threads
+    float xa[MAXV], pa[MAXV];
+#pragma unroll
+    for (int u = 0; u < MAXV; ++u) {
+      const int i = tid + u * (int)blockDim.x;
+      xa[u] = i < d ? __ldcg(P.x + i) : 0.f;
+      pa[u] = i < d ? __ldcg(P.part + i) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < MAXV; ++u) {
+      const int i = tid + u * (int)blockDim.x;
+      if (i < d) hs[i] = __fadd_rn(xa[u], pa[u]);
+    }
+  }
   tl_mark(P.site, 0);
   gemv::mbar_wait(&wbar, 0);
   __syncthreads();
@@ -649,18 +671,21 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   // engine.py:60-68): thread t owns expert t % E over rows t/E, t/E + nt/E, ...
   const int nt = (blockDim.x / E) * E;
   if (tid < nt) {
+    const int e = tid % E, rstep = nt / E;
     double a = 0.0, ag = 0.0;
     if (hg) {
-      for (int i = tid; i < d * E; i += nt) {
-        const double hv = hs[i / E];
-        a += hv * (double)__half2float(gls[i]);
-        if (guess) ag += hv * (double)__half2float(ggs[i]);
+#pragma unroll 4
+      for (int r = tid / E; r < d; r += rstep) {
+        const double hv = hs[r];
+        a = fma(hv, (double)__half2float(gls[r * E + e]), a);
+        if (guess) ag = fma(hv, (double)__half2float(ggs[r * E + e]), ag);
       }
     } else {
-      for (int i = tid; i < d * E; i += nt) {
-        const double hv = hs[i / E];
-        a += hv * (double)__ldg(P.gate_l + i);
-        if (guess) ag += hv * (double)__ldg(P.gate_g + i);
+#pragma unroll 4
+      for (int r = tid / E; r < d; r += rstep) {
+        const double hv = hs[r];
+        a = fma(hv, (double)__ldg(P.gate_l + r * E + e), a);
+        if (guess) ag = fma(hv, (double)__ldg(P.gate_g + r * E + e), ag);
       }
     }
     gpart[tid] = a;
@@ -734,7 +759,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   tl_mark(P.site, 5);
   if (P.mode == 0) {
     __syncthreads();
-    store::stage_out(P.st, S);
+    store::stage_out(P.st, sst);
   }
   tl_mark(P.site, 6);
   tl_end(P.site);
@@ -778,15 +803,38 @@ __global__ void k_combine(CombineParams P) {
   float w[MOE_MAX_TOPK];
   for (int j = 0; j < P.top_k; ++j) w[j] = P.route->w[j];
   const int step = P.xn ? blockDim.x : gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.d; i += step) {
-    float out = __ldcg(P.h + i);
-    for (int j = 0; j < P.top_k; ++j) {
-      float y = 0.f;
-      for (int s = 0; s < P.S; ++s) y += __ldcg(part + ((size_t)j * P.S + s) * P.d + i);
-      out = __fadd_rn(out, __fmul_rn(w[j], y));  // model.py:251-254, reference order
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int MAXV = 8;  // d <= 8192 on the single-CTA (fused LN) path
+  if (P.xn && P.S == 1 && P.top_k <= 2) {  // decode fast path: all loads first
+    float hv[MAXV], y0[MAXV], y1[MAXV];
+#pragma unroll
+    for (int u = 0; u < MAXV; ++u) {
+      const int i = i0 + u * step;
+      hv[u] = i < P.d ? __ldcg(P.h + i) : 0.f;
+      y0[u] = i < P.d ? __ldcg(part + i) : 0.f;
+      y1[u] = (i < P.d && P.top_k > 1) ? __ldcg(part + (size_t)P.d + i) : 0.f;
     }
-    P.out[i] = out;
-    if (P.xn) osh[i] = out;
+#pragma unroll
+    for (int u = 0; u < MAXV; ++u) {
+      const int i = i0 + u * step;
+      if (i < P.d) {
+        float out = __fadd_rn(hv[u], __fmul_rn(w[0], y0[u]));  // model.py:251-254
+        if (P.top_k > 1) out = __fadd_rn(out, __fmul_rn(w[1], y1[u]));
+        P.out[i] = out;
+        osh[i] = out;
+      }
+    }
+  } else {
+    for (int i = i0; i < P.d; i += step) {
+      float out = __ldcg(P.h + i);
+      for (int j = 0; j < P.top_k; ++j) {
+        float y = 0.f;
+        for (int s = 0; s < P.S; ++s) y += __ldcg(part + ((size_t)j * P.S + s) * P.d + i);
+        out = __fadd_rn(out, __fmul_rn(w[j], y));  // model.py:251-254, reference order
+      }
+      P.out[i] = out;
+      if (P.xn) osh[i] = out;
+    }
   }
   tl_mark(P.site, 0);
   if (P.xn) {  // fused LayerNorm of the residual stream (next LN1 or LN_f)
@@ -980,7 +1028,7 @@ cudaError_t preload_kernels() {
 // holds the cross-warp reduction scratch at the end)
 int gemv_smem_bytes(int bits, int xs_rows, int rb_full, int* nstages, int* stage_bytes) {
   const int WC = fmt_wc(bits);
-  const int stage = MOE_GEMV_QS * rb_full;
+  const int stage = gemv_qs(bits) * rb_full;
   int nst = MOE_GEMV_RING / stage;
   nst = nst < 2 ? 2 : (nst > 16 ? 16 : nst);
   int ring = nst * stage;
@@ -1071,7 +1119,7 @@ int tail_smem_bytes(const TailParams& P) {
   const bool hg = P.gh_l != nullptr && (!guess || P.gh_g != nullptr);
   const size_t head = (3 * (size_t)P.d * 4 +
                        (hg ? (guess ? 2 : 1) * (size_t)P.d * P.E * 2 : 0) + 15) & ~(size_t)15;
-  return (int)(head + 2 * 1024 * sizeof(double) + ((size_t)store::stage_ints(P.st) + 2) * 4);
+  return (int)(head + 2 * 1024 * sizeof(double) + ((size_t)store::stage_ints(P.st) + 4) * 4);
 }
 
 void launch_tail(const TailParams& P, cudaStream_t s, bool pdl) {

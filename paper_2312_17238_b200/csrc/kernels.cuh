@@ -5,7 +5,11 @@
 
 #define MOE_GEMV_WARPS 8     // consumer warps per CTA (+1 producer warp)
 #define MOE_GEMV_THREADS (MOE_GEMV_WARPS * 32 + 32)
-#define MOE_GEMV_QS 8        // quads per pipeline stage (one per consumer warp)
+#define MOE_GEMV_QS 8        // quads per pipeline stage for dense formats (one per warp)
+// quant formats: each consumer warp takes 2 quads per stage (more independent
+// work between barrier waits)
+__host__ __device__ constexpr int gemv_qpw(int bits) { return bits <= 4 ? 2 : 1; }
+__host__ __device__ constexpr int gemv_qs(int bits) { return MOE_GEMV_WARPS * gemv_qpw(bits); }
 #define MOE_GEMV_MAXJOBS 8
 #define MOE_GEMV_MINB 2            // CTAs per SM the kernel is register-limited for
 #define MOE_GEMV_RING (80 * 1024)  // bytes of stage ring per CTA (2 CTAs / SM)

@@ -87,6 +87,8 @@ struct StoreDev {
   const unsigned char* owned;  // [L][E] or null (expert parallel subset)
   int* err;
   const volatile uint32_t* flags;  // buffer ready generations (null: host simulator)
+  int* state_base;  // contiguous block holding every array above except ev (device)
+  int state_ints;
 };
 
 // Every store operation is __host__ __device__: the engine runs it on one GPU
@@ -287,61 +289,50 @@ MOE_HD void speculative_load(StoreDev& S, int tl, const int* es, int m, int pos,
 // ---- shared-memory staging of the store state for the bookkeeping kernels:
 // the single bookkeeping thread does a few hundred dependent accesses per
 // layer; on shared memory they cost ~30 cycles instead of an L2 round trip.
-MOE_HD int stage_ints(const StoreDev& S) {
-  const int kk = S.k > 1 ? S.k : 1, bb = S.b > 1 ? S.b : 1;
-  return 4 + 4 + S.L * kk + S.L + S.L * S.E + 4 * bb + 3 * S.nbuf;
-}
+MOE_HD int stage_ints(const StoreDev& S) { return S.state_ints; }
 
 #ifdef __CUDACC__
-// all threads: view V of global store G backed by `sm` (stage_ints ints, 8-aligned)
+// All the store arrays except the event log live in one contiguous block
+// (state_base, state_ints); the bookkeeping kernels copy it to shared memory
+// with one coalesced pass and rebase every pointer into the copy.
+template <class T>
+__device__ __forceinline__ T* rebase(T* p, const int* from, int* to) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(to) +
+                              (reinterpret_cast<const char*>(p) -
+                               reinterpret_cast<const char*>(from)));
+}
+
+// all threads: view of global store G backed by `sm` (16-byte aligned)
 __device__ __forceinline__ StoreDev stage_in(const StoreDev& G, int* sm) {
+  const int n4 = G.state_ints >> 2;
+  const int4* src = reinterpret_cast<const int4*>(G.state_base);
+  int4* dst = reinterpret_cast<int4*>(sm);
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = __ldcg(src + i);
+  for (int i = 4 * n4 + threadIdx.x; i < G.state_ints; i += blockDim.x)
+    sm[i] = __ldcg(G.state_base + i);
   StoreDev V = G;
-  const int kk = G.k > 1 ? G.k : 1, bb = G.b > 1 ? G.b : 1;
-  int* p = sm;
-  V.seq = reinterpret_cast<long long*>(p); p += 4;
-  V.scalars = p; p += 4;
-  V.lru = p; p += G.L * kk;
-  V.lru_len = p; p += G.L;
-  V.res_buf = p; p += G.L * G.E;
-  V.stg_layer = p; p += bb;
-  V.stg_exp = p; p += bb;
-  V.stg_stamp = p; p += bb;
-  V.stg_buf = p; p += bb;
-  V.free_stack = p; p += G.nbuf;
-  V.pending = p; p += G.nbuf;
-  V.gen = reinterpret_cast<uint32_t*>(p);
-  const int* src[11] = {G.scalars, G.lru, G.lru_len, G.res_buf, G.stg_layer, G.stg_exp,
-                        G.stg_stamp, G.stg_buf, G.free_stack, G.pending,
-                        reinterpret_cast<const int*>(G.gen)};
-  int* dst[11] = {V.scalars, V.lru, V.lru_len, V.res_buf, V.stg_layer, V.stg_exp,
-                  V.stg_stamp, V.stg_buf, V.free_stack, V.pending,
-                  reinterpret_cast<int*>(V.gen)};
-  const int n[11] = {4, G.L * kk, G.L, G.L * G.E, bb, bb, bb, bb, G.nbuf, G.nbuf, G.nbuf};
-  for (int a = 0; a < 11; ++a)
-    for (int i = threadIdx.x; i < n[a]; i += blockDim.x) dst[a][i] = src[a][i];
-  if (threadIdx.x == 0) {
-    V.seq[0] = G.seq[0];
-    V.seq[1] = G.seq[1];
-  }
-  return V;
+  V.lru = rebase(G.lru, G.state_base, sm);
+  V.lru_len = rebase(G.lru_len, G.state_base, sm);
+  V.res_buf = rebase(G.res_buf, G.state_base, sm);
+  V.stg_layer = rebase(G.stg_layer, G.state_base, sm);
+  V.stg_exp = rebase(G.stg_exp, G.state_base, sm);
+  V.stg_stamp = rebase(G.stg_stamp, G.state_base, sm);
+  V.stg_buf = rebase(G.stg_buf, G.state_base, sm);
+  V.scalars = rebase(G.scalars, G.state_base, sm);
+  V.seq = rebase(G.seq, G.state_base, sm);
+  V.free_stack = rebase(G.free_stack, G.state_base, sm);
+  V.pending = rebase(G.pending, G.state_base, sm);
+  V.gen = rebase(G.gen, G.state_base, sm);
+  return V;  // (caller synchronizes before use)
 }
 
 // all threads: write the staged state back
-__device__ __forceinline__ void stage_out(const StoreDev& G, const StoreDev& V) {
-  const int kk = G.k > 1 ? G.k : 1, bb = G.b > 1 ? G.b : 1;
-  const int* src[11] = {V.scalars, V.lru, V.lru_len, V.res_buf, V.stg_layer, V.stg_exp,
-                        V.stg_stamp, V.stg_buf, V.free_stack, V.pending,
-                        reinterpret_cast<const int*>(V.gen)};
-  int* dst[11] = {G.scalars, G.lru, G.lru_len, G.res_buf, G.stg_layer, G.stg_exp,
-                  G.stg_stamp, G.stg_buf, G.free_stack, G.pending,
-                  reinterpret_cast<int*>(G.gen)};
-  const int n[11] = {4, G.L * kk, G.L, G.L * G.E, bb, bb, bb, bb, G.nbuf, G.nbuf, G.nbuf};
-  for (int a = 0; a < 11; ++a)
-    for (int i = threadIdx.x; i < n[a]; i += blockDim.x) dst[a][i] = src[a][i];
-  if (threadIdx.x == 0) {
-    G.seq[0] = V.seq[0];
-    G.seq[1] = V.seq[1];
-  }
+__device__ __forceinline__ void stage_out(const StoreDev& G, const int* sm) {
+  const int n4 = G.state_ints >> 2;
+  const int4* src = reinterpret_cast<const int4*>(sm);
+  int4* dst = reinterpret_cast<int4*>(G.state_base);
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+  for (int i = 4 * n4 + threadIdx.x; i < G.state_ints; i += blockDim.x) G.state_base[i] = sm[i];
 }
 #endif
 
