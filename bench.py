@@ -236,7 +236,8 @@ def run_b200(args, rank, world):
                 kinds[nm] = {"avg_us": round((en[j] - st[j]) / 1e3, 2),
                              "sum_us": round((en[j] - st[j]) / 1e3, 1)}
         phases = {}
-        for nm, kind, nph in (("tail", 3, 7), ("combine_ln", 6, 3)):
+        for nm, kind, nph in (("tail", 3, 8), ("combine_ln", 6, 3), ("attention", 1, 3),
+                              ("qkv", 0, 3), ("expert_down", 5, 3)):
             rows = [marks[1 + 8 * l + kind] for l in range(nl) if ok[1 + 8 * l + kind]]
             starts = [st[1 + 8 * l + kind] for l in range(nl) if ok[1 + 8 * l + kind]]
             if rows:

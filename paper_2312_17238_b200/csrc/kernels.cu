@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
 #pragma unroll
     for (int w = 0; w < W; ++w) zo_sum += misc[w];
 
+  tl_mark(P.site, 0);  // prologue done (x slice, zero-point rows)
   float acc[WC];
 #pragma unroll
   for (int k = 0; k < WC; ++k) acc[k] = 0.f;
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       for (int o = Z.zpr; o < 32; o <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, o);
     ztot = __shfl_sync(0xffffffffu, zacc, (lane * WC) >> M.g_log2);
   }
+  tl_mark(P.site, 1);  // streaming loop done
   float y[WC];
   gemv::finish_lane<BITS>(y, acc, ztot);
   // cross-warp reduction through the (now idle) ring, fixed order
@@ -290,6 +292,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       dst[(size_t)(cb * 32 + l) * WC + k] = a + zo_out;
     }
   }
+  tl_mark(P.site, 2);  // cross-warp reduction + partial written
   if (J.S == 1) {
     tl_end(P.site);
     return;
@@ -672,24 +675,32 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   const int nt = (blockDim.x / E) * E;
   if (tid < nt) {
     const int e = tid % E, rstep = nt / E;
-    double a = 0.0, ag = 0.0;
+    // per-thread fp32 partials over 2 interleaved accumulators, combined in
+    // double across threads (fixed order below)
+    float a0 = 0.f, a1 = 0.f, g0 = 0.f, g1 = 0.f;
+    int r = tid / E;
     if (hg) {
-#pragma unroll 4
-      for (int r = tid / E; r < d; r += rstep) {
-        const double hv = hs[r];
-        a = fma(hv, (double)__half2float(gls[r * E + e]), a);
-        if (guess) ag = fma(hv, (double)__half2float(ggs[r * E + e]), ag);
+      for (; r + rstep < d; r += 2 * rstep) {
+        const float h0 = hs[r], h1 = hs[r + rstep];
+        a0 = fmaf(h0, __half2float(gls[r * E + e]), a0);
+        a1 = fmaf(h1, __half2float(gls[(r + rstep) * E + e]), a1);
+        if (guess) {
+          g0 = fmaf(h0, __half2float(ggs[r * E + e]), g0);
+          g1 = fmaf(h1, __half2float(ggs[(r + rstep) * E + e]), g1);
+        }
+      }
+      if (r < d) {
+        a0 = fmaf(hs[r], __half2float(gls[r * E + e]), a0);
+        if (guess) g0 = fmaf(hs[r], __half2float(ggs[r * E + e]), g0);
       }
     } else {
-#pragma unroll 4
-      for (int r = tid / E; r < d; r += rstep) {
-        const double hv = hs[r];
-        a = fma(hv, (double)__ldg(P.gate_l + r * E + e), a);
-        if (guess) ag = fma(hv, (double)__ldg(P.gate_g + r * E + e), ag);
+      for (; r < d; r += rstep) {
+        a0 = fmaf(hs[r], __ldg(P.gate_l + r * E + e), a0);
+        if (guess) g0 = fmaf(hs[r], __ldg(P.gate_g + r * E + e), g0);
       }
     }
-    gpart[tid] = a;
-    gpart[blockDim.x + tid] = ag;
+    gpart[tid] = (double)a0 + (double)a1;
+    gpart[blockDim.x + tid] = (double)g0 + (double)g1;
   }
   __syncthreads();
   tl_mark(P.site, 3);
@@ -704,18 +715,40 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   }
   __syncthreads();
   tl_mark(P.site, 4);
+  // top-k of this layer's logits and top-m of the guessed layer's, on warp 0:
+  // lane e holds logit e; each round is a warp argmax with ties -> lower index
+  // (np.argsort(-logits, kind="stable"), model.py:192-195, engine.py:60-68)
+  __shared__ int sel_sh[MOE_MAX_TOPK], gsel_sh[16];
+  if (warp == 0) {
+    const int k = P.top_k, mg = (guess && P.m > 0) ? P.m : 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      const float* lv = pass == 0 ? lg : lg + E;
+      const int rounds = pass == 0 ? k : mg;
+      bool taken = false;
+      for (int j = 0; j < rounds; ++j) {
+        float v = (lane < E && !taken) ? lv[lane] : -INFINITY;
+        int idx = (lane < E && !taken) ? lane : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+          if (ov > v || (ov == v && oi < idx)) {
+            v = ov;
+            idx = oi;
+          }
+        }
+        if (lane == idx) taken = true;
+        if (lane == 0) (pass == 0 ? sel_sh : gsel_sh)[j] = idx;
+      }
+    }
+  }
+  __syncthreads();
+  tl_mark(P.site, 5);
   if (tid == 0) {
     RouteRec R;
     const int k = P.top_k;
     int sel[MOE_MAX_TOPK];
-    unsigned long long used = 0ull;
-    for (int j = 0; j < k; ++j) {  // stable descending (ties -> lower index)
-      int best = -1;
-      for (int e = 0; e < E; ++e)
-        if (!((used >> e) & 1ull) && (best < 0 || lg[e] > lg[best])) best = e;
-      sel[j] = best;
-      used |= 1ull << best;
-    }
+    for (int j = 0; j < k; ++j) sel[j] = sel_sh[j];
     float ez[MOE_MAX_TOPK], sum = 0.f;
     for (int j = 0; j < k; ++j) {
       ez[j] = expf(__fsub_rn(lg[sel[j]], lg[sel[0]]));
@@ -738,30 +771,18 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     if (bad) {
       atomicOr(P.st.err, MOE_ERRF_NONFINITE_GATE);
     } else if (P.mode == 0) {
-      int g[16];
-      int m = 0;
-      if (guess && P.m > 0) {
-        unsigned long long gu = 0ull;
-        const float* lgg = lg + E;
-        for (int j = 0; j < P.m; ++j) {  // top-m, ties -> lower index (engine.py:60-68)
-          int best = -1;
-          for (int e = 0; e < E; ++e)
-            if (!((gu >> e) & 1ull) && (best < 0 || lgg[e] > lgg[best])) best = e;
-          g[j] = best;
-          gu |= 1ull << best;
-        }
-        m = P.m;
-      }
-      store::resolve_token(S, P.layer, sel, k, g, m, m ? P.guess_layer : -1, pos, R.buf, R.gen);
+      const int m = (guess && P.m > 0) ? P.m : 0;
+      store::resolve_token(S, P.layer, sel, k, gsel_sh, m, m ? P.guess_layer : -1, pos, R.buf,
+                           R.gen);
     }
     *P.route = R;
   }
-  tl_mark(P.site, 5);
+  tl_mark(P.site, 6);
   if (P.mode == 0) {
     __syncthreads();
     store::stage_out(P.st, sst);
   }
-  tl_mark(P.site, 6);
+  tl_mark(P.site, 7);
   tl_end(P.site);
 }
 
