@@ -164,21 +164,41 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const float xscale = QUANT ? gemv::kXScale : 1.f;
   const int gcb0 = QUANT ? ((cb * 32 * WC) >> M.g_log2) : 0;  // first zero group of the cb
   float zo_part = 0.f;
-  for (int i = threadIdx.x; i < nrows; i += nthr) {
-    const int r = row0 + i;
-    float xv;
-    if (J.xmode == X_PLAIN) {
-      xv = __ldcg(J.x + r);
-    } else {  // SwiGLU of the up projections (model.py:223-226)
-      const float a = __ldcg(J.up1 + r), b = __ldcg(J.up3 + r);
-      xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
+  const bool uni = QUANT && M.runs_uniform;
+  // batches of 4 rows per thread: every load of a batch is issued before any
+  // use (x or the up-projection pair, and the row's zero-point run)
+  for (int i0 = 0; i0 < nrows; i0 += 4 * nthr) {
+    float va[4], vb[4];
+    __half2 zr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * nthr + threadIdx.x;
+      const int r = row0 + i;
+      const bool in = i < nrows;
+      if (J.xmode == X_PLAIN) {
+        va[u] = in ? __ldcg(J.x + r) : 0.f;
+        vb[u] = 0.f;
+      } else {
+        va[u] = in ? __ldcg(J.up1 + r) : 0.f;
+        vb[u] = in ? __ldcg(J.up3 + r) : 0.f;
+      }
+      if (uni) zr[u] = in ? __ldg(M.zmeta + (((int64_t)r * M.G + gcb0) >> M.sg_log2))
+                          : __float2half2_rn(0.f);
     }
-    xv *= xscale;
-    xs[i] = xv;
-    if (QUANT && M.runs_uniform) {  // the cb's groups of this row share one zero run
-      const float2 zm = __half22float2(__ldg(M.zmeta + (((int64_t)r * M.G + gcb0) >> M.sg_log2)));
-      xz[i] = xv * zm.x;
-      zo_part = fmaf(xv, zm.y, zo_part);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * nthr + threadIdx.x;
+      if (i >= nrows) continue;
+      float xv = va[u];
+      if (J.xmode != X_PLAIN)  // SwiGLU of the up projections (model.py:223-226)
+        xv = __fmul_rn(__fmul_rn(va[u], sigmoid_ref(va[u])), vb[u]);
+      xv *= xscale;
+      xs[i] = xv;
+      if (uni) {  // the cb's groups of this row share one zero run
+        const float2 zm = __half22float2(zr[u]);
+        xz[i] = xv * zm.x;
+        zo_part = fmaf(xv, zm.y, zo_part);
+      }
     }
   }
   if (QUANT && M.runs_uniform) {
@@ -506,17 +526,18 @@ __global__ void __launch_bounds__(256) k_attention(AttnParams P) {
   }
 }
 
-// Fast path for head_dim % 128 == 0: one CTA of 128 threads per head.  The
-// current k/v row is appended first; scores use one thread per position
-// (a whole K row per thread, 4 independent accumulators), then softmax and
-// alpha @ V with one thread per head dimension.
-__global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
-  extern __shared__ float asm_[];  // q [HD], scores [T_max]
+// Fast path for head_dim % 128 == 0: one CTA of 256 threads per head.  The
+// current k/v row is appended first; scores use 4 threads per position (a
+// quarter of the K row each, all loads in flight, quad shuffle reduce), then
+// softmax and alpha @ V with each head dimension split over two threads.
+__global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
+  extern __shared__ float asm_[];  // q [HD], scores [T_max], ctx halves [2][HD]
   __shared__ float red[33];
   const int HD = P.hd, h = blockIdx.x, d = P.d;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   float* q = asm_;
   float* sc = asm_ + HD;
+  float* half2buf = sc + P.T_max;
   gemv::pdl_trigger();
   gemv::pdl_wait();
   tl_begin(P.site);
@@ -528,7 +549,7 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
   const float* vg = qg + 2 * d;
   float* krow = P.kc + (size_t)pos * rstride + (size_t)h * HD;
   float* vrow = P.vc + (size_t)pos * rstride + (size_t)h * HD;
-  for (int i = tid; i < HD; i += 128) {  // KV append (model.py:293, KVCache.append)
+  for (int i = tid; i < HD; i += blockDim.x) {  // KV append (model.py:293, KVCache.append)
     q[i] = __ldcg(qg + i);
     krow[i] = __ldcg(kg + i);
     vrow[i] = __ldcg(vg + i);
@@ -536,57 +557,73 @@ __global__ void __launch_bounds__(128) k_attention128(AttnParams P) {
   __syncthreads();
   tl_mark(P.site, 0);
   const float rs = sqrtf((float)HD);
-  const float4* q4 = reinterpret_cast<const float4*>(q);
-  for (int t = tid; t < T; t += 128) {
-    const float4* kr = reinterpret_cast<const float4*>(P.kc + (size_t)t * rstride + (size_t)h * HD);
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 4
-    for (int c = 0; c < HD / 4; c += 4) {
-      const float4 k0 = __ldcg(kr + c), k1 = __ldcg(kr + c + 1), k2 = __ldcg(kr + c + 2),
-                   k3 = __ldcg(kr + c + 3);
-      const float4 x0 = q4[c], x1 = q4[c + 1], x2 = q4[c + 2], x3 = q4[c + 3];
-      a0 = fmaf(x0.x, k0.x, fmaf(x0.y, k0.y, fmaf(x0.z, k0.z, fmaf(x0.w, k0.w, a0))));
-      a1 = fmaf(x1.x, k1.x, fmaf(x1.y, k1.y, fmaf(x1.z, k1.z, fmaf(x1.w, k1.w, a1))));
-      a2 = fmaf(x2.x, k2.x, fmaf(x2.y, k2.y, fmaf(x2.z, k2.z, fmaf(x2.w, k2.w, a2))));
-      a3 = fmaf(x3.x, k3.x, fmaf(x3.y, k3.y, fmaf(x3.z, k3.z, fmaf(x3.w, k3.w, a3))));
+  {
+    const int g = tid & 3, nf = HD / 16;  // float4s per quarter row
+    const float4* q4 = reinterpret_cast<const float4*>(q) + g * nf;
+    for (int t = tid >> 2; t < T; t += (int)blockDim.x >> 2) {
+      const float4* kr =
+          reinterpret_cast<const float4*>(P.kc + (size_t)t * rstride + (size_t)h * HD) + g * nf;
+      float a0 = 0.f, a1 = 0.f;
+      for (int c = 0; c < nf; c += 8) {
+        float4 kv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) kv[u] = __ldcg(kr + c + u);
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          const float4 x0 = q4[c + u], x1 = q4[c + u + 1];
+          a0 = fmaf(x0.x, kv[u].x, fmaf(x0.y, kv[u].y, fmaf(x0.z, kv[u].z, fmaf(x0.w, kv[u].w, a0))));
+          a1 = fmaf(x1.x, kv[u + 1].x,
+                    fmaf(x1.y, kv[u + 1].y, fmaf(x1.z, kv[u + 1].z, fmaf(x1.w, kv[u + 1].w, a1))));
+        }
+      }
+      float a = a0 + a1;
+      a += __shfl_xor_sync(0xffffffffu, a, 1);
+      a += __shfl_xor_sync(0xffffffffu, a, 2);
+      if (g == 0) sc[t] = __fdiv_rn(a, rs);
     }
-    sc[t] = __fdiv_rn((a0 + a1) + (a2 + a3), rs);
   }
   __syncthreads();
   tl_mark(P.site, 1);
   float mx = -INFINITY;
-  for (int t = tid; t < T; t += 128) mx = fmaxf(mx, sc[t]);
+  for (int t = tid; t < T; t += blockDim.x) mx = fmaxf(mx, sc[t]);
   mx = warp_max(mx);
-  if (lane == 0) red[warp] = mx;
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
   __syncthreads();
-  mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  mx = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
   __syncthreads();
   float su = 0.f;
-  for (int t = tid; t < T; t += 128) {
+  for (int t = tid; t < T; t += blockDim.x) {
     const float e = expf(__fsub_rn(sc[t], mx));
     sc[t] = e;
     su += e;
   }
   su = block_sum_f(su, red);
-  for (int t = tid; t < T; t += 128) sc[t] = __fdiv_rn(sc[t], su);
+  for (int t = tid; t < T; t += blockDim.x) sc[t] = __fdiv_rn(sc[t], su);
   __syncthreads();
   tl_mark(P.site, 2);
-  for (int i = tid; i < HD; i += 128) {
-    const float* vcol = P.vc + (size_t)h * HD + i;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    int t = 0;
-    for (; t + 3 < T; t += 4) {
-      const float v0 = __ldcg(vcol + (size_t)t * rstride), v1 = __ldcg(vcol + (size_t)(t + 1) * rstride),
-                  v2 = __ldcg(vcol + (size_t)(t + 2) * rstride),
-                  v3 = __ldcg(vcol + (size_t)(t + 3) * rstride);
-      a0 = fmaf(sc[t], v0, a0);
-      a1 = fmaf(sc[t + 1], v1, a1);
-      a2 = fmaf(sc[t + 2], v2, a2);
-      a3 = fmaf(sc[t + 3], v3, a3);
+  {
+    const int half = tid / 128, i0 = tid & 127;
+    for (int i = i0; i < HD; i += 128) {
+      const float* vcol = P.vc + (size_t)h * HD + i;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      int t = half;
+      for (; t + 6 < T; t += 8) {
+        const float v0 = __ldcg(vcol + (size_t)t * rstride),
+                    v1 = __ldcg(vcol + (size_t)(t + 2) * rstride),
+                    v2 = __ldcg(vcol + (size_t)(t + 4) * rstride),
+                    v3 = __ldcg(vcol + (size_t)(t + 6) * rstride);
+        a0 = fmaf(sc[t], v0, a0);
+        a1 = fmaf(sc[t + 2], v1, a1);
+        a2 = fmaf(sc[t + 4], v2, a2);
+        a3 = fmaf(sc[t + 6], v3, a3);
+      }
+      for (; t < T; t += 2) a0 = fmaf(sc[t], __ldcg(vcol + (size_t)t * rstride), a0);
+      half2buf[half * HD + i] = (a0 + a1) + (a2 + a3);
     }
-    for (; t < T; ++t) a0 = fmaf(sc[t], __ldcg(vcol + (size_t)t * rstride), a0);
-    P.ctx[h * HD + i] = (a0 + a1) + (a2 + a3);
   }
+  __syncthreads();
+  for (int i = tid; i < HD; i += blockDim.x) P.ctx[h * HD + i] = half2buf[i] + half2buf[HD + i];
   tl_end(P.site);
 }
 
@@ -1127,8 +1164,8 @@ void launch_layernorm(const float* x, const float* g, const float* b, float* y, 
 
 void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl) {
   if (P.hd % 128 == 0 && P.S == 1) {
-    launch_small(k_attention128, dim3(P.H), dim3(128), (size_t)(P.hd + P.T_max) * sizeof(float),
-                 s, pdl, P);
+    launch_small(k_attention128, dim3(P.H), dim3(256),
+                 (size_t)(3 * P.hd + P.T_max) * sizeof(float), s, pdl, P);
     return;
   }
   const size_t smem = (size_t)(P.hd + P.T_max) * sizeof(float);
