@@ -66,19 +66,32 @@ struct CopySched {
 
   bool empty() const { return demand.empty() && spec.empty(); }
 
-  // next chunk to issue, or false when idle
-  bool next(Chunk* c) {
+  void drop_stale() {
     while (!demand.empty() && stale(demand.front())) demand.pop_front();
     while (!spec.empty() && stale(spec.back())) spec.pop_back();
-    Job* j = nullptr;
-    bool from_demand = false;
-    if (!demand.empty()) {
-      j = &demand.front();
-      from_demand = true;
-    } else if (!spec.empty()) {
-      j = &spec.back();
-    }
-    if (!j) return false;
+  }
+
+  bool has_demand() {
+    drop_stale();
+    return !demand.empty();
+  }
+
+  // next chunk of the front demand job (whole remainder) or of the newest
+  // speculative job (one `chunk`)
+  bool next_demand(Chunk* c) {
+    drop_stale();
+    return !demand.empty() && take(&demand.front(), true, c);
+  }
+  bool next_spec(Chunk* c) {
+    drop_stale();
+    return !spec.empty() && take(&spec.back(), false, c);
+  }
+
+  // next chunk to issue under the single-stream policy, or false when idle
+  bool next(Chunk* c) { return next_demand(c) || next_spec(c); }
+
+ private:
+  bool take(Job* j, bool from_demand, Chunk* c) {
     const size_t left = xbytes - j->off;
     const size_t n = from_demand ? left : (chunk < left ? chunk : left);
     *c = Chunk{j->buf, j->layer, j->expert, j->gen, j->off, n, j->off + n == xbytes};

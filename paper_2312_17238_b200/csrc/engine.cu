@@ -237,7 +237,7 @@ struct moe_engine {
   moe_spec_cfg sc{};
   int dev = 0;
   bool rec_hidden = true;
-  cudaStream_t s_comp = nullptr, s_copy = nullptr;
+  cudaStream_t s_comp = nullptr, s_copy = nullptr, s_copy2 = nullptr;  // copy: demand, spec
   int attn_bits = 0, expert_bits = 0, lm_bits = 0;
   int d = 0, f = 0, V = 0, L = 0, E = 0, H = 0, hd = 0, T = 0, topk = 0;
 
@@ -405,6 +405,7 @@ moe_engine::~moe_engine() {
   stop.store(true);
   if (copier.joinable()) copier.join();
   if (s_copy) cudaStreamSynchronize(s_copy);
+  if (s_copy2) cudaStreamSynchronize(s_copy2);
   if (s_comp) cudaStreamSynchronize(s_comp);
   for (auto& c : copies) {
     cudaEventDestroy(c.a);
@@ -445,6 +446,7 @@ moe_engine::~moe_engine() {
   if (t1) cudaEventDestroy(t1);
   if (s_comp) cudaStreamDestroy(s_comp);
   if (s_copy) cudaStreamDestroy(s_copy);
+  if (s_copy2) cudaStreamDestroy(s_copy2);
 }
 
 // The copy engine: drains the device mailbox in FIFO order.  Each request is
@@ -456,10 +458,13 @@ int moe_engine::run_copier() {
   struct Inflight {
     cudaEvent_t a, b;
     int64_t bytes;
+    int buf;
   };
   CopySched sched;
   sched.init(nbuf, xbytes, copy_chunk);
-  std::deque<Inflight> inflight;
+  std::deque<Inflight> dq, sq;                    // demand / speculative stream chunks
+  std::vector<cudaEvent_t> last_ev(nbuf, nullptr);  // last chunk issued to each buffer
+  std::vector<cudaStream_t> last_stream(nbuf, nullptr);
   uint64_t tail = 0;
   int idle = 0;
   auto get_events = [&](cudaEvent_t& a, cudaEvent_t& b) {
@@ -494,40 +499,54 @@ int moe_engine::run_copier() {
       ++tail;
       work = true;
     }
-    // 2. retire finished chunks
-    while (!inflight.empty() && cudaEventQuery(inflight.front().b) == cudaSuccess) {
-      std::lock_guard<std::mutex> g(cmu);
-      const Inflight& c = inflight.front();
-      copies.push_back({c.a, c.b, c.bytes});
-      inflight.pop_front();
-      work = true;
-    }
-    // 3. keep <= 2 chunks queued on the copy stream
-    CopySched::Chunk c;
-    while (inflight.size() < 2 && sched.next(&c)) {
+    // 2. retire finished chunks (per stream, in order)
+    for (auto* q : {&dq, &sq})
+      while (!q->empty() && cudaEventQuery(q->front().b) == cudaSuccess) {
+        std::lock_guard<std::mutex> g(cmu);
+        const Inflight& c = q->front();
+        copies.push_back({c.a, c.b, c.bytes});
+        if (last_ev[c.buf] == c.b) last_ev[c.buf] = nullptr;
+        q->pop_front();
+        work = true;
+      }
+    // 3. demand copies on their own stream (<= 2 queued); speculative chunks
+    //    on a second stream, one at a time and only while no demand copy is
+    //    pending or running, so a demand copy never queues behind speculation
+    auto issue = [&](const CopySched::Chunk& c, cudaStream_t st, std::deque<Inflight>& q) {
       const uint8_t* src = arena + arena_off(c.layer, c.expert) + c.off;
       uint8_t* dst = pool + (size_t)c.buf * slot_stride + c.off;
+      // a chunk to this buffer still in flight on the other stream lands first
+      if (last_ev[c.buf] && last_stream[c.buf] != st &&
+          cudaEventQuery(last_ev[c.buf]) != cudaSuccess)
+        cudaStreamWaitEvent(st, last_ev[c.buf], 0);
       Inflight f;
       get_events(f.a, f.b);
       f.bytes = (int64_t)c.bytes;
-      cudaEventRecord(f.a, s_copy);
-      cudaMemcpyAsync(dst, src, c.bytes, cudaMemcpyHostToDevice, s_copy);
-      cudaEventRecord(f.b, s_copy);
+      f.buf = c.buf;
+      cudaEventRecord(f.a, st);
+      cudaMemcpyAsync(dst, src, c.bytes, cudaMemcpyHostToDevice, st);
+      cudaEventRecord(f.b, st);
+      last_ev[c.buf] = f.b;
+      last_stream[c.buf] = st;
       if (c.last)  // whole expert landed: publish its generation
-        write_value32()(reinterpret_cast<CUstream>(s_copy),
-                        reinterpret_cast<CUdeviceptr>(flags + c.buf), c.gen,
-                        CU_STREAM_WRITE_VALUE_DEFAULT);
+        write_value32()(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flags + c.buf),
+                        c.gen, CU_STREAM_WRITE_VALUE_DEFAULT);
       if (debug || trace_copies) {
-        fprintf(stderr, "[moe-copy %.3f] chunk buf %d gen %u off %zu bytes %zu last %d\n",
+        fprintf(stderr, "[moe-copy %.3f] %s chunk buf %d gen %u off %zu bytes %zu last %d\n",
                 std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
                     .count(),
-                c.buf, c.gen, c.off, c.bytes, (int)c.last);
+                st == s_copy ? "demand" : "spec", c.buf, c.gen, c.off, c.bytes, (int)c.last);
         fflush(stderr);
       }
-      inflight.push_back(f);
+      q.push_back(f);
       work = true;
-    }
-    if (inflight.empty() && sched.empty()) copier_tail.store(tail, std::memory_order_release);
+    };
+    CopySched::Chunk c;
+    while (dq.size() < 2 && sched.next_demand(&c)) issue(c, s_copy, dq);
+    if (dq.empty() && sq.empty() && !sched.has_demand() && sched.next_spec(&c))
+      issue(c, s_copy2, sq);
+    const bool idle_now = dq.empty() && sq.empty() && sched.empty();
+    if (idle_now) copier_tail.store(tail, std::memory_order_release);
     if (!work) {
       if (++idle > 20000) std::this_thread::yield();
 #if defined(__x86_64__)
@@ -968,6 +987,7 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   }
   cudaStreamCreateWithFlags(&e->s_comp, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&e->s_copy, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&e->s_copy2, cudaStreamNonBlocking);
   cudaEventCreate(&e->t0);
   cudaEventCreate(&e->t1);
   const int L = e->L;
