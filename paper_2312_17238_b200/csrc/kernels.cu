@@ -560,9 +560,13 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
   {
     const int g = tid & 3, nf = HD / 16;  // float4s per quarter row
     const float4* q4 = reinterpret_cast<const float4*>(q) + g * nf;
-    for (int t = tid >> 2; t < T; t += (int)blockDim.x >> 2) {
-      const float4* kr =
-          reinterpret_cast<const float4*>(P.kc + (size_t)t * rstride + (size_t)h * HD) + g * nf;
+    // warp-uniform trip count: every lane reaches the quad shuffles
+    const int step = (int)blockDim.x >> 2, tw = (tid & ~31) >> 2;
+    for (int t0 = tw; t0 < T; t0 += step) {
+      const int t = t0 + ((tid & 31) >> 2);
+      const bool live = t < T;
+      const float4* kr = reinterpret_cast<const float4*>(
+                             P.kc + (size_t)(live ? t : 0) * rstride + (size_t)h * HD) + g * nf;
       float a0 = 0.f, a1 = 0.f;
       for (int c = 0; c < nf; c += 8) {
         float4 kv[8];
@@ -579,7 +583,7 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
       float a = a0 + a1;
       a += __shfl_xor_sync(0xffffffffu, a, 1);
       a += __shfl_xor_sync(0xffffffffu, a, 2);
-      if (g == 0) sc[t] = __fdiv_rn(a, rs);
+      if (g == 0 && live) sc[t] = __fdiv_rn(a, rs);
     }
   }
   __syncthreads();
