@@ -573,12 +573,26 @@ GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* part, float
   return j;
 }
 
+// block offsets of the jobs, and the cluster size: the largest divisor of the
+// (common) split count S that is <= 8, so each cluster holds consecutive
+// splits of one column block and reduces them over distributed shared memory
 static int finalize_launch(GLaunch& P) {
   int blk = 0;
   for (int i = 0; i < P.nj; ++i) {
     P.j[i].blk0 = blk;
     blk += P.j[i].M.ncb * P.j[i].S;
   }
+  int c = 1;
+  const int S = P.j[0].S;
+  bool same = true;
+  for (int i = 1; i < P.nj; ++i) same = same && P.j[i].S == S;
+  if (same && !getenv("MOE_NO_CLUSTER"))
+    for (int k = 8; k > 1; --k)
+      if (S % k == 0) {
+        c = k;
+        break;
+      }
+  P.cluster = c;
   return blk;
 }
 
@@ -1975,6 +1989,7 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
   J.blk0 = 0;
   P.cnt = dcnt;
   P.site = -1;
+  finalize_launch(P);
   launch_gemv(L.bits, P, M.ncb * S, 0, false);
   CU(cudaGetLastError());
   CU(cudaDeviceSynchronize());

@@ -58,6 +58,18 @@ MOE_DEV float sigmoid_ref(float x) {  // model.py:229-235 branch-stable logistic
 // (copy engine -> cuStreamWriteValue32) before streaming it.  Dense weights
 // are prefetched before griddepcontrol.wait, overlapping the previous kernel
 // (programmatic dependent launch).
+MOE_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+}
+// load a float from the same shared-memory offset in cluster CTA `rank`
+MOE_DEV float ld_dsmem_f32(const float* p, int rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+  return v;
+}
+
 MOE_DEV bool wait_flag(const uint32_t* f, uint32_t gen, int* err, unsigned long long wait_ns) {
   if ((int)(ld_acquire_u32(f) - gen) >= 0) return true;
   const unsigned long long t0 = globaltimer();
@@ -114,11 +126,15 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   gemv::pdl_trigger();
 
   if (warp == W) {  // ---------------------------------------------- producer
+    if (J.rel_slot >= 0) {
+      gemv::pdl_wait();  // the route is written by the previous kernel
+      // expert parallel: another rank owns this expert -> the whole cluster
+      // (same job) skips, before any cluster barrier
+      if (P.route->buf[J.rel_slot] < 0) return;
+    }
     if (lane == 0) {
       if (J.rel_slot >= 0) {
-        gemv::pdl_wait();  // the route is written by the previous kernel
         const int buf = P.route->buf[J.rel_slot];
-        if (buf < 0) return;  // expert parallel: another rank owns this expert
         wait_flag(P.flags + buf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
         M.base = P.pool + (long long)buf * P.slot_stride + reinterpret_cast<size_t>(M.base);
       }
@@ -137,6 +153,11 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
           ph ^= 1;
         }
       }
+    }
+    __syncwarp();
+    if (P.cluster > 1) {  // the two cluster barriers of the split-K epilogue
+      cluster_sync();
+      cluster_sync();
     }
     return;
   }
@@ -297,33 +318,57 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   gemv::finish_lane<BITS>(y, acc, ztot);
   // cross-warp reduction through the (now idle) ring, fixed order
   float* red = reinterpret_cast<float*>(ring);
+  float* ysum = red + W * 32 * (WC + 1);  // this CTA's partial outputs [32*WC]
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
 #pragma unroll
   for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   const float zo_out = zo_sum * gemv::kZUnscale;
-  float* dst = J.S == 1 ? J.out : J.part + (size_t)s * M.N;
+  const int C = P.cluster, SC = J.S / C;  // cluster = C consecutive splits of one cb
+  const int crank = blockIdx.x % C, sc = s / C;
+  float* dst = SC == 1 ? J.out : J.part + (size_t)sc * M.N;
   for (int t = threadIdx.x; t < 32 * WC; t += nthr) {
     const int l = t / WC, k = t % WC;
     if (l < wcb) {
       float a = 0.f;
 #pragma unroll
       for (int w = 0; w < W; ++w) a += red[(w * 32 + l) * (WC + 1) + k];
-      dst[(size_t)(cb * 32 + l) * WC + k] = a + zo_out;
+      a += zo_out;
+      if (C == 1)
+        dst[(size_t)(cb * 32 + l) * WC + k] = a;
+      else
+        ysum[t] = a;
     }
   }
-  tl_mark(P.site, 2);  // cross-warp reduction + partial written
-  if (J.S == 1) {
+  if (C > 1) {
+    // split-K inside the cluster over distributed shared memory: rank 0 sums
+    // the C partials in rank order, the producer warp joins the barriers
+    cluster_sync();
+    if (crank == 0)
+      for (int t = threadIdx.x; t < wcb * WC; t += nthr) {
+        float a = 0.f;
+        for (int r = 0; r < C; ++r) a += ld_dsmem_f32(ysum + t, r);
+        dst[(size_t)cb * 32 * WC + t] = a;
+      }
+    cluster_sync();  // peers keep their shared memory until rank 0 has read it
+    if (crank != 0) {
+      tl_end(P.site);
+      return;
+    }
+  }
+  tl_mark(P.site, 2);  // cross-warp (+ cluster) reduction, partial written
+  if (SC == 1) {
     tl_end(P.site);
     return;
   }
-  // split-K: the last CTA of this column block sums the S partials in order
+  // split-K across clusters: the last cluster leader of this column block
+  // sums the S / C partials in order
   __threadfence();
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   int* flag = reinterpret_cast<int*>(misc + 8);
   if (threadIdx.x == 0) {
     const int old = atomicAdd(P.cnt + cnt_base + cb, 1);
-    *flag = old == J.S - 1;
+    *flag = old == SC - 1;
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   if (!*flag) {
@@ -334,7 +379,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   for (int t = threadIdx.x; t < wcb * WC; t += nthr) {
     const size_t o = (size_t)cb * 32 * WC + t;
     float a = 0.f;
-    for (int ss = 0; ss < J.S; ++ss) a += __ldcg(J.part + (size_t)ss * M.N + o);
+    for (int ss = 0; ss < SC; ++ss) a += __ldcg(J.part + (size_t)ss * M.N + o);
     J.out[o] = a;
   }
   if (threadIdx.x == 0) P.cnt[cnt_base + cb] = 0;
@@ -1094,7 +1139,7 @@ int gemv_smem_bytes(int bits, int xs_rows, int rb_full, int* nstages, int* stage
   int nst = MOE_GEMV_RING / stage;
   nst = nst < 2 ? 2 : (nst > 16 ? 16 : nst);
   int ring = nst * stage;
-  const int red = MOE_GEMV_WARPS * 32 * (WC + 1) * 4;
+  const int red = MOE_GEMV_WARPS * 32 * (WC + 1) * 4 + 32 * WC * 4;
   if (ring < red) ring = red;
   if (nstages) *nstages = nst;
   if (stage_bytes) *stage_bytes = stage;
@@ -1115,11 +1160,15 @@ static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pd
   cfg.blockDim = dim3(MOE_GEMV_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = P.cluster > 1 ? P.cluster : 1;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, nst, stage);
   g_launches.fetch_add(1);
 }

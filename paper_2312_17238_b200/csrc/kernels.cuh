@@ -37,6 +37,7 @@ struct GLaunch {
   long long slot_stride;
   const uint32_t* flags;        // buffer ready generations (copy engine)
   int* cnt;                     // split-K arrival counters [sum of ncb] (zero between launches)
+  int cluster;                  // CTAs per cluster along the split dimension (divides S)
   int* err;
   unsigned long long wait_ns;
   int site;  // timeline slot of this launch (profiling), -1 none
