@@ -203,9 +203,11 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y);
 
 /* GEMV microbenchmark (profiling aid): njobs K x N synthetic matrices of
  * `bits` per launch, weight sets rotated beyond L2; average us per launch and
- * algorithmic GB/s (reference payload bytes / time). */
+ * algorithmic GB/s (reference payload bytes / time); detail_out (4 doubles, or
+ * NULL): one timeline-traced launch's span and block 0's prologue / loop /
+ * reduction end times, us from the first CTA start. */
 int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t iters, int32_t pdl,
-                   double* us_out, double* gbs_out);
+                   double* us_out, double* gbs_out, double* detail_out);
 
 /* synthetic tensor (oracle/model.py synth_tensor) generated on device */
 int moe_synth_tensor_device(uint64_t seed, uint64_t tensor_id, int64_t count, float scale,

@@ -96,7 +96,7 @@ SIGNATURES = {
     "moe_gemv_device": (I32, [C.POINTER(Matrix), FP, FP]),
     "moe_synth_tensor_device": (I32, [U64, U64, I64, C.c_float, FP]),
     "moe_bench_gemv": (I32, [I32, I32, I32, I32, I32, I32, C.POINTER(C.c_double),
-                             C.POINTER(C.c_double)]),
+                             C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "moe_store_sim_create": (I32, [I32, I32, I32, I32, I64, I32, I32, P, C.POINTER(P)]),
     "moe_store_sim_token": (I32, [P, I32, I32, IP, I32, IP, I32, I32, IP]),
     "moe_store_sim_prefill": (I32, [P, I32, IP, I32, I32, IP]),

@@ -2018,7 +2018,7 @@ int moe_synth_tensor_device(uint64_t seed, uint64_t tensor_id, int64_t count, fl
 // rotated so the working set exceeds L2.  Returns the average device time per
 // launch (back-to-back, PDL as requested) and the algorithmic GB/s.
 int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t iters, int32_t pdl,
-                   double* us_out, double* gbs_out) {
+                   double* us_out, double* gbs_out, double* detail_out) {
   if (njobs < 1 || njobs > MOE_GEMV_MAXJOBS || iters < 1) return fail(MOE_ERR_VALUE, "bad args");
   CU(preload_kernels());
   CU(preload_tile_kernels());
@@ -2106,6 +2106,25 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
                                                  : 0.0));
   if (us_out) *us_out = us;
   if (gbs_out) *gbs_out = alg / (us * 1e-6) / 1e9;
+  if (detail_out) {  // one more launch with the timeline: span + block-0 phase marks
+    TimelineSlot* tl = nullptr;
+    CU(cudaMalloc(&tl, sizeof(TimelineSlot) + 64));
+    TimelineSlot init{~0ull, 0ull};
+    CU(cudaMemset(tl, 0, sizeof(TimelineSlot) + 64));
+    CU(cudaMemcpy(tl, &init, sizeof(init), cudaMemcpyHostToDevice));
+    CU(set_timeline(tl, 1));
+    GLaunch Q = P[0];
+    Q.site = 0;
+    CU(cudaStreamSynchronize(s));
+    launch_gemv(bits, Q, nblk, s, false);
+    CU(cudaStreamSynchronize(s));
+    CU(set_timeline(nullptr, 0));
+    unsigned long long h[10];
+    CU(cudaMemcpy(h, tl, sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(tl);
+    detail_out[0] = (h[1] - h[0]) / 1e3;  // span us
+    for (int i = 0; i < 3; ++i) detail_out[1 + i] = h[2 + i] ? (double)(h[2 + i] - h[0]) / 1e3 : -1;
+  }
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   for (auto p : mats)

@@ -27,9 +27,13 @@ def main():
     for name, bits, K, N, nj in CASES:
         for pdl in (0, 1):
             us, gbs = C.c_double(), C.c_double()
-            _lib.check(L.moe_bench_gemv(bits, K, N, nj, 50, pdl, C.byref(us), C.byref(gbs)))
+            det = (C.c_double * 4)()
+            _lib.check(L.moe_bench_gemv(bits, K, N, nj, 50, pdl, C.byref(us), C.byref(gbs), det))
             out.append({"case": name, "pdl": pdl, "us": round(us.value, 2),
-                        "gbs": round(gbs.value, 1)})
+                        "gbs": round(gbs.value, 1),
+                        "traced": {"span_us": round(det[0], 2), "blk0_prologue_us": round(det[1], 2),
+                                   "blk0_loop_end_us": round(det[2], 2),
+                                   "blk0_reduce_end_us": round(det[3], 2)}})
             print(json.dumps(out[-1]), flush=True)
 
 
