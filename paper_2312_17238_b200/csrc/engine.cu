@@ -586,7 +586,8 @@ static int finalize_launch(GLaunch& P) {
   const int S = P.j[0].S;
   bool same = true;
   for (int i = 1; i < P.nj; ++i) same = same && P.j[i].S == S;
-  if (same && !getenv("MOE_NO_CLUSTER"))
+  static const int min_s = getenv("MOE_CLUSTER_MIN_S") ? atoi(getenv("MOE_CLUSTER_MIN_S")) : 16;
+  if (same && S >= min_s)
     for (int k = 8; k > 1; --k)
       if (S % k == 0) {
         c = k;

@@ -344,31 +344,34 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     // split-K inside the cluster over distributed shared memory: rank 0 sums
     // the C partials in rank order, the producer warp joins the barriers
     cluster_sync();
-    if (crank == 0)
-      for (int t = threadIdx.x; t < wcb * WC; t += nthr) {
-        float a = 0.f;
-        for (int r = 0; r < C; ++r) a += ld_dsmem_f32(ysum + t, r);
-        dst[(size_t)cb * 32 * WC + t] = a;
-      }
-    cluster_sync();  // peers keep their shared memory until rank 0 has read it
-    if (crank != 0) {
-      tl_end(P.site);
-      return;
+    // every rank reduces 1/C of the outputs, reading that slice from all C
+    // ranks (loads first, then the sum in rank order)
+    const int no = wcb * WC, per = (no + C - 1) / C;
+    const int t0 = crank * per, t1 = min(no, t0 + per);
+    for (int t = t0 + threadIdx.x; t < t1; t += nthr) {
+      float v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = r < C ? ld_dsmem_f32(ysum + t, r) : 0.f;
+      float a = 0.f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a += v[r];
+      dst[(size_t)cb * 32 * WC + t] = a;
     }
+    cluster_sync();  // peers keep their shared memory until every slice is read
   }
   tl_mark(P.site, 2);  // cross-warp (+ cluster) reduction, partial written
   if (SC == 1) {
     tl_end(P.site);
     return;
   }
-  // split-K across clusters: the last cluster leader of this column block
-  // sums the S / C partials in order
+  // split-K across clusters: the last CTA of this column block to finish
+  // sums the S / C partials in order (every CTA wrote part of its cluster's)
   __threadfence();
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   int* flag = reinterpret_cast<int*>(misc + 8);
   if (threadIdx.x == 0) {
     const int old = atomicAdd(P.cnt + cnt_base + cb, 1);
-    *flag = old == SC - 1;
+    *flag = old == J.S - 1;
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   if (!*flag) {
