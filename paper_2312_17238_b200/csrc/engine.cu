@@ -586,7 +586,7 @@ static int finalize_launch(GLaunch& P) {
   const int S = P.j[0].S;
   bool same = true;
   for (int i = 1; i < P.nj; ++i) same = same && P.j[i].S == S;
-  static const int min_s = getenv("MOE_CLUSTER_MIN_S") ? atoi(getenv("MOE_CLUSTER_MIN_S")) : 16;
+  static const int min_s = getenv("MOE_CLUSTER_MIN_S") ? atoi(getenv("MOE_CLUSTER_MIN_S")) : 1 << 30;
   if (same && S >= min_s)
     for (int k = 8; k > 1; --k)
       if (S % k == 0) {
@@ -2108,6 +2108,10 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
   if (us_out) *us_out = us;
   if (gbs_out) *gbs_out = alg / (us * 1e-6) / 1e9;
   if (detail_out) {  // one more launch with the timeline: span + block-0 phase marks
+    unsigned long long* ct = nullptr;
+    CU(cudaMalloc(&ct, (size_t)nblk * 4 * 8));
+    CU(cudaMemset(ct, 0, (size_t)nblk * 4 * 8));
+    CU(set_cta_trace(ct));
     TimelineSlot* tl = nullptr;
     CU(cudaMalloc(&tl, sizeof(TimelineSlot) + 64));
     TimelineSlot init{~0ull, 0ull};
@@ -2125,6 +2129,21 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
     cudaFree(tl);
     detail_out[0] = (h[1] - h[0]) / 1e3;  // span us
     for (int i = 0; i < 3; ++i) detail_out[1 + i] = h[2 + i] ? (double)(h[2 + i] - h[0]) / 1e3 : -1;
+    CU(set_cta_trace(nullptr));
+    std::vector<unsigned long long> cv((size_t)nblk * 4);
+    CU(cudaMemcpy(cv.data(), ct, cv.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(ct);
+    if (const char* dump = getenv("MOE_CTA_TRACE_FILE")) {
+      FILE* fp = fopen(dump, "a");
+      if (fp) {
+        fprintf(fp, "# bits %d K %d N %d jobs %d grid %d\n", bits, K, N, njobs, nblk);
+        for (int i = 0; i < nblk; ++i)
+          fprintf(fp, "%d %llu %.3f %.3f %.3f\n", i, cv[i * 4 + 3],
+                  (cv[i * 4 + 0] - h[0]) / 1e3, (cv[i * 4 + 1] - h[0]) / 1e3,
+                  (cv[i * 4 + 2] - h[0]) / 1e3);
+        fclose(fp);
+      }
+    }
   }
   cudaEventDestroy(a);
   cudaEventDestroy(b);

@@ -14,6 +14,7 @@
 
 __device__ TimelineSlot* g_timeline = nullptr;
 __device__ int g_timeline_n = 0;  // span slots; phase marks follow
+__device__ unsigned long long* g_cta_trace = nullptr;  // GEMV microbench: [cta][4]
 
 namespace {
 
@@ -34,6 +35,17 @@ MOE_DEV void tl_mark(int site, int phase) {
   TimelineSlot* t = g_timeline;
   if (t && site >= 0 && threadIdx.x == 0 && blockIdx.x == 0)
     reinterpret_cast<unsigned long long*>(t + g_timeline_n)[site * 8 + phase] = globaltimer();
+}
+MOE_DEV void cta_mark(int slot) {
+  unsigned long long* t = g_cta_trace;
+  if (t && threadIdx.x == 0) {
+    if (slot == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      t[blockIdx.x * 4 + 3] = smid;
+    }
+    t[blockIdx.x * 4 + slot] = globaltimer();
+  }
 }
 MOE_DEV void tl_end(int site) {
   TimelineSlot* t = g_timeline;
@@ -166,12 +178,14 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const int nthr = W * 32;
   gemv::pdl_wait();
   tl_begin(P.site);
+  cta_mark(0);
   if (J.rel_slot >= 0) {
     const int buf = P.route->buf[J.rel_slot];
     if (buf < 0) {  // expert parallel: not ours; contribute zeros to the exchange
       if (s == 0)
         for (int t = threadIdx.x; t < wcb * WC; t += nthr) J.out[(size_t)cb * 32 * WC + t] = 0.f;
-      tl_end(P.site);
+      cta_mark(2);
+    tl_end(P.site);
       return;
     }
     M.zmeta = reinterpret_cast<const __half2*>(P.pool + (long long)buf * P.slot_stride +
@@ -314,6 +328,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     ztot = __shfl_sync(0xffffffffu, zacc, (lane * WC) >> M.g_log2);
   }
   tl_mark(P.site, 1);  // streaming loop done
+  cta_mark(1);
   float y[WC];
   gemv::finish_lane<BITS>(y, acc, ztot);
   // cross-warp reduction through the (now idle) ring, fixed order
@@ -361,6 +376,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   }
   tl_mark(P.site, 2);  // cross-warp (+ cluster) reduction, partial written
   if (SC == 1) {
+    cta_mark(2);
     tl_end(P.site);
     return;
   }
@@ -375,6 +391,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   if (!*flag) {
+    cta_mark(2);
     tl_end(P.site);
     return;
   }
@@ -386,7 +403,8 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     J.out[o] = a;
   }
   if (threadIdx.x == 0) P.cnt[cnt_base + cb] = 0;
-  tl_end(P.site);
+  cta_mark(2);
+    tl_end(P.site);
 }
 
 // ------------------------------------------------------------------ wait
@@ -1092,6 +1110,10 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
 
 // ------------------------------------------------------------------ launchers
 static std::atomic<long long> g_launches{0};
+
+cudaError_t set_cta_trace(unsigned long long* buf) {
+  return cudaMemcpyToSymbol(g_cta_trace, &buf, sizeof(buf));
+}
 
 cudaError_t set_timeline(TimelineSlot* table, int nslots) {
   cudaError_t e = cudaMemcpyToSymbol(g_timeline_n, &nslots, sizeof(nslots));

@@ -164,6 +164,7 @@ struct TimelineSlot {
   unsigned long long start, end;
 };
 cudaError_t set_timeline(TimelineSlot* table, int nslots);  // null disables
+cudaError_t set_cta_trace(unsigned long long* buf);          // GEMV microbench only
 
 // launchers (kernels.cu)
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
