@@ -56,7 +56,10 @@ struct DevMat {  // one tiled matrix in device memory
 // (MOE_GEMV_THREADS threads, ~100 KB smem each); QPS is a multiple of the
 // pipeline stage so every bulk copy stays 16-byte aligned
 int plan_qps(int total_cb, int nquads, int qs) {
-  const int target = MOE_GEMV_MINB * 148;
+  // CTAs per SM the split targets (MOE_GEMV_WAVES; 2 = one resident wave)
+  static const int waves = getenv("MOE_GEMV_WAVES") ? atoi(getenv("MOE_GEMV_WAVES"))
+                                                    : MOE_GEMV_MINB;
+  const int target = waves * 148;
   int S = std::max(1, target / total_cb);  // at most one wave
   int qps = (nquads + S - 1) / S;
   qps = (qps + qs - 1) / qs * qs;
