@@ -241,9 +241,9 @@ def run_b200(args, rank, world):
             rows = [marks[1 + 8 * l + kind] for l in range(nl) if ok[1 + 8 * l + kind]]
             starts = [st[1 + 8 * l + kind] for l in range(nl) if ok[1 + 8 * l + kind]]
             if rows:
-                m = np.array(rows)[:, :nph]
-                prev = np.concatenate([np.array(starts)[:, None], m[:, :-1]], axis=1)
-                phases[nm] = [round(float(x), 2) for x in ((m - prev) / 1e3).mean(axis=0)]
+                mk = np.array(rows)[:, :nph]
+                prev = np.concatenate([np.array(starts)[:, None], mk[:, :-1]], axis=1)
+                phases[nm] = [round(float(x), 2) for x in ((mk - prev) / 1e3).mean(axis=0)]
         span = (en[ok].max() - t0) / 1e3
         timeline = {"token_span_us": round(float(span), 1),
                     "busy_sum_us": round(float(sum(v["sum_us"] for v in kinds.values())), 1),
@@ -259,8 +259,9 @@ def run_b200(args, rank, world):
     if not args.no_e2e:
         def host_greedy(logits):
             return int(np.argmax(logits))
-        ke = min(args.steps, cfg["max_seq_len"] - 16)
+        ke = min(args.steps, cfg["max_seq_len"] - 16 - args.warmup)
         eng.prefill(prompt)
+        eng.decode(args.warmup, sampler=host_greedy)  # same warm cache as the timed run
         t0 = time.perf_counter()
         eng.decode(ke, sampler=host_greedy)
         dt = time.perf_counter() - t0

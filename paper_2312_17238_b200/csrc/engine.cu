@@ -234,6 +234,16 @@ PFN_writeValue32 write_value32() {
 
 }  // namespace
 
+// pinned readback block of finish_call: the device error words, the event
+// count of the call and the head of its event log (one token's worth)
+#define MOE_HSTAT_EV 1024
+struct HostStatus {
+  int err[8];
+  int nev;
+  int pad[3];
+  moe_event ev[MOE_HSTAT_EV];
+};
+
 struct moe_engine {
   moe_model_desc md{};
   moe_cache_cfg cc{};
@@ -336,6 +346,8 @@ struct moe_engine {
   cudaEvent_t tok_ev[4] = {};
   DecodeState* ds_dev = nullptr;        // device decode cursor
   DecodeState* ds_host = nullptr;       // pinned staging for the cursor
+  HostStatus* hstat = nullptr;          // pinned: status words + event-log head
+  float* logits_h = nullptr;            // pinned logits of the last position
   const DecodeState* cur_ds = nullptr;  // non-null while enqueuing a decode token
   std::atomic<uint64_t> copier_tail{0};   // mailbox entries fully copied (serial mode)
   size_t copy_chunk = 2u << 20;           // speculative H2D chunk (demand copies go whole)
@@ -398,7 +410,7 @@ struct moe_engine {
   int enq_logits(int p, float* out);
   int enq_token();
   int run_tokens(int n);
-  int finish_call();
+  int finish_call(bool want_logits = false);
   GJob dense_job(const DevMat& D, const float* x, float* part, float* out, int qps) const;
   int site_of(int l, int kind) const { return 1 + 8 * l + kind; }  // timeline slots
   TimelineSlot* timeline = nullptr;
@@ -425,6 +437,8 @@ moe_engine::~moe_engine() {
     cudaFree(timeline);
   }
   if (ds_host) cudaFreeHost(ds_host);
+  if (hstat) cudaFreeHost(hstat);
+  if (logits_h) cudaFreeHost(logits_h);
   void* ptrs[] = {wte, wpe, lm_head.mem, lnfg, lnfb, pool, flags, x, h, xn, ctx, logits,
                   qkv_part, wo_part, up_part, dn_part, lm_part, qkv_out, wo_out, up_out, dn_out,
                   cnt, kc, vc, route, trace,
@@ -903,8 +917,16 @@ int moe_engine::dbg(const char* what, int l, int p) {
   return ce == cudaSuccess ? MOE_OK : fail(MOE_ERR_CUDA, cudaGetErrorString(ce));
 }
 
-int moe_engine::finish_call() {
+int moe_engine::finish_call(bool want_logits) {
+  // one stream synchronisation per call: the status words, the first chunk
+  // of the event log and (optionally) the logits come back with async copies
+  // into pinned memory queued behind the work
   CU(cudaEventRecord(t1, s_comp));
+  CU(cudaMemcpyAsync(hstat->err, err, sizeof(hstat->err), cudaMemcpyDeviceToHost, s_comp));
+  CU(cudaMemcpyAsync(&hstat->nev, st.scalars + 3, sizeof(int), cudaMemcpyDeviceToHost, s_comp));
+  CU(cudaMemcpyAsync(hstat->ev, st.ev, sizeof(hstat->ev), cudaMemcpyDeviceToHost, s_comp));
+  if (want_logits)
+    CU(cudaMemcpyAsync(logits_h, logits, (size_t)V * 4, cudaMemcpyDeviceToHost, s_comp));
   CU(cudaStreamSynchronize(s_comp));
   units_done = units_issued;
   prof_collect();
@@ -912,20 +934,22 @@ int moe_engine::finish_call() {
   float ms = 0;
   cudaEventElapsedTime(&ms, t0, t1);
   last_ms = ms;
-  int e = 0;
-  CU(cudaMemcpy(&e, err, sizeof(int), cudaMemcpyDeviceToHost));
-  CU(cudaMemset(err, 0, sizeof(int)));
-  int nev = 0;
-  CU(cudaMemcpy(&nev, st.scalars + 3, sizeof(int), cudaMemcpyDeviceToHost));
+  const int e = hstat->err[0];
+  const int nev = hstat->nev;
   if (nev > 0) {
     const size_t old = events.size();
     events.resize(old + nev);
-    CU(cudaMemcpy(events.data() + old, st.ev, nev * sizeof(moe_event), cudaMemcpyDeviceToHost));
-    CU(cudaMemset(st.scalars + 3, 0, sizeof(int)));
+    const int nh = std::min(nev, (int)MOE_HSTAT_EV);
+    memcpy(events.data() + old, hstat->ev, nh * sizeof(moe_event));
+    if (nev > nh)
+      CU(cudaMemcpy(events.data() + old + nh, st.ev + nh, (nev - nh) * sizeof(moe_event),
+                    cudaMemcpyDeviceToHost));
+    CU(cudaMemsetAsync(st.scalars + 3, 0, sizeof(int), s_comp));
   }
+  if (e) CU(cudaMemsetAsync(err, 0, sizeof(int), s_comp));
   if (e & MOE_ERRF_TIMEOUT) {
     int diag[8] = {0};
-    cudaMemcpy(diag, err, sizeof(diag), cudaMemcpyDeviceToHost);
+    memcpy(diag, hstat->err, sizeof(diag));
     const int buf = (int)(((uintptr_t)diag[4] - ((uintptr_t)flags & 0x7fffffff)) / 4);
     cudaMemset(err, 0, sizeof(diag));
     return fail(MOE_ERR_TIMEOUT, "expert buffer never became ready (buffer " +
@@ -1286,6 +1310,8 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->err, 8))) return rc;
   if ((rc = e->dalloc(&e->ds_dev, 1))) return rc;
   CU(cudaHostAlloc(&e->ds_host, sizeof(DecodeState), cudaHostAllocDefault));
+  CU(cudaHostAlloc(&e->hstat, sizeof(HostStatus), cudaHostAllocDefault));
+  CU(cudaHostAlloc(&e->logits_h, (size_t)V * 4, cudaHostAllocDefault));
   // device store state
   const int kk = std::max(k, 1);
   e->ev_cap = std::max(4096, T * L * (3 * e->topk + e->sc.m + 2) + L * E * 3);
@@ -1459,10 +1485,10 @@ int moe_step(moe_engine* e, int32_t token, float* logits_out) {
   rc = e->run_tokens(1);
   if (rc) return rc;
   CU(cudaGetLastError());
-  rc = e->finish_call();
+  rc = e->finish_call(logits_out != nullptr);
   if (rc) return rc;
   e->pos += 1;
-  if (logits_out) CU(cudaMemcpy(logits_out, e->logits, (size_t)e->V * 4, cudaMemcpyDeviceToHost));
+  if (logits_out) memcpy(logits_out, e->logits_h, (size_t)e->V * 4);
   e->has_logits = true;
   return MOE_OK;
 }
@@ -1486,12 +1512,11 @@ int moe_decode_greedy(moe_engine* e, int32_t n, int32_t* tokens_out, float* fina
   rc = e->run_tokens(n);
   if (rc) return rc;
   CU(cudaGetLastError());
-  rc = e->finish_call();
+  rc = e->finish_call(final_logits_out != nullptr);
   if (rc) return rc;
   e->pos += n;
   if (tokens_out) CU(cudaMemcpy(tokens_out, e->tok_hist, (size_t)n * 4, cudaMemcpyDeviceToHost));
-  if (final_logits_out)
-    CU(cudaMemcpy(final_logits_out, e->logits, (size_t)e->V * 4, cudaMemcpyDeviceToHost));
+  if (final_logits_out) memcpy(final_logits_out, e->logits_h, (size_t)e->V * 4);
   return MOE_OK;
 }
 

@@ -311,7 +311,6 @@ class OffloadEngine:
         out = np.empty((max(toks.size, 1), V), np.float32)
         rc = lib().moe_prefill(self._h, toks.ctypes.data_as(_lib.IP), int(toks.size),
                                out.ctypes.data_as(_lib.FP))
-        self._sync_events()
         check(rc)
         self._pos = self._prompt_len = int(toks.size)
         self._last_logits = out[-1].copy()
@@ -324,7 +323,6 @@ class OffloadEngine:
             raise RuntimeError("prefill must run before decoding")
         out = np.empty(self.model.config.vocab_size, np.float32)
         rc = lib().moe_step(self._h, int(token), out.ctypes.data_as(_lib.FP))
-        self._sync_events()
         check(rc)
         self._pos += 1
         self._last_logits = out
@@ -347,7 +345,6 @@ class OffloadEngine:
             fin = np.empty(V, np.float32)
             rc = lib().moe_decode_greedy(self._h, int(n_tokens), toks.ctypes.data_as(_lib.IP),
                                          fin.ctypes.data_as(_lib.FP))
-            self._sync_events()
             check(rc)
             self._pos += n_tokens
             self._last_logits = fin
@@ -375,10 +372,11 @@ class OffloadEngine:
 
     @property
     def events(self) -> list[StoreEvent]:
+        self._sync_events()  # materialised lazily: the engine keeps the log
         return self._events
 
     def recall(self, definition: str = "device_or_staging") -> float:
-        return recall(self._events, definition)
+        return recall(self.events, definition)
 
     def trace(self) -> Trace:
         """engine.py:130-144 (records sorted by (token_pos, layer))."""
