@@ -237,13 +237,22 @@ def run_b200(args, rank, world):
                              "sum_us": round((en[j] - st[j]) / 1e3, 1)}
         phases = {}
         for nm, kind, nph in (("tail", 3, 8), ("combine_ln", 6, 3), ("attention", 1, 3),
-                              ("qkv", 0, 3), ("expert_down", 5, 3)):
+                              ("qkv", 0, 5), ("wo", 2, 5), ("expert_up", 4, 5),
+                              ("expert_down", 5, 5)):
             rows = [marks[1 + 8 * l + kind] for l in range(nl) if ok[1 + 8 * l + kind]]
             starts = [st[1 + 8 * l + kind] for l in range(nl) if ok[1 + 8 * l + kind]]
             if rows:
                 mk = np.array(rows)[:, :nph]
                 prev = np.concatenate([np.array(starts)[:, None], mk[:, :-1]], axis=1)
                 phases[nm] = [round(float(x), 2) for x in ((mk - prev) / 1e3).mean(axis=0)]
+        # tail thread-0 sub-phases (marks in the layer's exchange slot on one GPU)
+        if world == 1:
+            sub = [(marks[1 + 8 * l + 7][:2] - marks[1 + 8 * l + 3][5]) / 1e3 for l in range(nl)
+                   if ok[1 + 8 * l + 3] and marks[1 + 8 * l + 7][1] > 0]
+            if sub:
+                sub = np.array(sub)
+                phases["tail_thread0"] = [round(float(sub[:, 0].mean()), 2),
+                                          round(float((sub[:, 1] - sub[:, 0]).mean()), 2)]
         span = (en[ok].max() - t0) / 1e3
         timeline = {"token_span_us": round(float(span), 1),
                     "busy_sum_us": round(float(sum(v["sum_us"] for v in kinds.values())), 1),

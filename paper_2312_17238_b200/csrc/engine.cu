@@ -293,6 +293,8 @@ struct moe_engine {
 
   // activations
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
+  unsigned long long *wo_acc = nullptr, *dn_acc = nullptr, *qkv_acc = nullptr,
+                     *up_acc = nullptr;  // fixed-point split-K sums (reduce == 2)
   float *qkv_part = nullptr, *wo_part = nullptr, *up_part = nullptr, *dn_part = nullptr,
         *lm_part = nullptr;  // split-K partials
   float *qkv_out = nullptr, *wo_out = nullptr, *up_out = nullptr, *dn_out = nullptr;  // finals
@@ -440,7 +442,7 @@ moe_engine::~moe_engine() {
   if (hstat) cudaFreeHost(hstat);
   if (logits_h) cudaFreeHost(logits_h);
   void* ptrs[] = {wte, wpe, lm_head.mem, lnfg, lnfb, pool, flags, x, h, xn, ctx, logits,
-                  qkv_part, wo_part, up_part, dn_part, lm_part, qkv_out, wo_out, up_out, dn_out,
+                  qkv_part, wo_part, up_part, dn_part, lm_part, wo_acc, dn_acc, qkv_acc, up_acc, qkv_out, wo_out, up_out, dn_out,
                   cnt, kc, vc, route, trace,
                   trace_hidden, tok_dev, tok_hist, tok_in, cand_val, cand_idx, counter, err,
                   st_mem, ds_dev};
@@ -585,6 +587,7 @@ GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* part, float
   j.x = xin;
   j.part = part;
   j.out = out;
+  j.reduce = 1;
   j.QPS = qps;
   j.S = (D.M.nqp + qps - 1) / qps;
   return j;
@@ -629,13 +632,26 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   q.j[0] = dense_job(wq[l], xn, qkv_part, qkv_out, Q_qkv);
   q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, qkv_out + d, Q_qkv);
   q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, qkv_out + 2 * d, Q_qkv);
+  q.err = err;
+  if (cur_ds && l > 0) {  // decode: reset the previous layer's up-projection sums
+    q.zero = up_acc;
+    q.zero_n = 2 * topk * f;
+  }
+  for (int i = 0; i < 3; ++i) {  // fixed-point sums, read (and reset) by the attention
+    q.j[i].reduce = 2;
+    q.j[i].acc = qkv_acc + (size_t)i * d;
+  }
+  const int nq = finalize_launch(q);
+  if (q.cluster > 1)
+    for (int i = 0; i < 3; ++i) q.j[i].reduce = 0;  // partials summed by the attention
   prof_begin(K_QKV);
-  launch_gemv(attn_bits, q, finalize_launch(q), s_comp, pdl && !prof);
+  launch_gemv(attn_bits, q, nq, s_comp, pdl && !prof);
   prof_end(K_QKV);
   dbg("qkv", l, p);
   AttnParams a{};
-  a.qkv_part = qkv_out;
-  a.S = 1;
+  a.qkv_part = qkv_part;
+  a.S = S_qkv / q.cluster;
+  a.acc = q.j[0].reduce == 2 ? qkv_acc : nullptr;
   a.kc = kc + (size_t)l * T * d;
   a.vc = vc + (size_t)l * T * d;
   a.ctx = ctx;
@@ -652,15 +668,21 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   o.nj = 1;
   o.cnt = cnt;
   o.site = site_of(l, 2);
+  o.err = err;
   o.j[0] = dense_job(wo[l], ctx, wo_part, wo_out, Q_wo);
+  o.j[0].reduce = 2;  // fixed-point split-K sums, read (and reset) by the tail
+  o.j[0].acc = wo_acc;
+  const int no = finalize_launch(o);
+  if (o.cluster > 1) o.j[0].reduce = 1;
   prof_begin(K_WO);
-  launch_gemv(attn_bits, o, finalize_launch(o), s_comp, pdl && !prof);
+  launch_gemv(attn_bits, o, no, s_comp, pdl && !prof);
   prof_end(K_WO);
   dbg("wo", l, p);
   TailParams t{};
   t.x = xp;
   t.part = wo_out;
   t.S = 1;
+  t.acc = o.j[0].reduce == 2 ? wo_acc : nullptr;
   t.g2 = ln2g[l];
   t.b2 = ln2b[l];
   t.gate_l = gate[l];
@@ -717,6 +739,8 @@ int moe_engine::enq_experts(int l, int p) {
       J.x = h + (size_t)p * d;
       J.part = up_part + ((size_t)(2 * j + m) * S_up) * f;
       J.out = up_out + (size_t)(2 * j + m) * f;
+      J.reduce = 2;  // fixed-point sums read by the down GEMV's SwiGLU prologue
+      J.acc = up_acc + (size_t)(2 * j + m) * f;
       J.QPS = Q_up;
       J.S = S_up;
     }
@@ -726,15 +750,35 @@ int moe_engine::enq_experts(int l, int p) {
     J.M.zmeta = reinterpret_cast<const __half2*>(xoff[2][3]);
     J.rel_slot = j;
     J.xmode = X_SWIGLU;
-    J.up1 = up_out + (size_t)(2 * j) * f;
-    J.up3 = up_out + (size_t)(2 * j + 1) * f;
+    J.up1 = up_part + (size_t)(2 * j) * S_up * f;
+    J.up3 = up_part + (size_t)(2 * j + 1) * S_up * f;
+    J.xstride = f;
     J.part = dn_part + ((size_t)j * S_dn) * d;
     J.out = dn_out + (size_t)j * d;
+    // single GPU: fixed-point split-K sums read (and reset) by the combine;
+    // expert parallel: reduced in-kernel, the exchange ships dn_out
+    J.reduce = ep_world > 1 ? 1 : 2;
+    J.acc = dn_acc + (size_t)j * d;
     J.QPS = Q_dn;
     J.S = S_dn;
   }
   u.nj = 2 * topk;
   dn.nj = topk;
+  const int nu = finalize_launch(u);
+  if (u.cluster > 1)
+    for (int i = 0; i < u.nj; ++i) u.j[i].reduce = 0;
+  for (int j = 0; j < topk; ++j) {
+    GJob& J = dn.j[j];
+    if (u.j[0].reduce == 2) {
+      J.xfx = 1;
+      J.up1 = reinterpret_cast<const float*>(up_acc + (size_t)(2 * j) * f);
+      J.up3 = reinterpret_cast<const float*>(up_acc + (size_t)(2 * j + 1) * f);
+    }
+  }
+  const int ndn = finalize_launch(dn);
+  if (dn.cluster > 1)
+    for (int j = 0; j < topk; ++j) dn.j[j].reduce = 1;
+  for (int j = 0; j < topk; ++j) dn.j[j].xS = dn.j[j].xfx ? 1 : S_up / u.cluster;
   if (serial_copies) {  // ncu / debugging: the host drains the mailbox before the GEMV
     CU(cudaStreamSynchronize(s_comp));
     {  // entries posted so far = device-side head (seq[1])
@@ -748,17 +792,24 @@ int moe_engine::enq_experts(int l, int p) {
   if (prof)  // keep copy waits out of the GEMV's event-timed span
     launch_wait_ready(route + p, topk, flags, err, wait_ns, s_comp);
   prof_begin(K_UP);
-  launch_gemv(expert_bits, u, finalize_launch(u), s_comp, pdl && !prof);
+  launch_gemv(expert_bits, u, nu, s_comp, pdl && !prof);
   prof_end(K_UP);
   dbg("up", -1, p);
   prof_begin(K_DOWN);
-  launch_gemv(expert_bits, dn, finalize_launch(dn), s_comp, pdl && !prof);
+  launch_gemv(expert_bits, dn, ndn, s_comp, pdl && !prof);
   prof_end(K_DOWN);
   dbg("down", -1, p);
   CombineParams c{};
   c.h = h + (size_t)p * d;
   c.part = dn_out;
   c.S = 1;
+  c.acc = dn.j[0].reduce == 2 ? dn_acc : nullptr;
+  // the up sums are reset for the next layer by the next QKV / lm_head GEMV in
+  // decode; prefill interleaves positions, so its combine resets them itself
+  if (u.j[0].reduce == 2 && !cur_ds) {
+    c.zero = up_acc;
+    c.zero_n = 2 * topk * f;
+  }
   if (ep_world > 1) {  // sum-exchange of the slot buffers over peer memory
     ExchangeParams xp{};
     xp.src = dn_out;
@@ -806,12 +857,18 @@ int moe_engine::enq_logits(int p, float* out) {
   g.cnt = cnt;
   g.site = 1 + 8 * L;
   g.j[0] = dense_job(lm_head, xn, lm_part, out, Q_lm);
+  if (cur_ds) {  // decode: reset the last layer's up-projection sums
+    g.zero = up_acc;
+    g.zero_n = 2 * topk * f;
+  }
+  g.j[0].reduce = 0;  // the logits kernel sums the splits
+  const int ng = finalize_launch(g);
   prof_begin(K_LM);
-  launch_gemv(lm_bits, g, finalize_launch(g), s_comp, pl);
+  launch_gemv(lm_bits, g, ng, s_comp, pl);
   prof_end(K_LM);
   LogitsParams lp{};
-  lp.part = out;
-  lp.S = 1;
+  lp.part = lm_part;
+  lp.S = S_lm / g.cluster;
   lp.V = V;
   lp.logits = out;
   lp.cand_val = cand_val;
@@ -1056,7 +1113,7 @@ static int load_dense_mat(moe_engine* e, const moe_matrix* m, DevMat* D, const c
   int rc = make_layout(m, &Lo, nm);
   if (rc) return rc;
   if (D->mem) cudaFree(D->mem);
-  CU(cudaMalloc(&D->mem, Lo.total()));
+  CU(cudaMalloc(&D->mem, Lo.total() + 64));  // + slack: 16-byte bulk copies of zmeta
   e->dev_bytes += Lo.total();
   rc = upload_and_tile(m, Lo, static_cast<uint8_t*>(D->mem), e->s_comp);
   if (rc) return rc;
@@ -1264,7 +1321,7 @@ int moe_finalize(moe_engine* e) {
       return fail(MOE_ERR_UNKNOWN_EXPERT, "expert payload missing");
   const int k = e->cc.k, b = e->cc.b;
   e->nbuf = L * k + b + E + k + e->sc.m + 2;
-  CU(cudaMalloc(&e->pool, e->slot_stride * (size_t)e->nbuf));
+  CU(cudaMalloc(&e->pool, e->slot_stride * (size_t)e->nbuf + 64));
   e->dev_bytes += e->slot_stride * (size_t)e->nbuf;
   int rc;
   if ((rc = e->dalloc(&e->flags, e->nbuf))) return rc;
@@ -1289,6 +1346,10 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->wo_part, (size_t)e->S_wo * d))) return rc;
   if ((rc = e->dalloc(&e->up_part, (size_t)2 * e->topk * e->S_up * f))) return rc;
   if ((rc = e->dalloc(&e->dn_part, (size_t)e->topk * e->S_dn * d))) return rc;
+  if ((rc = e->dalloc(&e->wo_acc, (size_t)d))) return rc;
+  if ((rc = e->dalloc(&e->qkv_acc, (size_t)3 * d))) return rc;
+  if ((rc = e->dalloc(&e->up_acc, (size_t)2 * e->topk * f))) return rc;
+  if ((rc = e->dalloc(&e->dn_acc, (size_t)e->topk * d))) return rc;
   if ((rc = e->dalloc(&e->lm_part, (size_t)e->S_lm * V))) return rc;
   if ((rc = e->dalloc(&e->qkv_out, (size_t)3 * d))) return rc;
   if ((rc = e->dalloc(&e->wo_out, (size_t)d))) return rc;
@@ -1881,7 +1942,7 @@ int moe_synth_model(moe_engine* e, uint64_t seed, int32_t attn_bits, int32_t exp
       if (rc) break;
       DevMat& D = j == 0 ? e->wq[l] : j == 1 ? e->wk[l] : j == 2 ? e->wv[l] : e->wo[l];
       if (D.mem) cudaFree(D.mem);
-      CU(cudaMalloc(&D.mem, lo.total()));
+      CU(cudaMalloc(&D.mem, lo.total() + 64));
       e->dev_bytes += lo.total();
       CU(cudaMemcpyAsync(D.mem, Q.tiled, lo.total(), cudaMemcpyDeviceToDevice, s));
       D.M = matdev_from(lo, static_cast<uint8_t*>(D.mem));
@@ -2013,6 +2074,7 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
   J.x = dx;
   J.part = part;
   J.out = dy;
+  J.reduce = 1;
   J.S = S;
   J.QPS = qps;
   J.blk0 = 0;
@@ -2069,7 +2131,7 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
     Layout lo;
     rc = synth_matrix(Q, 7, 100 + i % 8, K, N, 0.01, bits, 0, &lo, s);
     if (rc) break;
-    CU(cudaMalloc(&mats[i], mbytes));
+    CU(cudaMalloc(&mats[i], mbytes + 64));
     CU(cudaMemcpyAsync(mats[i], Q.tiled, mbytes, cudaMemcpyDeviceToDevice, s));
   }
   CU(cudaStreamSynchronize(s));
@@ -2100,6 +2162,7 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
       J.x = x;
       J.part = part + (size_t)j * S * N;
       J.out = out + (size_t)j * N;
+      J.reduce = 1;
       J.QPS = qps;
       J.S = S;
     }
@@ -2116,7 +2179,7 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
     if (le != cudaSuccess)
       return fail(MOE_ERR_CUDA, std::string("gemv launch (grid ") + std::to_string(nblk) +
                                     ", smem " + std::to_string(gemv_smem_bytes(
-                                        bits, qps * 4, M0.rb_full, nullptr, nullptr)) +
+                                        bits, qps * 4, 0, M0.rb_full, nullptr, nullptr)) +
                                     "): " + cudaGetErrorString(le));
   }
   for (int w = 0; w < 3; ++w) launch_gemv(bits, P[w % nsets], nblk, s, pdl != 0);

@@ -99,9 +99,23 @@ MOE_DEV bool wait_flag(const uint32_t* f, uint32_t gen, int* err, unsigned long 
   return true;
 }
 
+MOE_DEV void fx_add(unsigned long long* p, float a, int* err) {
+  const float q = a * MOE_FX_SCALE;
+  if (!(fabsf(q) < 0x1p62f)) {  // non-finite or out of range: the reference would
+    if (err) atomicOr(err, MOE_ERRF_NONFINITE_GATE);  // fail on the next gate input
+    return;
+  }
+  atomicAdd(p, (unsigned long long)__float2ll_rn(q));
+}
+// consumer side: fixed-point sum -> fp32 (one rounding); the consumer resets
+// the sums (fx_clear) after all its loads are issued
+MOE_DEV float fx_val(unsigned long long v) {
+  return __double2float_rn((double)(long long)v * MOE_FX_UNSCALE);
+}
+
 template <int BITS>
 __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
-    k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int nst, int stage_bytes) {
+    k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int zs_cap, int nst, int stage_bytes) {
   constexpr int WC = Fmt<BITS>::WC;
   constexpr bool QUANT = BITS <= 4;
   constexpr int W = MOE_GEMV_WARPS, QPW = gemv_qpw(BITS), QS = gemv_qs(BITS);
@@ -109,9 +123,11 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 16;
   float* misc = reinterpret_cast<float*>(smem + 256);  // [16]: zo partials, flags
+  uint64_t* zbar = reinterpret_cast<uint64_t*>(smem + 384);  // zero-point slice landed
   float* xs = reinterpret_cast<float*>(smem + 512);
   float* xz = xs + xs_cap;  // x * zscale per row (uniform zero-point runs)
-  uint8_t* ring = smem + 512 + (((size_t)xs_cap * 8 + 127) & ~(size_t)127);
+  __half2* zsm = reinterpret_cast<__half2*>(xz + xs_cap);  // the CTA's zmeta slice [zs_cap]
+  uint8_t* ring = smem + 512 + (((size_t)xs_cap * 8 + (size_t)zs_cap * 4 + 127) & ~(size_t)127);
 
   int ji = 0, cnt_base = 0;
   for (int i = 1; i < P.nj; ++i)
@@ -126,12 +142,23 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const int rb = rec_bytes(BITS, wcb, M.g_log2, M.sg_log2);
   const int nit = (max(qe - qs, 0) + QS - 1) / QS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qv = min(qe, M.nquads);  // real quads of this split
+  const int row0 = qs * 4, nrows = max(qv - qs, 0) * 4;
+  const int gcb0 = QUANT ? ((cb * 32 * WC) >> M.g_log2) : 0;  // first zero group of the cb
+  const bool uni = QUANT && M.runs_uniform;
+  // uniform runs: the zero-point runs of the CTA's rows are one contiguous
+  // zmeta slice [z0, z1], streamed to smem by the producer ahead of the
+  // records (16-byte aligned bulk copy; `zlead` entries of alignment slack)
+  const bool zstage = uni && nrows > 0 && zs_cap > 0;
+  const int z0 = zstage ? (int)(((int64_t)row0 * M.G + gcb0) >> M.sg_log2) : 0;
+  const int z1 = zstage ? (int)(((int64_t)(row0 + nrows - 1) * M.G + gcb0) >> M.sg_log2) : 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) {
       gemv::mbar_init(full + i, 1);
       gemv::mbar_init(empty + i, W);
     }
+    gemv::mbar_init(zbar, 1);
     gemv::mbar_fence_init();
   }
   __syncthreads();
@@ -147,8 +174,19 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     if (lane == 0) {
       if (J.rel_slot >= 0) {
         const int buf = P.route->buf[J.rel_slot];
-        wait_flag(P.flags + buf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
-        M.base = P.pool + (long long)buf * P.slot_stride + reinterpret_cast<size_t>(M.base);
+        // the tail saw the buffer's copy already published: no flag round trip
+        if (!P.route->ready[J.rel_slot])
+          wait_flag(P.flags + buf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
+        const uint8_t* b = P.pool + (long long)buf * P.slot_stride;
+        M.base = b + reinterpret_cast<size_t>(M.base);
+        M.zmeta = reinterpret_cast<const __half2*>(b + reinterpret_cast<size_t>(M.zmeta));
+      }
+      if (zstage) {
+        const uintptr_t za = reinterpret_cast<uintptr_t>(M.zmeta + z0);
+        const uint32_t lead = (uint32_t)(za & 15u);
+        const uint32_t bytes = ((uint32_t)(z1 - z0 + 1) * 4u + lead + 15u) & ~15u;
+        gemv::mbar_arrive_tx(zbar, bytes);
+        gemv::bulk_g2s(zsm, reinterpret_cast<const void*>(za - lead), bytes, zbar);
       }
       const uint8_t* src = M.base + cb_offset(M, cb) + (int64_t)qs * rb;
       int st = 0;
@@ -179,46 +217,62 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   gemv::pdl_wait();
   tl_begin(P.site);
   cta_mark(0);
-  if (J.rel_slot >= 0) {
-    const int buf = P.route->buf[J.rel_slot];
-    if (buf < 0) {  // expert parallel: not ours; contribute zeros to the exchange
-      if (s == 0)
-        for (int t = threadIdx.x; t < wcb * WC; t += nthr) J.out[(size_t)cb * 32 * WC + t] = 0.f;
-      cta_mark(2);
-    tl_end(P.site);
-      return;
-    }
-    M.zmeta = reinterpret_cast<const __half2*>(P.pool + (long long)buf * P.slot_stride +
-                                               reinterpret_cast<size_t>(M.zmeta));
-    // the prologue reads this buffer's zero-point metadata: wait for the copy too
-    if (threadIdx.x == 0) wait_flag(P.flags + buf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
-    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  if (P.zero) {  // reset sums an earlier kernel consumed (e.g. the previous layer's up)
+    const int per = (P.zero_n + gridDim.x - 1) / gridDim.x;
+    const int z0 = blockIdx.x * per, z1 = min(P.zero_n, z0 + per);
+    for (int i = z0 + threadIdx.x; i < z1; i += nthr) P.zero[i] = 0ull;
   }
-  const int qv = min(qe, M.nquads);  // real quads of this split
-  const int row0 = qs * 4, nrows = max(qv - qs, 0) * 4;
+  // expert jobs: the route load is issued with the x loads (independent)
+  const int ebuf = J.rel_slot >= 0 ? P.route->buf[J.rel_slot] : 0;
   const float xscale = QUANT ? gemv::kXScale : 1.f;
-  const int gcb0 = QUANT ? ((cb * 32 * WC) >> M.g_log2) : 0;  // first zero group of the cb
-  float zo_part = 0.f;
-  const bool uni = QUANT && M.runs_uniform;
-  // batches of 4 rows per thread: every load of a batch is issued before any
-  // use (x or the up-projection pair, and the row's zero-point run)
+  // x (or the SwiGLU of the up projections) in batches of 4 rows per thread:
+  // every load of a batch is issued before any use
   for (int i0 = 0; i0 < nrows; i0 += 4 * nthr) {
     float va[4], vb[4];
-    __half2 zr[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int i = i0 + u * nthr + threadIdx.x;
       const int r = row0 + i;
       const bool in = i < nrows;
-      if (J.xmode == X_PLAIN) {
+      if (J.xfx) {  // fixed-point sums of a reduce == 2 producer
+        const unsigned long long* q1 =
+            reinterpret_cast<const unsigned long long*>(J.xmode == X_PLAIN ? J.x : J.up1);
+        va[u] = in ? fx_val(__ldcg(q1 + r)) : 0.f;
+        vb[u] = (in && J.xmode != X_PLAIN)
+                    ? fx_val(__ldcg(reinterpret_cast<const unsigned long long*>(J.up3) + r))
+                    : 0.f;
+      } else if (J.xS > 1) {  // unreduced producer partials: sum them in split order
+        // (up to 8 splits per round, every load of the round in flight)
+        float a = 0.f, b = 0.f;
+        if (in) {
+          const float* pa = J.xmode == X_PLAIN ? J.x : J.up1;
+          const bool two = J.xmode != X_PLAIN;
+          for (int s0 = 0; s0 < J.xS; s0 += 8) {
+            float ta[8], tb[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const bool ok = s0 + k < J.xS;
+              const size_t o = (size_t)(s0 + k) * J.xstride + r;
+              ta[k] = ok ? __ldcg(pa + o) : 0.f;
+              tb[k] = ok && two ? __ldcg(J.up3 + o) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (s0 + k < J.xS) {
+                a += ta[k];
+                b += tb[k];
+              }
+          }
+        }
+        va[u] = a;
+        vb[u] = b;
+      } else if (J.xmode == X_PLAIN) {
         va[u] = in ? __ldcg(J.x + r) : 0.f;
         vb[u] = 0.f;
       } else {
         va[u] = in ? __ldcg(J.up1 + r) : 0.f;
         vb[u] = in ? __ldcg(J.up3 + r) : 0.f;
       }
-      if (uni) zr[u] = in ? __ldg(M.zmeta + (((int64_t)r * M.G + gcb0) >> M.sg_log2))
-                          : __float2half2_rn(0.f);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -227,15 +281,54 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       float xv = va[u];
       if (J.xmode != X_PLAIN)  // SwiGLU of the up projections (model.py:223-226)
         xv = __fmul_rn(__fmul_rn(va[u], sigmoid_ref(va[u])), vb[u]);
-      xv *= xscale;
-      xs[i] = xv;
-      if (uni) {  // the cb's groups of this row share one zero run
-        const float2 zm = __half22float2(zr[u]);
+      xs[i] = xv * xscale;
+    }
+  }
+  tl_mark(P.site, 0);  // x slice in smem
+  if (J.rel_slot >= 0) {
+    if (ebuf < 0) {  // expert parallel: not ours; contribute zeros to the exchange
+      float* zdst = J.reduce == 2 ? nullptr : J.reduce ? (s == 0 ? J.out : nullptr)
+                             : (s % P.cluster == 0 ? J.part + (size_t)(s / P.cluster) * M.N
+                                                   : nullptr);
+      if (zdst)
+        for (int t = threadIdx.x; t < wcb * WC; t += nthr) zdst[(size_t)cb * 32 * WC + t] = 0.f;
+      cta_mark(2);
+      tl_end(P.site);
+      return;
+    }
+    if (QUANT && (!uni || zs_cap == 0)) {  // zmeta is read from global
+      M.zmeta = reinterpret_cast<const __half2*>(P.pool + (long long)ebuf * P.slot_stride +
+                                                 reinterpret_cast<size_t>(M.zmeta));
+      if (threadIdx.x == 0 && !P.route->ready[J.rel_slot])
+        wait_flag(P.flags + ebuf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
+      asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    }
+  }
+  float zo_part = 0.f;
+  if (uni && nrows > 0) {  // x * zscale per row and the CTA's sum of x * zoffset
+    int zlead = 0;
+    if (zstage) {
+      gemv::mbar_wait(zbar, 0);
+      // expert slots are 256-byte aligned: the offset has the address's alignment
+      const uintptr_t za = J.rel_slot >= 0
+          ? (uintptr_t)(reinterpret_cast<size_t>(M.zmeta) + (size_t)z0 * 4)
+          : reinterpret_cast<uintptr_t>(M.zmeta + z0);
+      zlead = (int)(za & 15u) >> 2;
+    }
+    for (int i0 = 0; i0 < nrows; i0 += 4 * nthr)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nthr + threadIdx.x;
+        if (i >= nrows) continue;
+        const int run = (int)(((int64_t)(row0 + i) * M.G + gcb0) >> M.sg_log2);
+        const float2 zm =
+            __half22float2(zstage ? zsm[zlead + run - z0] : __ldg(M.zmeta + run));
+        const float xv = xs[i];
         xz[i] = xv * zm.x;
         zo_part = fmaf(xv, zm.y, zo_part);
       }
-    }
   }
+  tl_mark(P.site, 1);  // zero-point slice landed, x * zscale done
   if (QUANT && M.runs_uniform) {
     zo_part = warp_sum(zo_part);
     if (lane == 0) misc[warp] = zo_part;
@@ -246,7 +339,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
 #pragma unroll
     for (int w = 0; w < W; ++w) zo_sum += misc[w];
 
-  tl_mark(P.site, 0);  // prologue done (x slice, zero-point rows)
+  tl_mark(P.site, 2);  // prologue done (x slice, zero-point rows)
   float acc[WC];
 #pragma unroll
   for (int k = 0; k < WC; ++k) acc[k] = 0.f;
@@ -327,7 +420,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       for (int o = Z.zpr; o < 32; o <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, o);
     ztot = __shfl_sync(0xffffffffu, zacc, (lane * WC) >> M.g_log2);
   }
-  tl_mark(P.site, 1);  // streaming loop done
+  tl_mark(P.site, 3);  // streaming loop done
   cta_mark(1);
   float y[WC];
   gemv::finish_lane<BITS>(y, acc, ztot);
@@ -341,7 +434,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const float zo_out = zo_sum * gemv::kZUnscale;
   const int C = P.cluster, SC = J.S / C;  // cluster = C consecutive splits of one cb
   const int crank = blockIdx.x % C, sc = s / C;
-  float* dst = SC == 1 ? J.out : J.part + (size_t)sc * M.N;
+  float* dst = (SC == 1 && J.reduce) ? J.out : J.part + (size_t)sc * M.N;
   for (int t = threadIdx.x; t < 32 * WC; t += nthr) {
     const int l = t / WC, k = t % WC;
     if (l < wcb) {
@@ -349,10 +442,12 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
 #pragma unroll
       for (int w = 0; w < W; ++w) a += red[(w * 32 + l) * (WC + 1) + k];
       a += zo_out;
-      if (C == 1)
-        dst[(size_t)(cb * 32 + l) * WC + k] = a;
-      else
+      if (C > 1)
         ysum[t] = a;
+      else if (J.reduce == 2)
+        fx_add(J.acc + (size_t)(cb * 32 + l) * WC + k, a, P.err);
+      else
+        dst[(size_t)(cb * 32 + l) * WC + k] = a;
     }
   }
   if (C > 1) {
@@ -374,19 +469,22 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     }
     cluster_sync();  // peers keep their shared memory until every slice is read
   }
-  tl_mark(P.site, 2);  // cross-warp (+ cluster) reduction, partial written
-  if (SC == 1) {
+  tl_mark(P.site, 4);  // cross-warp (+ cluster) reduction, partial written
+  if (SC == 1 || J.reduce != 1) {  // done, or the consumer sums the partials
     cta_mark(2);
     tl_end(P.site);
     return;
   }
   // split-K across clusters: the last CTA of this column block to finish
-  // sums the S / C partials in order (every CTA wrote part of its cluster's)
-  __threadfence();
+  // sums the S / C partials in order (every CTA wrote part of its cluster's).
+  // One thread publishes the CTA's partial (barrier, then a gpu-scope fence
+  // and the arrival count) and, in the last CTA, acquires the others'.
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   int* flag = reinterpret_cast<int*>(misc + 8);
   if (threadIdx.x == 0) {
+    __threadfence();
     const int old = atomicAdd(P.cnt + cnt_base + cb, 1);
+    __threadfence();
     *flag = old == J.S - 1;
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
@@ -395,12 +493,29 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     tl_end(P.site);
     return;
   }
-  __threadfence();
-  for (int t = threadIdx.x; t < wcb * WC; t += nthr) {
-    const size_t o = (size_t)cb * 32 * WC + t;
-    float a = 0.f;
-    for (int ss = 0; ss < SC; ++ss) a += __ldcg(J.part + (size_t)ss * M.N + o);
-    J.out[o] = a;
+  // 4 outputs x 8 splits per thread in flight, then the in-order sums
+  const int no = wcb * WC;
+  const float* pbase = J.part + (size_t)cb * 32 * WC;
+  for (int t0 = threadIdx.x; t0 < no; t0 += 4 * nthr) {
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int s0 = 0; s0 < SC; s0 += 8) {
+      float v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int t = t0 + u * nthr;
+          v[u][k] = (t < no && s0 + k < SC) ? __ldcg(pbase + (size_t)(s0 + k) * M.N + t) : 0.f;
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (s0 + k < SC) a[u] += v[u][k];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (t0 + u * nthr < no) J.out[(size_t)cb * 32 * WC + t0 + u * nthr] = a[u];
   }
   if (threadIdx.x == 0) P.cnt[cnt_base + cb] = 0;
   cta_mark(2);
@@ -532,10 +647,17 @@ __global__ void __launch_bounds__(256) k_attention(AttnParams P) {
   for (int i = threadIdx.x; i < hd; i += blockDim.x) {
     const int o = h * hd + i;
     float a = 0.f, bk = 0.f, bv = 0.f;
-    for (int s = 0; s < P.S; ++s) {
-      a += __ldcg(P.qkv_part + ((size_t)0 * P.S + s) * d + o);
-      bk += __ldcg(P.qkv_part + ((size_t)1 * P.S + s) * d + o);
-      bv += __ldcg(P.qkv_part + ((size_t)2 * P.S + s) * d + o);
+    if (P.acc) {
+      a = fx_val(__ldcg(P.acc + o));
+      bk = fx_val(__ldcg(P.acc + d + o));
+      bv = fx_val(__ldcg(P.acc + 2 * d + o));
+      P.acc[o] = P.acc[d + o] = P.acc[2 * d + o] = 0ull;
+    } else {
+      for (int s = 0; s < P.S; ++s) {
+        a += __ldcg(P.qkv_part + ((size_t)0 * P.S + s) * d + o);
+        bk += __ldcg(P.qkv_part + ((size_t)1 * P.S + s) * d + o);
+        bv += __ldcg(P.qkv_part + ((size_t)2 * P.S + s) * d + o);
+      }
     }
     q[i] = a;
     P.kc[kvrow + i] = bk;
@@ -611,14 +733,34 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
   const int T = pos + 1;
   const size_t rstride = (size_t)P.H * HD;
   const float* qg = P.qkv_part + (size_t)h * HD;
-  const float* kg = qg + d;
-  const float* vg = qg + 2 * d;
   float* krow = P.kc + (size_t)pos * rstride + (size_t)h * HD;
   float* vrow = P.vc + (size_t)pos * rstride + (size_t)h * HD;
-  for (int i = tid; i < HD; i += blockDim.x) {  // KV append (model.py:293, KVCache.append)
-    q[i] = __ldcg(qg + i);
-    krow[i] = __ldcg(kg + i);
-    vrow[i] = __ldcg(vg + i);
+  // KV append (model.py:293, KVCache.append); the QKV GEMV leaves its split-K
+  // partials [3][S][d] unreduced: summed here in split order
+  const size_t sstride = (size_t)P.S * d;
+  if (P.acc) {  // fixed-point sums of the QKV GEMV: read, then reset for the next layer
+    unsigned long long* qa = P.acc + (size_t)h * HD;
+    for (int i = tid; i < HD; i += blockDim.x) {
+      const unsigned long long a = __ldcg(qa + i), bk = __ldcg(qa + d + i),
+                               bv = __ldcg(qa + 2 * d + i);
+      q[i] = fx_val(a);
+      krow[i] = fx_val(bk);
+      vrow[i] = fx_val(bv);
+      qa[i] = qa[d + i] = qa[2 * d + i] = 0ull;
+    }
+  } else {
+    for (int i = tid; i < HD; i += blockDim.x) {
+      float a = 0.f, bk = 0.f, bv = 0.f;
+#pragma unroll 4
+      for (int s = 0; s < P.S; ++s) {
+        a += __ldcg(qg + (size_t)s * d + i);
+        bk += __ldcg(qg + sstride + (size_t)s * d + i);
+        bv += __ldcg(qg + 2 * sstride + (size_t)s * d + i);
+      }
+      q[i] = a;
+      krow[i] = bk;
+      vrow[i] = bv;
+    }
   }
   __syncthreads();
   tl_mark(P.site, 0);
@@ -704,6 +846,36 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
 // record (engine.py:122-128); then the device store: acquire each selected
 // expert in descending-weight order and speculative_load the guesses
 // (engine.py:222-231).
+// tail: hs = x + Wo output (fp32 partial or fixed-point sums, reset after
+// the loads), V values per thread with every load in flight first
+template <int V, bool FX>
+MOE_DEV void residual_in(const TailParams& P, float* hs, int tid) {
+  const int d = P.d, nt = (int)blockDim.x;
+  float xa[V], pa[V];
+  unsigned long long qa[FX ? V : 1];
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const int i = tid + u * nt;
+    xa[u] = i < d ? __ldcg(P.x + i) : 0.f;
+    if constexpr (FX)
+      qa[u] = i < d ? __ldcg(P.acc + i) : 0ull;
+    else
+      pa[u] = i < d ? __ldcg(P.part + i) : 0.f;
+  }
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const int i = tid + u * nt;
+    if constexpr (FX) pa[u] = fx_val(qa[u]);
+    if (i < d) hs[i] = __fadd_rn(xa[u], pa[u]);
+  }
+  if constexpr (FX)  // reset the fixed-point sums for the next Wo GEMV
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int i = tid + u * nt;
+      if (i < d) P.acc[i] = 0ull;
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   extern __shared__ __align__(128) unsigned char tsm[];
   const int d = P.d, E = P.E;
@@ -718,6 +890,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   double* gpart = reinterpret_cast<double*>(
       tsm + ((3 * (size_t)d * 4 + (hg ? (guess ? 2 : 1) * (size_t)d * E * 2 : 0) + 15) & ~15));
   int* sst = reinterpret_cast<int*>(gpart + 2 * blockDim.x);
+  uint32_t* fls = reinterpret_cast<uint32_t*>(sst + store::stage_ints(P.st) + 4);  // [nbuf]
   __shared__ float red[33];
   __shared__ float lg[64];
   __shared__ __align__(8) uint64_t wbar;
@@ -748,21 +921,22 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   const size_t slot = (size_t)pos * P.n_layers + P.layer;
   float* th = P.trace_hidden ? P.trace_hidden + slot * d : nullptr;
   StoreDev S = P.st;
-  if (P.mode == 0) S = store::stage_in(P.st, sst);  // overlaps the residual loads
-  {  // residual: all loads first, then the stores (no load waits behind a store)
-    constexpr int MAXV = 8;  // d <= 8192 with 1024 threads
-    float xa[MAXV], pa[MAXV];
-#pragma unroll
-    for (int u = 0; u < MAXV; ++u) {
-      const int i = tid + u * (int)blockDim.x;
-      xa[u] = i < d ? __ldcg(P.x + i) : 0.f;
-      pa[u] = i < d ? __ldcg(P.part + i) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < MAXV; ++u) {
-      const int i = tid + u * (int)blockDim.x;
-      if (i < d) hs[i] = __fadd_rn(xa[u], pa[u]);
-    }
+  if (P.mode == 0) {
+    S = store::stage_in(P.st, sst);  // overlaps the residual loads
+    // snapshot of the buffers' published copy generations: a routed buffer
+    // whose copy had landed is marked ready, so the GEMVs skip the flag wait
+    if (P.st.flags)
+      for (int i = tid; i < P.st.nbuf; i += blockDim.x)
+        fls[i] = ld_acquire_u32(const_cast<const uint32_t*>(P.st.flags) + i);
+  }
+  // residual: all loads first, then the stores (no load waits behind a store)
+  if (P.acc) {
+    if (d <= 4 * (int)blockDim.x)
+      residual_in<4, true>(P, hs, tid);
+    else
+      residual_in<8, true>(P, hs, tid);
+  } else {
+    residual_in<8, false>(P, hs, tid);  // d <= 8192 with 1024 threads
   }
   tl_mark(P.site, 0);
   gemv::mbar_wait(&wbar, 0);
@@ -866,6 +1040,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
       R.w[j] = j < k ? __fdiv_rn(ez[j], sum) : 0.f;
       R.buf[j] = -1;
       R.gen[j] = 0;
+      R.ready[j] = 0;
     }
     TraceRecDev tr;
     tr.pos = pos;
@@ -875,13 +1050,18 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
       tr.weights[j] = j < k ? R.w[j] : 0.f;
     }
     P.trace[slot] = tr;
+    tl_mark(P.site + 4, 0);  // profiling: softmax + trace record (exchange slot unused)
     if (bad) {
       atomicOr(P.st.err, MOE_ERRF_NONFINITE_GATE);
     } else if (P.mode == 0) {
       const int m = (guess && P.m > 0) ? P.m : 0;
       store::resolve_token(S, P.layer, sel, k, gsel_sh, m, m ? P.guess_layer : -1, pos, R.buf,
                            R.gen);
+      if (P.st.flags)
+        for (int j = 0; j < k; ++j)
+          R.ready[j] = R.buf[j] >= 0 && (int)(fls[R.buf[j]] - R.gen[j]) >= 0;
     }
+    tl_mark(P.site + 4, 1);  // store bookkeeping done
     *P.route = R;
   }
   tl_mark(P.site, 6);
@@ -905,6 +1085,7 @@ __global__ void k_prefill_bk(PrefillBKParams P) {
       [&](int p, int j, int b, uint32_t g) {
         R[p].buf[j] = b;
         R[p].gen[j] = g;
+        R[p].ready[j] = 0;
       });
 }
 
@@ -912,8 +1093,52 @@ __global__ void k_begin_call(StoreDev S) {
   if (threadIdx.x == 0 && blockIdx.x == 0) store::begin_call(S);
 }
 
+// combine decode fast path (top_k <= 2, one CTA): out = h + w0*y0 + w1*y1,
+// V values per thread, every load in flight first
+template <int V, bool FX>
+MOE_DEV void combine_fast(const CombineParams& P, const float* part, const float* w, float* osh,
+                          int i0, int step) {
+  float hv[V], y0[V], y1[V];
+  unsigned long long q0[FX ? V : 1], q1[FX ? V : 1];
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const int i = i0 + u * step;
+    hv[u] = i < P.d ? __ldcg(P.h + i) : 0.f;
+    if constexpr (FX) {
+      q0[u] = i < P.d ? __ldcg(P.acc + i) : 0ull;
+      q1[u] = (i < P.d && P.top_k > 1) ? __ldcg(P.acc + (size_t)P.d + i) : 0ull;
+    } else {
+      y0[u] = i < P.d ? __ldcg(part + i) : 0.f;
+      y1[u] = (i < P.d && P.top_k > 1) ? __ldcg(part + (size_t)P.d + i) : 0.f;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const int i = i0 + u * step;
+    if constexpr (FX) {
+      y0[u] = fx_val(q0[u]);
+      y1[u] = fx_val(q1[u]);
+    }
+    if (i < P.d) {
+      float out = __fadd_rn(hv[u], __fmul_rn(w[0], y0[u]));  // model.py:251-254
+      if (P.top_k > 1) out = __fadd_rn(out, __fmul_rn(w[1], y1[u]));
+      P.out[i] = out;
+      osh[i] = out;
+    }
+  }
+  if constexpr (FX)  // reset the sums for the next down GEMV
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int i = i0 + u * step;
+      if (i < P.d) {
+        P.acc[i] = 0ull;
+        if (P.top_k > 1) P.acc[(size_t)P.d + i] = 0ull;
+      }
+    }
+}
+
 // out = h + w0*y0 + w1*y1 in descending-weight order (model.py:251-254)
-__global__ void k_combine(CombineParams P) {
+__global__ void __launch_bounds__(1024) k_combine(CombineParams P) {
   __shared__ float red[33];
   extern __shared__ float osh[];  // out [d], then LN gamma / beta [d] each
   float* gs = osh + P.d;
@@ -932,38 +1157,32 @@ __global__ void k_combine(CombineParams P) {
   for (int j = 0; j < P.top_k; ++j) w[j] = P.route->w[j];
   const int step = P.xn ? blockDim.x : gridDim.x * blockDim.x;
   const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
-  constexpr int MAXV = 8;  // d <= 8192 on the single-CTA (fused LN) path
-  if (P.xn && P.S == 1 && P.top_k <= 2) {  // decode fast path: all loads first
-    float hv[MAXV], y0[MAXV], y1[MAXV];
-#pragma unroll
-    for (int u = 0; u < MAXV; ++u) {
-      const int i = i0 + u * step;
-      hv[u] = i < P.d ? __ldcg(P.h + i) : 0.f;
-      y0[u] = i < P.d ? __ldcg(part + i) : 0.f;
-      y1[u] = (i < P.d && P.top_k > 1) ? __ldcg(part + (size_t)P.d + i) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < MAXV; ++u) {
-      const int i = i0 + u * step;
-      if (i < P.d) {
-        float out = __fadd_rn(hv[u], __fmul_rn(w[0], y0[u]));  // model.py:251-254
-        if (P.top_k > 1) out = __fadd_rn(out, __fmul_rn(w[1], y1[u]));
-        P.out[i] = out;
-        osh[i] = out;
-      }
-    }
+  if (P.xn && (P.S == 1 || P.acc) && P.top_k <= 2) {  // decode fast path: all loads first
+    if (P.acc && P.d <= 4 * step)
+      combine_fast<4, true>(P, part, w, osh, i0, step);
+    else if (P.acc)
+      combine_fast<8, true>(P, part, w, osh, i0, step);
+    else
+      combine_fast<8, false>(P, part, w, osh, i0, step);  // d <= 8192 (one CTA)
   } else {
     for (int i = i0; i < P.d; i += step) {
       float out = __ldcg(P.h + i);
       for (int j = 0; j < P.top_k; ++j) {
         float y = 0.f;
-        for (int s = 0; s < P.S; ++s) y += __ldcg(part + ((size_t)j * P.S + s) * P.d + i);
+        if (P.acc) {
+          y = fx_val(__ldcg(P.acc + (size_t)j * P.d + i));
+          P.acc[(size_t)j * P.d + i] = 0ull;
+        } else
+          for (int s = 0; s < P.S; ++s) y += __ldcg(part + ((size_t)j * P.S + s) * P.d + i);
         out = __fadd_rn(out, __fmul_rn(w[j], y));  // model.py:251-254, reference order
       }
       P.out[i] = out;
       if (P.xn) osh[i] = out;
     }
   }
+  if (P.zero)  // the up projections' fixed-point sums (read by the down GEMV): reset
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.zero_n; i += gridDim.x * blockDim.x)
+      P.zero[i] = 0ull;
   tl_mark(P.site, 0);
   if (P.xn) {  // fused LayerNorm of the residual stream (next LN1 or LN_f)
     __syncthreads();
@@ -1034,6 +1253,7 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
   int idx = 0x7fffffff;
   if (v < P.V) {
     float a = 0.f;
+#pragma unroll 4
     for (int s = 0; s < P.S; ++s) a += __ldcg(P.part + (size_t)s * P.V + v);
     P.logits[v] = a;
     if (!isfinite(a)) atomicOr(P.err, MOE_ERRF_NONFINITE_LOGITS);
@@ -1158,7 +1378,8 @@ cudaError_t preload_kernels() {
 
 // shared memory of one GEMV CTA: barriers, x slice, stage ring (which also
 // holds the cross-warp reduction scratch at the end)
-int gemv_smem_bytes(int bits, int xs_rows, int rb_full, int* nstages, int* stage_bytes) {
+int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int rb_full, int* nstages,
+                    int* stage_bytes) {
   const int WC = fmt_wc(bits);
   const int stage = gemv_qs(bits) * rb_full;
   int nst = MOE_GEMV_RING / stage;
@@ -1168,7 +1389,22 @@ int gemv_smem_bytes(int bits, int xs_rows, int rb_full, int* nstages, int* stage
   if (ring < red) ring = red;
   if (nstages) *nstages = nst;
   if (stage_bytes) *stage_bytes = stage;
-  return 512 + ((xs_rows * 8 + 127) & ~127) + ring;
+  return 512 + ((xs_rows * 8 + zs_cap * 4 + 127) & ~127) + ring;
+}
+
+// zmeta entries of the largest per-CTA slice of the launch's uniform-run
+// jobs (0 when none, or when the slice would cost the kernel its 2 CTAs/SM:
+// the kernel then reads zmeta from global memory)
+static int gemv_zs_cap(const GLaunch& P, int bits, int xs_cap, int rbf) {
+  int cap = 0;
+  for (int i = 0; i < P.nj; ++i) {
+    const MatDev& M = P.j[i].M;
+    if (bits > 4 || !M.runs_uniform) continue;
+    const long long rows = (long long)P.j[i].QPS * 4;
+    cap = max(cap, (int)(((rows * M.G) >> M.sg_log2) + 8));
+  }
+  if (cap && gemv_smem_bytes(bits, xs_cap, cap, rbf, nullptr, nullptr) > 112 * 1024) cap = 0;
+  return cap;
 }
 
 template <int BITS>
@@ -1179,7 +1415,8 @@ static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pd
     rbf = max(rbf, P.j[i].M.rb_full);
   }
   int nst = 0, stage = 0;
-  const int smem = gemv_smem_bytes(BITS, xs_cap, rbf, &nst, &stage);
+  const int zs_cap = gemv_zs_cap(P, BITS, xs_cap, rbf);
+  const int smem = gemv_smem_bytes(BITS, xs_cap, zs_cap, rbf, &nst, &stage);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nblocks);
   cfg.blockDim = dim3(MOE_GEMV_THREADS);
@@ -1194,7 +1431,7 @@ static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pd
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, nst, stage);
+  cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, zs_cap, nst, stage);
   g_launches.fetch_add(1);
 }
 
@@ -1241,7 +1478,7 @@ void launch_layernorm(const float* x, const float* g, const float* b, float* y, 
 }
 
 void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl) {
-  if (P.hd % 128 == 0 && P.S == 1) {
+  if (P.hd % 128 == 0) {
     launch_small(k_attention128, dim3(P.H), dim3(256),
                  (size_t)(3 * P.hd + P.T_max) * sizeof(float), s, pdl, P);
     return;
@@ -1255,7 +1492,8 @@ int tail_smem_bytes(const TailParams& P) {
   const bool hg = P.gh_l != nullptr && (!guess || P.gh_g != nullptr);
   const size_t head = (3 * (size_t)P.d * 4 +
                        (hg ? (guess ? 2 : 1) * (size_t)P.d * P.E * 2 : 0) + 15) & ~(size_t)15;
-  return (int)(head + 2 * 1024 * sizeof(double) + ((size_t)store::stage_ints(P.st) + 4) * 4);
+  return (int)(head + 2 * 1024 * sizeof(double) + ((size_t)store::stage_ints(P.st) + 4) * 4 +
+               (size_t)P.st.nbuf * 4);
 }
 
 void launch_tail(const TailParams& P, cudaStream_t s, bool pdl) {

@@ -24,8 +24,14 @@ struct GJob {
   const float* x;      // X_PLAIN input (length K)
   const float* up1;    // X_SWIGLU: x@W1 [K]
   const float* up3;    //           x@W3 [K]
-  float* part;         // split-K partial outputs [S][N] (S > 1)
-  float* out;          // final outputs [N] (the last CTA of a cb reduces the partials)
+  int xS;              // the inputs are xS split-K partials [xS][xstride], summed in
+  int xstride;         //   order on load (a producer GEMV left them unreduced); 0/1: plain
+  int xfx;             // x (or up1/up3) are fixed-point sums (uint64, reduce == 2 producer)
+  float* part;         // split-K partial outputs [S][N]
+  float* out;          // final outputs [N] when reduce == 1 (the last CTA of a cb sums
+  int reduce;          //   the partials in order); 0: the consumer sums part[0..S);
+                       //   2: every CTA adds its partial into `acc` in fixed point
+  unsigned long long* acc;  // reduce == 2: [N] int64 sums, 2^-32 units (consumer zeroes)
   int S, QPS, blk0;    // splits of the quad range, quads per split (multiple of QS)
 };
 
@@ -38,10 +44,19 @@ struct GLaunch {
   const uint32_t* flags;        // buffer ready generations (copy engine)
   int* cnt;                     // split-K arrival counters [sum of ncb] (zero between launches)
   int cluster;                  // CTAs per cluster along the split dimension (divides S)
+  unsigned long long* zero;     // optional: fixed-point sums consumed by an earlier kernel,
+  int zero_n;                   //   reset by this launch's CTAs (a slice each)
   int* err;
   unsigned long long wait_ns;
   int site;  // timeline slot of this launch (profiling), -1 none
 };
+
+// Split-K by fixed-point atomics (GJob.reduce == 2): each CTA adds its fp32
+// partial p as round(p * 2^32) into an int64 sum; integer addition makes the
+// result independent of CTA order (deterministic), and the one rounding back
+// to fp32 happens in the consumer.  |p| >= 2^30 or non-finite raises an error.
+#define MOE_FX_SCALE 0x1p32f
+#define MOE_FX_UNSCALE 0x1p-32
 
 // Device-resident decode cursor: the kernels of one decode token read the
 // position and input token from here, and k_logits advances it, so one
@@ -56,6 +71,7 @@ struct DecodeState {
 struct AttnParams {
   const float* qkv_part;  // [3][S][d]
   int S;
+  unsigned long long* acc;  // or: q/k/v as fixed-point sums [3][d] (read, then zeroed)
   float* kc;              // this layer's K cache [max_seq][H][hd]
   float* vc;
   float* ctx;             // [d]
@@ -68,6 +84,7 @@ struct TailParams {
   const float* x;         // residual input [d]
   const float* part;      // Wo partials [S][d]
   int S;
+  unsigned long long* acc;  // or: Wo output as fixed-point sums [d] (read, then zeroed)
   const float* g2;        // ln2 gamma / beta
   const float* b2;
   const float* gate_l;    // [d][E] gate of this layer
@@ -96,6 +113,7 @@ struct CombineParams {
   const float* h;     // [d]
   const float* part;  // [top_k][S][d]
   int S;
+  unsigned long long* acc;  // or: expert outputs as fixed-point sums [top_k][d] (zeroed)
   const RouteRec* route;
   float* out;         // [d]
   int d, top_k;
@@ -108,6 +126,8 @@ struct CombineParams {
   const float* ln_g;
   const float* ln_b;
   float* xn;
+  unsigned long long* zero;  // optional: fixed-point sums consumed by this layer's down
+  int zero_n;                //   GEMV (the up projections), reset here for the next layer
   int site;  // timeline slot of this launch (profiling), -1 none
 };
 
@@ -168,7 +188,8 @@ cudaError_t set_cta_trace(unsigned long long* buf);          // GEMV microbench 
 
 // launchers (kernels.cu)
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
-int gemv_smem_bytes(int bits, int xs_rows, int rb_full, int* nstages, int* stage_bytes);
+int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int rb_full, int* nstages,
+                    int* stage_bytes);
 void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl = false);
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
                       cudaStream_t s, bool pdl = false);

@@ -58,6 +58,7 @@ struct RouteRec {  // per position: resolved experts of the current layer
   int buf[MOE_MAX_TOPK];
   uint32_t gen[MOE_MAX_TOPK];
   float w[MOE_MAX_TOPK];
+  int ready[MOE_MAX_TOPK];  // decode: the tail saw flags[buf] >= gen (no flag wait needed)
 };
 
 struct TraceRecDev {  // layout identical to moe_trace_rec
