@@ -245,6 +245,15 @@ def run_b200(args, rank, world):
                 mk = np.array(rows)[:, :nph]
                 prev = np.concatenate([np.array(starts)[:, None], mk[:, :-1]], axis=1)
                 phases[nm] = [round(float(x), 2) for x in ((mk - prev) / 1e3).mean(axis=0)]
+        # GEMV block 0: release delay after the earliest CTA, then its own prologue
+        for nm, kind in (("qkv", 0), ("wo", 2), ("expert_up", 4), ("expert_down", 5)):
+            rows = [(marks[1 + 8 * l + kind][5] - st[1 + 8 * l + kind],
+                     marks[1 + 8 * l + kind][0] - marks[1 + 8 * l + kind][5])
+                    for l in range(nl) if ok[1 + 8 * l + kind] and marks[1 + 8 * l + kind][5] > 0]
+            if rows:
+                r = np.array(rows) / 1e3
+                phases[nm + "_blk0"] = [round(float(r[:, 0].mean()), 2),
+                                        round(float(r[:, 1].mean()), 2)]
         # tail thread-0 sub-phases (marks in the layer's exchange slot on one GPU)
         if world == 1:
             sub = [(marks[1 + 8 * l + 7][:2] - marks[1 + 8 * l + 3][5]) / 1e3 for l in range(nl)

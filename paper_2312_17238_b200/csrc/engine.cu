@@ -2179,7 +2179,7 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
     if (le != cudaSuccess)
       return fail(MOE_ERR_CUDA, std::string("gemv launch (grid ") + std::to_string(nblk) +
                                     ", smem " + std::to_string(gemv_smem_bytes(
-                                        bits, qps * 4, 0, M0.rb_full, nullptr, nullptr)) +
+                                        bits, qps * 4, 0, 0, M0.rb_full, nullptr, nullptr)) +
                                     "): " + cudaGetErrorString(le));
   }
   for (int w = 0; w < 3; ++w) launch_gemv(bits, P[w % nsets], nblk, s, pdl != 0);

@@ -115,7 +115,8 @@ MOE_DEV float fx_val(unsigned long long v) {
 
 template <int BITS>
 __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
-    k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int zs_cap, int nst, int stage_bytes) {
+    k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int zs_cap, int xin_cap, int nst,
+           int stage_bytes) {
   constexpr int WC = Fmt<BITS>::WC;
   constexpr bool QUANT = BITS <= 4;
   constexpr int W = MOE_GEMV_WARPS, QPW = gemv_qpw(BITS), QS = gemv_qs(BITS);
@@ -126,8 +127,11 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   uint64_t* zbar = reinterpret_cast<uint64_t*>(smem + 384);  // zero-point slice landed
   float* xs = reinterpret_cast<float*>(smem + 512);
   float* xz = xs + xs_cap;  // x * zscale per row (uniform zero-point runs)
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(smem + 392);  // x rows landed
   __half2* zsm = reinterpret_cast<__half2*>(xz + xs_cap);  // the CTA's zmeta slice [zs_cap]
-  uint8_t* ring = smem + 512 + (((size_t)xs_cap * 8 + (size_t)zs_cap * 4 + 127) & ~(size_t)127);
+  const size_t xin_off = 512 + (((size_t)xs_cap * 8 + (size_t)zs_cap * 4 + 15) & ~(size_t)15);
+  uint8_t* xin = smem + xin_off;  // the CTA's raw x rows (bulk copied) [xin_cap bytes]
+  uint8_t* ring = smem + ((xin_off + (size_t)xin_cap + 127) & ~(size_t)127);
 
   int ji = 0, cnt_base = 0;
   for (int i = 1; i < P.nj; ++i)
@@ -152,6 +156,13 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const bool zstage = uni && nrows > 0 && zs_cap > 0;
   const int z0 = zstage ? (int)(((int64_t)row0 * M.G + gcb0) >> M.sg_log2) : 0;
   const int z1 = zstage ? (int)(((int64_t)(row0 + nrows - 1) * M.G + gcb0) >> M.sg_log2) : 0;
+  // the CTA's x rows (outputs of the previous kernel, L2-resident) come through
+  // the producer's bulk-copy queue ahead of the weight stream: consumer loads
+  // issued next to a saturating weight stream wait behind it for microseconds
+  const bool swiglu = J.xmode != X_PLAIN;
+  const int xes = J.xfx ? 8 : 4;  // bytes per x element (fixed-point sums or fp32)
+  const bool xstage = xin_cap > 0 && J.xS <= 1 && nrows > 0 &&
+                      (swiglu ? 2 : 1) * nrows * xes <= xin_cap;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) {
@@ -159,6 +170,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       gemv::mbar_init(empty + i, W);
     }
     gemv::mbar_init(zbar, 1);
+    gemv::mbar_init(xbar, 1);
     gemv::mbar_fence_init();
   }
   __syncthreads();
@@ -171,8 +183,21 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       // (same job) skips, before any cluster barrier
       if (P.route->buf[J.rel_slot] < 0) return;
     }
+    // x rows: one bulk copy per input array (after the previous kernel completed)
+    auto issue_x = [&]() {
+      if (!xstage) return;
+      if (J.rel_slot < 0) gemv::pdl_wait();
+      const uint32_t bytes = (uint32_t)(nrows * xes);
+      gemv::mbar_arrive_tx(xbar, (swiglu ? 2u : 1u) * bytes);
+      const uint8_t* a = reinterpret_cast<const uint8_t*>(swiglu ? J.up1 : J.x);
+      gemv::bulk_g2s(xin, a + (size_t)row0 * xes, bytes, xbar);
+      if (swiglu)
+        gemv::bulk_g2s(xin + bytes, reinterpret_cast<const uint8_t*>(J.up3) + (size_t)row0 * xes,
+                       bytes, xbar);
+    };
     if (lane == 0) {
       if (J.rel_slot >= 0) {
+        issue_x();
         const int buf = P.route->buf[J.rel_slot];
         // the tail saw the buffer's copy already published: no flag round trip
         if (!P.route->ready[J.rel_slot])
@@ -192,6 +217,8 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       int st = 0;
       uint32_t ph = 0;
       for (int it = 0; it < nit; ++it) {
+        // dense weights: the ring is prefetched before the previous kernel ends
+        if (it == nst && J.rel_slot < 0) issue_x();
         if (it >= nst) gemv::mbar_wait(empty + st, ph ^ 1);
         const int nq = min(QS, qe - (qs + it * QS));
         const uint32_t bytes = (uint32_t)(nq * rb);
@@ -203,6 +230,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
           ph ^= 1;
         }
       }
+      if (nit <= nst && J.rel_slot < 0) issue_x();
     }
     __syncwarp();
     if (P.cluster > 1) {  // the two cluster barriers of the split-K epilogue
@@ -216,6 +244,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const int nthr = W * 32;
   gemv::pdl_wait();
   tl_begin(P.site);
+  tl_mark(P.site, 5);  // block 0 released (profiling: its start vs the earliest CTA's)
   cta_mark(0);
   if (P.zero) {  // reset sums an earlier kernel consumed (e.g. the previous layer's up)
     const int per = (P.zero_n + gridDim.x - 1) / gridDim.x;
@@ -225,9 +254,35 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   // expert jobs: the route load is issued with the x loads (independent)
   const int ebuf = J.rel_slot >= 0 ? P.route->buf[J.rel_slot] : 0;
   const float xscale = QUANT ? gemv::kXScale : 1.f;
+  if (J.rel_slot >= 0) {
+    if (ebuf < 0) {  // expert parallel: not ours; contribute zeros to the exchange
+      float* zdst = J.reduce == 2 ? nullptr : J.reduce ? (s == 0 ? J.out : nullptr)
+                             : (s % P.cluster == 0 ? J.part + (size_t)(s / P.cluster) * M.N
+                                                   : nullptr);
+      if (zdst)
+        for (int t = threadIdx.x; t < wcb * WC; t += nthr) zdst[(size_t)cb * 32 * WC + t] = 0.f;
+      cta_mark(2);
+      tl_end(P.site);
+      return;
+    }
+  }
+  if (xstage) {  // x rows from the producer's bulk copy
+    gemv::mbar_wait(xbar, 0);
+    const float* xf = reinterpret_cast<const float*>(xin);
+    const unsigned long long* xq = reinterpret_cast<const unsigned long long*>(xin);
+    for (int i = threadIdx.x; i < nrows; i += nthr) {
+      const float a = J.xfx ? fx_val(xq[i]) : xf[i];
+      float xv = a;
+      if (swiglu) {  // SwiGLU of the up projections (model.py:223-226)
+        const float b = J.xfx ? fx_val(xq[nrows + i]) : xf[nrows + i];
+        xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
+      }
+      xs[i] = xv * xscale;
+    }
+  }
   // x (or the SwiGLU of the up projections) in batches of 4 rows per thread:
   // every load of a batch is issued before any use
-  for (int i0 = 0; i0 < nrows; i0 += 4 * nthr) {
+  for (int i0 = 0; !xstage && i0 < nrows; i0 += 4 * nthr) {
     float va[4], vb[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -286,16 +341,6 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   }
   tl_mark(P.site, 0);  // x slice in smem
   if (J.rel_slot >= 0) {
-    if (ebuf < 0) {  // expert parallel: not ours; contribute zeros to the exchange
-      float* zdst = J.reduce == 2 ? nullptr : J.reduce ? (s == 0 ? J.out : nullptr)
-                             : (s % P.cluster == 0 ? J.part + (size_t)(s / P.cluster) * M.N
-                                                   : nullptr);
-      if (zdst)
-        for (int t = threadIdx.x; t < wcb * WC; t += nthr) zdst[(size_t)cb * 32 * WC + t] = 0.f;
-      cta_mark(2);
-      tl_end(P.site);
-      return;
-    }
     if (QUANT && (!uni || zs_cap == 0)) {  // zmeta is read from global
       M.zmeta = reinterpret_cast<const __half2*>(P.pool + (long long)ebuf * P.slot_stride +
                                                  reinterpret_cast<size_t>(M.zmeta));
@@ -1378,7 +1423,7 @@ cudaError_t preload_kernels() {
 
 // shared memory of one GEMV CTA: barriers, x slice, stage ring (which also
 // holds the cross-warp reduction scratch at the end)
-int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int rb_full, int* nstages,
+int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full, int* nstages,
                     int* stage_bytes) {
   const int WC = fmt_wc(bits);
   const int stage = gemv_qs(bits) * rb_full;
@@ -1389,7 +1434,7 @@ int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int rb_full, int* nstages
   if (ring < red) ring = red;
   if (nstages) *nstages = nst;
   if (stage_bytes) *stage_bytes = stage;
-  return 512 + ((xs_rows * 8 + zs_cap * 4 + 127) & ~127) + ring;
+  return 512 + ((((xs_rows * 8 + zs_cap * 4 + 15) & ~15) + xin_cap + 127) & ~127) + ring;
 }
 
 // zmeta entries of the largest per-CTA slice of the launch's uniform-run
@@ -1403,7 +1448,23 @@ static int gemv_zs_cap(const GLaunch& P, int bits, int xs_cap, int rbf) {
     const long long rows = (long long)P.j[i].QPS * 4;
     cap = max(cap, (int)(((rows * M.G) >> M.sg_log2) + 8));
   }
-  if (cap && gemv_smem_bytes(bits, xs_cap, cap, rbf, nullptr, nullptr) > 112 * 1024) cap = 0;
+  if (cap && gemv_smem_bytes(bits, xs_cap, cap, 0, rbf, nullptr, nullptr) > 112 * 1024) cap = 0;
+  return cap;
+}
+
+// bytes of the x staging region: the largest job's x rows (two arrays for the
+// SwiGLU input), 0 when a job sums producer partials or the kernel would lose
+// its 2 CTAs/SM (x then comes through ordinary loads)
+static int gemv_xin_cap(const GLaunch& P, int bits, int xs_cap, int zs_cap, int rbf) {
+  int cap = 0;
+  for (int i = 0; i < P.nj; ++i) {
+    const GJob& J = P.j[i];
+    if (J.xS > 1) continue;
+    const int es = J.xfx ? 8 : 4, n = J.xmode != X_PLAIN ? 2 : 1;
+    cap = max(cap, n * es * J.QPS * 4);
+  }
+  if (cap && gemv_smem_bytes(bits, xs_cap, zs_cap, cap, rbf, nullptr, nullptr) > 112 * 1024)
+    cap = 0;
   return cap;
 }
 
@@ -1416,7 +1477,8 @@ static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pd
   }
   int nst = 0, stage = 0;
   const int zs_cap = gemv_zs_cap(P, BITS, xs_cap, rbf);
-  const int smem = gemv_smem_bytes(BITS, xs_cap, zs_cap, rbf, &nst, &stage);
+  const int xin_cap = gemv_xin_cap(P, BITS, xs_cap, zs_cap, rbf);
+  const int smem = gemv_smem_bytes(BITS, xs_cap, zs_cap, xin_cap, rbf, &nst, &stage);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nblocks);
   cfg.blockDim = dim3(MOE_GEMV_THREADS);
@@ -1431,7 +1493,7 @@ static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pd
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, zs_cap, nst, stage);
+  cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, zs_cap, xin_cap, nst, stage);
   g_launches.fetch_add(1);
 }
 

@@ -188,7 +188,7 @@ cudaError_t set_cta_trace(unsigned long long* buf);          // GEMV microbench 
 
 // launchers (kernels.cu)
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
-int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int rb_full, int* nstages,
+int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full, int* nstages,
                     int* stage_bytes);
 void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl = false);
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
