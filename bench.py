@@ -424,7 +424,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--k", type=int, default=None, help="sweep: override the LRU cache size")
+    ap.add_argument("--m", type=int, default=None, help="sweep: override the prefetch depth")
     args = ap.parse_args()
+    if args.k is not None or args.m is not None:  # C5 sweep point derived from --config
+        ab, xb, k, m = CONFIGS[args.config]
+        k = k if args.k is None else args.k
+        m = m if args.m is None else args.m
+        name = f"{args.config}_k{k}_m{m}"
+        CONFIGS[name] = (ab, xb, k, m)
+        args.config = name
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -1070,44 +1070,56 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   }
   __syncthreads();
   tl_mark(P.site, 5);
-  if (tid == 0) {
-    RouteRec R;
+  // warp 1: routing weights (softmax over the top-k logits, sequential sum in
+  // selection order), trace record and the route's expert/weight fields;
+  // meanwhile thread 0 runs the store bookkeeping (buffers of the route)
+  __shared__ int rbuf[MOE_MAX_TOPK];
+  __shared__ uint32_t rgen[MOE_MAX_TOPK];
+  if (warp == 1) {
     const int k = P.top_k;
-    int sel[MOE_MAX_TOPK];
-    for (int j = 0; j < k; ++j) sel[j] = sel_sh[j];
-    float ez[MOE_MAX_TOPK], sum = 0.f;
-    for (int j = 0; j < k; ++j) {
-      ez[j] = expf(__fsub_rn(lg[sel[j]], lg[sel[0]]));
-      sum = __fadd_rn(sum, ez[j]);
+    const float l0 = lg[sel_sh[0]];
+    const float ez = lane < k ? expf(__fsub_rn(lg[sel_sh[lane]], l0)) : 0.f;
+    float sum = 0.f;
+    for (int t = 0; t < k; ++t) sum = __fadd_rn(sum, __shfl_sync(0xffffffffu, ez, t));
+    const float wj = lane < k ? __fdiv_rn(ez, sum) : 0.f;
+    const int ej = lane < k ? sel_sh[lane] : -1;
+    if (lane < MOE_MAX_TOPK) {
+      P.route->e[lane] = ej;
+      P.route->w[lane] = wj;
     }
+    TraceRecDev* tr = P.trace + slot;
+    if (lane < 8) {
+      tr->experts[lane] = ej;
+      tr->weights[lane] = wj;
+    }
+    if (lane == 0) {
+      tr->pos = pos;
+      tr->layer = P.layer;
+    }
+  }
+  if (tid == 0) {
+    const int k = P.top_k;
+    tl_mark(P.site + 4, 0);  // profiling: bookkeeping start (exchange slot unused on 1 GPU)
     for (int j = 0; j < MOE_MAX_TOPK; ++j) {
-      R.e[j] = j < k ? sel[j] : -1;
-      R.w[j] = j < k ? __fdiv_rn(ez[j], sum) : 0.f;
-      R.buf[j] = -1;
-      R.gen[j] = 0;
-      R.ready[j] = 0;
+      rbuf[j] = -1;
+      rgen[j] = 0u;
     }
-    TraceRecDev tr;
-    tr.pos = pos;
-    tr.layer = P.layer;
-    for (int j = 0; j < 8; ++j) {
-      tr.experts[j] = j < k ? sel[j] : -1;
-      tr.weights[j] = j < k ? R.w[j] : 0.f;
-    }
-    P.trace[slot] = tr;
-    tl_mark(P.site + 4, 0);  // profiling: softmax + trace record (exchange slot unused)
     if (bad) {
       atomicOr(P.st.err, MOE_ERRF_NONFINITE_GATE);
     } else if (P.mode == 0) {
       const int m = (guess && P.m > 0) ? P.m : 0;
-      store::resolve_token(S, P.layer, sel, k, gsel_sh, m, m ? P.guess_layer : -1, pos, R.buf,
-                           R.gen);
-      if (P.st.flags)
-        for (int j = 0; j < k; ++j)
-          R.ready[j] = R.buf[j] >= 0 && (int)(fls[R.buf[j]] - R.gen[j]) >= 0;
+      store::resolve_token(S, P.layer, sel_sh, k, gsel_sh, m, m ? P.guess_layer : -1, pos, rbuf,
+                           rgen);
+    }
+#pragma unroll
+    for (int j = 0; j < MOE_MAX_TOPK; ++j) {
+      const int b = rbuf[j];
+      P.route->buf[j] = b;
+      P.route->gen[j] = rgen[j];
+      P.route->ready[j] = (P.mode == 0 && P.st.flags && b >= 0 && j < k)
+                              ? (int)((int)(fls[b] - rgen[j]) >= 0) : 0;
     }
     tl_mark(P.site + 4, 1);  // store bookkeeping done
-    *P.route = R;
   }
   tl_mark(P.site, 6);
   if (P.mode == 0) {
