@@ -230,6 +230,7 @@ def run_b200(args, rank, world):
             d = [(en[j] - st[j]) / 1e3 for j in idx if ok[j]]
             if d:
                 kinds[nm] = {"avg_us": round(float(np.mean(d)), 2),
+                             "median_us": round(float(np.median(d)), 2),
                              "sum_us": round(float(np.sum(d)), 1)}
         for nm, j in (("embed", 0), ("lm_head", 1 + 8 * nl), ("logits", 2 + 8 * nl)):
             if ok[j]:
@@ -337,6 +338,15 @@ def run_b200(args, rank, world):
               "bound": "h2d" if miss_bytes_tok / h2d_peak > hit_bytes_tok / hbm else "hbm"}
     if e2e is not None:
         e2e["h2d_expert_bytes_per_step"] = int(miss_bytes_tok)
+    # the same kernel from the device timeline (graph + PDL, as in the timed run):
+    # median span over the token's layers, i.e. the hit-path launches
+    try:
+        up_med = timeline["kernels"]["expert_up"]["median_us"]
+        roofline["timeline_median_us"] = up_med
+        roofline["achieved_timeline"] = round(up_bytes / (up_med * 1e-6) / 1e9, 1)
+        roofline["frac_timeline"] = round(up_bytes / (up_med * 1e-6) / 1e9 / hbm, 4)
+    except (KeyError, TypeError):
+        pass
     line = {
         "metric": METRIC, "value": round(tok_s, 3), "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
