@@ -255,6 +255,13 @@ def run_b200(args, rank, world):
                 r = np.array(rows) / 1e3
                 phases[nm + "_blk0"] = [round(float(r[:, 0].mean()), 2),
                                         round(float(r[:, 1].mean()), 2)]
+            # epilogue split: warp skew (loop done -> all warps), smem stores, sums + adds
+            ep = [(marks[1 + 8 * l + kind][6] - marks[1 + 8 * l + kind][3],
+                   marks[1 + 8 * l + kind][7] - marks[1 + 8 * l + kind][6],
+                   marks[1 + 8 * l + kind][4] - marks[1 + 8 * l + kind][7])
+                  for l in range(nl) if ok[1 + 8 * l + kind] and marks[1 + 8 * l + kind][7] > 0]
+            if ep:
+                phases[nm + "_epilogue"] = [round(float(x), 2) for x in np.array(ep).mean(0) / 1e3]
         # tail thread-0 sub-phases (marks in the layer's exchange slot on one GPU)
         if world == 1:
             sub = [(marks[1 + 8 * l + 7][:2] - marks[1 + 8 * l + 3][5]) / 1e3 for l in range(nl)

@@ -59,12 +59,15 @@ int plan_qps(int total_cb, int nquads, int qs) {
   // CTAs per SM the split targets (MOE_GEMV_WAVES; 2 = one resident wave)
   static const int waves = getenv("MOE_GEMV_WAVES") ? atoi(getenv("MOE_GEMV_WAVES"))
                                                     : MOE_GEMV_MINB;
+  // splits need not be whole pipeline stages (the last stage of a split is
+  // partial), so S is the largest split count that fits the resident wave:
+  // every SM gets the same number of CTAs whenever total_cb * S == target
   const int target = waves * 148;
-  int S = std::max(1, target / total_cb);  // at most one wave
+  const int S = std::max(1, target / total_cb);  // at most one wave
   int qps = (nquads + S - 1) / S;
-  qps = (qps + qs - 1) / qs * qs;
-  while (qps * 4 > MOE_XS_MAX) qps -= qs;
-  return std::max(qps, qs);
+  (void)qs;
+  while (qps * 4 > MOE_XS_MAX) qps -= 1;
+  return std::max(qps, 1);
 }
 
 struct Layout {  // byte sections of one tiled matrix
@@ -293,6 +296,7 @@ struct moe_engine {
 
   // activations
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
+  bool up_fx = false;  // MOE_UP_FX=1: up projections as fixed-point sums (else partials)
   unsigned long long *wo_acc = nullptr, *dn_acc = nullptr, *qkv_acc = nullptr,
                      *up_acc = nullptr;  // fixed-point split-K sums (reduce == 2)
   float *qkv_part = nullptr, *wo_part = nullptr, *up_part = nullptr, *dn_part = nullptr,
@@ -633,7 +637,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, qkv_out + d, Q_qkv);
   q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, qkv_out + 2 * d, Q_qkv);
   q.err = err;
-  if (cur_ds && l > 0) {  // decode: reset the previous layer's up-projection sums
+  if (cur_ds && l > 0 && up_fx) {  // decode: reset the previous layer's up-projection sums
     q.zero = up_acc;
     q.zero_n = 2 * topk * f;
   }
@@ -739,7 +743,9 @@ int moe_engine::enq_experts(int l, int p) {
       J.x = h + (size_t)p * d;
       J.part = up_part + ((size_t)(2 * j + m) * S_up) * f;
       J.out = up_out + (size_t)(2 * j + m) * f;
-      J.reduce = 2;  // fixed-point sums read by the down GEMV's SwiGLU prologue
+      // split-K partials, bulk-copied and summed in order by the down GEMV's
+      // SwiGLU prologue (fewer atomics than fixed-point sums for 5 splits)
+      J.reduce = up_fx ? 2 : 0;
       J.acc = up_acc + (size_t)(2 * j + m) * f;
       J.QPS = Q_up;
       J.S = S_up;
@@ -857,7 +863,7 @@ int moe_engine::enq_logits(int p, float* out) {
   g.cnt = cnt;
   g.site = 1 + 8 * L;
   g.j[0] = dense_job(lm_head, xn, lm_part, out, Q_lm);
-  if (cur_ds) {  // decode: reset the last layer's up-projection sums
+  if (cur_ds && up_fx) {  // decode: reset the last layer's up-projection sums
     g.zero = up_acc;
     g.zero_n = 2 * topk * f;
   }
@@ -1057,6 +1063,7 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* dbgv = getenv("MOE_DEBUG")) e->debug = atoi(dbgv) != 0;
   if (const char* sv = getenv("MOE_SERIAL_COPIES")) e->serial_copies = atoi(sv) != 0;
   if (const char* tv = getenv("MOE_COPY_TRACE")) e->trace_copies = atoi(tv) != 0;
+  if (const char* uf = getenv("MOE_UP_FX")) e->up_fx = atoi(uf) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
   for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);

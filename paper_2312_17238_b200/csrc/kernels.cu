@@ -161,8 +161,9 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   // issued next to a saturating weight stream wait behind it for microseconds
   const bool swiglu = J.xmode != X_PLAIN;
   const int xes = J.xfx ? 8 : 4;  // bytes per x element (fixed-point sums or fp32)
-  const bool xstage = xin_cap > 0 && J.xS <= 1 && nrows > 0 &&
-                      (swiglu ? 2 : 1) * nrows * xes <= xin_cap;
+  const int xparts = J.xS > 1 ? J.xS : 1;  // producer partials per input array
+  const bool xstage = xin_cap > 0 && nrows > 0 && !(J.xS > 1 && J.xfx) &&
+                      (swiglu ? 2 : 1) * xparts * nrows * xes <= xin_cap;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) {
@@ -188,12 +189,17 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       if (!xstage) return;
       if (J.rel_slot < 0) gemv::pdl_wait();
       const uint32_t bytes = (uint32_t)(nrows * xes);
-      gemv::mbar_arrive_tx(xbar, (swiglu ? 2u : 1u) * bytes);
+      gemv::mbar_arrive_tx(xbar, (swiglu ? 2u : 1u) * (uint32_t)xparts * bytes);
       const uint8_t* a = reinterpret_cast<const uint8_t*>(swiglu ? J.up1 : J.x);
-      gemv::bulk_g2s(xin, a + (size_t)row0 * xes, bytes, xbar);
+      const size_t pstride = (size_t)J.xstride * xes;  // between producer partials
+      for (int p = 0; p < xparts; ++p)
+        gemv::bulk_g2s(xin + (size_t)p * bytes, a + p * pstride + (size_t)row0 * xes, bytes, xbar);
       if (swiglu)
-        gemv::bulk_g2s(xin + bytes, reinterpret_cast<const uint8_t*>(J.up3) + (size_t)row0 * xes,
-                       bytes, xbar);
+        for (int p = 0; p < xparts; ++p)
+          gemv::bulk_g2s(xin + (size_t)(xparts + p) * bytes,
+                         reinterpret_cast<const uint8_t*>(J.up3) + p * pstride +
+                             (size_t)row0 * xes,
+                         bytes, xbar);
     };
     if (lane == 0) {
       if (J.rel_slot >= 0) {
@@ -271,12 +277,19 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     const float* xf = reinterpret_cast<const float*>(xin);
     const unsigned long long* xq = reinterpret_cast<const unsigned long long*>(xin);
     for (int i = threadIdx.x; i < nrows; i += nthr) {
-      const float a = J.xfx ? fx_val(xq[i]) : xf[i];
-      float xv = a;
-      if (swiglu) {  // SwiGLU of the up projections (model.py:223-226)
-        const float b = J.xfx ? fx_val(xq[nrows + i]) : xf[nrows + i];
-        xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
+      float a, b = 0.f;
+      if (J.xfx) {
+        a = fx_val(xq[i]);
+        if (swiglu) b = fx_val(xq[nrows + i]);
+      } else {  // fp32 producer partials, summed in split order
+        a = 0.f;
+        for (int p = 0; p < xparts; ++p) a += xf[p * nrows + i];
+        if (swiglu)
+          for (int p = 0; p < xparts; ++p) b += xf[(xparts + p) * nrows + i];
       }
+      float xv = a;
+      if (swiglu)  // SwiGLU of the up projections (model.py:223-226)
+        xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
       xs[i] = xv * xscale;
     }
   }
@@ -473,9 +486,11 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   float* red = reinterpret_cast<float*>(ring);
   float* ysum = red + W * 32 * (WC + 1);  // this CTA's partial outputs [32*WC]
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  tl_mark(P.site, 6);  // every consumer warp left the loop
 #pragma unroll
   for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  tl_mark(P.site, 7);  // per-warp results in smem
   const float zo_out = zo_sum * gemv::kZUnscale;
   const int C = P.cluster, SC = J.S / C;  // cluster = C consecutive splits of one cb
   const int crank = blockIdx.x % C, sc = s / C;
@@ -1471,8 +1486,8 @@ static int gemv_xin_cap(const GLaunch& P, int bits, int xs_cap, int zs_cap, int 
   int cap = 0;
   for (int i = 0; i < P.nj; ++i) {
     const GJob& J = P.j[i];
-    if (J.xS > 1) continue;
-    const int es = J.xfx ? 8 : 4, n = J.xmode != X_PLAIN ? 2 : 1;
+    if (J.xS > 1 && J.xfx) continue;
+    const int es = J.xfx ? 8 : 4, n = (J.xmode != X_PLAIN ? 2 : 1) * (J.xS > 1 ? J.xS : 1);
     cap = max(cap, n * es * J.QPS * 4);
   }
   if (cap && gemv_smem_bytes(bits, xs_cap, zs_cap, cap, rbf, nullptr, nullptr) > 112 * 1024)
