@@ -787,11 +787,21 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
   float* sc = asm_ + HD;
   float* half2buf = sc + P.T_max;
   gemv::pdl_trigger();
+  const size_t rstride = (size_t)P.H * HD;
+  if (P.ds) {  // decode: this head's K/V rows of earlier tokens are final -> pull them
+    // into L2 while the QKV GEMV runs (they were evicted by the weight stream)
+    const int pp = P.ds->pos;
+    const int lines = HD * 4 / 128;  // 128-byte lines per row
+    for (int i = tid; i < 2 * pp * lines; i += blockDim.x) {
+      const int t = i / (2 * lines), r = i % (2 * lines);
+      const float* base = (r < lines ? P.kc : P.vc) + (size_t)t * rstride + (size_t)h * HD;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (r % lines) * 32));
+    }
+  }
   gemv::pdl_wait();
   tl_begin(P.site);
   const int pos = P.ds ? P.ds->pos : P.pos;
   const int T = pos + 1;
-  const size_t rstride = (size_t)P.H * HD;
   const float* qg = P.qkv_part + (size_t)h * HD;
   float* krow = P.kc + (size_t)pos * rstride + (size_t)h * HD;
   float* vrow = P.vc + (size_t)pos * rstride + (size_t)h * HD;
