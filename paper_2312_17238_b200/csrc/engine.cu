@@ -297,6 +297,8 @@ struct moe_engine {
   // activations
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
   bool up_fx = false;  // MOE_UP_FX=1: up projections as fixed-point sums (else partials)
+  bool dn_fx = true;   // MOE_DN_FX=0: W2 reduced by the last CTA per column block instead
+  bool pf_w2 = false;  // MOE_PF_W2=1: L2 prefetch of W2 during the W1/W3 GEMV (measured slower)
   unsigned long long *wo_acc = nullptr, *dn_acc = nullptr, *qkv_acc = nullptr,
                      *up_acc = nullptr;  // fixed-point split-K sums (reduce == 2)
   float *qkv_part = nullptr, *wo_part = nullptr, *up_part = nullptr, *dn_part = nullptr,
@@ -763,13 +765,23 @@ int moe_engine::enq_experts(int l, int p) {
     J.out = dn_out + (size_t)j * d;
     // single GPU: fixed-point split-K sums read (and reset) by the combine;
     // expert parallel: reduced in-kernel, the exchange ships dn_out
-    J.reduce = ep_world > 1 ? 1 : 2;
+    J.reduce = (ep_world > 1 || !dn_fx) ? 1 : 2;
     J.acc = dn_acc + (size_t)j * d;
     J.QPS = Q_dn;
     J.S = S_dn;
   }
   u.nj = 2 * topk;
   dn.nj = topk;
+  if (pf_w2) {  // W1/W3 CTAs pull their expert's W2 records + zmeta into L2
+    u.pf_off[0] = (long long)xoff[2][0];
+    u.pf_len[0] = (long long)xl[2].rec;
+    u.pf_off[1] = (long long)xoff[2][3];
+    u.pf_len[1] = (long long)xl[2].zmeta;
+    for (int r = 0; r < 2; ++r) {  // bulk prefetches need 16-byte aligned ranges
+      u.pf_len[r] += u.pf_off[r] & 15;
+      u.pf_off[r] &= ~15ll;
+    }
+  }
   const int nu = finalize_launch(u);
   if (u.cluster > 1)
     for (int i = 0; i < u.nj; ++i) u.j[i].reduce = 0;
@@ -1064,6 +1076,8 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* sv = getenv("MOE_SERIAL_COPIES")) e->serial_copies = atoi(sv) != 0;
   if (const char* tv = getenv("MOE_COPY_TRACE")) e->trace_copies = atoi(tv) != 0;
   if (const char* uf = getenv("MOE_UP_FX")) e->up_fx = atoi(uf) != 0;
+  if (const char* df = getenv("MOE_DN_FX")) e->dn_fx = atoi(df) != 0;
+  if (const char* pf = getenv("MOE_PF_W2")) e->pf_w2 = atoi(pf) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
   for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);

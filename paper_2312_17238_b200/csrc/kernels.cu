@@ -220,23 +220,47 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
         gemv::bulk_g2s(zsm, reinterpret_cast<const void*>(za - lead), bytes, zbar);
       }
       const uint8_t* src = M.base + cb_offset(M, cb) + (int64_t)qs * rb;
+      const uint64_t pol = gemv::policy_evict_first();
+      // L2 prefetch of the next kernel's expert weights, once the ring is full
+      auto issue_prefetch = [&]() {
+        if (J.rel_slot < 0 || (P.pf_len[0] <= 0 && P.pf_len[1] <= 0)) return;
+        int n = 0, idx = -1;  // this CTA's index among the CTAs on the same expert
+        for (int i = 0; i < P.nj; ++i)
+          if (P.j[i].rel_slot == J.rel_slot) {
+            if (i == ji) idx = n + local;
+            n += P.j[i].M.ncb * P.j[i].S;
+          }
+        const uint8_t* b = P.pool + (long long)P.route->buf[J.rel_slot] * P.slot_stride;
+        for (int r = 0; r < 2; ++r) {
+          const long long len = P.pf_len[r];
+          if (len <= 0) continue;
+          const long long per = ((len + n - 1) / n + 15) & ~15ll;
+          long long o = (long long)idx * per, e = min(len, o + per);
+          for (; o < e; o += 65536) {
+            const uint32_t nb = (uint32_t)((min(e - o, 65536ll) + 15) & ~15ll);
+            gemv::bulk_prefetch_l2(b + P.pf_off[r] + o, nb);
+          }
+        }
+      };
       int st = 0;
       uint32_t ph = 0;
       for (int it = 0; it < nit; ++it) {
         // dense weights: the ring is prefetched before the previous kernel ends
         if (it == nst && J.rel_slot < 0) issue_x();
+        if (it == nst) issue_prefetch();
         if (it >= nst) gemv::mbar_wait(empty + st, ph ^ 1);
         const int nq = min(QS, qe - (qs + it * QS));
         const uint32_t bytes = (uint32_t)(nq * rb);
         gemv::mbar_arrive_tx(full + st, bytes);
-        gemv::bulk_g2s(ring + (size_t)st * stage_bytes, src + (int64_t)it * QS * rb, bytes,
-                       full + st);
+        gemv::bulk_g2s_hint(ring + (size_t)st * stage_bytes, src + (int64_t)it * QS * rb, bytes,
+                            full + st, pol);
         if (++st == nst) {
           st = 0;
           ph ^= 1;
         }
       }
       if (nit <= nst && J.rel_slot < 0) issue_x();
+      if (nit <= nst) issue_prefetch();
     }
     __syncwarp();
     if (P.cluster > 1) {  // the two cluster barriers of the split-K epilogue

@@ -48,6 +48,10 @@ struct GLaunch {
   int zero_n;                   //   reset by this launch's CTAs (a slice each)
   int* err;
   unsigned long long wait_ns;
+  // L2 prefetch for the next kernel: byte ranges [off, off + len) of each
+  // routed expert's buffer (e.g. W2 while W1/W3 stream), split over the CTAs
+  // of the jobs on that expert
+  long long pf_off[2], pf_len[2];
   int site;  // timeline slot of this launch (profiling), -1 none
 };
 
