@@ -298,6 +298,8 @@ struct moe_engine {
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
   bool up_fx = false;  // MOE_UP_FX=1: up projections as fixed-point sums (else partials)
   bool dn_fx = true;   // MOE_DN_FX=0: W2 reduced by the last CTA per column block instead
+  bool fuse_comb = true;  // MOE_FUSE_COMBINE=0: keep the combine kernel between layers
+  bool pend_comb = false;  // decode: layer l's combine + LN1(l+1) is fused into QKV(l+1)
   bool pf_w2 = false;  // MOE_PF_W2=1: L2 prefetch of W2 during the W1/W3 GEMV (measured slower)
   unsigned long long *wo_acc = nullptr, *dn_acc = nullptr, *qkv_acc = nullptr,
                      *up_acc = nullptr;  // fixed-point split-K sums (reduce == 2)
@@ -647,6 +649,19 @@ int moe_engine::enq_attention(int l, int p, int mode) {
     q.j[i].reduce = 2;
     q.j[i].acc = qkv_acc + (size_t)i * d;
   }
+  if (pend_comb) {  // previous layer's combine + this layer's LN1 in the QKV prologue
+    q.route = route + p;
+    for (int i = 0; i < 3; ++i) {
+      GJob& J = q.j[i];
+      J.xmode = X_COMBINE;
+      J.x = h + (size_t)p * d;
+      J.cacc = dn_acc;
+      J.ctop = topk;
+      J.lng = ln1g[l];
+      J.lnb = ln1b[l];
+      J.xout = xp;
+    }
+  }
   const int nq = finalize_launch(q);
   if (q.cluster > 1)
     for (int i = 0; i < 3; ++i) q.j[i].reduce = 0;  // partials summed by the attention
@@ -782,6 +797,11 @@ int moe_engine::enq_experts(int l, int p) {
       u.pf_off[r] &= ~15ll;
     }
   }
+  if (pend_comb && !up_fx) {  // the fused combine read dn_acc: reset it before W2 adds
+    u.zero = dn_acc;
+    u.zero_n = topk * d;
+  }
+  pend_comb = false;
   const int nu = finalize_launch(u);
   if (u.cluster > 1)
     for (int i = 0; i < u.nj; ++i) u.j[i].reduce = 0;
@@ -860,8 +880,12 @@ int moe_engine::enq_experts(int l, int p) {
     c.ln_b = l + 1 < L ? ln1b[l + 1] : lnfb;
     c.xn = xn;
   }
-  launch_combine(c, s_comp, pdl && !prof);
-  dbg("combine", -1, p);
+  if (cur_ds && fuse_comb && ep_world == 1 && c.acc && l + 1 < L && !up_fx) {
+    pend_comb = true;  // QKV(l+1) forms the residual and LN1 itself
+  } else {
+    launch_combine(c, s_comp, pdl && !prof);
+    dbg("combine", -1, p);
+  }
   unit_done();
   return MOE_OK;
 }
@@ -1078,6 +1102,7 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* uf = getenv("MOE_UP_FX")) e->up_fx = atoi(uf) != 0;
   if (const char* df = getenv("MOE_DN_FX")) e->dn_fx = atoi(df) != 0;
   if (const char* pf = getenv("MOE_PF_W2")) e->pf_w2 = atoi(pf) != 0;
+  if (const char* fc = getenv("MOE_FUSE_COMBINE")) e->fuse_comb = atoi(fc) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
   for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);

@@ -99,6 +99,19 @@ MOE_DEV bool wait_flag(const uint32_t* f, uint32_t gen, int* err, unsigned long 
   return true;
 }
 
+// sum over the GEMV's consumer warps (named barrier 1, fixed order); `red`
+// needs 9 floats and is free again when this returns
+MOE_DEV float cons_sum(float v, float* red, int nthr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = nthr >> 5;
+  v = warp_sum(v);
+  if (lane == 0) red[w] = v;
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  float t = 0.f;
+  for (int i = 0; i < nw; ++i) t += red[i];
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  return t;
+}
+
 MOE_DEV void fx_add(unsigned long long* p, float a, int* err) {
   const float q = a * MOE_FX_SCALE;
   if (!(fabsf(q) < 0x1p62f)) {  // non-finite or out of range: the reference would
@@ -159,10 +172,11 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   // the CTA's x rows (outputs of the previous kernel, L2-resident) come through
   // the producer's bulk-copy queue ahead of the weight stream: consumer loads
   // issued next to a saturating weight stream wait behind it for microseconds
-  const bool swiglu = J.xmode != X_PLAIN;
+  const bool swiglu = J.xmode == X_SWIGLU;
   const int xes = J.xfx ? 8 : 4;  // bytes per x element (fixed-point sums or fp32)
   const int xparts = J.xS > 1 ? J.xS : 1;  // producer partials per input array
-  const bool xstage = xin_cap > 0 && nrows > 0 && !(J.xS > 1 && J.xfx) &&
+  const bool xcomb = J.xmode == X_COMBINE;
+  const bool xstage = !xcomb && xin_cap > 0 && nrows > 0 && !(J.xS > 1 && J.xfx) &&
                       (swiglu ? 2 : 1) * xparts * nrows * xes <= xin_cap;
 
   if (threadIdx.x == 0) {
@@ -296,6 +310,51 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       return;
     }
   }
+  if (xcomb) {  // fused combine + LayerNorm of the previous layer's output
+    float* xf = reinterpret_cast<float*>(xin);  // the full residual [K]
+    const int K = M.K;
+    const float w0 = P.route->w[0], w1 = J.ctop > 1 ? P.route->w[1] : 0.f;
+    float s = 0.f;
+    for (int i0 = threadIdx.x; i0 < K; i0 += 8 * nthr) {  // 24 loads in flight
+      float hv[8];
+      unsigned long long q0[8], q1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * nthr;
+        hv[u] = i < K ? __ldcg(J.x + i) : 0.f;
+        q0[u] = i < K ? __ldcg(J.cacc + i) : 0ull;
+        q1[u] = (i < K && J.ctop > 1) ? __ldcg(J.cacc + K + i) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * nthr;
+        if (i < K) {
+          float o = __fadd_rn(hv[u], __fmul_rn(w0, fx_val(q0[u])));  // model.py:251-254
+          if (J.ctop > 1) o = __fadd_rn(o, __fmul_rn(w1, fx_val(q1[u])));
+          xf[i] = o;
+          s += o;
+          if (blockIdx.x == 0) J.xout[i] = o;
+        }
+      }
+    }
+    // LayerNorm statistics over the consumer warps (named barrier), the
+    // reference's rounding structure (model.py:186-189)
+    const float mu = __fdiv_rn(cons_sum(s, misc, nthr), (float)K);
+    float q = 0.f;
+    for (int i = threadIdx.x; i < K; i += nthr) {
+      const float t = __fsub_rn(xf[i], mu);
+      q = fmaf(t, t, q);
+    }
+    const float var = __fdiv_rn(cons_sum(q, misc, nthr), (float)K);
+    const float den = sqrtf(__fadd_rn(var, 1e-5f));
+    for (int i = threadIdx.x; i < nrows; i += nthr) {
+      const int r = row0 + i;
+      const float v =
+          __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(xf[r], mu), den), __ldg(J.lng + r)),
+                    __ldg(J.lnb + r));
+      xs[i] = v * xscale;
+    }
+  }
   if (xstage) {  // x rows from the producer's bulk copy
     gemv::mbar_wait(xbar, 0);
     const float* xf = reinterpret_cast<const float*>(xin);
@@ -319,7 +378,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   }
   // x (or the SwiGLU of the up projections) in batches of 4 rows per thread:
   // every load of a batch is issued before any use
-  for (int i0 = 0; !xstage && i0 < nrows; i0 += 4 * nthr) {
+  for (int i0 = 0; !xstage && !xcomb && i0 < nrows; i0 += 4 * nthr) {
     float va[4], vb[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -650,17 +709,34 @@ MOE_DEV float block_sum_f(float v, float* red) {
 // LayerNorm with the reference's rounding structure (model.py:186-189):
 // population mean / variance, then ((x - mu) / sqrt(var + eps)) * gamma + beta
 // with separately rounded float32 ops.  x, g, b may live in shared memory.
+// The statistics are reduced over exactly 256 lanes (thread t sums x[t +
+// 256k] in k order, butterfly warp sums, then the 8 warp sums in order)
+// whatever the block size, so every LN site -- the 1024-thread kernels and
+// the QKV GEMV's fused combine + LN1 on its 8 consumer warps -- rounds alike.
+MOE_DEV float ln_sum256(float v, float* red) {  // blockDim >= 256, all threads call
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0 && w < 8) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < 8; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
 MOE_DEV void layernorm_block(const float* x, const float* g, const float* b, float* y, float* ysh,
                              int d, float* red) {
+  const bool lane256 = threadIdx.x < 256;
   float s = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) s += x[i];
-  const float mu = __fdiv_rn(block_sum_f(s, red), (float)d);
+  if (lane256)
+    for (int i = threadIdx.x; i < d; i += 256) s += x[i];
+  const float mu = __fdiv_rn(ln_sum256(s, red), (float)d);
   float q = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float t = __fsub_rn(x[i], mu);
-    q = fmaf(t, t, q);
-  }
-  const float var = __fdiv_rn(block_sum_f(q, red), (float)d);
+  if (lane256)
+    for (int i = threadIdx.x; i < d; i += 256) {
+      const float t = __fsub_rn(x[i], mu);
+      q = fmaf(t, t, q);
+    }
+  const float var = __fdiv_rn(ln_sum256(q, red), (float)d);
   const float den = sqrtf(__fadd_rn(var, 1e-5f));
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float v = __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(x[i], mu), den), g[i]), b[i]);
@@ -1520,6 +1596,10 @@ static int gemv_xin_cap(const GLaunch& P, int bits, int xs_cap, int zs_cap, int 
   int cap = 0;
   for (int i = 0; i < P.nj; ++i) {
     const GJob& J = P.j[i];
+    if (J.xmode == X_COMBINE) {  // the full residual
+      cap = max(cap, J.M.K * 4);
+      continue;
+    }
     if (J.xS > 1 && J.xfx) continue;
     const int es = J.xfx ? 8 : 4, n = (J.xmode != X_PLAIN ? 2 : 1) * (J.xS > 1 ? J.xS : 1);
     cap = max(cap, n * es * J.QPS * 4);

@@ -15,7 +15,11 @@ __host__ __device__ constexpr int gemv_qs(int bits) { return MOE_GEMV_WARPS * ge
 #define MOE_GEMV_RING (80 * 1024)  // bytes of stage ring per CTA (2 CTAs / SM)
 #define MOE_XS_MAX 4096            // rows of x kept in smem per CTA
 
-enum XMode { X_PLAIN = 0, X_SWIGLU = 1 };
+// X_COMBINE: the input row slice is LayerNorm(h + w0*y0 + w1*y1) (the MoE
+// combine of the previous layer, model.py:251-254, fused with the next LN):
+// every CTA forms the full residual (fixed-point expert sums, reference
+// order) and its LN statistics; block 0 also stores the residual
+enum XMode { X_PLAIN = 0, X_SWIGLU = 1, X_COMBINE = 2 };
 
 struct GJob {
   MatDev M;            // absolute pointers, or byte offsets when rel_slot >= 0
@@ -27,6 +31,13 @@ struct GJob {
   int xS;              // the inputs are xS split-K partials [xS][xstride], summed in
   int xstride;         //   order on load (a producer GEMV left them unreduced); 0/1: plain
   int xfx;             // x (or up1/up3) are fixed-point sums (uint64, reduce == 2 producer)
+  // X_COMBINE inputs: x = h, expert sums `cacc` [ctop][K] (fixed point), LN
+  // affine, and the residual output (block 0)
+  const unsigned long long* cacc;
+  const float* lng;
+  const float* lnb;
+  float* xout;
+  int ctop;
   float* part;         // split-K partial outputs [S][N]
   float* out;          // final outputs [N] when reduce == 1 (the last CTA of a cb sums
   int reduce;          //   the partials in order); 0: the consumer sums part[0..S);
