@@ -262,6 +262,12 @@ def run_b200(args, rank, world):
                   for l in range(nl) if ok[1 + 8 * l + kind] and marks[1 + 8 * l + kind][7] > 0]
             if ep:
                 phases[nm + "_epilogue"] = [round(float(x), 2) for x in np.array(ep).mean(0) / 1e3]
+        # QKV with the fused combine: residual loads, LN statistics, own rows
+        cm = [(marks[1 + 8 * l][6] - marks[1 + 8 * l][5], marks[1 + 8 * l][7] - marks[1 + 8 * l][6],
+               marks[1 + 8 * l][0] - marks[1 + 8 * l][7])
+              for l in range(1, nl) if ok[1 + 8 * l] and marks[1 + 8 * l][7] > marks[1 + 8 * l][6] > 0]
+        if cm:
+            phases["qkv_combine"] = [round(float(x), 2) for x in np.array(cm).mean(0) / 1e3]
         # tail thread-0 sub-phases (marks in the layer's exchange slot on one GPU)
         if world == 1:
             sub = [(marks[1 + 8 * l + 7][:2] - marks[1 + 8 * l + 3][5]) / 1e3 for l in range(nl)

@@ -298,6 +298,7 @@ struct moe_engine {
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
   bool up_fx = false;  // MOE_UP_FX=1: up projections as fixed-point sums (else partials)
   bool dn_fx = true;   // MOE_DN_FX=0: W2 reduced by the last CTA per column block instead
+  int dn_cluster = 0;     // MOE_DN_CLUSTER=C: W2 split-K pre-reduced over clusters of C
   bool fuse_comb = true;  // MOE_FUSE_COMBINE=0: keep the combine kernel between layers
   bool pend_comb = false;  // decode: layer l's combine + LN1(l+1) is fused into QKV(l+1)
   bool pf_w2 = false;  // MOE_PF_W2=1: L2 prefetch of W2 during the W1/W3 GEMV (measured slower)
@@ -604,7 +605,7 @@ GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* part, float
 // block offsets of the jobs, and the cluster size: the largest divisor of the
 // (common) split count S that is <= 8, so each cluster holds consecutive
 // splits of one column block and reduces them over distributed shared memory
-static int finalize_launch(GLaunch& P) {
+static int finalize_launch(GLaunch& P, int want_cluster = 0) {
   int blk = 0;
   for (int i = 0; i < P.nj; ++i) {
     P.j[i].blk0 = blk;
@@ -621,6 +622,7 @@ static int finalize_launch(GLaunch& P) {
         c = k;
         break;
       }
+  if (same && want_cluster > 1 && S % want_cluster == 0) c = want_cluster;
   P.cluster = c;
   return blk;
 }
@@ -813,8 +815,8 @@ int moe_engine::enq_experts(int l, int p) {
       J.up3 = reinterpret_cast<const float*>(up_acc + (size_t)(2 * j + 1) * f);
     }
   }
-  const int ndn = finalize_launch(dn);
-  if (dn.cluster > 1)
+  const int ndn = finalize_launch(dn, dn_cluster);
+  if (dn.cluster > 1 && dn.j[0].reduce != 2)
     for (int j = 0; j < topk; ++j) dn.j[j].reduce = 1;
   for (int j = 0; j < topk; ++j) dn.j[j].xS = dn.j[j].xfx ? 1 : S_up / u.cluster;
   if (serial_copies) {  // ncu / debugging: the host drains the mailbox before the GEMV
@@ -1103,6 +1105,7 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* df = getenv("MOE_DN_FX")) e->dn_fx = atoi(df) != 0;
   if (const char* pf = getenv("MOE_PF_W2")) e->pf_w2 = atoi(pf) != 0;
   if (const char* fc = getenv("MOE_FUSE_COMBINE")) e->fuse_comb = atoi(fc) != 0;
+  if (const char* dc = getenv("MOE_DN_CLUSTER")) e->dn_cluster = atoi(dc);
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
   for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
@@ -1387,6 +1390,12 @@ int moe_finalize(moe_engine* e) {
   plan((d / wca + 31) / 32, d / 4, e->attn_bits, &e->Q_wo, &e->S_wo);
   plan(2 * e->topk * ((f / wcx + 31) / 32), d / 4, e->expert_bits, &e->Q_up, &e->S_up);
   plan(e->topk * ((d / wcx + 31) / 32), f / 4, e->expert_bits, &e->Q_dn, &e->S_dn);
+  if (e->dn_cluster > 1 && e->S_dn % e->dn_cluster) {  // splits in whole clusters
+    const int nq = (f / 4 + 7) / 8 * 8, S = std::max(e->dn_cluster,
+                                                       e->S_dn / e->dn_cluster * e->dn_cluster);
+    e->Q_dn = (nq + S - 1) / S;
+    e->S_dn = (nq + e->Q_dn - 1) / e->Q_dn;
+  }
   plan(e->lm_head.M.ncb, d / 4, e->lm_bits, &e->Q_lm, &e->S_lm);
   if ((rc = e->dalloc(&e->qkv_part, (size_t)3 * e->S_qkv * d))) return rc;
   if ((rc = e->dalloc(&e->wo_part, (size_t)e->S_wo * d))) return rc;

@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
         }
       }
     }
+    tl_mark(P.site, 6);  // residual formed (profiling; the epilogue reuses the slot)
     // LayerNorm statistics over the consumer warps (named barrier), the
     // reference's rounding structure (model.py:186-189)
     const float mu = __fdiv_rn(cons_sum(s, misc, nthr), (float)K);
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     }
     const float var = __fdiv_rn(cons_sum(q, misc, nthr), (float)K);
     const float den = sqrtf(__fadd_rn(var, 1e-5f));
+    tl_mark(P.site, 7);  // LN statistics
     for (int i = threadIdx.x; i < nrows; i += nthr) {
       const int r = row0 + i;
       const float v =
@@ -569,11 +571,11 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   float* red = reinterpret_cast<float*>(ring);
   float* ysum = red + W * 32 * (WC + 1);  // this CTA's partial outputs [32*WC]
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
-  tl_mark(P.site, 6);  // every consumer warp left the loop
+  if (!xcomb) tl_mark(P.site, 6);  // every consumer warp left the loop
 #pragma unroll
   for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
-  tl_mark(P.site, 7);  // per-warp results in smem
+  if (!xcomb) tl_mark(P.site, 7);  // per-warp results in smem
   const float zo_out = zo_sum * gemv::kZUnscale;
   const int C = P.cluster, SC = J.S / C;  // cluster = C consecutive splits of one cb
   const int crank = blockIdx.x % C, sc = s / C;
@@ -608,7 +610,10 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       float a = 0.f;
 #pragma unroll
       for (int r = 0; r < 8; ++r) a += v[r];
-      dst[(size_t)cb * 32 * WC + t] = a;
+      if (J.reduce == 2)
+        fx_add(J.acc + (size_t)cb * 32 * WC + t, a, P.err);
+      else
+        dst[(size_t)cb * 32 * WC + t] = a;
     }
     cluster_sync();  // peers keep their shared memory until every slice is read
   }
