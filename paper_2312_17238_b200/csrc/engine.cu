@@ -2201,6 +2201,11 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
   CU(cudaMalloc(&out, (size_t)njobs * N * 4));
   CU(cudaMalloc(&cnt, 4096 * 4));
   CU(cudaMemset(cnt, 0, 4096 * 4));
+  // split-K as in decode: fixed-point sums (MOE_BENCH_REDUCE=1: last-CTA reduction)
+  const int bred = getenv("MOE_BENCH_REDUCE") ? atoi(getenv("MOE_BENCH_REDUCE")) : 2;
+  unsigned long long* bacc = nullptr;
+  CU(cudaMalloc(&bacc, (size_t)njobs * N * 8));
+  CU(cudaMemset(bacc, 0, (size_t)njobs * N * 8));
   launch_synth(9, 9, K, 1e-5f, 0, x, s);
   std::vector<GLaunch> P(nsets);
   int nblk = 0;
@@ -2217,7 +2222,8 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
       J.x = x;
       J.part = part + (size_t)j * S * N;
       J.out = out + (size_t)j * N;
-      J.reduce = 1;
+      J.reduce = bred;
+      J.acc = bacc + (size_t)j * N;
       J.QPS = qps;
       J.S = S;
     }
@@ -2299,6 +2305,7 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
   cudaFree(part);
   cudaFree(out);
   cudaFree(cnt);
+  cudaFree(bacc);
   Q.release();
   cudaStreamDestroy(s);
   return rc;

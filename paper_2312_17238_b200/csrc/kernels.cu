@@ -1129,7 +1129,52 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   // gate logits of this layer and the guessed layer on the same h (model.py:210,
   // engine.py:60-68): thread t owns expert t % E over rows t/E, t/E + nt/E, ...
   const int nt = (blockDim.x / E) * E;
-  if (tid < nt) {
+  const bool gate8 = hg && E == 8;  // fast path: one 16-byte fp16 gate row per load
+  if (gate8) {
+    // thread t takes rows t, t + nthreads, ... for all 8 experts (and the
+    // guessed layer's 8): fp32 partials, then double sums in a fixed order
+    float pa[8], pg[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) pa[e] = pg[e] = 0.f;
+    for (int r = tid; r < d; r += blockDim.x) {
+      const float hv = hs[r];
+      const uint4 gl4 = *reinterpret_cast<const uint4*>(gls + (size_t)r * 8);
+      const __half2* gl2 = reinterpret_cast<const __half2*>(&gl4);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 g = __half22float2(gl2[e]);
+        pa[2 * e] = fmaf(hv, g.x, pa[2 * e]);
+        pa[2 * e + 1] = fmaf(hv, g.y, pa[2 * e + 1]);
+      }
+      if (guess) {
+        const uint4 gg4 = *reinterpret_cast<const uint4*>(ggs + (size_t)r * 8);
+        const __half2* gg2 = reinterpret_cast<const __half2*>(&gg4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 g = __half22float2(gg2[e]);
+          pg[2 * e] = fmaf(hv, g.x, pg[2 * e]);
+          pg[2 * e + 1] = fmaf(hv, g.y, pg[2 * e + 1]);
+        }
+      }
+    }
+    // fp32 butterfly sums of the 8 (16) partials, interleaved so the
+    // shuffles of different logits overlap; warp sums go to double below
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) pa[e] += __shfl_xor_sync(0xffffffffu, pa[e], o);
+      if (guess)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pg[e] += __shfl_xor_sync(0xffffffffu, pg[e], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        gpart[warp * 16 + e] = (double)pa[e];
+        gpart[warp * 16 + 8 + e] = (double)pg[e];
+      }
+    }
+  } else if (tid < nt) {
     const int e = tid % E, rstep = nt / E;
     // per-thread fp32 partials over 2 interleaved accumulators, combined in
     // double across threads (fixed order below)
@@ -1161,7 +1206,13 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   __syncthreads();
   tl_mark(P.site, 3);
   const int nlog = guess ? 2 * E : E;
-  if (warp < nlog) {  // warp w reduces logit w in a fixed order
+  if (gate8) {  // logit e: the warps' sums in warp order
+    if (tid < nlog) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += gpart[w * 16 + tid];
+      lg[tid] = (float)t;
+    }
+  } else if (warp < nlog) {  // warp w reduces logit w in a fixed order
     const int e = warp % E;
     const double* gp = gpart + (warp >= E ? blockDim.x : 0);
     double t = 0.0;

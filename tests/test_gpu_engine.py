@@ -269,3 +269,28 @@ def test_mixtral_width_parity_vs_oracle(ebits, k, m):
     err, tol = _close(res.final_logits, rlog)
     assert err <= tol, (err, tol)
     eng.close()
+
+
+def test_mixtral_width_decode_bitwise_reproducible():
+    """The split-K reductions are order independent (int64 fixed-point sums,
+    kernels.cuh MOE_FX_*), so two decodes of the same prompt give bit-identical
+    logits and tokens whatever the CTA timing and cache state."""
+    import bench
+    from paper_2312_17238_b200 import CacheConfig, OffloadEngine, SpeculationConfig
+    from paper_2312_17238_b200 import synthetic_model
+    cfg = dict(bench.MIXTRAL)
+    cfg["n_layers"] = 2
+    cobj = bench.cfg_obj(cfg)
+    eng = OffloadEngine(synthetic_model(cobj, 0), CacheConfig(k=1, b=4),
+                        SpeculationConfig(enabled=True, m=2), record_hidden=False,
+                        synth=(0, 4, 3), expert_bytes=bench.expert_bytes(bench.MIXTRAL, 3))
+    prompt = [int(t) for t in np.random.default_rng(1).integers(0, cobj.vocab_size, 4)]
+    runs = []
+    for _ in range(2):
+        eng.reset_session()
+        eng.prefill(prompt)
+        r = eng.decode(4)
+        runs.append((r.tokens, r.final_logits.copy()))
+    eng.close()
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
