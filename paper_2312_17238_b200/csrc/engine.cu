@@ -298,6 +298,7 @@ struct moe_engine {
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
   bool up_fx = false;  // MOE_UP_FX=1: up projections as fixed-point sums (else partials)
   bool dn_fx = true;   // MOE_DN_FX=0: W2 reduced by the last CTA per column block instead
+  bool comb_hold = false;  // MOE_COMB_HOLD=1: fused-combine QKV streams weights after the wait
   int dn_cluster = 0;     // MOE_DN_CLUSTER=C: W2 split-K pre-reduced over clusters of C
   bool fuse_comb = true;  // MOE_FUSE_COMBINE=0: keep the combine kernel between layers
   bool pend_comb = false;  // decode: layer l's combine + LN1(l+1) is fused into QKV(l+1)
@@ -653,6 +654,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   }
   if (pend_comb) {  // previous layer's combine + this layer's LN1 in the QKV prologue
     q.route = route + p;
+    q.hold = comb_hold ? 1 : 0;
     for (int i = 0; i < 3; ++i) {
       GJob& J = q.j[i];
       J.xmode = X_COMBINE;
@@ -1106,6 +1108,7 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* pf = getenv("MOE_PF_W2")) e->pf_w2 = atoi(pf) != 0;
   if (const char* fc = getenv("MOE_FUSE_COMBINE")) e->fuse_comb = atoi(fc) != 0;
   if (const char* dc = getenv("MOE_DN_CLUSTER")) e->dn_cluster = atoi(dc);
+  if (const char* ch = getenv("MOE_COMB_HOLD")) e->comb_hold = atoi(ch) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
   for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);

@@ -233,6 +233,9 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
         gemv::mbar_arrive_tx(zbar, bytes);
         gemv::bulk_g2s(zsm, reinterpret_cast<const void*>(za - lead), bytes, zbar);
       }
+      // the fused combine reads 80 KB of residual inputs per CTA right after the
+      // previous kernel: hold the weight ring until then (MOE_COMB_HOLD)
+      if (xcomb && P.hold) gemv::pdl_wait();
       const uint8_t* src = M.base + cb_offset(M, cb) + (int64_t)qs * rb;
       const uint64_t pol = gemv::policy_evict_first();
       // L2 prefetch of the next kernel's expert weights, once the ring is full

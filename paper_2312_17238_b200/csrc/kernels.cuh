@@ -63,6 +63,7 @@ struct GLaunch {
   // routed expert's buffer (e.g. W2 while W1/W3 stream), split over the CTAs
   // of the jobs on that expert
   long long pf_off[2], pf_len[2];
+  int hold;  // X_COMBINE launches: start the weight stream only after griddepcontrol.wait
   int site;  // timeline slot of this launch (profiling), -1 none
 };
 
