@@ -299,6 +299,8 @@ struct moe_engine {
   bool up_fx = false;  // MOE_UP_FX=1: up projections as fixed-point sums (else partials)
   bool dn_fx = true;   // MOE_DN_FX=0: W2 reduced by the last CTA per column block instead
   bool comb_hold = false;  // MOE_COMB_HOLD=1: fused-combine QKV streams weights after the wait
+  bool route_stamps = false;  // MOE_ROUTE_STAMPS=1: expert GEMVs spin on the route stamp (neutral)
+  unsigned int tok_seq = 0;  // decode tokens issued (DecodeState.seq, route stamps)
   int dn_cluster = 0;     // MOE_DN_CLUSTER=C: W2 split-K pre-reduced over clusters of C
   bool fuse_comb = true;  // MOE_FUSE_COMBINE=0: keep the combine kernel between layers
   bool pend_comb = false;  // decode: layer l's combine + LN1(l+1) is fused into QKV(l+1)
@@ -751,6 +753,8 @@ int moe_engine::enq_experts(int l, int p) {
   u.wait_ns = wait_ns;
   u.cnt = cnt;
   u.site = site_of(l, 4);
+  u.ds = route_stamps ? cur_ds : nullptr;  // decode: spin on the route stamp, not the grid
+  u.layer = l;
   GLaunch dn = u;
   dn.site = site_of(l, 5);
   for (int j = 0; j < topk; ++j) {
@@ -1108,6 +1112,7 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* pf = getenv("MOE_PF_W2")) e->pf_w2 = atoi(pf) != 0;
   if (const char* fc = getenv("MOE_FUSE_COMBINE")) e->fuse_comb = atoi(fc) != 0;
   if (const char* dc = getenv("MOE_DN_CLUSTER")) e->dn_cluster = atoi(dc);
+  if (const char* rs = getenv("MOE_ROUTE_STAMPS")) e->route_stamps = atoi(rs) != 0;
   if (const char* ch = getenv("MOE_COMB_HOLD")) e->comb_hold = atoi(ch) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
@@ -1598,7 +1603,7 @@ int moe_step(moe_engine* e, int32_t token, float* logits_out) {
                                    std::to_string(e->T));
   e->launches = 0;
   CU(cudaEventRecord(e->t0, e->s_comp));
-  *e->ds_host = DecodeState{e->pos, 0, token, 0};
+  *e->ds_host = DecodeState{e->pos, 0, token, e->tok_seq};
   CU(cudaMemcpyAsync(e->ds_dev, e->ds_host, sizeof(DecodeState), cudaMemcpyHostToDevice,
                      e->s_comp));
   rc = e->run_tokens(1);
@@ -1607,6 +1612,7 @@ int moe_step(moe_engine* e, int32_t token, float* logits_out) {
   rc = e->finish_call(logits_out != nullptr);
   if (rc) return rc;
   e->pos += 1;
+  e->tok_seq += 1;
   if (logits_out) memcpy(logits_out, e->logits_h, (size_t)e->V * 4);
   e->has_logits = true;
   return MOE_OK;
@@ -1623,7 +1629,7 @@ int moe_decode_greedy(moe_engine* e, int32_t n, int32_t* tokens_out, float* fina
   e->launches = 0;
   CU(cudaEventRecord(e->t0, e->s_comp));
   // cursor: position from the host, first token = argmax of the last logits
-  *e->ds_host = DecodeState{e->pos, 0, 0, 0};
+  *e->ds_host = DecodeState{e->pos, 0, 0, e->tok_seq};
   CU(cudaMemcpyAsync(e->ds_dev, e->ds_host, sizeof(DecodeState), cudaMemcpyHostToDevice,
                      e->s_comp));
   CU(cudaMemcpyAsync(&e->ds_dev->tok, e->tok_dev, sizeof(int), cudaMemcpyDeviceToDevice,
@@ -1634,6 +1640,7 @@ int moe_decode_greedy(moe_engine* e, int32_t n, int32_t* tokens_out, float* fina
   rc = e->finish_call(final_logits_out != nullptr);
   if (rc) return rc;
   e->pos += n;
+  e->tok_seq += (unsigned)n;
   if (tokens_out) CU(cudaMemcpy(tokens_out, e->tok_hist, (size_t)n * 4, cudaMemcpyDeviceToHost));
   if (final_logits_out) memcpy(final_logits_out, e->logits_h, (size_t)e->V * 4);
   return MOE_OK;

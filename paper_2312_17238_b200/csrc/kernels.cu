@@ -192,7 +192,21 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   gemv::pdl_trigger();
 
   if (warp == W) {  // ---------------------------------------------- producer
-    if (J.rel_slot >= 0) {
+    if (J.rel_slot >= 0 && P.ds) {
+      // decode: the route of (token, layer) is published by the tail with a
+      // stamp; spinning on it lets the weight stream start before the
+      // previous grid completes (x still waits for griddepcontrol.wait)
+      const unsigned int want = route_stamp(P.ds->seq, P.layer);
+      const unsigned long long t0 = globaltimer();
+      while (ld_acquire_u32(&P.route->stamp) != want) {
+        __nanosleep(64);
+        if (globaltimer() - t0 > P.wait_ns) {
+          if (lane == 0) atomicOr(P.err, MOE_ERRF_TIMEOUT);
+          break;
+        }
+      }
+      if (P.route->buf[J.rel_slot] < 0) return;
+    } else if (J.rel_slot >= 0) {
       gemv::pdl_wait();  // the route is written by the previous kernel
       // expert parallel: another rank owns this expert -> the whole cluster
       // (same job) skips, before any cluster barrier
@@ -200,8 +214,8 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     }
     // x rows: one bulk copy per input array (after the previous kernel completed)
     auto issue_x = [&]() {
+      if (J.rel_slot < 0 || P.ds) gemv::pdl_wait();  // x is the previous kernel's output
       if (!xstage) return;
-      if (J.rel_slot < 0) gemv::pdl_wait();
       const uint32_t bytes = (uint32_t)(nrows * xes);
       gemv::mbar_arrive_tx(xbar, (swiglu ? 2u : 1u) * (uint32_t)xparts * bytes);
       const uint8_t* a = reinterpret_cast<const uint8_t*>(swiglu ? J.up1 : J.x);
@@ -217,7 +231,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     };
     if (lane == 0) {
       if (J.rel_slot >= 0) {
-        issue_x();
+        if (!P.ds) issue_x();
         const int buf = P.route->buf[J.rel_slot];
         // the tail saw the buffer's copy already published: no flag round trip
         if (!P.route->ready[J.rel_slot])
@@ -263,7 +277,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       uint32_t ph = 0;
       for (int it = 0; it < nit; ++it) {
         // dense weights: the ring is prefetched before the previous kernel ends
-        if (it == nst && J.rel_slot < 0) issue_x();
+        if (it == nst && (J.rel_slot < 0 || P.ds)) issue_x();
         if (it == nst) issue_prefetch();
         if (it >= nst) gemv::mbar_wait(empty + st, ph ^ 1);
         const int nq = min(QS, qe - (qs + it * QS));
@@ -276,7 +290,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
           ph ^= 1;
         }
       }
-      if (nit <= nst && J.rel_slot < 0) issue_x();
+      if (nit <= nst && (J.rel_slot < 0 || P.ds)) issue_x();
       if (nit <= nst) issue_prefetch();
     }
     __syncwarp();
@@ -1308,6 +1322,11 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   tl_mark(P.site, 6);
   if (P.mode == 0) {
     __syncthreads();
+    if (tid == 0 && P.ds) {  // every route field is written: publish the stamp
+      const unsigned int st = route_stamp(P.ds->seq, P.layer);
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&P.route->stamp), "r"(st)
+                   : "memory");
+    }
     store::stage_out(P.st, sst);
   }
   tl_mark(P.site, 7);
@@ -1561,6 +1580,7 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
       ds->tok = t;
       ds->step += 1;
       ds->pos += 1;
+      ds->seq += 1;
     }
     *P.counter = 0u;
   }

@@ -46,6 +46,8 @@ struct GJob {
   int S, QPS, blk0;    // splits of the quad range, quads per split (multiple of QS)
 };
 
+struct DecodeState;
+
 struct GLaunch {
   GJob j[MOE_GEMV_MAXJOBS];
   int nj;
@@ -63,6 +65,8 @@ struct GLaunch {
   // routed expert's buffer (e.g. W2 while W1/W3 stream), split over the CTAs
   // of the jobs on that expert
   long long pf_off[2], pf_len[2];
+  const DecodeState* ds;  // decode: expert jobs spin on the route stamp of (ds->seq, layer)
+  int layer;
   int hold;  // X_COMBINE launches: start the weight stream only after griddepcontrol.wait
   int site;  // timeline slot of this launch (profiling), -1 none
 };
@@ -81,8 +85,14 @@ struct DecodeState {
   int pos;   // position of the token being decoded
   int step;  // index of this token within the current decode call
   int tok;   // token to embed
-  int pad;
+  unsigned int seq;  // decode tokens since the engine was created (never reused)
 };
+// route publication stamp of (token, layer): the tail writes it last
+// (release); expert GEMVs spin on it (acquire) instead of waiting for the
+// whole previous grid, so their weight streams start early
+__host__ __device__ inline unsigned int route_stamp(unsigned int seq, int layer) {
+  return seq * 64u + (unsigned)layer + 1u;
+}
 
 struct AttnParams {
   const float* qkv_part;  // [3][S][d]
