@@ -735,6 +735,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   t.pos = p;
   t.mode = mode;
   t.ep_size = 1;
+  t.stamp = route_stamps ? 1 : 0;
   if (tail_smem_bytes(t) > 226 * 1024) t.gh_l = t.gh_g = nullptr;  // gates too big to stage
   launch_tail(t, s_comp, pl);
   dbg("tail", l, p);

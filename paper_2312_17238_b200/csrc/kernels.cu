@@ -1083,7 +1083,6 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
       tsm + ((3 * (size_t)d * 4 + (hg ? (guess ? 2 : 1) * (size_t)d * E * 2 : 0) + 15) & ~15));
   int* sst = reinterpret_cast<int*>(gpart + 2 * blockDim.x);
   uint32_t* fls = reinterpret_cast<uint32_t*>(sst + store::stage_ints(P.st) + 4);  // [nbuf]
-  __shared__ float red[33];
   __shared__ float lg[64];
   __shared__ __align__(8) uint64_t wbar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1134,7 +1133,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   gemv::mbar_wait(&wbar, 0);
   __syncthreads();
   tl_mark(P.site, 1);
-  layernorm_block(hs, g2s, b2s, P.h, hs, d, red);
+  layernorm_block(hs, g2s, b2s, P.h, hs, d, reinterpret_cast<float*>(gpart));
   __syncthreads();
   tl_mark(P.site, 2);
   int bad = 0;
@@ -1243,9 +1242,10 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   // lane e holds logit e; each round is a warp argmax with ties -> lower index
   // (np.argsort(-logits, kind="stable"), model.py:192-195, engine.py:60-68)
   __shared__ int sel_sh[MOE_MAX_TOPK], gsel_sh[16];
-  if (warp == 0) {
+  if (warp < 2) {  // warp 0: this layer's top-k, warp 1: the guessed layer's top-m
     const int k = P.top_k, mg = (guess && P.m > 0) ? P.m : 0;
-    for (int pass = 0; pass < 2; ++pass) {
+    {
+      const int pass = warp;
       const float* lv = pass == 0 ? lg : lg + E;
       const int rounds = pass == 0 ? k : mg;
       bool taken = false;
@@ -1322,7 +1322,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   tl_mark(P.site, 6);
   if (P.mode == 0) {
     __syncthreads();
-    if (tid == 0 && P.ds) {  // every route field is written: publish the stamp
+    if (tid == 0 && P.ds && P.stamp) {  // every route field is written: publish the stamp
       const unsigned int st = route_stamp(P.ds->seq, P.layer);
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&P.route->stamp), "r"(st)
                    : "memory");

@@ -126,6 +126,7 @@ struct TailParams {
   StoreDev st;
   int d, E, top_k, m, layer, guess_layer, pos, mode;  // mode 0 decode, 1 prefill (no store)
   int ep_rank, ep_size;   // expert parallel (ep_size 1 = off)
+  int stamp;              // decode: publish the route stamp (expert GEMVs spin on it)
   int site;  // timeline slot of this launch (profiling), -1 none
 };
 
