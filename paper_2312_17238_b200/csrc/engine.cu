@@ -301,6 +301,7 @@ struct moe_engine {
   bool comb_hold = false;  // MOE_COMB_HOLD=1: fused-combine QKV streams weights after the wait
   bool route_stamps = false;  // MOE_ROUTE_STAMPS=1: expert GEMVs spin on the route stamp (neutral)
   unsigned int tok_seq = 0;  // decode tokens issued (DecodeState.seq, route stamps)
+  bool pf_qkv = true;  // MOE_PF_QKV=0: no L2 prefetch of the next layer's QKV during W2
   int dn_cluster = 0;     // MOE_DN_CLUSTER=C: W2 split-K pre-reduced over clusters of C
   bool fuse_comb = true;  // MOE_FUSE_COMBINE=0: keep the combine kernel between layers
   bool pend_comb = false;  // decode: layer l's combine + LN1(l+1) is fused into QKV(l+1)
@@ -822,6 +823,14 @@ int moe_engine::enq_experts(int l, int p) {
       J.up3 = reinterpret_cast<const float*>(up_acc + (size_t)(2 * j + 1) * f);
     }
   }
+  if (cur_ds && pf_qkv && l + 1 < L) {  // pull the next layer's Wq/Wk/Wv into L2
+    const std::vector<DevMat>* ws[3] = {&wq, &wk, &wv};
+    for (int i = 0; i < 3; ++i) {
+      const DevMat& D = (*ws[i])[l + 1];
+      dn.pfa[i] = reinterpret_cast<const uint8_t*>(D.mem);
+      dn.pfl[i] = (long long)(D.bytes & ~size_t(15));
+    }
+  }
   const int ndn = finalize_launch(dn, dn_cluster);
   if (dn.cluster > 1 && dn.j[0].reduce != 2)
     for (int j = 0; j < topk; ++j) dn.j[j].reduce = 1;
@@ -1113,6 +1122,7 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* pf = getenv("MOE_PF_W2")) e->pf_w2 = atoi(pf) != 0;
   if (const char* fc = getenv("MOE_FUSE_COMBINE")) e->fuse_comb = atoi(fc) != 0;
   if (const char* dc = getenv("MOE_DN_CLUSTER")) e->dn_cluster = atoi(dc);
+  if (const char* pq = getenv("MOE_PF_QKV")) e->pf_qkv = atoi(pq) != 0;
   if (const char* rs = getenv("MOE_ROUTE_STAMPS")) e->route_stamps = atoi(rs) != 0;
   if (const char* ch = getenv("MOE_COMB_HOLD")) e->comb_hold = atoi(ch) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
@@ -1172,6 +1182,7 @@ static int load_dense_mat(moe_engine* e, const moe_matrix* m, DevMat* D, const c
   if (rc) return rc;
   if (D->mem) cudaFree(D->mem);
   CU(cudaMalloc(&D->mem, Lo.total() + 64));  // + slack: 16-byte bulk copies of zmeta
+  D->bytes = Lo.total();
   e->dev_bytes += Lo.total();
   rc = upload_and_tile(m, Lo, static_cast<uint8_t*>(D->mem), e->s_comp);
   if (rc) return rc;
@@ -2009,6 +2020,7 @@ int moe_synth_model(moe_engine* e, uint64_t seed, int32_t attn_bits, int32_t exp
       DevMat& D = j == 0 ? e->wq[l] : j == 1 ? e->wk[l] : j == 2 ? e->wv[l] : e->wo[l];
       if (D.mem) cudaFree(D.mem);
       CU(cudaMalloc(&D.mem, lo.total() + 64));
+      D.bytes = lo.total();
       e->dev_bytes += lo.total();
       CU(cudaMemcpyAsync(D.mem, Q.tiled, lo.total(), cudaMemcpyDeviceToDevice, s));
       D.M = matdev_from(lo, static_cast<uint8_t*>(D.mem));

@@ -254,6 +254,15 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       const uint64_t pol = gemv::policy_evict_first();
       // L2 prefetch of the next kernel's expert weights, once the ring is full
       auto issue_prefetch = [&]() {
+        for (int r = 0; r < 3; ++r) {  // absolute ranges, a slice per CTA
+          const long long len = P.pfl[r];
+          if (len <= 0) continue;
+          const long long per = ((len + gridDim.x - 1) / gridDim.x + 15) & ~15ll;
+          long long o = (long long)blockIdx.x * per;
+          const long long e = min(len, o + per);
+          for (; o < e; o += 65536)
+            gemv::bulk_prefetch_l2(P.pfa[r] + o, (uint32_t)((min(e - o, 65536ll) + 15) & ~15ll));
+        }
         if (J.rel_slot < 0 || (P.pf_len[0] <= 0 && P.pf_len[1] <= 0)) return;
         int n = 0, idx = -1;  // this CTA's index among the CTAs on the same expert
         for (int i = 0; i < P.nj; ++i)

@@ -65,6 +65,10 @@ struct GLaunch {
   // routed expert's buffer (e.g. W2 while W1/W3 stream), split over the CTAs
   // of the jobs on that expert
   long long pf_off[2], pf_len[2];
+  // L2 prefetch of absolute byte ranges (e.g. the next layer's Wq/Wk/Wv while
+  // W2 streams), split over every CTA of the launch
+  const uint8_t* pfa[3];
+  long long pfl[3];
   const DecodeState* ds;  // decode: expert jobs spin on the route stamp of (ds->seq, layer)
   int layer;
   int hold;  // X_COMBINE launches: start the weight stream only after griddepcontrol.wait
