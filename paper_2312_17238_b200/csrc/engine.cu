@@ -301,7 +301,7 @@ struct moe_engine {
   bool comb_hold = false;  // MOE_COMB_HOLD=1: fused-combine QKV streams weights after the wait
   bool route_stamps = false;  // MOE_ROUTE_STAMPS=1: expert GEMVs spin on the route stamp (neutral)
   unsigned int tok_seq = 0;  // decode tokens issued (DecodeState.seq, route stamps)
-  bool pf_qkv = true;  // MOE_PF_QKV=0: no L2 prefetch of the next layer's QKV during W2
+  bool pf_qkv = false;  // MOE_PF_QKV=1: L2 prefetch of the next layer's QKV during W2 (neutral)
   int dn_cluster = 0;     // MOE_DN_CLUSTER=C: W2 split-K pre-reduced over clusters of C
   bool fuse_comb = true;  // MOE_FUSE_COMBINE=0: keep the combine kernel between layers
   bool pend_comb = false;  // decode: layer l's combine + LN1(l+1) is fused into QKV(l+1)

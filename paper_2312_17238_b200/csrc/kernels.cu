@@ -123,7 +123,8 @@ MOE_DEV void fx_add(unsigned long long* p, float a, int* err) {
 // consumer side: fixed-point sum -> fp32 (one rounding); the consumer resets
 // the sums (fx_clear) after all its loads are issued
 MOE_DEV float fx_val(unsigned long long v) {
-  return __double2float_rn((double)(long long)v * MOE_FX_UNSCALE);
+  // one rounding of the exact integer to fp32, then an exact power-of-two scale
+  return __ll2float_rn((long long)v) * (float)MOE_FX_UNSCALE;
 }
 
 template <int BITS>
