@@ -177,6 +177,10 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const int xes = J.xfx ? 8 : 4;  // bytes per x element (fixed-point sums or fp32)
   const int xparts = J.xS > 1 ? J.xS : 1;  // producer partials per input array
   const bool xcomb = J.xmode == X_COMBINE;
+  // decode with route stamps: a W1/W3 launch reads only data the tail published
+  // before the stamp (route, h), so it starts without griddepcontrol.wait and
+  // waits for the tail's grid only before it exits (completion stays transitive)
+  const bool early = J.rel_slot >= 0 && P.ds != nullptr && J.xmode == X_PLAIN;
   const bool xstage = !xcomb && xin_cap > 0 && nrows > 0 && !(J.xS > 1 && J.xfx) &&
                       (swiglu ? 2 : 1) * xparts * nrows * xes <= xin_cap;
 
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     }
     // x rows: one bulk copy per input array (after the previous kernel completed)
     auto issue_x = [&]() {
-      if (J.rel_slot < 0 || P.ds) gemv::pdl_wait();  // x is the previous kernel's output
+      if ((J.rel_slot < 0 || P.ds) && !early) gemv::pdl_wait();  // x: previous kernel's output
       if (!xstage) return;
       const uint32_t bytes = (uint32_t)(nrows * xes);
       gemv::mbar_arrive_tx(xbar, (swiglu ? 2u : 1u) * (uint32_t)xparts * bytes);
@@ -313,7 +317,22 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
 
   // ------------------------------------------------------------ consumers
   const int nthr = W * 32;
-  gemv::pdl_wait();
+  if (early) {  // the route stamp of (token, layer) instead of the whole tail grid
+    if (threadIdx.x == 0) {
+      const unsigned int want = route_stamp(P.ds->seq, P.layer);
+      const unsigned long long t0 = globaltimer();
+      while (ld_acquire_u32(&P.route->stamp) != want) {
+        __nanosleep(64);
+        if (globaltimer() - t0 > P.wait_ns) {
+          atomicOr(P.err, MOE_ERRF_TIMEOUT);
+          break;
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  } else {
+    gemv::pdl_wait();
+  }
   tl_begin(P.site);
   tl_mark(P.site, 5);  // block 0 released (profiling: its start vs the earliest CTA's)
   cta_mark(0);
@@ -332,6 +351,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
                                                    : nullptr);
       if (zdst)
         for (int t = threadIdx.x; t < wcb * WC; t += nthr) zdst[(size_t)cb * 32 * WC + t] = 0.f;
+      if (early) gemv::pdl_wait();
       cta_mark(2);
       tl_end(P.site);
       return;
@@ -590,6 +610,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       for (int o = Z.zpr; o < 32; o <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, o);
     ztot = __shfl_sync(0xffffffffu, zacc, (lane * WC) >> M.g_log2);
   }
+  if (early) gemv::pdl_wait();  // the tail's grid is long done: completion stays transitive
   tl_mark(P.site, 3);  // streaming loop done
   cta_mark(1);
   float y[WC];
