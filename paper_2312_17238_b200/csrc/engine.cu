@@ -610,6 +610,8 @@ GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* part, float
 // (common) split count S that is <= 8, so each cluster holds consecutive
 // splits of one column block and reduces them over distributed shared memory
 static int finalize_launch(GLaunch& P, int want_cluster = 0) {
+  static const int bulk = getenv("MOE_BULK_EPI") ? atoi(getenv("MOE_BULK_EPI")) : 1;
+  P.bulk_epi = bulk;
   int blk = 0;
   for (int i = 0; i < P.nj; ++i) {
     P.j[i].blk0 = blk;

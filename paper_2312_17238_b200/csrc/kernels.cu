@@ -112,6 +112,16 @@ MOE_DEV float cons_sum(float v, float* red, int nthr) {
   return t;
 }
 
+// fixed-point image of one partial (0 and an error flag when out of range)
+MOE_DEV unsigned long long fx_bits(float a, int* err) {
+  const float q = a * MOE_FX_SCALE;
+  if (!(fabsf(q) < 0x1p62f)) {
+    if (err) atomicOr(err, MOE_ERRF_NONFINITE_GATE);
+    return 0ull;
+  }
+  return (unsigned long long)__float2ll_rn(q);
+}
+
 MOE_DEV void fx_add(unsigned long long* p, float a, int* err) {
   const float q = a * MOE_FX_SCALE;
   if (!(fabsf(q) < 0x1p62f)) {  // non-finite or out of range: the reference would
@@ -628,6 +638,10 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const int C = P.cluster, SC = J.S / C;  // cluster = C consecutive splits of one cb
   const int crank = blockIdx.x % C, sc = s / C;
   float* dst = (SC == 1 && J.reduce) ? J.out : J.part + (size_t)sc * M.N;
+  // the CTA's outputs leave with one bulk (TMA) copy: a plain store of the
+  // split-K partials, or a bulk fixed-point add (cp.reduce.async.bulk .add.u64)
+  const bool bulk_out = C == 1 && J.reduce != 1 && P.bulk_epi;
+  unsigned long long* fxs = reinterpret_cast<unsigned long long*>(ysum);
   for (int t = threadIdx.x; t < 32 * WC; t += nthr) {
     const int l = t / WC, k = t % WC;
     if (l < wcb) {
@@ -637,10 +651,32 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       a += zo_out;
       if (C > 1)
         ysum[t] = a;
+      else if (bulk_out && J.reduce == 2)
+        fxs[t] = fx_bits(a, P.err);
+      else if (bulk_out)
+        ysum[t] = a;
       else if (J.reduce == 2)
         fx_add(J.acc + (size_t)(cb * 32 + l) * WC + k, a, P.err);
       else
         dst[(size_t)(cb * 32 + l) * WC + k] = a;
+    }
+  }
+  if (bulk_out) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> TMA
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    if (threadIdx.x == 0) {
+      const size_t o = (size_t)cb * 32 * WC;
+      if (J.reduce == 2)
+        asm volatile(
+            "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(
+                J.acc + o),
+            "r"(gemv::smem_u32(fxs)), "r"((uint32_t)(wcb * WC * 8))
+            : "memory");
+      else
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + o),
+                     "r"(gemv::smem_u32(ysum)), "r"((uint32_t)(wcb * WC * 4))
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
     }
   }
   if (C > 1) {

@@ -65,6 +65,7 @@ struct GLaunch {
   // routed expert's buffer (e.g. W2 while W1/W3 stream), split over the CTAs
   // of the jobs on that expert
   long long pf_off[2], pf_len[2];
+  int bulk_epi;  // split-K outputs by one bulk copy / bulk fixed-point add per CTA
   // L2 prefetch of absolute byte ranges (e.g. the next layer's Wq/Wk/Wv while
   // W2 streams), split over every CTA of the launch
   const uint8_t* pfa[3];
