@@ -318,7 +318,9 @@ def run_b200(args, rank, world):
     traffic = None
     if os.path.exists(prof_path):
         with open(prof_path) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            prof = json.load(fh)
+        if f"k_gemv<{xb}>" in prof.get("kernel", ""):  # the capture is of this config's kernel
+            traffic = prof.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "kernel": f"k_gemv<{xb}> expert up-projection (W1+W3 of 2 experts)",
                 "achieved": round(up_gbs, 1) if up_gbs else None, "peak": hbm, "unit": "GB/s",
                 "frac": round(up_gbs / hbm, 4) if up_gbs else None, "traffic": traffic,
