@@ -463,6 +463,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     args.device = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("MOE_BENCH_DEVICE") is not None:  # test aid: all ranks on one GPU
+        args.device = int(os.environ["MOE_BENCH_DEVICE"])
 
     if args.impl == "reference":
         if rank != 0:
