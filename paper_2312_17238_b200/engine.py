@@ -96,7 +96,7 @@ class _Marshal:
         m.rows, m.cols = (shape if len(shape) == 2 else (1, int(np.prod(shape))))
         m.bits = sch.bits
         m.pad_count = int(b.pad_count)
-        codes = np.frombuffer(bytes(b.packed_codes), dtype=np.uint8)
+        codes = np.frombuffer(b.packed_codes, dtype=np.uint8)
         m.codes, _ = self._ptr(codes)
         m.codes_len = codes.size
         if sch.bits == 16:
@@ -259,7 +259,7 @@ class OffloadEngine:
                 put(f"{pre}.{nm}", p[f"{pre}.{nm}"])
             for nm in ("wq", "wk", "wv", "wo"):
                 key = f"{pre}.attn.{nm}"
-                put(key, attn_blocks.get(key, p[key]))
+                put(key, attn_blocks[key] if key in attn_blocks else p[key])
         from .expert_parallel import owner_of
         for key, payload in payloads.items():
             k = ExpertKey(*key)
