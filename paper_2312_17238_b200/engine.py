@@ -415,6 +415,18 @@ class OffloadEngine:
         return {f: getattr(s, f) for f, _ in _lib.Stats._fields_}
 
 
+class DenseRunner(OffloadEngine):
+    """B200 counterpart of the reference ``DenseRunner`` (engine.py:185-197): the
+    in-memory path, every expert resident (k = n_experts, no staging, no
+    speculation).  It runs the same kernels in the same order as any
+    OffloadEngine, so offloading and speculation stay bit-transparent against it
+    (reference tests/test_engine.py:112-128)."""
+
+    def __init__(self, model, record_hidden: bool = True, **kw):
+        super().__init__(model, CacheConfig(k=model.config.n_experts, b=0),
+                         SpeculationConfig(enabled=False), record_hidden=record_hidden, **kw)
+
+
 def synthetic_model(cfg, seed: int = 0):
     """A model object for the device-synthesized weights (no host params).
     ``trace()`` gate matrices are regenerated from the counter hash on demand."""
