@@ -160,6 +160,13 @@ int moe_device_state(moe_engine* eng, int32_t* lru_out, int32_t* staged_out);
 
 int moe_get_stats(moe_engine* eng, moe_stats* out);
 
+/* Host-link peak for the roofline (SURVEY §8(d) "H2D_peak must be measured on
+ * the box"): `reps` copies of one whole expert (expert_bytes) from the pinned
+ * arena into an HBM pool buffer on the copy engine's demand stream, timed
+ * with CUDA events; best and median GB/s.  Engine must be idle (between
+ * calls).  No reference counterpart. */
+int moe_measure_h2d(moe_engine* eng, int32_t reps, double* best_gbs, double* median_gbs);
+
 /* Expert parallel over N GPUs; no reference counterpart (the
  * reference is single-process).  configure: before any expert is loaded; this
  * rank then owns experts e with e*world/E == rank in every layer (its arena,
@@ -187,6 +194,10 @@ int moe_read_timeline(moe_engine* eng, uint64_t* out, int32_t cap, int32_t* n_ou
 /* cudaProfilerStart/Stop, so `ncu --profile-from-start off` captures only the
  * bench's timed decode region. */
 int moe_profiler_range(int32_t on);
+
+/* cudaSetDevice for the library's own runtime (host helpers such as
+ * moe_quantize_device run on the calling thread's current device). */
+int moe_set_device(int32_t device);
 const char* moe_last_error(void);
 int moe_destroy(moe_engine* eng);
 

@@ -72,6 +72,8 @@ SIGNATURES = {
                               C.POINTER(Matrix)]),
     "moe_synth_model": (I32, [P, U64, I32, I32]),
     "moe_finalize": (I32, [P]),
+    "moe_set_device": (I32, [I32]),
+    "moe_measure_h2d": (I32, [P, I32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "moe_prefill": (I32, [P, IP, I32, FP]),
     "moe_step": (I32, [P, I32, FP]),
     "moe_decode_greedy": (I32, [P, I32, IP, FP]),

@@ -1704,6 +1704,41 @@ int moe_device_state(moe_engine* e, int32_t* lru_out, int32_t* staged_out) {
   return MOE_OK;
 }
 
+int moe_measure_h2d(moe_engine* e, int32_t reps, double* best_gbs, double* median_gbs) {
+  if (!e || !best_gbs || reps < 1) return fail(MOE_ERR_VALUE, "bad argument");
+  if (!e->finalized || !e->arena || !e->pool || e->xbytes == 0)
+    return fail(MOE_ERR_RUNTIME, "engine not finalized");
+  cudaSetDevice(e->dev);
+  CU(cudaStreamSynchronize(e->s_comp));
+  CU(cudaStreamSynchronize(e->s_copy));
+  CU(cudaStreamSynchronize(e->s_copy2));
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  std::vector<double> g;
+  // the last pool buffer: a transient slot the store never holds between calls
+  uint8_t* dst = e->pool + (size_t)(e->nbuf - 1) * e->slot_stride;
+  int x0 = 0;
+  while (x0 < (int)e->arena_idx.size() && e->arena_idx[x0] < 0) ++x0;
+  const uint8_t* src = e->arena + (size_t)e->arena_idx[x0] * e->xbytes;
+  for (int r = 0; r < reps; ++r) {
+    CU(cudaEventRecord(a, e->s_copy));
+    CU(cudaMemcpyAsync(dst, src, e->xbytes, cudaMemcpyHostToDevice, e->s_copy));
+    CU(cudaEventRecord(b, e->s_copy));
+    CU(cudaEventSynchronize(b));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, a, b));
+    if (ms > 0) g.push_back(e->xbytes / (ms * 1e6));
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (g.empty()) return fail(MOE_ERR_RUNTIME, "no timed copy");
+  std::sort(g.begin(), g.end());
+  *best_gbs = g.back();
+  if (median_gbs) *median_gbs = g[g.size() / 2];
+  return MOE_OK;
+}
+
 int moe_get_stats(moe_engine* e, moe_stats* out) {
   if (!e || !out) return fail(MOE_ERR_VALUE, "null argument");
   {
@@ -2086,6 +2121,11 @@ int moe_synth_model(moe_engine* e, uint64_t seed, int32_t attn_bits, int32_t exp
   if (xtmp) cudaFree(xtmp);
   Q.release();
   return rc;
+}
+
+int moe_set_device(int32_t device) {
+  CU(cudaSetDevice(device));
+  return MOE_OK;
 }
 
 int moe_quantize_device(const float* w, int32_t rows, int32_t cols, int32_t bits,
