@@ -4,6 +4,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include "mma_layout.cuh"
+
 #define MOE_DEV __device__ __forceinline__
 
 // ---------------------------------------------------------------- loads
@@ -94,6 +96,13 @@ struct MatDev {
   int sg_log2;           // scale group size (weights) = zmeta run length (groups)
   int bits;              // 2,3,4 quant; 16, 32 dense
   int runs_uniform;      // 1: in every row the groups of a cb share one zero run
+  // tensor-core tile layout (mma_layout.cuh; quant formats with N % 128 == 0,
+  // K % 16 == 0, preset grouping): a "quad" is then a 16-row k-step, a cb is
+  // 1024 outputs, nchunks counts 128-output slices, and the f16 scales live in
+  // their own section [cb][row][1024/sg] at `scl` (absolute, or a byte offset
+  // when the matrix is relative like zmeta)
+  int mma;
+  const __half* scl;
 };
 
 template <int BITS> struct Fmt;
@@ -122,4 +131,19 @@ __host__ __device__ inline int rec_bytes(int bits, int wcb, int g_log2, int sg_l
 }
 __host__ __device__ inline int64_t cb_offset(const MatDev& M, int cb) {
   return (int64_t)cb * M.nqp * M.rb_full;
+}
+// tensor-core layout: record bytes of column block cb (slices it holds), and
+// its first slice / row rows of the scale section
+__host__ __device__ inline int mma_slices(const MatDev& M, int cb) {
+  return M.nchunks - cb * mt::CBS < mt::CBS ? M.nchunks - cb * mt::CBS : mt::CBS;
+}
+__host__ __device__ inline int mma_rec_bytes(const MatDev& M, int cb) {
+  return mma_slices(M, cb) * mt::slice_bytes(M.bits, 1 << M.g_log2);
+}
+// scales per row of cb (1024 / sg for a full cb)
+__host__ __device__ inline int mma_nsc(const MatDev& M, int cb) {
+  return (mma_slices(M, cb) * mt::SO) >> M.sg_log2;
+}
+__host__ __device__ inline int64_t mma_scl_offset(const MatDev& M, int cb) {  // in halves
+  return (int64_t)cb * M.K * (mt::CBO >> M.sg_log2);
 }

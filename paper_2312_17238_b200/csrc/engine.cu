@@ -55,7 +55,7 @@ struct DevMat {  // one tiled matrix in device memory
 // split the quad range of every job so one launch is ~2 CTAs per SM
 // (MOE_GEMV_THREADS threads, ~100 KB smem each); QPS is a multiple of the
 // pipeline stage so every bulk copy stays 16-byte aligned
-int plan_qps(int total_cb, int nquads, int qs) {
+int plan_qps(int total_cb, int nquads, int qs, bool mma = false) {
   // CTAs per SM the split targets (MOE_GEMV_WAVES; 2 = one resident wave)
   static const int waves = getenv("MOE_GEMV_WAVES") ? atoi(getenv("MOE_GEMV_WAVES"))
                                                     : MOE_GEMV_MINB;
@@ -66,6 +66,7 @@ int plan_qps(int total_cb, int nquads, int qs) {
   const int S = std::max(1, target / total_cb);  // at most one wave
   int qps = (nquads + S - 1) / S;
   (void)qs;
+  if (mma) return std::max(1, std::min(qps, MOE_MMA_UNITS_MAX));  // k-steps (B table)
   while (qps * 4 > MOE_XS_MAX) qps -= 1;
   return std::max(qps, 1);
 }
@@ -73,6 +74,7 @@ int plan_qps(int total_cb, int nquads, int qs) {
 struct Layout {  // byte sections of one tiled matrix
   int bits = 0, K = 0, N = 0, g = 0, sg = 0;
   int runs_uniform = 0;  // see MatDev::runs_uniform
+  int mma = 0;           // tensor-core tile layout (mma_layout.cuh)
   size_t rec = 0, scales = 0, zeros = 0, zmeta = 0;
   int64_t nruns = 0;
   size_t total() const { return rec + scales + zeros + zmeta; }
@@ -123,11 +125,33 @@ int make_layout(const moe_matrix* m, Layout* L, const char* what) {
     return fail(MOE_ERR_FORMAT, std::string(what) + ": block arrays inconsistent with shape");
   L->g = g;
   L->sg = sg;
+  L->zmeta = (size_t)nruns * 4;
+  L->nruns = nruns;
+  // tensor-core layout for the reference presets (mma_layout.cuh): records of
+  // codes + zero codes per (1024-output cb, 16-row k-step), then the scales
+  // section; the zero-point runs of a row's cb must be one run (uniform)
+  static const bool no_mma = getenv("MOE_NO_MMA") && atoi(getenv("MOE_NO_MMA")) != 0;
+  if (!no_mma && N % mt::SO == 0 && K % mt::KS == 0 && (g == 16 || g == 64) && mt::SO % g == 0 &&
+      (sg == 128 || sg == 256) && N % sg == 0) {
+    const int64_t G = N / g, cbg = mt::CBO / g;
+    const int ncb = (N + mt::CBO - 1) / mt::CBO, lg = ilog2(sg);
+    bool uni = true;
+    for (int64_t r = 0; r < K && uni; ++r)
+      for (int c = 0; c < ncb && uni; ++c) {
+        const int64_t f0 = r * G + c * cbg, n = std::min<int64_t>(cbg, G - c * cbg);
+        uni = (f0 >> lg) == ((f0 + n - 1) >> lg);
+      }
+    if (uni) {
+      L->mma = 1;
+      L->runs_uniform = 1;
+      L->rec = (size_t)K * N * bits / 8 + (size_t)K * N / g;
+      L->scales = (size_t)K * N / sg * 2;
+      return MOE_OK;
+    }
+  }
   // records = codes + zeros (1 B per group) + scales (f16 per scale group);
   // equal to the reference byte count whenever K % 32 == 0 (no pad quads)
   L->rec = layout_rec_bytes(*L);
-  L->zmeta = (size_t)nruns * 4;
-  L->nruns = nruns;
   // does any row's slice of a column block straddle a zero-point run?
   {
     const int64_t G = N / g, cbg = 32 * wc / g;
@@ -146,10 +170,24 @@ int make_layout(const moe_matrix* m, Layout* L, const char* what) {
 MatDev matdev_from(const Layout& L, const uint8_t* base) {
   MatDev M{};
   M.base = base;
-  M.zmeta = reinterpret_cast<const __half2*>(base + L.rec);
+  M.zmeta = reinterpret_cast<const __half2*>(base + L.rec + L.scales + L.zeros);
   M.K = L.K;
   M.N = L.N;
   M.bits = L.bits;
+  if (L.mma) {  // units are 16-row k-steps, cbs 1024 outputs of 128-output slices
+    M.mma = 1;
+    M.scl = reinterpret_cast<const __half*>(base + L.rec);
+    M.nquads = L.K / mt::KS;
+    M.nqp = M.nquads;
+    M.nchunks = L.N / mt::SO;
+    M.ncb = (L.N + mt::CBO - 1) / mt::CBO;
+    M.G = L.N / L.g;
+    M.g_log2 = ilog2(L.g);
+    M.sg_log2 = ilog2(L.sg);
+    M.rb_full = mt::CBS * mt::slice_bytes(L.bits, L.g);
+    M.runs_uniform = 1;
+    return M;
+  }
   M.nquads = L.K / 4;
   M.nqp = (M.nquads + 7) / 8 * 8;
   M.nchunks = L.N / fmt_wc(L.bits);
@@ -167,7 +205,8 @@ MatDev matdev_from(const Layout& L, const uint8_t* base) {
 // tile a reference-layout matrix already resident on device into `dst`
 int tile_device(const RefMat& R, const Layout& L, uint8_t* dst, cudaStream_t s) {
   CU(cudaMemsetAsync(dst, 0, L.rec, s));  // pad quads / pad bytes are zero
-  launch_tile(R, matdev_from(L, dst), dst, reinterpret_cast<__half2*>(dst + L.rec), s);
+  const MatDev M = matdev_from(L, dst);
+  launch_tile(R, M, dst, const_cast<__half2*>(M.zmeta), s);
   CU(cudaGetLastError());
   return MOE_OK;
 }
@@ -767,6 +806,7 @@ int moe_engine::enq_experts(int l, int p) {
       J = GJob{};
       J.M = matdev_from(xl[m], reinterpret_cast<const uint8_t*>(xoff[m][0]));
       J.M.zmeta = reinterpret_cast<const __half2*>(xoff[m][3]);
+      J.M.scl = reinterpret_cast<const __half*>(xoff[m][1]);
       J.rel_slot = j;
       J.xmode = X_PLAIN;
       J.x = h + (size_t)p * d;
@@ -783,6 +823,7 @@ int moe_engine::enq_experts(int l, int p) {
     J = GJob{};
     J.M = matdev_from(xl[2], reinterpret_cast<const uint8_t*>(xoff[2][0]));
     J.M.zmeta = reinterpret_cast<const __half2*>(xoff[2][3]);
+    J.M.scl = reinterpret_cast<const __half*>(xoff[2][1]);
     J.rel_slot = j;
     J.xmode = X_SWIGLU;
     J.up1 = up_part + (size_t)(2 * j) * S_up * f;
@@ -1402,23 +1443,23 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->xn, d))) return rc;
   if ((rc = e->dalloc(&e->ctx, d))) return rc;
   if ((rc = e->dalloc(&e->logits, (size_t)T * V))) return rc;
-  const int wca = fmt_wc(e->attn_bits), wcx = fmt_wc(e->expert_bits);
-  auto plan = [](int total_cb, int nquads, int bits, int* Q, int* S) {
-    nquads = (nquads + 7) / 8 * 8;  // storage quads (MatDev.nqp)
-    *Q = plan_qps(total_cb, nquads, gemv_qs(bits));
-    *S = (nquads + *Q - 1) / *Q;
+  // split planning in storage units (MatDev.nqp: quads, or k-steps for the
+  // tensor-core layout) over column blocks (MatDev.ncb)
+  auto plan = [](int njobs, const MatDev& M, int* Q, int* S) {
+    *Q = plan_qps(njobs * M.ncb, M.nqp, gemv_qs(M.bits), M.mma != 0);
+    *S = (M.nqp + *Q - 1) / *Q;
   };
-  plan(3 * ((d / wca + 31) / 32), d / 4, e->attn_bits, &e->Q_qkv, &e->S_qkv);
-  plan((d / wca + 31) / 32, d / 4, e->attn_bits, &e->Q_wo, &e->S_wo);
-  plan(2 * e->topk * ((f / wcx + 31) / 32), d / 4, e->expert_bits, &e->Q_up, &e->S_up);
-  plan(e->topk * ((d / wcx + 31) / 32), f / 4, e->expert_bits, &e->Q_dn, &e->S_dn);
+  const MatDev xm0 = matdev_from(e->xl[0], nullptr), xm2 = matdev_from(e->xl[2], nullptr);
+  plan(3, e->wq[0].M, &e->Q_qkv, &e->S_qkv);
+  plan(1, e->wo[0].M, &e->Q_wo, &e->S_wo);
+  plan(2 * e->topk, xm0, &e->Q_up, &e->S_up);
+  plan(e->topk, xm2, &e->Q_dn, &e->S_dn);
   if (e->dn_cluster > 1 && e->S_dn % e->dn_cluster) {  // splits in whole clusters
-    const int nq = (f / 4 + 7) / 8 * 8, S = std::max(e->dn_cluster,
-                                                       e->S_dn / e->dn_cluster * e->dn_cluster);
+    const int nq = xm2.nqp, S = std::max(e->dn_cluster, e->S_dn / e->dn_cluster * e->dn_cluster);
     e->Q_dn = (nq + S - 1) / S;
     e->S_dn = (nq + e->Q_dn - 1) / e->Q_dn;
   }
-  plan(e->lm_head.M.ncb, d / 4, e->lm_bits, &e->Q_lm, &e->S_lm);
+  plan(1, e->lm_head.M, &e->Q_lm, &e->S_lm);
   if ((rc = e->dalloc(&e->qkv_part, (size_t)3 * e->S_qkv * d))) return rc;
   if ((rc = e->dalloc(&e->wo_part, (size_t)e->S_wo * d))) return rc;
   if ((rc = e->dalloc(&e->up_part, (size_t)2 * e->topk * e->S_up * f))) return rc;
@@ -2176,7 +2217,7 @@ int moe_gemv_device(const moe_matrix* m, const float* x, float* y) {
     return rc;
   }
   const MatDev M = matdev_from(L, mem);
-  const int qps = plan_qps(M.ncb, M.nqp, gemv_qs(L.bits)), S = (M.nqp + qps - 1) / qps;
+  const int qps = plan_qps(M.ncb, M.nqp, gemv_qs(L.bits), M.mma != 0), S = (M.nqp + qps - 1) / qps;
   float *dx, *part, *dy;
   int* dcnt;
   CU(cudaMalloc(&dx, (size_t)L.K * 4));
@@ -2260,7 +2301,8 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
   float *x, *part, *out;
   int* cnt;
   const MatDev M0 = matdev_from(L, nullptr);
-  const int qps = plan_qps(M0.ncb * njobs, M0.nqp, gemv_qs(bits)), S = (M0.nqp + qps - 1) / qps;
+  const int qps = plan_qps(M0.ncb * njobs, M0.nqp, gemv_qs(bits), M0.mma != 0),
+            S = (M0.nqp + qps - 1) / qps;
   CU(cudaMalloc(&x, (size_t)K * 4));
   CU(cudaMalloc(&part, (size_t)njobs * S * N * 4));
   CU(cudaMalloc(&out, (size_t)njobs * N * 4));
@@ -2305,7 +2347,8 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
     if (le != cudaSuccess)
       return fail(MOE_ERR_CUDA, std::string("gemv launch (grid ") + std::to_string(nblk) +
                                     ", smem " + std::to_string(gemv_smem_bytes(
-                                        bits, qps * 4, 0, 0, M0.rb_full, nullptr, nullptr)) +
+                                        bits, qps * (M0.mma ? mt::KS : 4), 0, 0, M0.rb_full,
+                                        nullptr, nullptr, M0.mma)) +
                                     "): " + cudaGetErrorString(le));
   }
   for (int w = 0; w < 3; ++w) launch_gemv(bits, P[w % nsets], nblk, s, pdl != 0);

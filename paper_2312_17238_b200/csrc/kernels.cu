@@ -11,6 +11,7 @@
 
 #include "kernels.cuh"
 #include "gemv.cuh"
+#include "mma_gemv.cuh"
 
 __device__ TimelineSlot* g_timeline = nullptr;
 __device__ int g_timeline_n = 0;  // span slots; phase marks follow
@@ -112,6 +113,18 @@ MOE_DEV float cons_sum(float v, float* red, int nthr) {
   return t;
 }
 
+// max over the GEMV's consumer warps (named barrier 1)
+MOE_DEV float cons_max(float v, float* red, int nthr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = nthr >> 5;
+  v = warp_max(v);
+  if (lane == 0) red[w] = v;
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  float t = 0.f;
+  for (int i = 0; i < nw; ++i) t = fmaxf(t, red[i]);
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  return t;
+}
+
 // fixed-point image of one partial (0 and an error flag when out of range)
 MOE_DEV unsigned long long fx_bits(float a, int* err) {
   const float q = a * MOE_FX_SCALE;
@@ -140,7 +153,7 @@ MOE_DEV float fx_val(unsigned long long v) {
 template <int BITS>
 __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int zs_cap, int xin_cap, int nst,
-           int stage_bytes) {
+           int stage_bytes, int mcap) {
   constexpr int WC = Fmt<BITS>::WC;
   constexpr bool QUANT = BITS <= 4;
   constexpr int W = MOE_GEMV_WARPS, QPW = gemv_qpw(BITS), QS = gemv_qs(BITS);
@@ -155,7 +168,13 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   __half2* zsm = reinterpret_cast<__half2*>(xz + xs_cap);  // the CTA's zmeta slice [zs_cap]
   const size_t xin_off = 512 + (((size_t)xs_cap * 8 + (size_t)zs_cap * 4 + 15) & ~(size_t)15);
   uint8_t* xin = smem + xin_off;  // the CTA's raw x rows (bulk copied) [xin_cap bytes]
-  uint8_t* ring = smem + ((xin_off + (size_t)xin_cap + 127) & ~(size_t)127);
+  // tensor-core layout: the CTA's scale slice [rows][nsc] and the B-operand
+  // table [k-step][slice][48 halves] (mcap rows; 0 for the CUDA-core layout)
+  const size_t scl_off = (xin_off + (size_t)xin_cap + 15) & ~(size_t)15;
+  __half* scl_s = reinterpret_cast<__half*>(smem + scl_off);
+  __half* btab = reinterpret_cast<__half*>(smem + scl_off + (size_t)mcap * 16);
+  uint64_t* sbar = reinterpret_cast<uint64_t*>(smem + 400);  // scale slice landed
+  uint8_t* ring = smem + ((scl_off + (size_t)mcap * 64 + 127) & ~(size_t)127);
 
   int ji = 0, cnt_base = 0;
   for (int i = 1; i < P.nj; ++i)
@@ -165,14 +184,21 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const int local = blockIdx.x - J.blk0;
   const int cb = local / J.S, s = local % J.S;
   MatDev M = J.M;
+  // storage units: quads of 4 rows (CUDA-core layout) or 16-row k-steps
+  // (tensor-core layout, mma_layout.cuh); a cb is 32 chunks or 8 slices
+  const bool mmal = QUANT && M.mma;
+  const int RPU = mmal ? mt::KS : 4;
   const int qs = s * J.QPS, qe = min(M.nqp, qs + J.QPS);  // storage quads (pads are zero)
-  const int wcb = min(32, M.nchunks - cb * 32);
-  const int rb = rec_bytes(BITS, wcb, M.g_log2, M.sg_log2);
-  const int nit = (max(qe - qs, 0) + QS - 1) / QS;
+  const int wcb = mmal ? mma_slices(M, cb) : min(32, M.nchunks - cb * 32);
+  const int rb = mmal ? mma_rec_bytes(M, cb) : rec_bytes(BITS, wcb, M.g_log2, M.sg_log2);
+  const int QSr = mmal ? stage_bytes / M.rb_full : QS;  // units per pipeline stage
+  const int nit = (max(qe - qs, 0) + QSr - 1) / QSr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qv = min(qe, M.nquads);  // real quads of this split
-  const int row0 = qs * 4, nrows = max(qv - qs, 0) * 4;
-  const int gcb0 = QUANT ? ((cb * 32 * WC) >> M.g_log2) : 0;  // first zero group of the cb
+  const int row0 = qs * RPU, nrows = max(qv - qs, 0) * RPU;
+  const int nout = mmal ? wcb * mt::SO : wcb * WC;                 // outputs of this cb
+  const size_t obase = mmal ? (size_t)cb * mt::CBO : (size_t)cb * 32 * WC;
+  const int gcb0 = QUANT ? (int)(obase >> M.g_log2) : 0;  // first zero group of the cb
   const bool uni = QUANT && M.runs_uniform;
   // uniform runs: the zero-point runs of the CTA's rows are one contiguous
   // zmeta slice [z0, z1], streamed to smem by the producer ahead of the
@@ -201,6 +227,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     }
     gemv::mbar_init(zbar, 1);
     gemv::mbar_init(xbar, 1);
+    gemv::mbar_init(sbar, 1);
     gemv::mbar_fence_init();
   }
   __syncthreads();
@@ -254,6 +281,13 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
         const uint8_t* b = P.pool + (long long)buf * P.slot_stride;
         M.base = b + reinterpret_cast<size_t>(M.base);
         M.zmeta = reinterpret_cast<const __half2*>(b + reinterpret_cast<size_t>(M.zmeta));
+        M.scl = reinterpret_cast<const __half*>(b + reinterpret_cast<size_t>(M.scl));
+      }
+      if (mmal && nrows > 0) {  // the CTA's scales, ahead of the weight stream
+        const int nsc = mma_nsc(M, cb);
+        const uint32_t bytes = (uint32_t)nrows * nsc * 2;
+        gemv::mbar_arrive_tx(sbar, bytes);
+        gemv::bulk_g2s(scl_s, M.scl + mma_scl_offset(M, cb) + (int64_t)row0 * nsc, bytes, sbar);
       }
       if (zstage) {
         const uintptr_t za = reinterpret_cast<uintptr_t>(M.zmeta + z0);
@@ -304,10 +338,10 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
         if (it == nst && (J.rel_slot < 0 || P.ds)) issue_x();
         if (it == nst) issue_prefetch();
         if (it >= nst) gemv::mbar_wait(empty + st, ph ^ 1);
-        const int nq = min(QS, qe - (qs + it * QS));
+        const int nq = min(QSr, qe - (qs + it * QSr));
         const uint32_t bytes = (uint32_t)(nq * rb);
         gemv::mbar_arrive_tx(full + st, bytes);
-        gemv::bulk_g2s_hint(ring + (size_t)st * stage_bytes, src + (int64_t)it * QS * rb, bytes,
+        gemv::bulk_g2s_hint(ring + (size_t)st * stage_bytes, src + (int64_t)it * QSr * rb, bytes,
                             full + st, pol);
         if (++st == nst) {
           st = 0;
@@ -360,7 +394,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
                              : (s % P.cluster == 0 ? J.part + (size_t)(s / P.cluster) * M.N
                                                    : nullptr);
       if (zdst)
-        for (int t = threadIdx.x; t < wcb * WC; t += nthr) zdst[(size_t)cb * 32 * WC + t] = 0.f;
+        for (int t = threadIdx.x; t < nout; t += nthr) zdst[obase + t] = 0.f;
       if (early) gemv::pdl_wait();
       cta_mark(2);
       tl_end(P.site);
@@ -529,6 +563,24 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       }
   }
   tl_mark(P.site, 1);  // zero-point slice landed, x * zscale done
+  // tensor-core layout: B-operand table b = x * s * 2^E in three fp16 pieces
+  // per (row, slice), E from the CTA's largest |x * s| (mma_gemv.cuh)
+  int Eb = 0;
+  if (mmal && nrows > 0) {
+    gemv::mbar_wait(sbar, 0);
+    const int nsc = mma_nsc(M, cb), nsl = wcb;
+    float mx = 0.f;
+    for (int i = threadIdx.x; i < nrows * nsc; i += nthr)
+      mx = fmaxf(mx, fabsf(xs[i / nsc] * __half2float(scl_s[i])));
+    mx = cons_max(mx, misc, nthr);
+    Eb = mx > 0.f ? min(14 - ilogbf(mx), 60) : 0;
+    const float p2 = __uint_as_float(gemv::pow2_bits(Eb));
+    for (int idx = threadIdx.x; idx < nrows * nsl; idx += nthr) {
+      const int i = idx / nsl, w = idx - i * nsl;
+      const float sv = __half2float(scl_s[i * nsc + ((w * mt::SO) >> M.sg_log2)]);
+      mg::put_pieces(btab + ((i >> 4) * nsl + w) * mt::BTAB, i & 15, __fmul_rn(xs[i], sv) * p2);
+    }
+  }
   if (QUANT && M.runs_uniform) {
     zo_part = warp_sum(zo_part);
     if (lane == 0) misc[warp] = zo_part;
@@ -560,7 +612,33 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const bool fast = QUANT && wcb == 32 && M.runs_uniform &&
                     M.g_log2 == (BITS == 2 ? 4 : 6);
   float ztot = 0.f;
-  if (fast || !QUANT) {
+  float D[8][4], zq[4] = {0.f, 0.f, 0.f, 0.f};
+  if (mmal) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) D[i][0] = D[i][1] = D[i][2] = D[i][3] = 0.f;
+    const int g = lane >> 2, t = lane & 3, nsl = wcb;
+    const int sb = mt::slice_bytes(BITS, 1 << M.g_log2);
+    const uint2* bt = reinterpret_cast<const uint2*>(btab);
+    int st = 0;
+    uint32_t ph = 0;
+    for (int it = 0; it < nit; ++it) {
+      gemv::mbar_wait(full + st, ph);
+      if (warp < nsl)
+        for (int u = 0; u < QSr; ++u) {
+          const int ul = it * QSr + u;
+          if (qs + ul < qv)
+            mg::step<BITS>(D, zq, ring + (size_t)st * stage_bytes + (size_t)u * rb + warp * sb,
+                           bt[(ul * nsl + warp) * (mt::BTAB / 4) + min(g, 2) * 4 + t],
+                           xz + ul * mt::KS, lane);
+        }
+      __syncwarp();
+      if (lane == 0) gemv::mbar_arrive(empty + st);
+      if (++st == nst) {
+        st = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (fast || !QUANT) {
     int st = 0;
     uint32_t ph = 0;
     for (int it = 0; it < nit; ++it) {
@@ -625,13 +703,19 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   cta_mark(1);
   float y[WC];
   gemv::finish_lane<BITS>(y, acc, ztot);
-  // cross-warp reduction through the (now idle) ring, fixed order
+  // cross-warp reduction through the (now idle) ring, fixed order; the
+  // tensor-core layout's warps own disjoint outputs: ymm[o] directly
   float* red = reinterpret_cast<float*>(ring);
-  float* ysum = red + W * 32 * (WC + 1);  // this CTA's partial outputs [32*WC]
+  float* ymm = red;
+  float* ysum = mmal ? red + mt::CBO : red + W * 32 * (WC + 1);  // the CTA's partial outputs
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   if (!xcomb) tl_mark(P.site, 6);  // every consumer warp left the loop
+  if (mmal) {
+    if (warp < wcb) mg::finish<BITS>(D, zq, Eb, lane, ymm + warp * mt::SO);
+  } else {
 #pragma unroll
-  for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
+    for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
+  }
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   if (!xcomb) tl_mark(P.site, 7);  // per-warp results in smem
   const float zo_out = zo_sum * gemv::kZUnscale;
@@ -642,12 +726,16 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   // split-K partials, or a bulk fixed-point add (cp.reduce.async.bulk .add.u64)
   const bool bulk_out = C == 1 && J.reduce != 1 && P.bulk_epi;
   unsigned long long* fxs = reinterpret_cast<unsigned long long*>(ysum);
-  for (int t = threadIdx.x; t < 32 * WC; t += nthr) {
+  for (int t = threadIdx.x; t < (mmal ? nout : 32 * WC); t += nthr) {
     const int l = t / WC, k = t % WC;
-    if (l < wcb) {
+    if (mmal || l < wcb) {
       float a = 0.f;
+      if (mmal) {
+        a = ymm[t];
+      } else {
 #pragma unroll
-      for (int w = 0; w < W; ++w) a += red[(w * 32 + l) * (WC + 1) + k];
+        for (int w = 0; w < W; ++w) a += red[(w * 32 + l) * (WC + 1) + k];
+      }
       a += zo_out;
       if (C > 1)
         ysum[t] = a;
@@ -656,25 +744,25 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       else if (bulk_out)
         ysum[t] = a;
       else if (J.reduce == 2)
-        fx_add(J.acc + (size_t)(cb * 32 + l) * WC + k, a, P.err);
+        fx_add(J.acc + obase + t, a, P.err);
       else
-        dst[(size_t)(cb * 32 + l) * WC + k] = a;
+        dst[obase + t] = a;
     }
   }
   if (bulk_out) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> TMA
     asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
     if (threadIdx.x == 0) {
-      const size_t o = (size_t)cb * 32 * WC;
+      const size_t o = obase;
       if (J.reduce == 2)
         asm volatile(
             "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(
                 J.acc + o),
-            "r"(gemv::smem_u32(fxs)), "r"((uint32_t)(wcb * WC * 8))
+            "r"(gemv::smem_u32(fxs)), "r"((uint32_t)(nout * 8))
             : "memory");
       else
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + o),
-                     "r"(gemv::smem_u32(ysum)), "r"((uint32_t)(wcb * WC * 4))
+                     "r"(gemv::smem_u32(ysum)), "r"((uint32_t)(nout * 4))
                      : "memory");
       asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
     }
@@ -685,7 +773,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     cluster_sync();
     // every rank reduces 1/C of the outputs, reading that slice from all C
     // ranks (loads first, then the sum in rank order)
-    const int no = wcb * WC, per = (no + C - 1) / C;
+    const int no = nout, per = (no + C - 1) / C;
     const int t0 = crank * per, t1 = min(no, t0 + per);
     for (int t = t0 + threadIdx.x; t < t1; t += nthr) {
       float v[8];
@@ -695,9 +783,9 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
 #pragma unroll
       for (int r = 0; r < 8; ++r) a += v[r];
       if (J.reduce == 2)
-        fx_add(J.acc + (size_t)cb * 32 * WC + t, a, P.err);
+        fx_add(J.acc + obase + t, a, P.err);
       else
-        dst[(size_t)cb * 32 * WC + t] = a;
+        dst[obase + t] = a;
     }
     cluster_sync();  // peers keep their shared memory until every slice is read
   }
@@ -726,8 +814,8 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     return;
   }
   // 4 outputs x 8 splits per thread in flight, then the in-order sums
-  const int no = wcb * WC;
-  const float* pbase = J.part + (size_t)cb * 32 * WC;
+  const int no = nout;
+  const float* pbase = J.part + obase;
   for (int t0 = threadIdx.x; t0 < no; t0 += 4 * nthr) {
     float a[4] = {0.f, 0.f, 0.f, 0.f};
     for (int s0 = 0; s0 < SC; s0 += 8) {
@@ -747,7 +835,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (t0 + u * nthr < no) J.out[(size_t)cb * 32 * WC + t0 + u * nthr] = a[u];
+      if (t0 + u * nthr < no) J.out[obase + t0 + u * nthr] = a[u];
   }
   if (threadIdx.x == 0) P.cnt[cnt_base + cb] = 0;
   cta_mark(2);
@@ -1706,9 +1794,25 @@ cudaError_t preload_kernels() {
 
 // shared memory of one GEMV CTA: barriers, x slice, stage ring (which also
 // holds the cross-warp reduction scratch at the end)
+// (mma: tensor-core layout -- the scale slice and B table (64 B per row) come
+// before the ring, which takes what is left of the 2-CTAs/SM budget, 16 KB
+// stages of whole k-step records)
 int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full, int* nstages,
-                    int* stage_bytes) {
+                    int* stage_bytes, int mma) {
   const int WC = fmt_wc(bits);
+  const int head = 512 + (((xs_rows * 8 + zs_cap * 4 + 15) & ~15) + xin_cap + 15 & ~15);
+  if (mma) {
+    const int units = rb_full >= 16384 ? 1 : 16384 / rb_full;
+    const int stage = units * rb_full;
+    const int pre = ((head + xs_rows * 64) + 127) & ~127;
+    int nst = (MOE_GEMV_SMEM_CAP - pre) / stage;
+    nst = nst < 2 ? 2 : (nst > 6 ? 6 : nst);
+    int ring = nst * stage;
+    if (ring < 12 * 1024) ring = 12 * 1024;  // epilogue: outputs + fixed-point staging
+    if (nstages) *nstages = nst;
+    if (stage_bytes) *stage_bytes = stage;
+    return pre + ring;
+  }
   const int stage = gemv_qs(bits) * rb_full;
   int nst = MOE_GEMV_RING / stage;
   nst = nst < 2 ? 2 : (nst > 16 ? 16 : nst);
@@ -1717,28 +1821,29 @@ int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full,
   if (ring < red) ring = red;
   if (nstages) *nstages = nst;
   if (stage_bytes) *stage_bytes = stage;
-  return 512 + ((((xs_rows * 8 + zs_cap * 4 + 15) & ~15) + xin_cap + 127) & ~127) + ring;
+  return ((head + 127) & ~127) + ring;
 }
 
 // zmeta entries of the largest per-CTA slice of the launch's uniform-run
 // jobs (0 when none, or when the slice would cost the kernel its 2 CTAs/SM:
 // the kernel then reads zmeta from global memory)
-static int gemv_zs_cap(const GLaunch& P, int bits, int xs_cap, int rbf) {
+static int gemv_zs_cap(const GLaunch& P, int bits, int xs_cap, int rbf, int mma) {
   int cap = 0;
   for (int i = 0; i < P.nj; ++i) {
     const MatDev& M = P.j[i].M;
     if (bits > 4 || !M.runs_uniform) continue;
-    const long long rows = (long long)P.j[i].QPS * 4;
+    const long long rows = (long long)P.j[i].QPS * (M.mma ? mt::KS : 4);
     cap = max(cap, (int)(((rows * M.G) >> M.sg_log2) + 8));
   }
-  if (cap && gemv_smem_bytes(bits, xs_cap, cap, 0, rbf, nullptr, nullptr) > 112 * 1024) cap = 0;
+  if (cap && !mma && gemv_smem_bytes(bits, xs_cap, cap, 0, rbf, nullptr, nullptr, 0) > 112 * 1024)
+    cap = 0;
   return cap;
 }
 
 // bytes of the x staging region: the largest job's x rows (two arrays for the
 // SwiGLU input), 0 when a job sums producer partials or the kernel would lose
 // its 2 CTAs/SM (x then comes through ordinary loads)
-static int gemv_xin_cap(const GLaunch& P, int bits, int xs_cap, int zs_cap, int rbf) {
+static int gemv_xin_cap(const GLaunch& P, int bits, int xs_cap, int zs_cap, int rbf, int mma) {
   int cap = 0;
   for (int i = 0; i < P.nj; ++i) {
     const GJob& J = P.j[i];
@@ -1748,24 +1853,26 @@ static int gemv_xin_cap(const GLaunch& P, int bits, int xs_cap, int zs_cap, int 
     }
     if (J.xS > 1 && J.xfx) continue;
     const int es = J.xfx ? 8 : 4, n = (J.xmode != X_PLAIN ? 2 : 1) * (J.xS > 1 ? J.xS : 1);
-    cap = max(cap, n * es * J.QPS * 4);
+    cap = max(cap, n * es * J.QPS * (J.M.mma ? mt::KS : 4));
   }
-  if (cap && gemv_smem_bytes(bits, xs_cap, zs_cap, cap, rbf, nullptr, nullptr) > 112 * 1024)
+  // the tensor-core layout keeps x staging and shrinks the ring instead
+  if (cap && !mma && gemv_smem_bytes(bits, xs_cap, zs_cap, cap, rbf, nullptr, nullptr, 0) > 112 * 1024)
     cap = 0;
   return cap;
 }
 
 template <int BITS>
 static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
-  int xs_cap = 0, rbf = 0;
+  int xs_cap = 0, rbf = 0, mma = 0;
   for (int i = 0; i < P.nj; ++i) {
-    xs_cap = max(xs_cap, P.j[i].QPS * 4);
+    mma |= P.j[i].M.mma;
+    xs_cap = max(xs_cap, P.j[i].QPS * (P.j[i].M.mma ? mt::KS : 4));
     rbf = max(rbf, P.j[i].M.rb_full);
   }
   int nst = 0, stage = 0;
-  const int zs_cap = gemv_zs_cap(P, BITS, xs_cap, rbf);
-  const int xin_cap = gemv_xin_cap(P, BITS, xs_cap, zs_cap, rbf);
-  const int smem = gemv_smem_bytes(BITS, xs_cap, zs_cap, xin_cap, rbf, &nst, &stage);
+  const int zs_cap = gemv_zs_cap(P, BITS, xs_cap, rbf, mma);
+  const int xin_cap = gemv_xin_cap(P, BITS, xs_cap, zs_cap, rbf, mma);
+  const int smem = gemv_smem_bytes(BITS, xs_cap, zs_cap, xin_cap, rbf, &nst, &stage, mma);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nblocks);
   cfg.blockDim = dim3(MOE_GEMV_THREADS);
@@ -1780,7 +1887,8 @@ static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pd
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, zs_cap, xin_cap, nst, stage);
+  cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, zs_cap, xin_cap, nst, stage,
+                     mma ? xs_cap : 0);
   g_launches.fetch_add(1);
 }
 

@@ -14,6 +14,8 @@ __host__ __device__ constexpr int gemv_qs(int bits) { return MOE_GEMV_WARPS * ge
 #define MOE_GEMV_MINB 2            // CTAs per SM the kernel is register-limited for
 #define MOE_GEMV_RING (80 * 1024)  // bytes of stage ring per CTA (2 CTAs / SM)
 #define MOE_XS_MAX 4096            // rows of x kept in smem per CTA
+#define MOE_GEMV_SMEM_CAP (112 * 1024)  // dynamic smem per CTA at 2 CTAs / SM
+#define MOE_MMA_UNITS_MAX 64       // k-steps per CTA in the tensor-core layout (B table)
 
 // X_COMBINE: the input row slice is LayerNorm(h + w0*y0 + w1*y1) (the MoE
 // combine of the previous layer, model.py:251-254, fused with the next LN):
@@ -221,7 +223,7 @@ cudaError_t set_cta_trace(unsigned long long* buf);          // GEMV microbench 
 // launchers (kernels.cu)
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
 int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full, int* nstages,
-                    int* stage_bytes);
+                    int* stage_bytes, int mma);
 void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl = false);
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
                       cudaStream_t s, bool pdl = false);

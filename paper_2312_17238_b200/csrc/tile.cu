@@ -75,6 +75,80 @@ __global__ void k_tile_meta(RefMat R, MatDev M, uint8_t* dst, __half2* zmeta) {
     zmeta[i] = __halves2half2(__ushort_as_half(R.zs[i]), __ushort_as_half(R.zo[i]));
 }
 
+// ------------------------------------------------------------------ tiling (tensor-core layout)
+// mma_layout.cuh.  One thread per (cb, k-step, slice, lane): gathers the
+// lane's 64 codes from the reference bitstream and packs them into the words
+// the GEMV's LOP3 masks extract as fp16 A-fragment halves.
+MOE_DEV uint32_t ref_code(const RefMat& R, int64_t row, int64_t col) {
+  const int64_t bit = (row * R.N + col) * R.bits, byte = bit >> 3;
+  const int64_t nbytes = ((int64_t)R.K * R.N * R.bits + 7) >> 3;
+  const uint32_t v = (uint32_t)R.codes[byte] | (byte + 1 < nbytes ? (uint32_t)R.codes[byte + 1] << 8 : 0u);
+  return (v >> (bit & 7)) & ((1u << R.bits) - 1u);
+}
+
+__global__ void k_tile_mma_codes(RefMat R, MatDev M, uint8_t* dst) {
+  const int nks = M.nquads, b = R.bits, sb = mt::slice_bytes(b, R.g);
+  const int64_t n = (int64_t)M.ncb * nks * mt::CBS * 32;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(idx & 31), w = (int)((idx >> 5) % mt::CBS);
+    const int64_t rest = (idx >> 5) / mt::CBS;
+    const int ks = (int)(rest % nks), cb = (int)(rest / nks);
+    if (w >= mma_slices(M, cb)) continue;
+    const int g = lane >> 2, t = lane & 3;
+    uint32_t W[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < 16; ++p)
+      for (int e = 0; e < 2; ++e) {
+        const int r = mt::pair_reg(b, p, e);
+        const int64_t col = (int64_t)cb * mt::CBO + w * mt::SO + mt::out_of(p >> 1, p & 1, g);
+        const int64_t row = (int64_t)ks * mt::KS + mt::k_of(e, t);
+        const uint32_t lo = ref_code(R, row, col), hi = ref_code(R, row + 1, col);
+        const int v = mt::reg_word(b, r);
+        if (v >= 0) {
+          const int o = mt::reg_off(b, r);
+          W[v] |= (lo << o) | (hi << (16 + o));
+        } else {  // 3-bit assembled register: code bit k in bit 15 / 31 of word 3j + k
+          const int j = r - 30;
+          for (int kb = 0; kb < 3; ++kb)
+            W[3 * j + kb] |= (((lo >> kb) & 1u) << 15) | (((hi >> kb) & 1u) << 31);
+        }
+      }
+    uint2* sl = reinterpret_cast<uint2*>(dst + cb_offset(M, cb) + (int64_t)ks * mma_rec_bytes(M, cb) +
+                                         (int64_t)w * sb);
+    for (int pl = 0; pl < b; ++pl) sl[pl * 32 + lane] = make_uint2(W[2 * pl], W[2 * pl + 1]);
+  }
+}
+
+// zero codes into the slices, scales into their section, runs into zmeta
+__global__ void k_tile_mma_meta(RefMat R, MatDev M, uint8_t* dst, __half* scl, __half2* zmeta) {
+  const int nks = M.nquads, b = R.bits, sb = mt::slice_bytes(b, R.g), zb = mt::zero_bytes(R.g);
+  const int G = R.N / R.g, S = R.N / R.sg;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nz = (int64_t)M.ncb * nks * mt::CBS * zb;
+  for (int64_t i = t0; i < nz; i += stride) {
+    const int byte = (int)(i % zb);
+    const int64_t rest = i / zb;
+    const int w = (int)(rest % mt::CBS), ks = (int)((rest / mt::CBS) % nks);
+    const int cb = (int)(rest / mt::CBS / nks);
+    if (w >= mma_slices(M, cb)) continue;
+    int grp, row;
+    mt::zero_pos(R.g, byte, &grp, &row);
+    const int64_t gz = ((int64_t)cb * mt::CBO + w * mt::SO) / R.g + grp;
+    dst[cb_offset(M, cb) + (int64_t)ks * mma_rec_bytes(M, cb) + (int64_t)w * sb +
+        mt::code_bytes(b) + byte] = R.zeros[((int64_t)ks * mt::KS + row) * G + gz];
+  }
+  const int64_t ns = (int64_t)R.K * S;
+  for (int64_t i = t0; i < ns; i += stride) {
+    const int row = (int)(i / S), gs = (int)(i % S);
+    const int cb = (gs * R.sg) / mt::CBO, j = gs - cb * (mt::CBO / R.sg);
+    scl[mma_scl_offset(M, cb) + (int64_t)row * mma_nsc(M, cb) + j] =
+        __ushort_as_half(R.scales[(int64_t)row * S + gs]);
+  }
+  for (int64_t i = t0; i < R.nruns; i += stride)
+    zmeta[i] = __halves2half2(__ushort_as_half(R.zs[i]), __ushort_as_half(R.zo[i]));
+}
+
 // ------------------------------------------------------------------ quantize
 // per group of g weights: min, and (max - min) / levels in float32
 __global__ void k_q_groups(const float* w, int64_t ngroups, int g, int top, float* gmin,
@@ -184,6 +258,14 @@ int grid_for(int64_t n) {
 
 void launch_tile(const RefMat& R, const MatDev& M, uint8_t* rec, __half2* zmeta,
                  cudaStream_t s) {
+  if (M.mma) {
+    const int64_t n = (int64_t)M.ncb * M.nquads * mt::CBS * 32;
+    k_tile_mma_codes<<<grid_for(n), 256, 0, s>>>(R, M, rec);
+    const int64_t nm = (int64_t)M.ncb * M.nquads * mt::CBS * mt::zero_bytes(R.g);
+    k_tile_mma_meta<<<grid_for(nm > (int64_t)R.K * (R.N / R.sg) ? nm : (int64_t)R.K * (R.N / R.sg)),
+                      256, 0, s>>>(R, M, rec, const_cast<__half*>(M.scl), zmeta);
+    return;
+  }
   const int64_t nrec = (int64_t)M.nquads * M.nchunks;
   k_tile_rec<<<grid_for(nrec), 256, 0, s>>>(R, M, rec);
   if (R.bits <= 4) {

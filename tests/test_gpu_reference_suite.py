@@ -29,5 +29,7 @@ def test_reference_suite_on_b200(suite):
                         "-p", "paper_2312_17238_b200.refshim", os.path.join("tests", suite)],
                        cwd=REF_TESTS, env=env, capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
-    assert "(B200 backend)" in out, out[-3000:]
+    import re
+    m = re.search(r"B200 backend engines created: OffloadEngine (\d+), DenseRunner (\d+)", out)
+    assert m and int(m.group(1)) > 0, out[-3000:]
     assert r.returncode == 0, out[-6000:]
