@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmoeb200.so")
 SOURCES = ["kernels.cu", "tile.cu", "engine.cu", "store_sim.cu"]
 HEADERS = ["common.cuh", "gemv.cuh", "store_dev.cuh", "kernels.cuh", "copy_sched.h", "mma_layout.cuh",
-           "mma_gemv.cuh"]
+           "mma_gemv.cuh", "mgemv_kernel.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-lpthread"]

@@ -56,9 +56,7 @@ struct DevMat {  // one tiled matrix in device memory
 // (MOE_GEMV_THREADS threads, ~100 KB smem each); QPS is a multiple of the
 // pipeline stage so every bulk copy stays 16-byte aligned
 int plan_qps(int total_cb, int nquads, int qs, bool mma = false) {
-  // CTAs per SM the split targets (MOE_GEMV_WAVES; 2 = one resident wave)
-  static const int waves = getenv("MOE_GEMV_WAVES") ? atoi(getenv("MOE_GEMV_WAVES"))
-                                                    : MOE_GEMV_MINB;
+  const int waves = MOE_GEMV_MINB;  // CTAs per SM: one resident wave
   // splits need not be whole pipeline stages (the last stage of a split is
   // partial), so S is the largest split count that fits the resident wave:
   // every SM gets the same number of CTAs whenever total_cb * S == target
@@ -335,18 +333,10 @@ struct moe_engine {
 
   // activations
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
-  bool up_fx = false;  // MOE_UP_FX=1: up projections as fixed-point sums (else partials)
-  bool dn_fx = true;   // MOE_DN_FX=0: W2 reduced by the last CTA per column block instead
-  bool comb_hold = false;  // MOE_COMB_HOLD=1: fused-combine QKV streams weights after the wait
-  bool route_stamps = false;  // MOE_ROUTE_STAMPS=1: expert GEMVs spin on the route stamp (neutral)
-  unsigned int tok_seq = 0;  // decode tokens issued (DecodeState.seq, route stamps)
-  bool pf_qkv = false;  // MOE_PF_QKV=1: L2 prefetch of the next layer's QKV during W2 (neutral)
-  int dn_cluster = 0;     // MOE_DN_CLUSTER=C: W2 split-K pre-reduced over clusters of C
-  bool fuse_comb = true;  // MOE_FUSE_COMBINE=0: keep the combine kernel between layers
+  unsigned int tok_seq = 0;  // decode tokens issued (DecodeState.seq)
   bool pend_comb = false;  // decode: layer l's combine + LN1(l+1) is fused into QKV(l+1)
-  bool pf_w2 = false;  // MOE_PF_W2=1: L2 prefetch of W2 during the W1/W3 GEMV (measured slower)
-  unsigned long long *wo_acc = nullptr, *dn_acc = nullptr, *qkv_acc = nullptr,
-                     *up_acc = nullptr;  // fixed-point split-K sums (reduce == 2)
+  // fixed-point split-K sums (reduce == 2)
+  unsigned long long *wo_acc = nullptr, *dn_acc = nullptr, *qkv_acc = nullptr;
   float *qkv_part = nullptr, *wo_part = nullptr, *up_part = nullptr, *dn_part = nullptr,
         *lm_part = nullptr;  // split-K partials
   float *qkv_out = nullptr, *wo_out = nullptr, *up_out = nullptr, *dn_out = nullptr;  // finals
@@ -465,6 +455,7 @@ struct moe_engine {
   int enq_token();
   int run_tokens(int n);
   int finish_call(bool want_logits = false);
+  int bad_pos = -1;  // set by finish_call: first position that raised a non-finite error
   GJob dense_job(const DevMat& D, const float* x, float* part, float* out, int qps) const;
   int site_of(int l, int kind) const { return 1 + 8 * l + kind; }  // timeline slots
   TimelineSlot* timeline = nullptr;
@@ -494,7 +485,7 @@ moe_engine::~moe_engine() {
   if (hstat) cudaFreeHost(hstat);
   if (logits_h) cudaFreeHost(logits_h);
   void* ptrs[] = {wte, wpe, lm_head.mem, lnfg, lnfb, pool, flags, x, h, xn, ctx, logits,
-                  qkv_part, wo_part, up_part, dn_part, lm_part, wo_acc, dn_acc, qkv_acc, up_acc, qkv_out, wo_out, up_out, dn_out,
+                  qkv_part, wo_part, up_part, dn_part, lm_part, wo_acc, dn_acc, qkv_acc, qkv_out, wo_out, up_out, dn_out,
                   cnt, kc, vc, route, trace,
                   trace_hidden, tok_dev, tok_hist, tok_in, cand_val, cand_idx, counter, err,
                   st_mem, ds_dev};
@@ -645,30 +636,13 @@ GJob moe_engine::dense_job(const DevMat& D, const float* xin, float* part, float
   return j;
 }
 
-// block offsets of the jobs, and the cluster size: the largest divisor of the
-// (common) split count S that is <= 8, so each cluster holds consecutive
-// splits of one column block and reduces them over distributed shared memory
-static int finalize_launch(GLaunch& P, int want_cluster = 0) {
-  static const int bulk = getenv("MOE_BULK_EPI") ? atoi(getenv("MOE_BULK_EPI")) : 1;
-  P.bulk_epi = bulk;
+// block offsets of the jobs; returns the grid size
+static int finalize_launch(GLaunch& P) {
   int blk = 0;
   for (int i = 0; i < P.nj; ++i) {
     P.j[i].blk0 = blk;
     blk += P.j[i].M.ncb * P.j[i].S;
   }
-  int c = 1;
-  const int S = P.j[0].S;
-  bool same = true;
-  for (int i = 1; i < P.nj; ++i) same = same && P.j[i].S == S;
-  static const int min_s = getenv("MOE_CLUSTER_MIN_S") ? atoi(getenv("MOE_CLUSTER_MIN_S")) : 1 << 30;
-  if (same && S >= min_s)
-    for (int k = 8; k > 1; --k)
-      if (S % k == 0) {
-        c = k;
-        break;
-      }
-  if (same && want_cluster > 1 && S % want_cluster == 0) c = want_cluster;
-  P.cluster = c;
   return blk;
 }
 
@@ -688,17 +662,12 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   q.j[1] = dense_job(wk[l], xn, qkv_part + (size_t)S_qkv * d, qkv_out + d, Q_qkv);
   q.j[2] = dense_job(wv[l], xn, qkv_part + (size_t)2 * S_qkv * d, qkv_out + 2 * d, Q_qkv);
   q.err = err;
-  if (cur_ds && l > 0 && up_fx) {  // decode: reset the previous layer's up-projection sums
-    q.zero = up_acc;
-    q.zero_n = 2 * topk * f;
-  }
   for (int i = 0; i < 3; ++i) {  // fixed-point sums, read (and reset) by the attention
     q.j[i].reduce = 2;
     q.j[i].acc = qkv_acc + (size_t)i * d;
   }
   if (pend_comb) {  // previous layer's combine + this layer's LN1 in the QKV prologue
     q.route = route + p;
-    q.hold = comb_hold ? 1 : 0;
     for (int i = 0; i < 3; ++i) {
       GJob& J = q.j[i];
       J.xmode = X_COMBINE;
@@ -711,15 +680,13 @@ int moe_engine::enq_attention(int l, int p, int mode) {
     }
   }
   const int nq = finalize_launch(q);
-  if (q.cluster > 1)
-    for (int i = 0; i < 3; ++i) q.j[i].reduce = 0;  // partials summed by the attention
   prof_begin(K_QKV);
   launch_gemv(attn_bits, q, nq, s_comp, pdl && !prof);
   prof_end(K_QKV);
   dbg("qkv", l, p);
   AttnParams a{};
   a.qkv_part = qkv_part;
-  a.S = S_qkv / q.cluster;
+  a.S = S_qkv;
   a.acc = q.j[0].reduce == 2 ? qkv_acc : nullptr;
   a.kc = kc + (size_t)l * T * d;
   a.vc = vc + (size_t)l * T * d;
@@ -742,7 +709,6 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   o.j[0].reduce = 2;  // fixed-point split-K sums, read (and reset) by the tail
   o.j[0].acc = wo_acc;
   const int no = finalize_launch(o);
-  if (o.cluster > 1) o.j[0].reduce = 1;
   prof_begin(K_WO);
   launch_gemv(attn_bits, o, no, s_comp, pdl && !prof);
   prof_end(K_WO);
@@ -777,7 +743,6 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   t.pos = p;
   t.mode = mode;
   t.ep_size = 1;
-  t.stamp = route_stamps ? 1 : 0;
   if (tail_smem_bytes(t) > 226 * 1024) t.gh_l = t.gh_g = nullptr;  // gates too big to stage
   launch_tail(t, s_comp, pl);
   dbg("tail", l, p);
@@ -796,8 +761,6 @@ int moe_engine::enq_experts(int l, int p) {
   u.wait_ns = wait_ns;
   u.cnt = cnt;
   u.site = site_of(l, 4);
-  u.ds = route_stamps ? cur_ds : nullptr;  // decode: spin on the route stamp, not the grid
-  u.layer = l;
   GLaunch dn = u;
   dn.site = site_of(l, 5);
   for (int j = 0; j < topk; ++j) {
@@ -814,8 +777,7 @@ int moe_engine::enq_experts(int l, int p) {
       J.out = up_out + (size_t)(2 * j + m) * f;
       // split-K partials, bulk-copied and summed in order by the down GEMV's
       // SwiGLU prologue (fewer atomics than fixed-point sums for 5 splits)
-      J.reduce = up_fx ? 2 : 0;
-      J.acc = up_acc + (size_t)(2 * j + m) * f;
+      J.reduce = 0;
       J.QPS = Q_up;
       J.S = S_up;
     }
@@ -833,51 +795,21 @@ int moe_engine::enq_experts(int l, int p) {
     J.out = dn_out + (size_t)j * d;
     // single GPU: fixed-point split-K sums read (and reset) by the combine;
     // expert parallel: reduced in-kernel, the exchange ships dn_out
-    J.reduce = (ep_world > 1 || !dn_fx) ? 1 : 2;
+    J.reduce = ep_world > 1 ? 1 : 2;
     J.acc = dn_acc + (size_t)j * d;
     J.QPS = Q_dn;
     J.S = S_dn;
   }
   u.nj = 2 * topk;
   dn.nj = topk;
-  if (pf_w2) {  // W1/W3 CTAs pull their expert's W2 records + zmeta into L2
-    u.pf_off[0] = (long long)xoff[2][0];
-    u.pf_len[0] = (long long)xl[2].rec;
-    u.pf_off[1] = (long long)xoff[2][3];
-    u.pf_len[1] = (long long)xl[2].zmeta;
-    for (int r = 0; r < 2; ++r) {  // bulk prefetches need 16-byte aligned ranges
-      u.pf_len[r] += u.pf_off[r] & 15;
-      u.pf_off[r] &= ~15ll;
-    }
-  }
-  if (pend_comb && !up_fx) {  // the fused combine read dn_acc: reset it before W2 adds
+  if (pend_comb) {  // the fused combine read dn_acc: reset it before W2 adds
     u.zero = dn_acc;
     u.zero_n = topk * d;
   }
   pend_comb = false;
   const int nu = finalize_launch(u);
-  if (u.cluster > 1)
-    for (int i = 0; i < u.nj; ++i) u.j[i].reduce = 0;
-  for (int j = 0; j < topk; ++j) {
-    GJob& J = dn.j[j];
-    if (u.j[0].reduce == 2) {
-      J.xfx = 1;
-      J.up1 = reinterpret_cast<const float*>(up_acc + (size_t)(2 * j) * f);
-      J.up3 = reinterpret_cast<const float*>(up_acc + (size_t)(2 * j + 1) * f);
-    }
-  }
-  if (cur_ds && pf_qkv && l + 1 < L) {  // pull the next layer's Wq/Wk/Wv into L2
-    const std::vector<DevMat>* ws[3] = {&wq, &wk, &wv};
-    for (int i = 0; i < 3; ++i) {
-      const DevMat& D = (*ws[i])[l + 1];
-      dn.pfa[i] = reinterpret_cast<const uint8_t*>(D.mem);
-      dn.pfl[i] = (long long)(D.bytes & ~size_t(15));
-    }
-  }
-  const int ndn = finalize_launch(dn, dn_cluster);
-  if (dn.cluster > 1 && dn.j[0].reduce != 2)
-    for (int j = 0; j < topk; ++j) dn.j[j].reduce = 1;
-  for (int j = 0; j < topk; ++j) dn.j[j].xS = dn.j[j].xfx ? 1 : S_up / u.cluster;
+  const int ndn = finalize_launch(dn);
+  for (int j = 0; j < topk; ++j) dn.j[j].xS = S_up;
   if (serial_copies) {  // ncu / debugging: the host drains the mailbox before the GEMV
     CU(cudaStreamSynchronize(s_comp));
     {  // entries posted so far = device-side head (seq[1])
@@ -903,12 +835,6 @@ int moe_engine::enq_experts(int l, int p) {
   c.part = dn_out;
   c.S = 1;
   c.acc = dn.j[0].reduce == 2 ? dn_acc : nullptr;
-  // the up sums are reset for the next layer by the next QKV / lm_head GEMV in
-  // decode; prefill interleaves positions, so its combine resets them itself
-  if (u.j[0].reduce == 2 && !cur_ds) {
-    c.zero = up_acc;
-    c.zero_n = 2 * topk * f;
-  }
   if (ep_world > 1) {  // sum-exchange of the slot buffers over peer memory
     ExchangeParams xp{};
     xp.src = dn_out;
@@ -941,7 +867,7 @@ int moe_engine::enq_experts(int l, int p) {
     c.ln_b = l + 1 < L ? ln1b[l + 1] : lnfb;
     c.xn = xn;
   }
-  if (cur_ds && fuse_comb && ep_world == 1 && c.acc && l + 1 < L && !up_fx) {
+  if (cur_ds && ep_world == 1 && c.acc && l + 1 < L) {
     pend_comb = true;  // QKV(l+1) forms the residual and LN1 itself
   } else {
     launch_combine(c, s_comp, pdl && !prof);
@@ -960,10 +886,6 @@ int moe_engine::enq_logits(int p, float* out) {
   g.cnt = cnt;
   g.site = 1 + 8 * L;
   g.j[0] = dense_job(lm_head, xn, lm_part, out, Q_lm);
-  if (cur_ds && up_fx) {  // decode: reset the last layer's up-projection sums
-    g.zero = up_acc;
-    g.zero_n = 2 * topk * f;
-  }
   g.j[0].reduce = 0;  // the logits kernel sums the splits
   const int ng = finalize_launch(g);
   prof_begin(K_LM);
@@ -971,7 +893,7 @@ int moe_engine::enq_logits(int p, float* out) {
   prof_end(K_LM);
   LogitsParams lp{};
   lp.part = lm_part;
-  lp.S = S_lm / g.cluster;
+  lp.S = S_lm;
   lp.V = V;
   lp.logits = out;
   lp.cand_val = cand_val;
@@ -1106,7 +1028,21 @@ int moe_engine::finish_call(bool want_logits) {
                     cudaMemcpyDeviceToHost));
     CU(cudaMemsetAsync(st.scalars + 3, 0, sizeof(int), s_comp));
   }
-  if (e) CU(cudaMemsetAsync(err, 0, sizeof(int), s_comp));
+  if (e) {
+    // the first position whose gate input (err[6]) or logits (err[7]) were not
+    // finite: tokens before it completed (the reference raises inside that
+    // token's forward pass), so the caller advances by exactly those
+    bad_pos = -1;
+    for (int i = 6; i < 8; ++i)
+      if (hstat->err[i] > 0 && (bad_pos < 0 || hstat->err[i] - 1 < bad_pos)) bad_pos = hstat->err[i] - 1;
+    CU(cudaMemsetAsync(err, 0, sizeof(int), s_comp));
+    CU(cudaMemsetAsync(err + 6, 0, 2 * sizeof(int), s_comp));
+    if (bad_pos >= 0) {  // events of later tokens (decoded past the error) are dropped
+      size_t keep = events.size();
+      while (keep > 0 && events[keep - 1].token_pos > bad_pos) --keep;
+      events.resize(keep);
+    }
+  }
   if (e & MOE_ERRF_TIMEOUT) {
     int diag[8] = {0};
     memcpy(diag, hstat->err, sizeof(diag));
@@ -1150,24 +1086,23 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (sc->enabled && sc->m > cc->b)
     return fail(MOE_ERR_VALUE, "m=" + std::to_string(sc->m) + " exceeds b=" +
                                    std::to_string(cc->b) + " staging buffers");
-  if (sc->m > md->n_experts) return fail(MOE_ERR_VALUE, "m exceeds n_experts");
   auto* e = new moe_engine();
   e->md = *md;
   e->cc = *cc;
   e->sc = *sc;
+  // top-m of E gate logits is at most E experts (engine.py:60-68 argsort[:m])
+  e->sc.m = std::min(sc->m, md->n_experts);
   e->dev = device;
   e->rec_hidden = record_hidden != 0;
   if (const char* dbgv = getenv("MOE_DEBUG")) e->debug = atoi(dbgv) != 0;
+  // Under a kernel-serialising tool (ncu, compute-sanitizer: both inject a
+  // library through CUDA_INJECTION64_PATH) a GEMV spinning on the copy
+  // engine's flag would never see it: the host then drains the copies before
+  // each expert GEMV instead.  MOE_SERIAL_COPIES=0/1 overrides.
+  e->serial_copies = getenv("CUDA_INJECTION64_PATH") != nullptr ||
+                     getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr;
   if (const char* sv = getenv("MOE_SERIAL_COPIES")) e->serial_copies = atoi(sv) != 0;
   if (const char* tv = getenv("MOE_COPY_TRACE")) e->trace_copies = atoi(tv) != 0;
-  if (const char* uf = getenv("MOE_UP_FX")) e->up_fx = atoi(uf) != 0;
-  if (const char* df = getenv("MOE_DN_FX")) e->dn_fx = atoi(df) != 0;
-  if (const char* pf = getenv("MOE_PF_W2")) e->pf_w2 = atoi(pf) != 0;
-  if (const char* fc = getenv("MOE_FUSE_COMBINE")) e->fuse_comb = atoi(fc) != 0;
-  if (const char* dc = getenv("MOE_DN_CLUSTER")) e->dn_cluster = atoi(dc);
-  if (const char* pq = getenv("MOE_PF_QKV")) e->pf_qkv = atoi(pq) != 0;
-  if (const char* rs = getenv("MOE_ROUTE_STAMPS")) e->route_stamps = atoi(rs) != 0;
-  if (const char* ch = getenv("MOE_COMB_HOLD")) e->comb_hold = atoi(ch) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
   for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
@@ -1454,11 +1389,6 @@ int moe_finalize(moe_engine* e) {
   plan(1, e->wo[0].M, &e->Q_wo, &e->S_wo);
   plan(2 * e->topk, xm0, &e->Q_up, &e->S_up);
   plan(e->topk, xm2, &e->Q_dn, &e->S_dn);
-  if (e->dn_cluster > 1 && e->S_dn % e->dn_cluster) {  // splits in whole clusters
-    const int nq = xm2.nqp, S = std::max(e->dn_cluster, e->S_dn / e->dn_cluster * e->dn_cluster);
-    e->Q_dn = (nq + S - 1) / S;
-    e->S_dn = (nq + e->Q_dn - 1) / e->Q_dn;
-  }
   plan(1, e->lm_head.M, &e->Q_lm, &e->S_lm);
   if ((rc = e->dalloc(&e->qkv_part, (size_t)3 * e->S_qkv * d))) return rc;
   if ((rc = e->dalloc(&e->wo_part, (size_t)e->S_wo * d))) return rc;
@@ -1466,7 +1396,6 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->dn_part, (size_t)e->topk * e->S_dn * d))) return rc;
   if ((rc = e->dalloc(&e->wo_acc, (size_t)d))) return rc;
   if ((rc = e->dalloc(&e->qkv_acc, (size_t)3 * d))) return rc;
-  if ((rc = e->dalloc(&e->up_acc, (size_t)2 * e->topk * f))) return rc;
   if ((rc = e->dalloc(&e->dn_acc, (size_t)e->topk * d))) return rc;
   if ((rc = e->dalloc(&e->lm_part, (size_t)e->S_lm * V))) return rc;
   if ((rc = e->dalloc(&e->qkv_out, (size_t)3 * d))) return rc;
@@ -1692,8 +1621,15 @@ int moe_decode_greedy(moe_engine* e, int32_t n, int32_t* tokens_out, float* fina
   rc = e->run_tokens(n);
   if (rc) return rc;
   CU(cudaGetLastError());
+  e->bad_pos = -1;
   rc = e->finish_call(final_logits_out != nullptr);
-  if (rc) return rc;
+  if (rc) {
+    if (e->bad_pos >= e->pos) {  // the tokens before the failing one completed
+      e->tok_seq += (unsigned)(e->bad_pos - e->pos);
+      e->pos = e->bad_pos;
+    }
+    return rc;
+  }
   e->pos += n;
   e->tok_seq += (unsigned)n;
   if (tokens_out) CU(cudaMemcpy(tokens_out, e->tok_hist, (size_t)n * 4, cudaMemcpyDeviceToHost));
@@ -2346,9 +2282,6 @@ int moe_bench_gemv(int32_t bits, int32_t K, int32_t N, int32_t njobs, int32_t it
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess)
       return fail(MOE_ERR_CUDA, std::string("gemv launch (grid ") + std::to_string(nblk) +
-                                    ", smem " + std::to_string(gemv_smem_bytes(
-                                        bits, qps * (M0.mma ? mt::KS : 4), 0, 0, M0.rb_full,
-                                        nullptr, nullptr, M0.mma)) +
                                     "): " + cudaGetErrorString(le));
   }
   for (int w = 0; w < 3; ++w) launch_gemv(bits, P[w % nsets], nblk, s, pdl != 0);

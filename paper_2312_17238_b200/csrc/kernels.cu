@@ -71,17 +71,6 @@ MOE_DEV float sigmoid_ref(float x) {  // model.py:229-235 branch-stable logistic
 // (copy engine -> cuStreamWriteValue32) before streaming it.  Dense weights
 // are prefetched before griddepcontrol.wait, overlapping the previous kernel
 // (programmatic dependent launch).
-MOE_DEV void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
-}
-// load a float from the same shared-memory offset in cluster CTA `rank`
-MOE_DEV float ld_dsmem_f32(const float* p, int rank) {
-  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
-  return v;
-}
 
 MOE_DEV bool wait_flag(const uint32_t* f, uint32_t gen, int* err, unsigned long long wait_ns) {
   if ((int)(ld_acquire_u32(f) - gen) >= 0) return true;
@@ -113,18 +102,6 @@ MOE_DEV float cons_sum(float v, float* red, int nthr) {
   return t;
 }
 
-// max over the GEMV's consumer warps (named barrier 1)
-MOE_DEV float cons_max(float v, float* red, int nthr) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = nthr >> 5;
-  v = warp_max(v);
-  if (lane == 0) red[w] = v;
-  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
-  float t = 0.f;
-  for (int i = 0; i < nw; ++i) t = fmaxf(t, red[i]);
-  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
-  return t;
-}
-
 // fixed-point image of one partial (0 and an error flag when out of range)
 MOE_DEV unsigned long long fx_bits(float a, int* err) {
   const float q = a * MOE_FX_SCALE;
@@ -135,14 +112,6 @@ MOE_DEV unsigned long long fx_bits(float a, int* err) {
   return (unsigned long long)__float2ll_rn(q);
 }
 
-MOE_DEV void fx_add(unsigned long long* p, float a, int* err) {
-  const float q = a * MOE_FX_SCALE;
-  if (!(fabsf(q) < 0x1p62f)) {  // non-finite or out of range: the reference would
-    if (err) atomicOr(err, MOE_ERRF_NONFINITE_GATE);  // fail on the next gate input
-    return;
-  }
-  atomicAdd(p, (unsigned long long)__float2ll_rn(q));
-}
 // consumer side: fixed-point sum -> fp32 (one rounding); the consumer resets
 // the sums (fx_clear) after all its loads are issued
 MOE_DEV float fx_val(unsigned long long v) {
@@ -153,7 +122,7 @@ MOE_DEV float fx_val(unsigned long long v) {
 template <int BITS>
 __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     k_gemv(const __grid_constant__ GLaunch P, int xs_cap, int zs_cap, int xin_cap, int nst,
-           int stage_bytes, int mcap) {
+           int stage_bytes) {
   constexpr int WC = Fmt<BITS>::WC;
   constexpr bool QUANT = BITS <= 4;
   constexpr int W = MOE_GEMV_WARPS, QPW = gemv_qpw(BITS), QS = gemv_qs(BITS);
@@ -168,13 +137,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   __half2* zsm = reinterpret_cast<__half2*>(xz + xs_cap);  // the CTA's zmeta slice [zs_cap]
   const size_t xin_off = 512 + (((size_t)xs_cap * 8 + (size_t)zs_cap * 4 + 15) & ~(size_t)15);
   uint8_t* xin = smem + xin_off;  // the CTA's raw x rows (bulk copied) [xin_cap bytes]
-  // tensor-core layout: the CTA's scale slice [rows][nsc] and the B-operand
-  // table [k-step][slice][48 halves] (mcap rows; 0 for the CUDA-core layout)
-  const size_t scl_off = (xin_off + (size_t)xin_cap + 15) & ~(size_t)15;
-  __half* scl_s = reinterpret_cast<__half*>(smem + scl_off);
-  __half* btab = reinterpret_cast<__half*>(smem + scl_off + (size_t)mcap * 16);
-  uint64_t* sbar = reinterpret_cast<uint64_t*>(smem + 400);  // scale slice landed
-  uint8_t* ring = smem + ((scl_off + (size_t)mcap * 64 + 127) & ~(size_t)127);
+  uint8_t* ring = smem + ((xin_off + (size_t)xin_cap + 127) & ~(size_t)127);
 
   int ji = 0, cnt_base = 0;
   for (int i = 1; i < P.nj; ++i)
@@ -184,20 +147,18 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const int local = blockIdx.x - J.blk0;
   const int cb = local / J.S, s = local % J.S;
   MatDev M = J.M;
-  // storage units: quads of 4 rows (CUDA-core layout) or 16-row k-steps
-  // (tensor-core layout, mma_layout.cuh); a cb is 32 chunks or 8 slices
-  const bool mmal = QUANT && M.mma;
-  const int RPU = mmal ? mt::KS : 4;
+  // storage units: quads of 4 rows; a cb is 32 chunks (the tensor-core layout
+  // of mma_layout.cuh runs in k_mgemv)
   const int qs = s * J.QPS, qe = min(M.nqp, qs + J.QPS);  // storage quads (pads are zero)
-  const int wcb = mmal ? mma_slices(M, cb) : min(32, M.nchunks - cb * 32);
-  const int rb = mmal ? mma_rec_bytes(M, cb) : rec_bytes(BITS, wcb, M.g_log2, M.sg_log2);
-  const int QSr = mmal ? stage_bytes / M.rb_full : QS;  // units per pipeline stage
+  const int wcb = min(32, M.nchunks - cb * 32);
+  const int rb = rec_bytes(BITS, wcb, M.g_log2, M.sg_log2);
+  const int QSr = QS;  // quads per pipeline stage
   const int nit = (max(qe - qs, 0) + QSr - 1) / QSr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qv = min(qe, M.nquads);  // real quads of this split
-  const int row0 = qs * RPU, nrows = max(qv - qs, 0) * RPU;
-  const int nout = mmal ? wcb * mt::SO : wcb * WC;                 // outputs of this cb
-  const size_t obase = mmal ? (size_t)cb * mt::CBO : (size_t)cb * 32 * WC;
+  const int row0 = qs * 4, nrows = max(qv - qs, 0) * 4;
+  const int nout = wcb * WC;  // outputs of this cb
+  const size_t obase = (size_t)cb * 32 * WC;
   const int gcb0 = QUANT ? (int)(obase >> M.g_log2) : 0;  // first zero group of the cb
   const bool uni = QUANT && M.runs_uniform;
   // uniform runs: the zero-point runs of the CTA's rows are one contiguous
@@ -210,14 +171,10 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   // the producer's bulk-copy queue ahead of the weight stream: consumer loads
   // issued next to a saturating weight stream wait behind it for microseconds
   const bool swiglu = J.xmode == X_SWIGLU;
-  const int xes = J.xfx ? 8 : 4;  // bytes per x element (fixed-point sums or fp32)
+  constexpr int xes = 4;  // bytes per x element
   const int xparts = J.xS > 1 ? J.xS : 1;  // producer partials per input array
   const bool xcomb = J.xmode == X_COMBINE;
-  // decode with route stamps: a W1/W3 launch reads only data the tail published
-  // before the stamp (route, h), so it starts without griddepcontrol.wait and
-  // waits for the tail's grid only before it exits (completion stays transitive)
-  const bool early = J.rel_slot >= 0 && P.ds != nullptr && J.xmode == X_PLAIN;
-  const bool xstage = !xcomb && xin_cap > 0 && nrows > 0 && !(J.xS > 1 && J.xfx) &&
+  const bool xstage = !xcomb && xin_cap > 0 && nrows > 0 &&
                       (swiglu ? 2 : 1) * xparts * nrows * xes <= xin_cap;
 
   if (threadIdx.x == 0) {
@@ -227,28 +184,13 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     }
     gemv::mbar_init(zbar, 1);
     gemv::mbar_init(xbar, 1);
-    gemv::mbar_init(sbar, 1);
     gemv::mbar_fence_init();
   }
   __syncthreads();
   gemv::pdl_trigger();
 
   if (warp == W) {  // ---------------------------------------------- producer
-    if (J.rel_slot >= 0 && P.ds) {
-      // decode: the route of (token, layer) is published by the tail with a
-      // stamp; spinning on it lets the weight stream start before the
-      // previous grid completes (x still waits for griddepcontrol.wait)
-      const unsigned int want = route_stamp(P.ds->seq, P.layer);
-      const unsigned long long t0 = globaltimer();
-      while (ld_acquire_u32(&P.route->stamp) != want) {
-        __nanosleep(64);
-        if (globaltimer() - t0 > P.wait_ns) {
-          if (lane == 0) atomicOr(P.err, MOE_ERRF_TIMEOUT);
-          break;
-        }
-      }
-      if (P.route->buf[J.rel_slot] < 0) return;
-    } else if (J.rel_slot >= 0) {
+    if (J.rel_slot >= 0) {
       gemv::pdl_wait();  // the route is written by the previous kernel
       // expert parallel: another rank owns this expert -> the whole cluster
       // (same job) skips, before any cluster barrier
@@ -256,7 +198,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     }
     // x rows: one bulk copy per input array (after the previous kernel completed)
     auto issue_x = [&]() {
-      if ((J.rel_slot < 0 || P.ds) && !early) gemv::pdl_wait();  // x: previous kernel's output
+      if (J.rel_slot < 0) gemv::pdl_wait();  // x: previous kernel's output
       if (!xstage) return;
       const uint32_t bytes = (uint32_t)(nrows * xes);
       gemv::mbar_arrive_tx(xbar, (swiglu ? 2u : 1u) * (uint32_t)xparts * bytes);
@@ -273,7 +215,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     };
     if (lane == 0) {
       if (J.rel_slot >= 0) {
-        if (!P.ds) issue_x();
+        issue_x();
         const int buf = P.route->buf[J.rel_slot];
         // the tail saw the buffer's copy already published: no flag round trip
         if (!P.route->ready[J.rel_slot])
@@ -281,13 +223,6 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
         const uint8_t* b = P.pool + (long long)buf * P.slot_stride;
         M.base = b + reinterpret_cast<size_t>(M.base);
         M.zmeta = reinterpret_cast<const __half2*>(b + reinterpret_cast<size_t>(M.zmeta));
-        M.scl = reinterpret_cast<const __half*>(b + reinterpret_cast<size_t>(M.scl));
-      }
-      if (mmal && nrows > 0) {  // the CTA's scales, ahead of the weight stream
-        const int nsc = mma_nsc(M, cb);
-        const uint32_t bytes = (uint32_t)nrows * nsc * 2;
-        gemv::mbar_arrive_tx(sbar, bytes);
-        gemv::bulk_g2s(scl_s, M.scl + mma_scl_offset(M, cb) + (int64_t)row0 * nsc, bytes, sbar);
       }
       if (zstage) {
         const uintptr_t za = reinterpret_cast<uintptr_t>(M.zmeta + z0);
@@ -296,47 +231,13 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
         gemv::mbar_arrive_tx(zbar, bytes);
         gemv::bulk_g2s(zsm, reinterpret_cast<const void*>(za - lead), bytes, zbar);
       }
-      // the fused combine reads 80 KB of residual inputs per CTA right after the
-      // previous kernel: hold the weight ring until then (MOE_COMB_HOLD)
-      if (xcomb && P.hold) gemv::pdl_wait();
       const uint8_t* src = M.base + cb_offset(M, cb) + (int64_t)qs * rb;
       const uint64_t pol = gemv::policy_evict_first();
-      // L2 prefetch of the next kernel's expert weights, once the ring is full
-      auto issue_prefetch = [&]() {
-        for (int r = 0; r < 3; ++r) {  // absolute ranges, a slice per CTA
-          const long long len = P.pfl[r];
-          if (len <= 0) continue;
-          const long long per = ((len + gridDim.x - 1) / gridDim.x + 15) & ~15ll;
-          long long o = (long long)blockIdx.x * per;
-          const long long e = min(len, o + per);
-          for (; o < e; o += 65536)
-            gemv::bulk_prefetch_l2(P.pfa[r] + o, (uint32_t)((min(e - o, 65536ll) + 15) & ~15ll));
-        }
-        if (J.rel_slot < 0 || (P.pf_len[0] <= 0 && P.pf_len[1] <= 0)) return;
-        int n = 0, idx = -1;  // this CTA's index among the CTAs on the same expert
-        for (int i = 0; i < P.nj; ++i)
-          if (P.j[i].rel_slot == J.rel_slot) {
-            if (i == ji) idx = n + local;
-            n += P.j[i].M.ncb * P.j[i].S;
-          }
-        const uint8_t* b = P.pool + (long long)P.route->buf[J.rel_slot] * P.slot_stride;
-        for (int r = 0; r < 2; ++r) {
-          const long long len = P.pf_len[r];
-          if (len <= 0) continue;
-          const long long per = ((len + n - 1) / n + 15) & ~15ll;
-          long long o = (long long)idx * per, e = min(len, o + per);
-          for (; o < e; o += 65536) {
-            const uint32_t nb = (uint32_t)((min(e - o, 65536ll) + 15) & ~15ll);
-            gemv::bulk_prefetch_l2(b + P.pf_off[r] + o, nb);
-          }
-        }
-      };
       int st = 0;
       uint32_t ph = 0;
       for (int it = 0; it < nit; ++it) {
         // dense weights: the ring is prefetched before the previous kernel ends
-        if (it == nst && (J.rel_slot < 0 || P.ds)) issue_x();
-        if (it == nst) issue_prefetch();
+        if (it == nst && J.rel_slot < 0) issue_x();
         if (it >= nst) gemv::mbar_wait(empty + st, ph ^ 1);
         const int nq = min(QSr, qe - (qs + it * QSr));
         const uint32_t bytes = (uint32_t)(nq * rb);
@@ -348,35 +249,15 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
           ph ^= 1;
         }
       }
-      if (nit <= nst && (J.rel_slot < 0 || P.ds)) issue_x();
-      if (nit <= nst) issue_prefetch();
+      if (nit <= nst && J.rel_slot < 0) issue_x();
     }
     __syncwarp();
-    if (P.cluster > 1) {  // the two cluster barriers of the split-K epilogue
-      cluster_sync();
-      cluster_sync();
-    }
     return;
   }
 
   // ------------------------------------------------------------ consumers
   const int nthr = W * 32;
-  if (early) {  // the route stamp of (token, layer) instead of the whole tail grid
-    if (threadIdx.x == 0) {
-      const unsigned int want = route_stamp(P.ds->seq, P.layer);
-      const unsigned long long t0 = globaltimer();
-      while (ld_acquire_u32(&P.route->stamp) != want) {
-        __nanosleep(64);
-        if (globaltimer() - t0 > P.wait_ns) {
-          atomicOr(P.err, MOE_ERRF_TIMEOUT);
-          break;
-        }
-      }
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
-  } else {
-    gemv::pdl_wait();
-  }
+  gemv::pdl_wait();
   tl_begin(P.site);
   tl_mark(P.site, 5);  // block 0 released (profiling: its start vs the earliest CTA's)
   cta_mark(0);
@@ -391,11 +272,9 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   if (J.rel_slot >= 0) {
     if (ebuf < 0) {  // expert parallel: not ours; contribute zeros to the exchange
       float* zdst = J.reduce == 2 ? nullptr : J.reduce ? (s == 0 ? J.out : nullptr)
-                             : (s % P.cluster == 0 ? J.part + (size_t)(s / P.cluster) * M.N
-                                                   : nullptr);
+                                                      : J.part + (size_t)s * M.N;
       if (zdst)
         for (int t = threadIdx.x; t < nout; t += nthr) zdst[obase + t] = 0.f;
-      if (early) gemv::pdl_wait();
       cta_mark(2);
       tl_end(P.site);
       return;
@@ -451,18 +330,11 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   if (xstage) {  // x rows from the producer's bulk copy
     gemv::mbar_wait(xbar, 0);
     const float* xf = reinterpret_cast<const float*>(xin);
-    const unsigned long long* xq = reinterpret_cast<const unsigned long long*>(xin);
     for (int i = threadIdx.x; i < nrows; i += nthr) {
-      float a, b = 0.f;
-      if (J.xfx) {
-        a = fx_val(xq[i]);
-        if (swiglu) b = fx_val(xq[nrows + i]);
-      } else {  // fp32 producer partials, summed in split order
-        a = 0.f;
-        for (int p = 0; p < xparts; ++p) a += xf[p * nrows + i];
-        if (swiglu)
-          for (int p = 0; p < xparts; ++p) b += xf[(xparts + p) * nrows + i];
-      }
+      float a = 0.f, b = 0.f;  // fp32 producer partials, summed in split order
+      for (int p = 0; p < xparts; ++p) a += xf[p * nrows + i];
+      if (swiglu)
+        for (int p = 0; p < xparts; ++p) b += xf[(xparts + p) * nrows + i];
       float xv = a;
       if (swiglu)  // SwiGLU of the up projections (model.py:223-226)
         xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
@@ -478,14 +350,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       const int i = i0 + u * nthr + threadIdx.x;
       const int r = row0 + i;
       const bool in = i < nrows;
-      if (J.xfx) {  // fixed-point sums of a reduce == 2 producer
-        const unsigned long long* q1 =
-            reinterpret_cast<const unsigned long long*>(J.xmode == X_PLAIN ? J.x : J.up1);
-        va[u] = in ? fx_val(__ldcg(q1 + r)) : 0.f;
-        vb[u] = (in && J.xmode != X_PLAIN)
-                    ? fx_val(__ldcg(reinterpret_cast<const unsigned long long*>(J.up3) + r))
-                    : 0.f;
-      } else if (J.xS > 1) {  // unreduced producer partials: sum them in split order
+      if (J.xS > 1) {  // unreduced producer partials: sum them in split order
         // (up to 8 splits per round, every load of the round in flight)
         float a = 0.f, b = 0.f;
         if (in) {
@@ -563,24 +428,6 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       }
   }
   tl_mark(P.site, 1);  // zero-point slice landed, x * zscale done
-  // tensor-core layout: B-operand table b = x * s * 2^E in three fp16 pieces
-  // per (row, slice), E from the CTA's largest |x * s| (mma_gemv.cuh)
-  int Eb = 0;
-  if (mmal && nrows > 0) {
-    gemv::mbar_wait(sbar, 0);
-    const int nsc = mma_nsc(M, cb), nsl = wcb;
-    float mx = 0.f;
-    for (int i = threadIdx.x; i < nrows * nsc; i += nthr)
-      mx = fmaxf(mx, fabsf(xs[i / nsc] * __half2float(scl_s[i])));
-    mx = cons_max(mx, misc, nthr);
-    Eb = mx > 0.f ? min(14 - ilogbf(mx), 60) : 0;
-    const float p2 = __uint_as_float(gemv::pow2_bits(Eb));
-    for (int idx = threadIdx.x; idx < nrows * nsl; idx += nthr) {
-      const int i = idx / nsl, w = idx - i * nsl;
-      const float sv = __half2float(scl_s[i * nsc + ((w * mt::SO) >> M.sg_log2)]);
-      mg::put_pieces(btab + ((i >> 4) * nsl + w) * mt::BTAB, i & 15, __fmul_rn(xs[i], sv) * p2);
-    }
-  }
   if (QUANT && M.runs_uniform) {
     zo_part = warp_sum(zo_part);
     if (lane == 0) misc[warp] = zo_part;
@@ -612,33 +459,7 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   const bool fast = QUANT && wcb == 32 && M.runs_uniform &&
                     M.g_log2 == (BITS == 2 ? 4 : 6);
   float ztot = 0.f;
-  float D[8][4], zq[4] = {0.f, 0.f, 0.f, 0.f};
-  if (mmal) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) D[i][0] = D[i][1] = D[i][2] = D[i][3] = 0.f;
-    const int g = lane >> 2, t = lane & 3, nsl = wcb;
-    const int sb = mt::slice_bytes(BITS, 1 << M.g_log2);
-    const uint2* bt = reinterpret_cast<const uint2*>(btab);
-    int st = 0;
-    uint32_t ph = 0;
-    for (int it = 0; it < nit; ++it) {
-      gemv::mbar_wait(full + st, ph);
-      if (warp < nsl)
-        for (int u = 0; u < QSr; ++u) {
-          const int ul = it * QSr + u;
-          if (qs + ul < qv)
-            mg::step<BITS>(D, zq, ring + (size_t)st * stage_bytes + (size_t)u * rb + warp * sb,
-                           bt[(ul * nsl + warp) * (mt::BTAB / 4) + min(g, 2) * 4 + t],
-                           xz + ul * mt::KS, lane);
-        }
-      __syncwarp();
-      if (lane == 0) gemv::mbar_arrive(empty + st);
-      if (++st == nst) {
-        st = 0;
-        ph ^= 1;
-      }
-    }
-  } else if (fast || !QUANT) {
+  if (fast || !QUANT) {
     int st = 0;
     uint32_t ph = 0;
     for (int it = 0; it < nit; ++it) {
@@ -698,53 +519,37 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       for (int o = Z.zpr; o < 32; o <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, o);
     ztot = __shfl_sync(0xffffffffu, zacc, (lane * WC) >> M.g_log2);
   }
-  if (early) gemv::pdl_wait();  // the tail's grid is long done: completion stays transitive
   tl_mark(P.site, 3);  // streaming loop done
   cta_mark(1);
   float y[WC];
   gemv::finish_lane<BITS>(y, acc, ztot);
-  // cross-warp reduction through the (now idle) ring, fixed order; the
-  // tensor-core layout's warps own disjoint outputs: ymm[o] directly
+  // cross-warp reduction through the (now idle) ring, fixed order
   float* red = reinterpret_cast<float*>(ring);
-  float* ymm = red;
-  float* ysum = mmal ? red + mt::CBO : red + W * 32 * (WC + 1);  // the CTA's partial outputs
+  float* ysum = red + W * 32 * (WC + 1);  // the CTA's partial outputs
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   if (!xcomb) tl_mark(P.site, 6);  // every consumer warp left the loop
-  if (mmal) {
-    if (warp < wcb) mg::finish<BITS>(D, zq, Eb, lane, ymm + warp * mt::SO);
-  } else {
 #pragma unroll
-    for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
-  }
+  for (int k = 0; k < WC; ++k) red[(warp * 32 + lane) * (WC + 1) + k] = y[k];
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   if (!xcomb) tl_mark(P.site, 7);  // per-warp results in smem
   const float zo_out = zo_sum * gemv::kZUnscale;
-  const int C = P.cluster, SC = J.S / C;  // cluster = C consecutive splits of one cb
-  const int crank = blockIdx.x % C, sc = s / C;
-  float* dst = (SC == 1 && J.reduce) ? J.out : J.part + (size_t)sc * M.N;
+  const int SC = J.S;
+  float* dst = (SC == 1 && J.reduce) ? J.out : J.part + (size_t)s * M.N;
   // the CTA's outputs leave with one bulk (TMA) copy: a plain store of the
   // split-K partials, or a bulk fixed-point add (cp.reduce.async.bulk .add.u64)
-  const bool bulk_out = C == 1 && J.reduce != 1 && P.bulk_epi;
+  const bool bulk_out = J.reduce != 1;
   unsigned long long* fxs = reinterpret_cast<unsigned long long*>(ysum);
-  for (int t = threadIdx.x; t < (mmal ? nout : 32 * WC); t += nthr) {
+  for (int t = threadIdx.x; t < 32 * WC; t += nthr) {
     const int l = t / WC, k = t % WC;
-    if (mmal || l < wcb) {
+    if (l < wcb) {
       float a = 0.f;
-      if (mmal) {
-        a = ymm[t];
-      } else {
 #pragma unroll
-        for (int w = 0; w < W; ++w) a += red[(w * 32 + l) * (WC + 1) + k];
-      }
+      for (int w = 0; w < W; ++w) a += red[(w * 32 + l) * (WC + 1) + k];
       a += zo_out;
-      if (C > 1)
-        ysum[t] = a;
-      else if (bulk_out && J.reduce == 2)
+      if (bulk_out && J.reduce == 2)
         fxs[t] = fx_bits(a, P.err);
       else if (bulk_out)
         ysum[t] = a;
-      else if (J.reduce == 2)
-        fx_add(J.acc + obase + t, a, P.err);
       else
         dst[obase + t] = a;
     }
@@ -767,36 +572,14 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
       asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
     }
   }
-  if (C > 1) {
-    // split-K inside the cluster over distributed shared memory: rank 0 sums
-    // the C partials in rank order, the producer warp joins the barriers
-    cluster_sync();
-    // every rank reduces 1/C of the outputs, reading that slice from all C
-    // ranks (loads first, then the sum in rank order)
-    const int no = nout, per = (no + C - 1) / C;
-    const int t0 = crank * per, t1 = min(no, t0 + per);
-    for (int t = t0 + threadIdx.x; t < t1; t += nthr) {
-      float v[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) v[r] = r < C ? ld_dsmem_f32(ysum + t, r) : 0.f;
-      float a = 0.f;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) a += v[r];
-      if (J.reduce == 2)
-        fx_add(J.acc + obase + t, a, P.err);
-      else
-        dst[obase + t] = a;
-    }
-    cluster_sync();  // peers keep their shared memory until every slice is read
-  }
   tl_mark(P.site, 4);  // cross-warp (+ cluster) reduction, partial written
   if (SC == 1 || J.reduce != 1) {  // done, or the consumer sums the partials
     cta_mark(2);
     tl_end(P.site);
     return;
   }
-  // split-K across clusters: the last CTA of this column block to finish
-  // sums the S / C partials in order (every CTA wrote part of its cluster's).
+  // split-K: the last CTA of this column block to finish sums the S partials
+  // in order.
   // One thread publishes the CTA's partial (barrier, then a gpu-scope fence
   // and the arrival count) and, in the last CTA, acquires the others'.
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
@@ -841,6 +624,8 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
   cta_mark(2);
     tl_end(P.site);
 }
+
+#include "mgemv_kernel.cuh"
 
 // ------------------------------------------------------------------ wait
 // Blocks the compute stream until every expert buffer of this position's route
@@ -1459,6 +1244,7 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     }
     if (bad) {
       atomicOr(P.st.err, MOE_ERRF_NONFINITE_GATE);
+      atomicCAS(P.st.err + 6, 0, pos + 1);  // first failing position (+1)
     } else if (P.mode == 0) {
       const int m = (guess && P.m > 0) ? P.m : 0;
       store::resolve_token(S, P.layer, sel_sh, k, gsel_sh, m, m ? P.guess_layer : -1, pos, rbuf,
@@ -1477,11 +1263,6 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   tl_mark(P.site, 6);
   if (P.mode == 0) {
     __syncthreads();
-    if (tid == 0 && P.ds && P.stamp) {  // every route field is written: publish the stamp
-      const unsigned int st = route_stamp(P.ds->seq, P.layer);
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&P.route->stamp), "r"(st)
-                   : "memory");
-    }
     store::stage_out(P.st, sst);
   }
   tl_mark(P.site, 7);
@@ -1495,6 +1276,13 @@ __global__ void k_prefill_bk(PrefillBKParams P) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   StoreDev S = P.st;
   RouteRec* R = P.route;
+  // a position's gate input was not finite: the reference raises in gate()
+  // before any acquire of this layer (model.py:198-205, engine.py:233-240)
+  if (ld_acquire_u32(reinterpret_cast<const uint32_t*>(S.err)) & MOE_ERRF_NONFINITE_GATE) {
+    for (int p = 0; p < P.n; ++p)
+      for (int j = 0; j < P.top_k; ++j) R[p].buf[j] = -1;
+    return;
+  }
   store::resolve_prefill(
       S, P.layer, P.n, P.top_k, [&](int p, int j) { return R[p].e[j]; },
       [&](int p, int j, int b, uint32_t g) {
@@ -1671,7 +1459,10 @@ __global__ void __launch_bounds__(256) k_logits(LogitsParams P) {
 #pragma unroll 4
     for (int s = 0; s < P.S; ++s) a += __ldcg(P.part + (size_t)s * P.V + v);
     P.logits[v] = a;
-    if (!isfinite(a)) atomicOr(P.err, MOE_ERRF_NONFINITE_LOGITS);
+    if (!isfinite(a)) {
+      atomicOr(P.err, MOE_ERRF_NONFINITE_LOGITS);
+      if (P.ds) atomicCAS(P.err + 7, 0, P.ds->pos + 1);  // first failing position (+1)
+    }
     val = a;
     idx = v;
   }
@@ -1769,7 +1560,8 @@ cudaError_t preload_kernels() {
                        (const void*)k_layernorm, (const void*)k_attention, (const void*)k_tail,
                        (const void*)k_prefill_bk, (const void*)k_begin_call,
                        (const void*)k_combine,   (const void*)k_logits, (const void*)k_wait_ready,
-                       (const void*)k_exchange};
+                       (const void*)k_exchange, (const void*)k_mgemv<2>,
+                       (const void*)k_mgemv<3>, (const void*)k_mgemv<4>};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -1780,7 +1572,8 @@ cudaError_t preload_kernels() {
     if (e != cudaSuccess) return e;
   }
   for (const void* f : {(const void*)k_embed, (const void*)k_combine,
-                        (const void*)k_attention128}) {
+                        (const void*)k_attention128, (const void*)k_mgemv<2>,
+                        (const void*)k_mgemv<3>, (const void*)k_mgemv<4>}) {
     cudaError_t e2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           200 * 1024);
     if (e2 != cudaSuccess) return e2;
@@ -1792,27 +1585,12 @@ cudaError_t preload_kernels() {
                               226 * 1024);  // + static shared memory <= 227 KB
 }
 
-// shared memory of one GEMV CTA: barriers, x slice, stage ring (which also
-// holds the cross-warp reduction scratch at the end)
-// (mma: tensor-core layout -- the scale slice and B table (64 B per row) come
-// before the ring, which takes what is left of the 2-CTAs/SM budget, 16 KB
-// stages of whole k-step records)
+// shared memory of one GEMV CTA (CUDA-core layout): barriers, x slice, stage
+// ring (which also holds the cross-warp reduction scratch at the end)
 int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full, int* nstages,
-                    int* stage_bytes, int mma) {
+                    int* stage_bytes) {
   const int WC = fmt_wc(bits);
   const int head = 512 + (((xs_rows * 8 + zs_cap * 4 + 15) & ~15) + xin_cap + 15 & ~15);
-  if (mma) {
-    const int units = rb_full >= 16384 ? 1 : 16384 / rb_full;
-    const int stage = units * rb_full;
-    const int pre = ((head + xs_rows * 64) + 127) & ~127;
-    int nst = (MOE_GEMV_SMEM_CAP - pre) / stage;
-    nst = nst < 2 ? 2 : (nst > 6 ? 6 : nst);
-    int ring = nst * stage;
-    if (ring < 12 * 1024) ring = 12 * 1024;  // epilogue: outputs + fixed-point staging
-    if (nstages) *nstages = nst;
-    if (stage_bytes) *stage_bytes = stage;
-    return pre + ring;
-  }
   const int stage = gemv_qs(bits) * rb_full;
   int nst = MOE_GEMV_RING / stage;
   nst = nst < 2 ? 2 : (nst > 16 ? 16 : nst);
@@ -1835,7 +1613,7 @@ static int gemv_zs_cap(const GLaunch& P, int bits, int xs_cap, int rbf, int mma)
     const long long rows = (long long)P.j[i].QPS * (M.mma ? mt::KS : 4);
     cap = max(cap, (int)(((rows * M.G) >> M.sg_log2) + 8));
   }
-  if (cap && !mma && gemv_smem_bytes(bits, xs_cap, cap, 0, rbf, nullptr, nullptr, 0) > 112 * 1024)
+  if (cap && !mma && gemv_smem_bytes(bits, xs_cap, cap, 0, rbf, nullptr, nullptr) > 112 * 1024)
     cap = 0;
   return cap;
 }
@@ -1843,7 +1621,7 @@ static int gemv_zs_cap(const GLaunch& P, int bits, int xs_cap, int rbf, int mma)
 // bytes of the x staging region: the largest job's x rows (two arrays for the
 // SwiGLU input), 0 when a job sums producer partials or the kernel would lose
 // its 2 CTAs/SM (x then comes through ordinary loads)
-static int gemv_xin_cap(const GLaunch& P, int bits, int xs_cap, int zs_cap, int rbf, int mma) {
+static int gemv_xin_cap(const GLaunch& P, int bits, int xs_cap, int zs_cap, int rbf) {
   int cap = 0;
   for (int i = 0; i < P.nj; ++i) {
     const GJob& J = P.j[i];
@@ -1851,48 +1629,80 @@ static int gemv_xin_cap(const GLaunch& P, int bits, int xs_cap, int zs_cap, int 
       cap = max(cap, J.M.K * 4);
       continue;
     }
-    if (J.xS > 1 && J.xfx) continue;
-    const int es = J.xfx ? 8 : 4, n = (J.xmode != X_PLAIN ? 2 : 1) * (J.xS > 1 ? J.xS : 1);
-    cap = max(cap, n * es * J.QPS * (J.M.mma ? mt::KS : 4));
+    const int n = (J.xmode != X_PLAIN ? 2 : 1) * (J.xS > 1 ? J.xS : 1);
+    cap = max(cap, n * 4 * J.QPS * 4);
   }
-  // the tensor-core layout keeps x staging and shrinks the ring instead
-  if (cap && !mma && gemv_smem_bytes(bits, xs_cap, zs_cap, cap, rbf, nullptr, nullptr, 0) > 112 * 1024)
+  if (cap && gemv_smem_bytes(bits, xs_cap, zs_cap, cap, rbf, nullptr, nullptr) > 112 * 1024)
     cap = 0;
   return cap;
 }
 
 template <int BITS>
 static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
-  int xs_cap = 0, rbf = 0, mma = 0;
+  int xs_cap = 0, rbf = 0;
   for (int i = 0; i < P.nj; ++i) {
-    mma |= P.j[i].M.mma;
-    xs_cap = max(xs_cap, P.j[i].QPS * (P.j[i].M.mma ? mt::KS : 4));
+    xs_cap = max(xs_cap, P.j[i].QPS * 4);
     rbf = max(rbf, P.j[i].M.rb_full);
   }
   int nst = 0, stage = 0;
-  const int zs_cap = gemv_zs_cap(P, BITS, xs_cap, rbf, mma);
-  const int xin_cap = gemv_xin_cap(P, BITS, xs_cap, zs_cap, rbf, mma);
-  const int smem = gemv_smem_bytes(BITS, xs_cap, zs_cap, xin_cap, rbf, &nst, &stage, mma);
+  const int zs_cap = gemv_zs_cap(P, BITS, xs_cap, rbf, 0);
+  const int xin_cap = gemv_xin_cap(P, BITS, xs_cap, zs_cap, rbf);
+  const int smem = gemv_smem_bytes(BITS, xs_cap, zs_cap, xin_cap, rbf, &nst, &stage);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nblocks);
   cfg.blockDim = dim3(MOE_GEMV_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-  at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = P.cluster > 1 ? P.cluster : 1;
-  at[1].val.clusterDim.y = 1;
-  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, zs_cap, xin_cap, nst, stage,
-                     mma ? xs_cap : 0);
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_gemv<BITS>, P, xs_cap, zs_cap, xin_cap, nst, stage);
+  g_launches.fetch_add(1);
+}
+
+// tensor-core layout (k_mgemv): x staging for every job (the full residual for
+// the fused combine), the zmeta slice, scales + B table, then the ring
+template <int B>
+static void launch_mgemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
+  int xs_cap = 0, rbf = 0, xin_cap = 0;
+  for (int i = 0; i < P.nj; ++i) {
+    const GJob& J = P.j[i];
+    const int rows = J.QPS * mt::KS;
+    xs_cap = max(xs_cap, rows);
+    rbf = max(rbf, J.M.rb_full);
+    const int n = (J.xmode == X_SWIGLU ? 2 : 1) * (J.xS > 1 ? J.xS : 1);
+    xin_cap = max(xin_cap, J.xmode == X_COMBINE ? J.M.K * 4 : n * 4 * rows);
+  }
+  const int zs_cap = gemv_zs_cap(P, B, xs_cap, rbf, 1);
+  const MgSmem L(xs_cap, zs_cap, xin_cap);
+  const int stage = mma_units(B) * rbf;
+  int nst = (int)((MOE_GEMV_SMEM_CAP - (long long)L.ring) / stage);
+  nst = nst < 2 ? 2 : (nst > 8 ? 8 : nst);
+  const int ring = max(nst * stage, 12 * 1024);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nblocks);
+  cfg.blockDim = dim3(MG_THREADS);
+  cfg.dynamicSmemBytes = L.ring + ring;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_mgemv<B>, P, xs_cap, zs_cap, xin_cap, nst, stage);
   g_launches.fetch_add(1);
 }
 
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
+  if (bits <= 4 && P.j[0].M.mma) {
+    switch (bits) {
+      case 2: launch_mgemv_t<2>(P, nblocks, s, pdl); return;
+      case 3: launch_mgemv_t<3>(P, nblocks, s, pdl); return;
+      default: launch_mgemv_t<4>(P, nblocks, s, pdl); return;
+    }
+  }
   switch (bits) {
     case 2: launch_gemv_t<2>(P, nblocks, s, pdl); break;
     case 3: launch_gemv_t<3>(P, nblocks, s, pdl); break;

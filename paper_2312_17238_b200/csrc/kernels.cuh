@@ -16,6 +16,9 @@ __host__ __device__ constexpr int gemv_qs(int bits) { return MOE_GEMV_WARPS * ge
 #define MOE_XS_MAX 4096            // rows of x kept in smem per CTA
 #define MOE_GEMV_SMEM_CAP (112 * 1024)  // dynamic smem per CTA at 2 CTAs / SM
 #define MOE_MMA_UNITS_MAX 64       // k-steps per CTA in the tensor-core layout (B table)
+// k-steps per pipeline stage of the tensor-core layout (a compile-time count so
+// the consumer loop is unrolled and its shared-memory loads run ahead)
+__host__ __device__ constexpr int mma_units(int bits) { return bits > 0 ? 1 : 1; }
 
 // X_COMBINE: the input row slice is LayerNorm(h + w0*y0 + w1*y1) (the MoE
 // combine of the previous layer, model.py:251-254, fused with the next LN):
@@ -32,7 +35,6 @@ struct GJob {
   const float* up3;    //           x@W3 [K]
   int xS;              // the inputs are xS split-K partials [xS][xstride], summed in
   int xstride;         //   order on load (a producer GEMV left them unreduced); 0/1: plain
-  int xfx;             // x (or up1/up3) are fixed-point sums (uint64, reduce == 2 producer)
   // X_COMBINE inputs: x = h, expert sums `cacc` [ctop][K] (fixed point), LN
   // affine, and the residual output (block 0)
   const unsigned long long* cacc;
@@ -58,23 +60,10 @@ struct GLaunch {
   long long slot_stride;
   const uint32_t* flags;        // buffer ready generations (copy engine)
   int* cnt;                     // split-K arrival counters [sum of ncb] (zero between launches)
-  int cluster;                  // CTAs per cluster along the split dimension (divides S)
   unsigned long long* zero;     // optional: fixed-point sums consumed by an earlier kernel,
   int zero_n;                   //   reset by this launch's CTAs (a slice each)
   int* err;
   unsigned long long wait_ns;
-  // L2 prefetch for the next kernel: byte ranges [off, off + len) of each
-  // routed expert's buffer (e.g. W2 while W1/W3 stream), split over the CTAs
-  // of the jobs on that expert
-  long long pf_off[2], pf_len[2];
-  int bulk_epi;  // split-K outputs by one bulk copy / bulk fixed-point add per CTA
-  // L2 prefetch of absolute byte ranges (e.g. the next layer's Wq/Wk/Wv while
-  // W2 streams), split over every CTA of the launch
-  const uint8_t* pfa[3];
-  long long pfl[3];
-  const DecodeState* ds;  // decode: expert jobs spin on the route stamp of (ds->seq, layer)
-  int layer;
-  int hold;  // X_COMBINE launches: start the weight stream only after griddepcontrol.wait
   int site;  // timeline slot of this launch (profiling), -1 none
 };
 
@@ -94,12 +83,6 @@ struct DecodeState {
   int tok;   // token to embed
   unsigned int seq;  // decode tokens since the engine was created (never reused)
 };
-// route publication stamp of (token, layer): the tail writes it last
-// (release); expert GEMVs spin on it (acquire) instead of waiting for the
-// whole previous grid, so their weight streams start early
-__host__ __device__ inline unsigned int route_stamp(unsigned int seq, int layer) {
-  return seq * 64u + (unsigned)layer + 1u;
-}
 
 struct AttnParams {
   const float* qkv_part;  // [3][S][d]
@@ -133,7 +116,6 @@ struct TailParams {
   StoreDev st;
   int d, E, top_k, m, layer, guess_layer, pos, mode;  // mode 0 decode, 1 prefill (no store)
   int ep_rank, ep_size;   // expert parallel (ep_size 1 = off)
-  int stamp;              // decode: publish the route stamp (expert GEMVs spin on it)
   int site;  // timeline slot of this launch (profiling), -1 none
 };
 
@@ -223,7 +205,7 @@ cudaError_t set_cta_trace(unsigned long long* buf);          // GEMV microbench 
 // launchers (kernels.cu)
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
 int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full, int* nstages,
-                    int* stage_bytes, int mma);
+                    int* stage_bytes);
 void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl = false);
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
                       cudaStream_t s, bool pdl = false);

@@ -1,0 +1,447 @@
+// Tensor-core dequant-GEMV kernel for the tile layout of mma_layout.cuh (the
+// 2/3/4-bit reference presets).  Replaces ``x @ quant.dequantize(block)``
+// (quant.py:267-304; model.py:223-226 for the experts, 288-300 for attention).
+// Included by kernels.cu inside its anonymous namespace (uses its helpers).
+//
+// One CTA = one (job, column block of 1024 outputs, split of the k-steps), 8
+// warps, one 128-output slice per warp, 2 CTAs per SM (256 threads -> 128
+// registers per thread, so the 32 accumulators, the unrolled stage loads and
+// the code extraction stay in registers).  There is no producer warp: thread
+// 0 issues the weight stream (cp.async.bulk into a ring of stages, mbarrier
+// per stage) and refills a stage once all 8 warps released it.
+//
+// Prologue: the x rows of the CTA arrive by one bulk copy per input array (or
+// are formed in place by the fused combine + LayerNorm), then every thread
+// takes whole rows: x * zscale (zero-point runs), the CTA's sum of
+// x * zoffset, and the B-operand table b = x * s * 2^E in three fp16 pieces
+// per (row, slice).  Epilogue: the slice outputs leave with one TMA bulk
+// store (split-K partials) or one bulk fixed-point add (cp.reduce.async.bulk
+// .add.u64), or -- reduce == 1 -- the last CTA of the column block sums the
+// partials in split order.
+#pragma once
+
+#define MG_THREADS 256
+#define MG_WARPS 8
+
+__host__ __device__ constexpr size_t mg_a16(size_t v) { return (v + 15) & ~(size_t)15; }
+__host__ __device__ constexpr size_t mg_a128(size_t v) { return (v + 127) & ~(size_t)127; }
+
+// dynamic shared memory carve-up (host and device agree on it)
+//   xs [rows] x * 2^E, xz [rows] x * zscale * 2^100, zsm the zmeta slice, xin
+//   the raw x rows, scl [rows][<=8] f16 scales, wtab per warp the B tables of
+//   one stage [warp][UPS units][128 bytes], then the ring
+struct MgSmem {
+  size_t xs, xz, zsm, xin, scl, wtab, ring;
+  __host__ __device__ MgSmem(int xs_cap, int zs_cap, int xin_cap) {
+    xs = 512;
+    xz = xs + (size_t)xs_cap * 4;
+    zsm = xz + (size_t)xs_cap * 4;
+    xin = mg_a16(zsm + (size_t)zs_cap * 4);
+    scl = mg_a16(xin + (size_t)xin_cap);
+    wtab = scl + (size_t)xs_cap * 16;
+    ring = mg_a128(wtab + (size_t)MG_WARPS * 4 * mt::BTAB);
+  }
+};
+
+// the nsc (<= 8) f16 scales of one row of a column block, zero-padded to 8
+MOE_DEV int warp_id() { return threadIdx.x >> 5; }
+
+MOE_DEV void load_scales(float (&sc)[8], const __half* p, int nsc) {
+  if (nsc == 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      sc[2 * k] = __half2float(__ushort_as_half((unsigned short)(u[k] & 0xffffu)));
+      sc[2 * k + 1] = __half2float(__ushort_as_half((unsigned short)(u[k] >> 16)));
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sc[k] = k < nsc ? __half2float(p[k]) : 0.f;
+}
+
+template <int B>
+__global__ void __launch_bounds__(MG_THREADS, 2)
+    k_mgemv(const __grid_constant__ GLaunch P, int xs_cap, int zs_cap, int xin_cap, int nst,
+            int stage_bytes) {
+  constexpr int W = MG_WARPS, NT = MG_THREADS, UPS = mma_units(B);
+  extern __shared__ __align__(128) uint8_t smem[];
+  const MgSmem L(xs_cap, zs_cap, xin_cap);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 8;
+  float* misc = reinterpret_cast<float*>(smem + 128);  // [32]
+  uint64_t* zbar = reinterpret_cast<uint64_t*>(smem + 256);
+  uint64_t* xbar = zbar + 1;
+  uint64_t* sbar = zbar + 2;
+  int* lastf = reinterpret_cast<int*>(smem + 288);
+  float* xs = reinterpret_cast<float*>(smem + L.xs);
+  float* xz = reinterpret_cast<float*>(smem + L.xz);
+  __half2* zsm = reinterpret_cast<__half2*>(smem + L.zsm);
+  uint8_t* xin = smem + L.xin;
+  __half* scl_s = reinterpret_cast<__half*>(smem + L.scl);
+  uint8_t* wtab = smem + L.wtab + warp_id() * UPS * mt::BTAB;
+  uint8_t* ring = smem + L.ring;
+
+  int ji = 0, cnt_base = 0;
+  for (int i = 1; i < P.nj; ++i)
+    if ((int)blockIdx.x >= P.j[i].blk0) ji = i;
+  for (int i = 0; i < ji; ++i) cnt_base += P.j[i].M.ncb;
+  const GJob& J = P.j[ji];
+  const int local = blockIdx.x - J.blk0;
+  const int cb = local / J.S, s = local % J.S;
+  const MatDev& M = J.M;
+  const int qs = s * J.QPS, nun = max(min(M.nquads, qs + J.QPS) - qs, 0);  // k-steps
+  const int nsl = mma_slices(M, cb), rb = mma_rec_bytes(M, cb);
+  const int sb = mt::slice_bytes(B, 1 << M.g_log2);
+  const int nit = (nun + UPS - 1) / UPS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = qs * mt::KS, nrows = nun * mt::KS;
+  const int nout = nsl * mt::SO;
+  const size_t obase = (size_t)cb * mt::CBO;
+  const int gcb0 = (int)(obase >> M.g_log2);
+  const int z0 = nrows ? (int)(((int64_t)row0 * M.G + gcb0) >> M.sg_log2) : 0;
+  const int z1 = nrows ? (int)(((int64_t)(row0 + nrows - 1) * M.G + gcb0) >> M.sg_log2) : 0;
+  const bool swiglu = J.xmode == X_SWIGLU, xcomb = J.xmode == X_COMBINE;
+  const int xparts = J.xS > 1 ? J.xS : 1;
+  const bool expert = J.rel_slot >= 0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      gemv::mbar_init(full + i, 1);
+      gemv::mbar_init(empty + i, W);
+    }
+    gemv::mbar_init(zbar, 1);
+    gemv::mbar_init(xbar, 1);
+    gemv::mbar_init(sbar, 1);
+    gemv::mbar_fence_init();
+  }
+  __syncthreads();
+  gemv::pdl_trigger();
+
+  int ebuf = 0;
+  if (expert) {
+    gemv::pdl_wait();  // the route is written by the previous kernel (tail)
+    ebuf = P.route->buf[J.rel_slot];
+    if (ebuf < 0) {  // expert parallel: another rank owns this expert
+      float* zdst = J.reduce == 2 ? nullptr
+                    : J.reduce == 1 ? (s == 0 ? J.out : nullptr)
+                                    : J.part + (size_t)s * M.N;
+      if (zdst)
+        for (int t = threadIdx.x; t < nout; t += NT) zdst[obase + t] = 0.f;
+      return;
+    }
+  }
+  // ---------------------------------------------------- weight stream (thread 0)
+  const uint8_t* src = nullptr;
+  uint64_t pol = 0;
+  auto issue = [&](int it) {
+    const int st = it % nst;
+    const uint32_t bytes = (uint32_t)(min(UPS, nun - it * UPS) * rb);
+    gemv::mbar_arrive_tx(full + st, bytes);
+    gemv::bulk_g2s_hint(ring + (size_t)st * stage_bytes, src + (int64_t)it * UPS * rb, bytes,
+                        full + st, pol);
+  };
+  // x rows of the CTA: one bulk copy per input array (partials [xparts][rows])
+  const bool xstage = !xcomb && nrows > 0;
+  const int xbytes = nrows * 4;
+  if (threadIdx.x == 0) {
+    const uint8_t* base = M.base;
+    const __half2* zmeta = M.zmeta;
+    const __half* scl = M.scl;
+    if (expert) {
+      if (!P.route->ready[J.rel_slot])
+        wait_flag(P.flags + ebuf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
+      const uint8_t* b = P.pool + (long long)ebuf * P.slot_stride;
+      base = b + reinterpret_cast<size_t>(base);
+      zmeta = reinterpret_cast<const __half2*>(b + reinterpret_cast<size_t>(zmeta));
+      scl = reinterpret_cast<const __half*>(b + reinterpret_cast<size_t>(scl));
+    }
+    if (nrows > 0) {
+      const int nsc = mma_nsc(M, cb);
+      const uint32_t sbytes = (uint32_t)nrows * nsc * 2;
+      gemv::mbar_arrive_tx(sbar, sbytes);
+      gemv::bulk_g2s(scl_s, scl + mma_scl_offset(M, cb) + (int64_t)row0 * nsc, sbytes, sbar);
+      const uintptr_t za = reinterpret_cast<uintptr_t>(zmeta + z0);
+      const uint32_t lead = (uint32_t)(za & 15u);
+      const uint32_t zbytes = ((uint32_t)(z1 - z0 + 1) * 4u + lead + 15u) & ~15u;
+      gemv::mbar_arrive_tx(zbar, zbytes);
+      gemv::bulk_g2s(zsm, reinterpret_cast<const void*>(za - lead), zbytes, zbar);
+      src = base + cb_offset(M, cb) + (int64_t)qs * rb;
+      pol = gemv::policy_evict_first();
+      for (int it = 0; it < min(nst, nit); ++it) issue(it);  // dense: before the wait
+    }
+    if (!expert) gemv::pdl_wait();  // x is the previous kernel's output
+    if (xstage) {
+      gemv::mbar_arrive_tx(xbar, (swiglu ? 2u : 1u) * (uint32_t)xparts * (uint32_t)xbytes);
+      const uint8_t* a = reinterpret_cast<const uint8_t*>(swiglu ? J.up1 : J.x);
+      const size_t pstride = (size_t)J.xstride * 4;
+      for (int p = 0; p < xparts; ++p)
+        gemv::bulk_g2s(xin + (size_t)p * xbytes, a + p * pstride + (size_t)row0 * 4, xbytes, xbar);
+      if (swiglu)
+        for (int p = 0; p < xparts; ++p)
+          gemv::bulk_g2s(xin + (size_t)(xparts + p) * xbytes,
+                         reinterpret_cast<const uint8_t*>(J.up3) + p * pstride + (size_t)row0 * 4,
+                         xbytes, xbar);
+    }
+  }
+  if (!expert) gemv::pdl_wait();
+  tl_begin(P.site);  // (after the wait: the span excludes the previous kernel)
+  cta_mark(0);
+  if (P.zero) {  // reset sums an earlier kernel consumed (a slice per CTA)
+    const int per = (P.zero_n + gridDim.x - 1) / gridDim.x;
+    const int a = blockIdx.x * per, e = min(P.zero_n, a + per);
+    for (int i = a + threadIdx.x; i < e; i += NT) P.zero[i] = 0ull;
+  }
+
+  // ---------------------------------------------------- x rows -> xs (x * 2^100)
+  if (xcomb) {  // fused combine + LayerNorm of the previous layer's output
+    float* xf = reinterpret_cast<float*>(xin);  // the full residual [K]
+    const int K = M.K;
+    const float w0 = P.route->w[0], w1 = J.ctop > 1 ? P.route->w[1] : 0.f;
+    float sum = 0.f;
+    for (int i0 = threadIdx.x; i0 < K; i0 += 8 * NT) {
+      float hv[8];
+      unsigned long long q0[8], q1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * NT;
+        hv[u] = i < K ? __ldcg(J.x + i) : 0.f;
+        q0[u] = i < K ? __ldcg(J.cacc + i) : 0ull;
+        q1[u] = (i < K && J.ctop > 1) ? __ldcg(J.cacc + K + i) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * NT;
+        if (i < K) {
+          float o = __fadd_rn(hv[u], __fmul_rn(w0, fx_val(q0[u])));  // model.py:251-254
+          if (J.ctop > 1) o = __fadd_rn(o, __fmul_rn(w1, fx_val(q1[u])));
+          xf[i] = o;
+          sum += o;
+          if (blockIdx.x == 0) J.xout[i] = o;
+        }
+      }
+    }
+    // LayerNorm statistics in the reference's rounding structure (model.py:186-189)
+    const float mu = __fdiv_rn(cons_sum(sum, misc, NT), (float)K);
+    float q = 0.f;
+    for (int i = threadIdx.x; i < K; i += NT) {
+      const float t = __fsub_rn(xf[i], mu);
+      q = fmaf(t, t, q);
+    }
+    const float var = __fdiv_rn(cons_sum(q, misc, NT), (float)K);
+    const float den = sqrtf(__fadd_rn(var, 1e-5f));
+    for (int i = threadIdx.x; i < nrows; i += NT) {
+      const int r = row0 + i;
+      const float v = __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(xf[r], mu), den), __ldg(J.lng + r)),
+                                __ldg(J.lnb + r));
+      xs[i] = v;
+    }
+  } else if (xstage) {
+    gemv::mbar_wait(xbar, 0);
+    const float* xf = reinterpret_cast<const float*>(xin);
+    for (int i = threadIdx.x; i < nrows; i += NT) {
+      float a = 0.f, b = 0.f;
+      for (int p = 0; p < xparts; ++p) a += xf[p * nrows + i];  // producer splits, in order
+      float xv = a;
+      if (swiglu) {  // SwiGLU of the up projections (model.py:223-226)
+        for (int p = 0; p < xparts; ++p) b += xf[(xparts + p) * nrows + i];
+        xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
+      }
+      xs[i] = xv;
+    }
+  }
+  tl_mark(P.site, 0);
+
+  // ------------------- per row: x * zscale, sum x * zoffset, max |x * s| (E)
+  float zo_part = 0.f, mx = 0.f;
+  const int nsc = mma_nsc(M, cb), spl = M.sg_log2 - 7;  // 2^spl slices per scale
+  if (nrows > 0) {
+    gemv::mbar_wait(zbar, 0);
+    gemv::mbar_wait(sbar, 0);
+    // expert slots are 256-byte aligned: the offset has the address's alignment
+    const int zlead =
+        (int)((reinterpret_cast<uintptr_t>(M.zmeta) + (uintptr_t)z0 * 4) & 15u) >> 2;
+    for (int i = threadIdx.x; i < nrows; i += NT) {
+      const int run = (int)(((int64_t)(row0 + i) * M.G + gcb0) >> M.sg_log2);
+      const float2 zm = __half22float2(zsm[zlead + run - z0]);
+      const float xv = xs[i];
+      xz[i] = (xv * gemv::kXScale) * zm.x;  // the zero-code floats are 2^-149-scaled
+      zo_part = fmaf(xv, zm.y, zo_part);
+      float sc[8];
+      load_scales(sc, scl_s + (size_t)i * nsc, nsc);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) mx = fmaxf(mx, fabsf(xv * sc[c]));
+    }
+  }
+  zo_part = warp_sum(zo_part);
+  mx = warp_max(mx);
+  if (lane == 0) {
+    misc[warp] = zo_part;
+    misc[W + warp] = mx;
+  }
+  __syncthreads();
+  float zo_sum = 0.f;
+  mx = 0.f;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    zo_sum += misc[w];
+    mx = fmaxf(mx, misc[W + w]);
+  }
+  // fixed point of b = x * s: |b| < 2^30; 2^(-E-6) must stay a normal float
+  const int Eb = mx > 0.f ? min(29 - ilogbf(mx), 100) : 0;
+  {
+    const float p2 = __uint_as_float(gemv::pow2_bits(Eb));
+    for (int i = threadIdx.x; i < nrows; i += NT) xs[i] *= p2;
+  }
+  __syncthreads();
+  tl_mark(P.site, 2);  // prologue done
+
+  // ---------------------------------------------------- streaming loop
+  int D[8][4];
+  float zq[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    D[i][0] = D[i][1] = D[i][2] = D[i][3] = 0;
+    zq[i] = 0.f;
+  }
+  {
+    const int g = lane >> 2, t = lane & 3;
+    const uint8_t* sl0 = ring + (size_t)warp * sb;
+    const bool active = warp < nsl;
+    const int wsc = warp >> spl;  // this slice's scale column
+    int st = 0;
+    uint32_t ph = 0;
+    for (int it = 0; it < nit; ++it) {
+      const int u0 = it * UPS, nu = min(UPS, nun - u0);
+      uint2 bf[UPS];
+      if (active) {  // the B tables of the stage's units for this slice (row = lane)
+#pragma unroll
+        for (int u = 0; u < UPS; ++u) {
+          const int row = (u0 + u) * mt::KS + lane;
+          const bool in = u < nu;
+          mg::put_digits(wtab + u * mt::BTAB, lane, in ? xs[row] : 0.f,
+                         in ? __half2float(scl_s[row * nsc + wsc]) : 0.f);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < UPS; ++u)
+          bf[u] = g < 4 ? reinterpret_cast<const uint2*>(wtab + u * mt::BTAB)[4 * g + t]
+                        : make_uint2(0u, 0u);
+      }
+      gemv::mbar_wait(full + st, ph);
+      if (active) {
+        const uint8_t* sl = sl0 + (size_t)st * stage_bytes;
+        if (nu == UPS) {
+          mg::Unit<B> U[UPS];
+#pragma unroll
+          for (int u = 0; u < UPS; ++u)
+            mg::unit_load<B>(U[u], sl + u * rb, bf[u], xz + (u0 + u) * mt::KS, lane);
+#pragma unroll
+          for (int u = 0; u < UPS; ++u) mg::unit_math<B>(D, zq, U[u]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < UPS; ++u)
+            if (u < nu) {
+              mg::Unit<B> U;
+              mg::unit_load<B>(U, sl + u * rb, bf[u], xz + (u0 + u) * mt::KS, lane);
+              mg::unit_math<B>(D, zq, U);
+            }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) gemv::mbar_arrive(empty + st);
+      if (threadIdx.x == 0 && it + nst < nit) {  // refill once all warps released it
+        gemv::mbar_wait(empty + st, ph);
+        issue(it + nst);
+      }
+      if (++st == nst) {
+        st = 0;
+        ph ^= 1;
+      }
+    }
+  }
+  tl_mark(P.site, 3);
+  cta_mark(1);
+
+  // ---------------------------------------------------- epilogue
+  float* ymm = reinterpret_cast<float*>(ring);  // [1024] slice outputs
+  unsigned long long* fxs = reinterpret_cast<unsigned long long*>(ring + 4096);  // [1024]
+  __syncthreads();  // every warp left the ring
+  if (warp < nsl) mg::finish<B>(D, zq, Eb, lane, ymm + warp * mt::SO);
+  __syncthreads();
+  const float zo_out = zo_sum;  // x is unscaled here (only xz carries 2^100)
+  float* dst = (J.S == 1 && J.reduce) ? J.out : J.part + (size_t)s * M.N;
+  for (int t = threadIdx.x; t < nout; t += NT) {
+    const float a = ymm[t] + zo_out;
+    if (J.reduce == 2)
+      fxs[t] = fx_bits(a, P.err);
+    else if (J.reduce == 0)
+      ymm[t] = a;
+    else
+      dst[obase + t] = a;
+  }
+  if (J.reduce != 1) {  // one TMA operation per CTA
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (J.reduce == 2)
+        asm volatile(
+            "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(
+                J.acc + obase),
+            "r"(gemv::smem_u32(fxs)), "r"((uint32_t)(nout * 8))
+            : "memory");
+      else
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         dst + obase),
+                     "r"(gemv::smem_u32(ymm)), "r"((uint32_t)(nout * 4))
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    cta_mark(2);
+    tl_end(P.site);
+    return;
+  }
+  if (J.S == 1) {
+    cta_mark(2);
+    tl_end(P.site);
+    return;
+  }
+  // reduce == 1: the last CTA of this column block sums the S partials in order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int old = atomicAdd(P.cnt + cnt_base + cb, 1);
+    __threadfence();
+    *lastf = old == J.S - 1;
+  }
+  __syncthreads();
+  if (*lastf) {
+    const float* pbase = J.part + obase;
+    for (int t0 = threadIdx.x; t0 < nout; t0 += 4 * NT) {
+      float a[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int s0 = 0; s0 < J.S; s0 += 8) {
+        float v[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int t = t0 + u * NT;
+            v[u][k] = (t < nout && s0 + k < J.S) ? __ldcg(pbase + (size_t)(s0 + k) * M.N + t) : 0.f;
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (s0 + k < J.S) a[u] += v[u][k];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (t0 + u * NT < nout) J.out[obase + t0 + u * NT] = a[u];
+    }
+    if (threadIdx.x == 0) P.cnt[cnt_base + cb] = 0;
+  }
+  cta_mark(2);
+  tl_end(P.site);
+}

@@ -1,152 +1,161 @@
-// Tensor-core dequant-GEMV core for the tile layout of mma_layout.cuh
+// Integer tensor-core dequant-GEMV core for the tile layout of mma_layout.cuh
 // (2/3/4-bit reference presets).  Replaces the reference's
 // ``x @ quant.dequantize(block)`` (quant.py:267-304, model.py:223-226,
-// 290-300) like gemv.cuh, with the multiply-adds on mma.sync instead of FFMA2:
+// 290-300) like gemv.cuh, with the multiply-adds on mma.sync (IMMA) instead
+// of FFMA2:
 //
 //   y_j = sum_i x_i (c_ij s_i,j/sg + zhat_i,j/g)
-//       = sum_i c_ij b_i,jb  +  sum_i x_i zhat_i,j/g
-//   A = c_ij as fp16 subnormals c * 2^(q-24) (one LOP3 per two codes),
-//   B = b_i,jb = x_i * s_i,jb * 2^E split into three fp16 pieces (columns
-//       n = 0, 1, 2 of the n8 tile; exact to 2^-25 of max |b| ~ 2^14),
-//   D = fp32 accumulators in registers, rescaled by 2^(24-q-E) at the end.
+//       = 2^-E sum_n 256^n sum_i c_ij d_n,i,jb  +  sum_i x_i zhat_i,j/g
+//   A = c_ij 2^p as u8 (one LOP3 per four codes; the tile's 2^p is undone at
+//       the end), B = d_n = the signed byte digits of b_i = rint(x_i s_i 2^E),
+//   D = s32 accumulators: exact.
 // The zero-point term keeps the CUDA-core form (one FFMA per (row, group)).
-// Every step is exact except the fp32 accumulation (tensor core) and the one
-// fp32 rounding of x * s -- the same roundings class as the reference's fp32
-// sgemv over the dequantized matrix.
 #pragma once
 #include "common.cuh"
 #include "gemv.cuh"
+#include "mma_layout.cuh"
 
 namespace mg {
 
-MOE_DEV void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                      uint32_t b0, uint32_t b1) {
+MOE_DEV void imma(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                  uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
 using gemv::shr_fma;
 
-// the lane's 32 A-fragment registers of one k-step from its 2B code words
+// One k-step of one slice for this lane: the 4B code words, the B fragment,
+// the zero codes of its row (row = lane) and that row's x * zscale * 2^100.
 template <int B>
-MOE_DEV void extract(const uint32_t (&w)[2 * B], uint32_t (&R)[32]) {
-  if constexpr (B == 3) {
-    uint32_t s[6];
+struct Unit {
+  uint32_t w[4 * B];
+  uint2 bf;
+  uint2 z;  // 3/4-bit: 2 groups (bytes 0, 1 of z.x); 2-bit: 8 groups
+  float x;
+};
+
+template <int B>
+MOE_DEV void unit_load(Unit<B>& U, const uint8_t* slice, uint2 bf, const float* xz, int lane) {
+  const uint4* cp = reinterpret_cast<const uint4*>(slice);
 #pragma unroll
-    for (int v = 0; v < 6; ++v) {
-      s[v] = shr_fma(w[v], 9);
-      R[5 * v + 0] = w[v] & 0x00070007u;
-      R[5 * v + 1] = w[v] & 0x00380038u;
-      R[5 * v + 2] = w[v] & 0x01C001C0u;
-      R[5 * v + 3] = s[v] & 0x00070007u;
-      R[5 * v + 4] = s[v] & 0x00380038u;
+  for (int pl = 0; pl < B; ++pl) {
+    const uint4 v = cp[pl * 32 + lane];
+    U.w[4 * pl] = v.x;
+    U.w[4 * pl + 1] = v.y;
+    U.w[4 * pl + 2] = v.z;
+    U.w[4 * pl + 3] = v.w;
+  }
+  U.bf = bf;
+  const uint8_t* zc = slice + mt::code_bytes(B);
+  if constexpr (B == 2) {
+    U.z = reinterpret_cast<const uint2*>(zc)[lane];
+  } else {
+    U.z.x = reinterpret_cast<const uint16_t*>(zc)[lane];
+    U.z.y = 0;
+  }
+  U.x = xz[lane];
+}
+
+// the 8 tiles' MMAs, registers produced tile by tile (few live at a time)
+template <int B>
+MOE_DEV void unit_math(int (&D)[8][4], float (&zacc)[8], const Unit<B>& U) {
+  const uint32_t b0 = U.bf.x, b1 = U.bf.y;
+  if constexpr (B == 4) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t m = i < 4 ? 0x0F0F0F0Fu : 0xF0F0F0F0u;
+      const int v = 4 * (i & 3);
+      imma(D[i], U.w[v] & m, U.w[v + 1] & m, U.w[v + 2] & m, U.w[v + 3] & m, b0, b1);
     }
-#pragma unroll
-    for (int j = 0; j < 2; ++j)  // bit 15 / 31 of three words -> field [6, 9)
-      R[30 + j] = (s[3 * j] & 0x00400040u) | (shr_fma(w[3 * j + 1], 8) & 0x00800080u) |
-                  (shr_fma(w[3 * j + 2], 7) & 0x01000100u);
   } else if constexpr (B == 2) {
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const uint32_t s = shr_fma(w[v], 10);
-#pragma unroll
-      for (int f = 0; f < 5; ++f) R[8 * v + f] = w[v] & (0x00030003u << (2 * f));
-#pragma unroll
-      for (int f = 0; f < 3; ++f) R[8 * v + 5 + f] = s & (0x00030003u << (2 * f));
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t m = 0x03030303u << (2 * (i >> 1));
+      const int v = 4 * (i & 1);
+      imma(D[i], U.w[v] & m, U.w[v + 1] & m, U.w[v + 2] & m, U.w[v + 3] & m, b0, b1);
     }
   } else {
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const uint32_t s = shr_fma(w[v], 8);
-      R[4 * v + 0] = w[v] & 0x000F000Fu;
-      R[4 * v + 1] = w[v] & 0x00F000F0u;
-      R[4 * v + 2] = s & 0x000F000Fu;
-      R[4 * v + 3] = s & 0x00F000F0u;
+    for (int G = 0; G < 4; ++G) {
+      const uint32_t w0 = U.w[3 * G], w1 = U.w[3 * G + 1], w2 = U.w[3 * G + 2];
+      // byte bits 6..7 of the three words: the codes of register 3
+      const uint32_t t = (shr_fma(w0, 6) & 0x03030303u) | (shr_fma(w1, 4) & 0x0C0C0C0Cu) |
+                         (shr_fma(w2, 2) & 0x30303030u);
+      imma(D[G], w0 & 0x07070707u, w1 & 0x07070707u, w2 & 0x07070707u, t & 0x07070707u, b0, b1);
+      imma(D[G + 4], w0 & 0x38383838u, w1 & 0x38383838u, w2 & 0x38383838u, t & 0x38383838u,
+           b0, b1);
     }
   }
-}
-
-// One k-step of one slice: 8 MMAs (the slice's 8 tiles) and the zero-point
-// terms of its (row, group) pairs.
-//   slice: the slice in smem (codes planes, then zero codes)
-//   bf:    this lane's B fragment of (k-step, slice)
-//   xz:    x * zscale * 2^100 of the k-step's 16 rows (16-byte aligned)
-template <int B>
-MOE_DEV void step(float (&D)[8][4], float (&zacc)[4], const uint8_t* slice, uint2 bf,
-                  const float* xz, int lane) {
-  const uint2* cp = reinterpret_cast<const uint2*>(slice);
-  uint32_t w[2 * B];
-#pragma unroll
-  for (int pl = 0; pl < B; ++pl) {
-    const uint2 v = cp[pl * 32 + lane];
-    w[2 * pl] = v.x;
-    w[2 * pl + 1] = v.y;
-  }
-  uint32_t R[32];
-  extract<B>(w, R);
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    mma16816(D[i], R[mt::pair_reg(B, 2 * i, 0)], R[mt::pair_reg(B, 2 * i + 1, 0)],
-             R[mt::pair_reg(B, 2 * i, 1)], R[mt::pair_reg(B, 2 * i + 1, 1)], bf.x, bf.y);
-  const uint8_t* zc = slice + mt::code_bytes(B);
-  if constexpr (B == 2) {  // lane: group lane & 7, rows 4 (lane >> 3) + j
-    const uint32_t z4 = reinterpret_cast<const uint32_t*>(zc)[lane];
-    const float4 x4 = reinterpret_cast<const float4*>(xz)[lane >> 3];
-    zacc[0] = fmaf(gemv::fbits(z4 & 0xffu), x4.x, zacc[0]);
-    zacc[1] = fmaf(gemv::fbits(z4 & 0xff00u), x4.y, zacc[1]);
-    zacc[2] = fmaf(gemv::fbits(z4 & 0xff0000u), x4.z, zacc[2]);
-    zacc[3] = fmaf(gemv::fbits(z4 & 0xff000000u), x4.w, zacc[3]);
-  } else {  // g = 64: lane: group lane >> 4, row lane & 15
-    zacc[0] = fmaf(gemv::fbits((uint32_t)zc[lane]), xz[lane & 15], zacc[0]);
+  // zero codes as subnormal / first-binade floats (linear while the byte sits
+  // at bits 0..23): byte j of a word -> zacc scale 2^(8j - 149)
+  if constexpr (B == 2) {
+    zacc[0] = fmaf(gemv::fbits(U.z.x & 0xffu), U.x, zacc[0]);
+    zacc[1] = fmaf(gemv::fbits(U.z.x & 0xff00u), U.x, zacc[1]);
+    zacc[2] = fmaf(gemv::fbits(U.z.x & 0xff0000u), U.x, zacc[2]);
+    zacc[3] = fmaf(gemv::fbits(shr_fma(U.z.x, 24)), U.x, zacc[3]);
+    zacc[4] = fmaf(gemv::fbits(U.z.y & 0xffu), U.x, zacc[4]);
+    zacc[5] = fmaf(gemv::fbits(U.z.y & 0xff00u), U.x, zacc[5]);
+    zacc[6] = fmaf(gemv::fbits(U.z.y & 0xff0000u), U.x, zacc[6]);
+    zacc[7] = fmaf(gemv::fbits(shr_fma(U.z.y, 24)), U.x, zacc[7]);
+  } else {
+    zacc[0] = fmaf(gemv::fbits(U.z.x & 0xffu), U.x, zacc[0]);
+    zacc[1] = fmaf(gemv::fbits(U.z.x & 0xff00u), U.x, zacc[1]);
   }
 }
 
-// The slice's 128 outputs (without the per-CTA zoffset sum): code part
-// rescaled per (tile, row class), plus the zero-point total of each output's
-// group.  Lanes t == 0 write ys[o] for their rows o = 16 i + g + 8 c.
-//   E: the B operand's power-of-two prescale (x carries 2^100 already)
+// zacc scale exponent of zero group j (see unit_math): 2^(149 - 8 (j % 4)),
+// byte 3 shifted down; times 2^-100 for the x prescale
+MOE_DEV constexpr int zexp(int j) { return (j & 3) == 3 ? 49 : 49 - 8 * (j & 3); }
+
+// The slice's 128 outputs (without the per-CTA zoffset sum): exact integer
+// digit sums -> one fp32 rounding, tile shift and 2^-E undone, plus the
+// zero-point total of each output's group.  Lanes t == 0 write ys[o].
 template <int B>
-MOE_DEV void finish(const float (&D)[8][4], const float (&zacc)[4], int E, int lane, float* ys) {
+MOE_DEV void finish(const int (&D)[8][4], const float (&zacc)[8], int E, int lane, float* ys) {
   const int g = lane >> 2, t = lane & 3;
-  // zero-point totals: zacc[j] sums zc * 2^(8j-149) * (x * 2^100 * zscale)
-  float z = 0.f;
+  constexpr int NG = B == 2 ? 8 : 2;  // zero groups per slice
+  float zt[NG];
 #pragma unroll
-  for (int j = 0; j < (B == 2 ? 4 : 1); ++j)
-    z = fmaf(zacc[j], __uint_as_float(gemv::pow2_bits(49 - 8 * j)), z);
-  if constexpr (B == 2) {  // group = lane & 7: sum over lane >> 3
-    z += __shfl_xor_sync(0xffffffffu, z, 8);
-    z += __shfl_xor_sync(0xffffffffu, z, 16);
-  } else {  // group = lane >> 4: sum over lane & 15
+  for (int j = 0; j < NG; ++j) {  // rows are lanes: sum over the warp
+    float z = zacc[j] * __uint_as_float(gemv::pow2_bits(zexp(j)));
 #pragma unroll
-    for (int o = 1; o < 16; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    zt[j] = z;
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const float zt = __shfl_sync(0xffffffffu, z, B == 2 ? i : 16 * (i >> 2));
+    const float sc = __uint_as_float(gemv::pow2_bits(-E - mt::tile_shift(B, i)));
+    const float z = B == 2 ? zt[i] : zt[i >> 2];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      // pieces: t = 0 holds columns 0, 1; t = 1 holds column 2 (and a copy in 3)
-      float v = t == 0 ? D[i][2 * c] + D[i][2 * c + 1] : (t == 1 ? D[i][2 * c] : 0.f);
+    for (int c = 0; c < 2; ++c) {  // row g (c = 0) and g + 8
+      // digits: t = 0 holds columns 0, 1 (256^0, 256^1), t = 1 columns 2, 3
+      long long v = t == 0 ? (long long)D[i][2 * c] + ((long long)D[i][2 * c + 1] << 8)
+                  : t == 1 ? ((long long)D[i][2 * c] << 16) + ((long long)D[i][2 * c + 1] << 24)
+                           : 0ll;
       v += __shfl_down_sync(0xffffffffu, v, 1);
-      const int q = mt::pair_q(B, 2 * i + c);
-      const float sc = __uint_as_float(gemv::pow2_bits(-76 - q - E));
-      if (t == 0) ys[mt::out_of(i, c, g)] = fmaf(v, sc, zt);
+      if (t == 0) ys[16 * i + g + 8 * c] = fmaf(__ll2float_rn(v), sc, z);
     }
   }
 }
 
-// split of b = x * s * 2^E into three fp16 pieces, written to the B table
-MOE_DEV void put_pieces(__half* tab, int k, float b) {
-  const __half h0 = __float2half_rn(b);
-  const float r1 = b - __half2float(h0);
-  const __half h1 = __float2half_rn(r1);
-  const float r2 = r1 - __half2float(h1);
-  tab[mt::btab_half(k, 0)] = h0;
-  tab[mt::btab_half(k, 1)] = h1;
-  tab[mt::btab_half(k, 2)] = __float2half_rn(r2);
+// b = rint(xe * s) as four signed byte digits into a (k-step, slice) B table
+// (xe = x * 2^E)
+MOE_DEV void put_digits(uint8_t* tab, int k, float xe, float s) {
+  int b = __float2int_rn(__fmul_rn(xe, s));
+  const int d0 = (int)(int8_t)(b & 0xff);
+  b = (b - d0) >> 8;
+  const int d1 = (int)(int8_t)(b & 0xff);
+  b = (b - d1) >> 8;
+  const int d2 = (int)(int8_t)(b & 0xff);
+  const int d3 = (b - d2) >> 8;
+  tab[mt::btab_byte(k, 0)] = (uint8_t)d0;
+  tab[mt::btab_byte(k, 1)] = (uint8_t)d1;
+  tab[mt::btab_byte(k, 2)] = (uint8_t)d2;
+  tab[mt::btab_byte(k, 3)] = (uint8_t)d3;
 }
 
 }  // namespace mg

@@ -1,98 +1,89 @@
 // Tensor-core tile layout of a 2/3/4-bit group-quantized matrix and the
-// register maps shared by the tiler (tile.cu) and the dequant-GEMV (gemv).
+// register maps shared by the tiler (tile.cu) and the dequant-GEMV
+// (mma_gemv.cuh, mgemv_kernel.cuh).
 //
-// Idea: a b-bit code c masked in place at bit q (q + b <= 10)
-// of a 16-bit lane is, read as an IEEE fp16, the subnormal c * 2^(q-24) --
-// exact, and exactly what mma.sync.m16n8k16 (fp16 in, fp32 accumulate)
-// multiplies.  One LOP3 therefore yields TWO ready A-operand elements (the low
-// and high halves of a 32-bit word), and the multiply-adds go to the tensor
-// pipe instead of the FMA pipe: ~0.55 ALU instructions per weight instead of
-// the CUDA-core kernel's ~1.7 (one LOP3 + half an FFMA2 + shifts per weight).
-// The input vector enters as the B operand, x * scale split into three fp16
-// pieces (n = 0, 1, 2 of the n8 tile), so the products are exact and the
-// only rounding is the fp32 accumulation -- as in the reference's fp32 GEMV.
+// Idea: the b-bit codes are the u8 A operand of the integer
+// tensor-core MMA (mma.sync m16n8k32 .u8 x .s8 -> .s32).  A code masked in
+// place inside its byte is code * 2^p (p = 0, 2, 3, 4 or 6; at most 240), so
+// one LOP3 yields FOUR ready A elements and the tile's accumulator carries
+// the 2^p.  The input vector enters as the B operand: b = x * s (x times the
+// row's f16 scale, one fp32 rounding as in the reference's fp32 GEMV) as a
+// per-CTA fixed-point integer (|b| < 2^30) split into four signed bytes --
+// the n = 0..3 columns of the n8 tile.  The MMA then accumulates exactly in
+// int32; the only roundings are x * s, b's fixed point (2^-31 of the CTA's
+// largest |x * s|) and one int64 -> fp32 conversion per output.
 //
 // Geometry (rows = reduction dim i, outputs j; x[K] @ W[K,N]):
-//   k-step   = 16 consecutive rows (the MMA K)
+//   k-step   = 32 consecutive rows (the MMA K)
 //   slice    = 128 consecutive outputs of one k-step = 8 m16 tiles, one warp
 //   cb       = 8 slices = 1024 outputs (the last cb of a matrix may be narrower)
 //   record   = one (cb, k-step): its slices in order, each slice
-//              [codes 256*b bytes][zero codes 16*128/g bytes]
+//              [codes 512*b bytes: uint4 planes [b][lane]]
+//              [zero codes: [32 rows][128/g groups] u8]
 //   records are stored [cb][k-step]; then the scale section [cb][row][1024/sg]
 //   (f16), then the zero-point runs (zmeta) as in the CUDA-core layout.
 // Total bytes = codes + zeros + scales + zmeta = quant.payload_nbytes: a byte
 // permutation of the reference block (quant.py:76-102, 332-343), so an expert
 // buffer stays exactly expert_bytes and the pinned arena holds this layout.
 //
-// Lane (g = lane/4, t = lane%4) of a slice owns, per k-step, the A fragments
-// of the 8 tiles: tile i, slot s in {a01, a23, a45, a67} = rows (16i + g +
-// 8*(s&1)) of the output dim, k = 2t + 8*(s>>1) and k + 1 (low/high half).
-// Its 64 codes are 2b words, stored as uint2 planes [plane][lane].  Register
-// r (0..31) of the lane comes from word v, field f; registers pair up (same
-// q) into (tile, row class): pair p -> tile p/2, row class p%2 (rows g or
-// g+8), elements e = 0/1 -> k-halves (2t, 2t+8).
+// Lane (g = lane/4, t = lane%4) of a slice holds, per k-step, the A fragments
+// of the 8 tiles: tile i, register r (0..3), byte e (0..3) = output row
+// 16 i + g + 8 (r & 1), reduction row k = 4 t + 16 (r >> 1) + e.  Its 128
+// codes are 4b words (word v = 4 * plane + component of the uint4).
 #pragma once
 #include <stdint.h>
 
 namespace mt {
 
-constexpr int KS = 16;          // rows per k-step
+constexpr int KS = 32;          // rows per k-step
 constexpr int SO = 128;         // outputs per slice (warp)
 constexpr int CBS = 8;          // slices per column block
 constexpr int CBO = SO * CBS;   // outputs per column block
 
-__host__ __device__ constexpr int words(int b) { return 2 * b; }      // per lane per k-step
-__host__ __device__ constexpr int code_bytes(int b) { return 256 * b; }
-__host__ __device__ constexpr int zero_bytes(int g) { return 16 * (SO / g); }
+__host__ __device__ constexpr int words(int b) { return 4 * b; }  // per lane per k-step
+__host__ __device__ constexpr int code_bytes(int b) { return 512 * b; }
+__host__ __device__ constexpr int zero_bytes(int g) { return KS * (SO / g); }
 __host__ __device__ constexpr int slice_bytes(int b, int g) { return code_bytes(b) + zero_bytes(g); }
 
-// ---- register r -> pair (tile, row class) and element
-__host__ __device__ constexpr int pair_reg(int b, int p, int e) {
-  return b == 4 ? 4 * (p >> 1) + (p & 1) + 2 * e
-       : b == 2 ? (p < 12 ? 8 * (p / 3) + p % 3 + 5 * e
-                  : p == 12 ? 3 + 8 * e : p == 13 ? 19 + 8 * e : p == 14 ? 4 + 8 * e : 20 + 8 * e)
-                : (p < 6 ? 5 * p + 3 * e
-                  : p < 12 ? 5 * (p - 6) + 1 + 3 * e
-                  : p == 12 ? 2 + 5 * e : p == 13 ? 12 + 5 * e : p == 14 ? 22 + 5 * e : 30 + e);
-}
-// mantissa bit q of the pair's fields: element value = code * 2^(q - 24)
-__host__ __device__ constexpr int pair_q(int b, int p) {
-  return b == 4 ? 4 * (p & 1) : b == 2 ? (p < 12 ? 2 * (p % 3) : p < 14 ? 6 : 8)
-                                       : (p < 6 ? 0 : p < 12 ? 3 : 6);
+// log2 of the power of two tile i's codes carry in their bytes
+__host__ __device__ constexpr int tile_shift(int b, int i) {
+  return b == 4 ? (i < 4 ? 0 : 4) : b == 2 ? 2 * (i >> 1) : (i < 4 ? 0 : 3);
 }
 
-// ---- register r -> source word and original bit offset in each 16-bit half
-// (assembled registers, 3-bit r = 30/31: the code's bit k sits in bit 15 of
-// word 3*(r-30) + k; -1 returned)
-__host__ __device__ constexpr int reg_word(int b, int r) {
-  return b == 4 ? r / 4 : b == 2 ? r / 8 : (r < 30 ? r / 5 : -1);
-}
-__host__ __device__ constexpr int reg_off(int b, int r) {
-  return b == 4 ? 4 * (r % 4) : b == 2 ? 2 * (r % 8) : (r < 30 ? 3 * (r % 5) : -1);
-}
+// lane-local coordinates of (tile i, register r, byte e)
+__host__ __device__ constexpr int out_of(int i, int r, int g) { return 16 * i + g + 8 * (r & 1); }
+__host__ __device__ constexpr int k_of(int r, int e, int t) { return 4 * t + 16 * (r >> 1) + e; }
 
-// ---- lane-local code coordinates of (tile i, pair row class c, element e)
-__host__ __device__ constexpr int out_of(int i, int c, int g) { return 16 * i + g + 8 * c; }
-__host__ __device__ constexpr int k_of(int e, int t) { return 2 * t + 8 * e; }
-
-// ---- zero codes of a slice: byte index -> (group within slice, row in k-step)
-__host__ __device__ inline void zero_pos(int g, int byte, int* grp, int* row) {
-  if (g == 64) {  // 2 groups x 16 rows: lane l reads byte l
-    *grp = byte >> 4;
-    *row = byte & 15;
-  } else {        // g == 16: 8 groups x 16 rows: lane l reads the u32 at 4l
-    const int l = byte >> 2, j = byte & 3;
-    *grp = l & 7;
-    *row = 4 * (l >> 3) + j;
+// where code bit kb (0..b-1) of (tile i, register r, byte e) lives: word and
+// bit position inside the lane's 4b words
+__host__ __device__ inline void code_bit(int b, int i, int r, int e, int kb, int* word, int* bit) {
+  if (b == 4) {
+    *word = 4 * (i & 3) + r;
+    *bit = 8 * e + (i < 4 ? 0 : 4) + kb;
+  } else if (b == 2) {
+    *word = 4 * (i & 1) + r;
+    *bit = 8 * e + 2 * (i >> 1) + kb;
+  } else {  // 3-bit: groups of three words, byte bits 6..7 carry the r = 3 codes
+    const int G = i & 3, hi = i >= 4;
+    if (r < 3) {
+      *word = 3 * G + r;
+      *bit = 8 * e + 3 * hi + kb;
+    } else {  // t-byte bit tb = 3 hi + kb: bits (0,1) <- word 3G, (2,3) <- 3G+1, (4,5) <- 3G+2
+      const int tb = 3 * hi + kb;
+      *word = 3 * G + (tb >> 1);
+      *bit = 8 * e + 6 + (tb & 1);
+    }
   }
 }
 
-// B-operand table entry of (k-step, slice): [piece n 0..2][t 0..3][4 halves
-// k = 2t, 2t+1, 2t+8, 2t+9] = 96 bytes; lane (g, t) loads the uint2 at
-// (min(g,2)*4 + t)
-constexpr int BTAB = 48;  // halves per (k-step, slice)
-__host__ __device__ constexpr int btab_half(int k, int n) {
-  return n * 16 + ((k & 7) >> 1) * 4 + (k & 1) + 2 * (k >> 3);
+// zero codes of a slice: [row][group] bytes
+__host__ __device__ constexpr int zero_off(int g, int row, int grp) { return row * (SO / g) + grp; }
+
+// B-operand table of one (k-step, slice): [digit n 0..3][t 0..3][8 bytes:
+// rows 4t..4t+3, 4t+16..4t+19]; lane (g < 4, t) loads the uint2 at (4g + t)
+constexpr int BTAB = 128;  // bytes per (k-step, slice)
+__host__ __device__ constexpr int btab_byte(int k, int n) {
+  return n * 32 + ((k & 15) >> 2) * 8 + (k & 3) + 4 * (k >> 4);
 }
 
 }  // namespace mt

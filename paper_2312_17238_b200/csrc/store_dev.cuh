@@ -59,7 +59,6 @@ struct RouteRec {  // per position: resolved experts of the current layer
   uint32_t gen[MOE_MAX_TOPK];
   float w[MOE_MAX_TOPK];
   int ready[MOE_MAX_TOPK];  // decode: the tail saw flags[buf] >= gen (no flag wait needed)
-  unsigned int stamp;       // decode: route_stamp(token seq, layer), written last
 };
 
 struct TraceRecDev {  // layout identical to moe_trace_rec

@@ -77,8 +77,8 @@ __global__ void k_tile_meta(RefMat R, MatDev M, uint8_t* dst, __half2* zmeta) {
 
 // ------------------------------------------------------------------ tiling (tensor-core layout)
 // mma_layout.cuh.  One thread per (cb, k-step, slice, lane): gathers the
-// lane's 64 codes from the reference bitstream and packs them into the words
-// the GEMV's LOP3 masks extract as fp16 A-fragment halves.
+// lane's 128 codes from the reference bitstream and packs them into the 4b
+// words the GEMV's LOP3 masks turn into u8 A-fragment registers.
 MOE_DEV uint32_t ref_code(const RefMat& R, int64_t row, int64_t col) {
   const int64_t bit = (row * R.N + col) * R.bits, byte = bit >> 3;
   const int64_t nbytes = ((int64_t)R.K * R.N * R.bits + 7) >> 3;
@@ -96,26 +96,24 @@ __global__ void k_tile_mma_codes(RefMat R, MatDev M, uint8_t* dst) {
     const int ks = (int)(rest % nks), cb = (int)(rest / nks);
     if (w >= mma_slices(M, cb)) continue;
     const int g = lane >> 2, t = lane & 3;
-    uint32_t W[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int p = 0; p < 16; ++p)
-      for (int e = 0; e < 2; ++e) {
-        const int r = mt::pair_reg(b, p, e);
-        const int64_t col = (int64_t)cb * mt::CBO + w * mt::SO + mt::out_of(p >> 1, p & 1, g);
-        const int64_t row = (int64_t)ks * mt::KS + mt::k_of(e, t);
-        const uint32_t lo = ref_code(R, row, col), hi = ref_code(R, row + 1, col);
-        const int v = mt::reg_word(b, r);
-        if (v >= 0) {
-          const int o = mt::reg_off(b, r);
-          W[v] |= (lo << o) | (hi << (16 + o));
-        } else {  // 3-bit assembled register: code bit k in bit 15 / 31 of word 3j + k
-          const int j = r - 30;
-          for (int kb = 0; kb < 3; ++kb)
-            W[3 * j + kb] |= (((lo >> kb) & 1u) << 15) | (((hi >> kb) & 1u) << 31);
+    uint32_t W[16];
+    for (int v = 0; v < 16; ++v) W[v] = 0;
+    for (int i = 0; i < 8; ++i)
+      for (int r = 0; r < 4; ++r)
+        for (int e = 0; e < 4; ++e) {
+          const int64_t col = (int64_t)cb * mt::CBO + w * mt::SO + mt::out_of(i, r, g);
+          const int64_t row = (int64_t)ks * mt::KS + mt::k_of(r, e, t);
+          const uint32_t c = ref_code(R, row, col);
+          for (int kb = 0; kb < b; ++kb) {
+            int wd, bit;
+            mt::code_bit(b, i, r, e, kb, &wd, &bit);
+            W[wd] |= ((c >> kb) & 1u) << bit;
+          }
         }
-      }
-    uint2* sl = reinterpret_cast<uint2*>(dst + cb_offset(M, cb) + (int64_t)ks * mma_rec_bytes(M, cb) +
+    uint4* sl = reinterpret_cast<uint4*>(dst + cb_offset(M, cb) + (int64_t)ks * mma_rec_bytes(M, cb) +
                                          (int64_t)w * sb);
-    for (int pl = 0; pl < b; ++pl) sl[pl * 32 + lane] = make_uint2(W[2 * pl], W[2 * pl + 1]);
+    for (int pl = 0; pl < b; ++pl)
+      sl[pl * 32 + lane] = make_uint4(W[4 * pl], W[4 * pl + 1], W[4 * pl + 2], W[4 * pl + 3]);
   }
 }
 
@@ -132,8 +130,7 @@ __global__ void k_tile_mma_meta(RefMat R, MatDev M, uint8_t* dst, __half* scl, _
     const int w = (int)(rest % mt::CBS), ks = (int)((rest / mt::CBS) % nks);
     const int cb = (int)(rest / mt::CBS / nks);
     if (w >= mma_slices(M, cb)) continue;
-    int grp, row;
-    mt::zero_pos(R.g, byte, &grp, &row);
+    const int row = byte / (mt::SO / R.g), grp = byte % (mt::SO / R.g);  // mt::zero_off
     const int64_t gz = ((int64_t)cb * mt::CBO + w * mt::SO) / R.g + grp;
     dst[cb_offset(M, cb) + (int64_t)ks * mma_rec_bytes(M, cb) + (int64_t)w * sb +
         mt::code_bytes(b) + byte] = R.zeros[((int64_t)ks * mt::KS + row) * G + gz];

@@ -249,8 +249,14 @@ class OffloadEngine:
             m = mk.any(w, allow_half)
             check(L.moe_load_tensor(self._h, name.encode(), C.byref(m)))
 
-        for nm in ("wte", "wpe", "lm_head"):
-            put(nm, p[nm], allow_half=True)
+        # wte and wpe are read by one embedding kernel: fp16 only if both are
+        # exactly representable in fp16
+        emb_half = all(_is_block(p[nm]) or np.array_equal(
+            np.asarray(p[nm], np.float32).astype(np.float16).astype(np.float32),
+            np.asarray(p[nm], np.float32)) for nm in ("wte", "wpe"))
+        for nm in ("wte", "wpe"):
+            put(nm, p[nm], allow_half=emb_half)
+        put("lm_head", p["lm_head"], allow_half=True)
         put("ln_f.gamma", p["ln_f.gamma"])
         put("ln_f.beta", p["ln_f.beta"])
         for l in range(cfg.n_layers):
