@@ -13,7 +13,8 @@ import os
 from .errors import NonFiniteError, QuantFormatError, UnknownExpertError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmoeb200.so")
+# MOE_LIB_PATH: an A/B build of the same sources (tools/ab_build.sh), profiling only
+LIB_PATH = os.environ.get("MOE_LIB_PATH") or os.path.join(HERE, "libmoeb200.so")
 
 MOE_OK, MOE_ERR_VALUE, MOE_ERR_RUNTIME, MOE_ERR_NONFINITE = 0, 1, 2, 3
 MOE_ERR_UNKNOWN_EXPERT, MOE_ERR_FORMAT, MOE_ERR_CUDA, MOE_ERR_TIMEOUT = 4, 5, 6, 7

@@ -449,6 +449,16 @@ struct moe_engine {
     return MOE_OK;
   }
   int run_copier();
+  // batched prefill (tensor-core layout, one GPU): buffers for PB positions
+  int PB = 0;
+  float *pf_xn = nullptr, *pf_ctx = nullptr, *pf_up = nullptr;
+  unsigned long long *pf_qkv_acc = nullptr, *pf_wo_acc = nullptr, *pf_dn_acc = nullptr;
+  int2* pf_cols = nullptr;       // device: [PB] identity, then up / down column tables
+  int2* pf_cols_h = nullptr;     // pinned staging of the expert column tables
+  RouteRec* pf_route_h = nullptr;  // pinned: the layer's routes (read after bookkeeping)
+  bool batched_prefill_ok() const;
+  int prefill_alloc();
+  int prefill_batched(int n);
   int enq_attention(int l, int p, int mode);
   int enq_experts(int l, int p);
   int enq_logits(int p, float* out);
@@ -506,6 +516,11 @@ moe_engine::~moe_engine() {
   if (mb_host) cudaFreeHost(mb_host);
   if (t0) cudaEventDestroy(t0);
   if (t1) cudaEventDestroy(t1);
+  for (void* p : {(void*)pf_xn, (void*)pf_ctx, (void*)pf_up, (void*)pf_qkv_acc,
+                  (void*)pf_wo_acc, (void*)pf_dn_acc, (void*)pf_cols})
+    if (p) cudaFree(p);
+  if (pf_cols_h) cudaFreeHost(pf_cols_h);
+  if (pf_route_h) cudaFreeHost(pf_route_h);
   if (s_comp) cudaStreamDestroy(s_comp);
   if (s_copy) cudaStreamDestroy(s_copy);
   if (s_copy2) cudaStreamDestroy(s_copy2);
@@ -641,7 +656,7 @@ static int finalize_launch(GLaunch& P) {
   int blk = 0;
   for (int i = 0; i < P.nj; ++i) {
     P.j[i].blk0 = blk;
-    blk += P.j[i].M.ncb * P.j[i].S;
+    blk += P.j[i].M.ncb * P.j[i].S * (P.j[i].ncg > 1 ? P.j[i].ncg : 1);
   }
   return blk;
 }
@@ -874,6 +889,269 @@ int moe_engine::enq_experts(int l, int p) {
     dbg("combine", -1, p);
   }
   unit_done();
+  return MOE_OK;
+}
+
+// ---------------------------------------------------------------- batched prefill
+// The reference encodes a prompt layer by layer (model.py:343-367): attention
+// of every position, the gates, one store resolution of the layer
+// (engine.py:233-240: each distinct expert acquired once), then every
+// position's MoE.  On B200 every weight byte of a layer is streamed once per
+// group of MG_PREFILL_COLS positions: the Q/K/V and Wo GEMVs take the
+// positions as input columns, and the expert GEMVs take, per distinct routed
+// expert, the (position, slot) pairs that chose it.  Each column is computed
+// exactly like the decode kernel computes it (same split geometry and
+// fixed-point sums), so prefill equals teacher-forced decode bit for bit.
+bool moe_engine::batched_prefill_ok() const {
+  if (ep_world > 1 || !xl_set) return false;
+  if (const char* v = getenv("MOE_PREFILL_BATCH"))
+    if (atoi(v) == 0) return false;
+  if (attn_bits > 4 || expert_bits > 4) return false;
+  for (int l = 0; l < L; ++l)
+    if (!wq[l].M.mma || !wk[l].M.mma || !wv[l].M.mma || !wo[l].M.mma) return false;
+  for (int m = 0; m < 3; ++m)
+    if (!matdev_from(xl[m], nullptr).mma) return false;
+  return true;
+}
+
+int moe_engine::prefill_alloc() {
+  if (PB) return MOE_OK;
+  const int pb = std::min(T, 64);
+  int rc;
+  if ((rc = dalloc(&pf_xn, (size_t)pb * d))) return rc;
+  if ((rc = dalloc(&pf_ctx, (size_t)pb * d))) return rc;
+  if ((rc = dalloc(&pf_up, (size_t)pb * topk * 2 * S_up * f))) return rc;
+  if ((rc = dalloc(&pf_qkv_acc, (size_t)pb * 3 * d))) return rc;
+  if ((rc = dalloc(&pf_wo_acc, (size_t)pb * d))) return rc;
+  if ((rc = dalloc(&pf_dn_acc, (size_t)pb * topk * d))) return rc;
+  if ((rc = dalloc(&pf_cols, (size_t)pb * (1 + 2 * topk)))) return rc;
+  CU(cudaHostAlloc(&pf_cols_h, (size_t)pb * 2 * topk * sizeof(int2), cudaHostAllocDefault));
+  CU(cudaHostAlloc(&pf_route_h, (size_t)T * sizeof(RouteRec), cudaHostAllocDefault));
+  std::vector<int2> id(pb);
+  for (int i = 0; i < pb; ++i) id[i] = make_int2(i, i);
+  CU(cudaMemcpy(pf_cols, id.data(), pb * sizeof(int2), cudaMemcpyHostToDevice));
+  PB = pb;
+  return MOE_OK;
+}
+
+int moe_engine::prefill_batched(int n) {
+  int rc = prefill_alloc();
+  if (rc) return rc;
+  const int NCc = MG_PREFILL_COLS;
+  auto dense_cols = [&](GJob& J, int nc, long long xcs, long long ocs) {
+    J.cols = pf_cols;
+    J.ncol = nc;
+    J.ncg = (nc + NCc - 1) / NCc;
+    J.xcs = xcs;
+    J.ocs = ocs;
+  };
+  int2* up_cols = pf_cols + PB;
+  int2* dn_cols = up_cols + (size_t)PB * topk;
+  for (int l = 0; l < L; ++l) {
+    // ---- attention of every position, chunk by chunk
+    for (int c0 = 0; c0 < n; c0 += PB) {
+      const int nc = std::min(PB, n - c0);
+      launch_layernorm_rows(x + (size_t)c0 * d, ln1g[l], ln1b[l], pf_xn, d, nc, s_comp);
+      GLaunch q{};
+      q.nj = 3;
+      q.cnt = cnt;
+      q.site = -1;
+      q.err = err;
+      const DevMat* W[3] = {&wq[l], &wk[l], &wv[l]};
+      for (int i = 0; i < 3; ++i) {
+        q.j[i] = dense_job(*W[i], pf_xn, qkv_part, qkv_out, Q_qkv);
+        q.j[i].reduce = 2;
+        q.j[i].acc = pf_qkv_acc + (size_t)i * d;
+        dense_cols(q.j[i], nc, d, 3LL * d);
+      }
+      launch_gemv_cols(attn_bits, q, finalize_launch(q), s_comp);
+      for (int i = 0; i < nc; ++i) {
+        AttnParams a{};
+        a.qkv_part = qkv_part;
+        a.S = S_qkv;
+        a.acc = pf_qkv_acc + (size_t)i * 3 * d;
+        a.kc = kc + (size_t)l * T * d;
+        a.vc = vc + (size_t)l * T * d;
+        a.ctx = pf_ctx + (size_t)i * d;
+        a.site = -1;
+        a.pos = c0 + i;
+        a.H = H;
+        a.hd = hd;
+        a.d = d;
+        a.T_max = T;
+        launch_attention(a, s_comp, false);
+      }
+      GLaunch o{};
+      o.nj = 1;
+      o.cnt = cnt;
+      o.site = -1;
+      o.err = err;
+      o.j[0] = dense_job(wo[l], pf_ctx, wo_part, wo_out, Q_wo);
+      o.j[0].reduce = 2;
+      o.j[0].acc = pf_wo_acc;
+      dense_cols(o.j[0], nc, d, d);
+      launch_gemv_cols(attn_bits, o, finalize_launch(o), s_comp);
+      for (int i = 0; i < nc; ++i) {
+        const int p = c0 + i;
+        TailParams t{};
+        t.x = x + (size_t)p * d;
+        t.part = wo_out;
+        t.S = 1;
+        t.acc = pf_wo_acc + (size_t)i * d;
+        t.g2 = ln2g[l];
+        t.b2 = ln2b[l];
+        t.gate_l = gate[l];
+        t.gh_l = gate_h[l];
+        t.guess_layer = -1;
+        t.h = h + (size_t)p * d;
+        t.route = route + p;
+        t.trace = trace;
+        t.trace_hidden = rec_hidden ? trace_hidden : nullptr;
+        t.n_layers = L;
+        t.site = -1;
+        t.st = st;
+        t.d = d;
+        t.E = E;
+        t.top_k = topk;
+        t.layer = l;
+        t.pos = p;
+        t.mode = 1;
+        t.ep_size = 1;
+        if (tail_smem_bytes(t) > 226 * 1024) t.gh_l = t.gh_g = nullptr;
+        launch_tail(t, s_comp, false);
+      }
+      dbg("prefill attention", l, c0);
+    }
+    // ---- one store resolution of the layer (store.py acquire per distinct expert)
+    PrefillBKParams pb{};
+    pb.route = route;
+    pb.st = st;
+    pb.layer = l;
+    pb.n = n;
+    pb.top_k = topk;
+    launch_prefill_bk(pb, s_comp);
+    CU(cudaMemcpyAsync(pf_route_h, route, (size_t)n * sizeof(RouteRec), cudaMemcpyDeviceToHost,
+                       s_comp));
+    CU(cudaStreamSynchronize(s_comp));
+    // ---- the experts, grouped by buffer (= distinct expert), chunk by chunk
+    for (int c0 = 0; c0 < n; c0 += PB) {
+      const int nc = std::min(PB, n - c0);
+      std::vector<int> bufs;                 // distinct buffers in first-use order
+      std::vector<std::vector<int2>> refs;   // per buffer: (position, slot)
+      for (int i = 0; i < nc; ++i)
+        for (int j = 0; j < topk; ++j) {
+          const int b = pf_route_h[c0 + i].buf[j];
+          if (b < 0) continue;  // error raised by the bookkeeping / not owned
+          size_t k = 0;
+          while (k < bufs.size() && bufs[k] != b) ++k;
+          if (k == bufs.size()) {
+            bufs.push_back(b);
+            refs.emplace_back();
+          }
+          refs[k].push_back(make_int2(c0 + i, j));
+        }
+      // column tables: up (h row, slot column), down (slot column twice)
+      std::vector<int> first(bufs.size());
+      size_t ncols = 0;
+      for (size_t k = 0; k < bufs.size(); ++k) {
+        first[k] = (int)ncols;
+        for (const int2& r : refs[k]) {
+          const int q = (r.x - c0) * topk + r.y;
+          pf_cols_h[ncols] = make_int2(r.x, q);
+          pf_cols_h[(size_t)PB * topk + ncols] = make_int2(q, q);
+          ++ncols;
+        }
+      }
+      if (ncols) {
+        CU(cudaMemcpyAsync(up_cols, pf_cols_h, ncols * sizeof(int2), cudaMemcpyHostToDevice,
+                           s_comp));
+        CU(cudaMemcpyAsync(dn_cols, pf_cols_h + (size_t)PB * topk, ncols * sizeof(int2),
+                           cudaMemcpyHostToDevice, s_comp));
+      }
+      const long long upcs = 2LL * S_up * f;  // floats per (position, slot) of pf_up
+      auto expert_job = [&](GJob& J, int m, size_t k) {
+        J = GJob{};
+        J.M = matdev_from(xl[m], reinterpret_cast<const uint8_t*>(xoff[m][0]));
+        J.M.zmeta = reinterpret_cast<const __half2*>(xoff[m][3]);
+        J.M.scl = reinterpret_cast<const __half*>(xoff[m][1]);
+        J.rel_pos = refs[k][0].x;
+        J.rel_slot = refs[k][0].y;
+        J.ncol = (int)refs[k].size();
+        J.ncg = (J.ncol + NCc - 1) / NCc;
+      };
+      // W1 || W3 (split-K partials), four experts per launch
+      for (size_t k0 = 0; k0 < bufs.size(); k0 += MOE_GEMV_MAXJOBS / 2) {
+        GLaunch u{};
+        u.route = route;
+        u.pool = pool;
+        u.slot_stride = slot_stride;
+        u.flags = flags;
+        u.err = err;
+        u.wait_ns = wait_ns;
+        u.cnt = cnt;
+        u.site = -1;
+        for (size_t k = k0; k < std::min(bufs.size(), k0 + MOE_GEMV_MAXJOBS / 2); ++k)
+          for (int m = 0; m < 2; ++m) {
+            GJob& J = u.j[u.nj++];
+            expert_job(J, m, k);
+            J.xmode = X_PLAIN;
+            J.x = h;
+            J.xcs = d;
+            J.cols = up_cols + first[k];
+            J.part = pf_up + (size_t)m * S_up * f;
+            J.ocs = upcs;
+            J.reduce = 0;
+            J.QPS = Q_up;
+            J.S = S_up;
+          }
+        launch_gemv_cols(expert_bits, u, finalize_launch(u), s_comp);
+      }
+      // W2 with the SwiGLU prologue (fixed-point sums per (position, slot))
+      for (size_t k0 = 0; k0 < bufs.size(); k0 += MOE_GEMV_MAXJOBS) {
+        GLaunch dn{};
+        dn.route = route;
+        dn.pool = pool;
+        dn.slot_stride = slot_stride;
+        dn.flags = flags;
+        dn.err = err;
+        dn.wait_ns = wait_ns;
+        dn.cnt = cnt;
+        dn.site = -1;
+        for (size_t k = k0; k < std::min(bufs.size(), k0 + MOE_GEMV_MAXJOBS); ++k) {
+          GJob& J = dn.j[dn.nj++];
+          expert_job(J, 2, k);
+          J.xmode = X_SWIGLU;
+          J.up1 = pf_up;
+          J.up3 = pf_up + (size_t)S_up * f;
+          J.xcs = upcs;
+          J.xstride = f;
+          J.xS = S_up;
+          J.cols = dn_cols + first[k];
+          J.acc = pf_dn_acc;
+          J.ocs = d;
+          J.reduce = 2;
+          J.QPS = Q_dn;
+          J.S = S_dn;
+        }
+        launch_gemv_cols(expert_bits, dn, finalize_launch(dn), s_comp);
+      }
+      for (int i = 0; i < nc; ++i) {
+        const int p = c0 + i;
+        CombineParams c{};
+        c.h = h + (size_t)p * d;
+        c.part = dn_out;
+        c.S = 1;
+        c.acc = pf_dn_acc + (size_t)i * topk * d;
+        c.route = route + p;
+        c.out = x + (size_t)p * d;
+        c.d = d;
+        c.top_k = topk;
+        c.site = -1;
+        launch_combine(c, s_comp, false);
+      }
+      dbg("prefill experts", l, c0);
+    }
+  }
   return MOE_OK;
 }
 
@@ -1549,6 +1827,10 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
     ep.site = 0;
     launch_embed(ep, e->s_comp, e->pdl);
   }
+  if (e->batched_prefill_ok()) {
+    rc = e->prefill_batched(n);
+    if (rc) return rc;
+  } else {
   for (int l = 0; l < e->L; ++l) {
     for (int p = 0; p < n; ++p) e->enq_attention(l, p, 1);
     PrefillBKParams pb{};
@@ -1560,6 +1842,7 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
     launch_prefill_bk(pb, e->s_comp);
     e->dbg("prefill_bk", l, n);
     for (int p = 0; p < n; ++p) e->enq_experts(l, p);
+  }
   }
   for (int p = 0; p < n; ++p) e->enq_logits(p, e->logits + (size_t)p * e->V);
   e->launches = launch_count() - c0;

@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(1024) k_layernorm(const float* x, const float*
   __shared__ float red[33];
   gemv::pdl_trigger();
   gemv::pdl_wait();
-  layernorm_block(x, g, b, y, nullptr, d, red);
+  layernorm_block(x + (size_t)blockIdx.x * d, g, b, y + (size_t)blockIdx.x * d, nullptr, d, red);
 }
 
 // ------------------------------------------------------------------ attention
@@ -1560,8 +1560,11 @@ cudaError_t preload_kernels() {
                        (const void*)k_layernorm, (const void*)k_attention, (const void*)k_tail,
                        (const void*)k_prefill_bk, (const void*)k_begin_call,
                        (const void*)k_combine,   (const void*)k_logits, (const void*)k_wait_ready,
-                       (const void*)k_exchange, (const void*)k_mgemv<2>,
-                       (const void*)k_mgemv<3>, (const void*)k_mgemv<4>};
+                       (const void*)k_exchange, (const void*)k_mgemv<2, 1>,
+                       (const void*)k_mgemv<3, 1>, (const void*)k_mgemv<4, 1>,
+                       (const void*)k_mgemv<2, MG_PREFILL_NM>,
+                       (const void*)k_mgemv<3, MG_PREFILL_NM>,
+                       (const void*)k_mgemv<4, MG_PREFILL_NM>};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -1572,10 +1575,13 @@ cudaError_t preload_kernels() {
     if (e != cudaSuccess) return e;
   }
   for (const void* f : {(const void*)k_embed, (const void*)k_combine,
-                        (const void*)k_attention128, (const void*)k_mgemv<2>,
-                        (const void*)k_mgemv<3>, (const void*)k_mgemv<4>}) {
+                        (const void*)k_attention128, (const void*)k_mgemv<2, 1>,
+                        (const void*)k_mgemv<3, 1>, (const void*)k_mgemv<4, 1>,
+                        (const void*)k_mgemv<2, MG_PREFILL_NM>,
+                        (const void*)k_mgemv<3, MG_PREFILL_NM>,
+                        (const void*)k_mgemv<4, MG_PREFILL_NM>}) {
     cudaError_t e2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          200 * 1024);
+                                          224 * 1024);
     if (e2 != cudaSuccess) return e2;
   }
   cudaError_t e = cudaFuncSetAttribute((const void*)k_attention,
@@ -1664,8 +1670,9 @@ static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pd
 
 // tensor-core layout (k_mgemv): x staging for every job (the full residual for
 // the fused combine), the zmeta slice, scales + B table, then the ring
-template <int B>
+template <int B, int NM>
 static void launch_mgemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
+  constexpr int NC = mg_cols(NM);
   int xs_cap = 0, rbf = 0, xin_cap = 0;
   for (int i = 0; i < P.nj; ++i) {
     const GJob& J = P.j[i];
@@ -1676,11 +1683,13 @@ static void launch_mgemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool p
     xin_cap = max(xin_cap, J.xmode == X_COMBINE ? J.M.K * 4 : n * 4 * rows);
   }
   const int zs_cap = gemv_zs_cap(P, B, xs_cap, rbf, 1);
-  const MgSmem L(xs_cap, zs_cap, xin_cap);
+  const MgSmem L(xs_cap, zs_cap, xin_cap, NM);
   const int stage = mma_units(B) * rbf;
-  int nst = (int)((MOE_GEMV_SMEM_CAP - (long long)L.ring) / stage);
+  // 2 CTAs per SM for decode; the batched kernel runs 1 CTA per SM
+  const long long cap = NM == 1 ? MOE_GEMV_SMEM_CAP : 220 * 1024;
+  int nst = (int)((cap - (long long)L.ring) / stage);
   nst = nst < 2 ? 2 : (nst > 8 ? 8 : nst);
-  const int ring = max(nst * stage, 12 * 1024);
+  const int ring = max(nst * stage, NC * 12 * 1024);  // the epilogue reuses the ring
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nblocks);
   cfg.blockDim = dim3(MG_THREADS);
@@ -1691,16 +1700,16 @@ static void launch_mgemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool p
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_mgemv<B>, P, xs_cap, zs_cap, xin_cap, nst, stage);
+  cudaLaunchKernelEx(&cfg, k_mgemv<B, NM>, P, xs_cap, zs_cap, xin_cap, nst, stage);
   g_launches.fetch_add(1);
 }
 
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
   if (bits <= 4 && P.j[0].M.mma) {
     switch (bits) {
-      case 2: launch_mgemv_t<2>(P, nblocks, s, pdl); return;
-      case 3: launch_mgemv_t<3>(P, nblocks, s, pdl); return;
-      default: launch_mgemv_t<4>(P, nblocks, s, pdl); return;
+      case 2: launch_mgemv_t<2, 1>(P, nblocks, s, pdl); return;
+      case 3: launch_mgemv_t<3, 1>(P, nblocks, s, pdl); return;
+      default: launch_mgemv_t<4, 1>(P, nblocks, s, pdl); return;
     }
   }
   switch (bits) {
@@ -1709,6 +1718,15 @@ void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool p
     case 4: launch_gemv_t<4>(P, nblocks, s, pdl); break;
     case 16: launch_gemv_t<16>(P, nblocks, s, pdl); break;
     default: launch_gemv_t<32>(P, nblocks, s, pdl); break;
+  }
+}
+
+// batched prefill: MG_PREFILL_NM column groups (2 columns each) per CTA
+void launch_gemv_cols(int bits, const GLaunch& P, int nblocks, cudaStream_t s) {
+  switch (bits) {
+    case 2: launch_mgemv_t<2, MG_PREFILL_NM>(P, nblocks, s, false); return;
+    case 3: launch_mgemv_t<3, MG_PREFILL_NM>(P, nblocks, s, false); return;
+    default: launch_mgemv_t<4, MG_PREFILL_NM>(P, nblocks, s, false); return;
   }
 }
 
@@ -1737,6 +1755,11 @@ void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl) {
     launch_small(k_embed, dim3(1), dim3(1024), (size_t)P.d * 12, s, pdl, P);
   else
     launch_small(k_embed, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
+}
+
+void launch_layernorm_rows(const float* x, const float* g, const float* b, float* y, int d,
+                          int rows, cudaStream_t s) {
+  launch_small(k_layernorm, dim3(rows), dim3(1024), 0, s, false, x, g, b, y, d);
 }
 
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,

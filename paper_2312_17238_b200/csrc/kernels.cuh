@@ -15,10 +15,13 @@ __host__ __device__ constexpr int gemv_qs(int bits) { return MOE_GEMV_WARPS * ge
 #define MOE_GEMV_RING (80 * 1024)  // bytes of stage ring per CTA (2 CTAs / SM)
 #define MOE_XS_MAX 4096            // rows of x kept in smem per CTA
 #define MOE_GEMV_SMEM_CAP (112 * 1024)  // dynamic smem per CTA at 2 CTAs / SM
+#ifndef MOE_UPS3
+#define MOE_UPS3 1
+#endif
 #define MOE_MMA_UNITS_MAX 64       // k-steps per CTA in the tensor-core layout (B table)
 // k-steps per pipeline stage of the tensor-core layout (a compile-time count so
 // the consumer loop is unrolled and its shared-memory loads run ahead)
-__host__ __device__ constexpr int mma_units(int bits) { return bits > 0 ? 1 : 1; }
+__host__ __device__ constexpr int mma_units(int bits) { return bits == 3 ? MOE_UPS3 : 1; }
 
 // X_COMBINE: the input row slice is LayerNorm(h + w0*y0 + w1*y1) (the MoE
 // combine of the previous layer, model.py:251-254, fused with the next LN):
@@ -48,6 +51,15 @@ struct GJob {
                        //   2: every CTA adds its partial into `acc` in fixed point
   unsigned long long* acc;  // reduce == 2: [N] int64 sums, 2^-32 units (consumer zeroes)
   int S, QPS, blk0;    // splits of the quad range, quads per split (multiple of QS)
+  // batched prefill (tensor-core layout): `ncol` input columns, (input index,
+  // output index) pairs in device memory; column c reads x (up1/up3) at
+  // + in * xcs floats and writes part/acc at + out * ocs.  cols == null: the
+  // single decode column (indices 0).  ncg = column groups of the launch's
+  // columns per CTA (the grid covers ncb * S * ncg CTAs of this job).
+  const int2* cols;
+  int ncol, ncg;
+  long long xcs, ocs;
+  int rel_pos;         // expert jobs: the route is P.route[rel_pos] (decode: 0)
 };
 
 struct DecodeState;
@@ -204,11 +216,19 @@ cudaError_t set_cta_trace(unsigned long long* buf);          // GEMV microbench 
 
 // launchers (kernels.cu)
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
+// batched prefill (tensor-core layout only): jobs with `cols`, MG_PREFILL_COLS
+// input columns per CTA
+#define MG_PREFILL_NM 2
+#define MG_PREFILL_COLS (2 * MG_PREFILL_NM)
+void launch_gemv_cols(int bits, const GLaunch& P, int nblocks, cudaStream_t s);
 int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full, int* nstages,
                     int* stage_bytes);
 void launch_embed(const EmbedParams& P, cudaStream_t s, bool pdl = false);
 void launch_layernorm(const float* x, const float* g, const float* b, float* y, int d,
                       cudaStream_t s, bool pdl = false);
+// one CTA per row: y[r] = LN(x[r]) for r < rows (batched prefill)
+void launch_layernorm_rows(const float* x, const float* g, const float* b, float* y, int d,
+                           int rows, cudaStream_t s);
 void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl = false);
 void launch_tail(const TailParams& P, cudaStream_t s, bool pdl = false);
 int tail_smem_bytes(const TailParams& P);

@@ -3,21 +3,29 @@
 // (quant.py:267-304; model.py:223-226 for the experts, 288-300 for attention).
 // Included by kernels.cu inside its anonymous namespace (uses its helpers).
 //
-// One CTA = one (job, column block of 1024 outputs, split of the k-steps), 8
-// warps, one 128-output slice per warp, 2 CTAs per SM (256 threads -> 128
-// registers per thread, so the 32 accumulators, the unrolled stage loads and
-// the code extraction stay in registers).  There is no producer warp: thread
-// 0 issues the weight stream (cp.async.bulk into a ring of stages, mbarrier
-// per stage) and refills a stage once all 8 warps released it.
+// One CTA = one (job, column group, column block of 1024 outputs, split of
+// the k-steps), 8 warps, one 128-output slice per warp.  Decode (NM = 1): one
+// input column, 2 CTAs per SM (256 threads -> 128 registers per thread, so
+// the 32 accumulators, the unrolled stage loads and the code extraction stay
+// in registers).  Batched prefill (NM >= 2): NC = 2 NM input columns (prompt
+// positions) per CTA share every weight byte -- each k-step's A fragments feed
+// NM MMAs whose n8 tiles hold two columns' four digits each -- 1 CTA per SM.
+// A column's arithmetic is exactly the decode kernel's (same split geometry,
+// same per-CTA exponent, exact integer accumulation), so batched prefill
+// equals teacher-forced decode bit for bit.
 //
-// Prologue: the x rows of the CTA arrive by one bulk copy per input array (or
-// are formed in place by the fused combine + LayerNorm), then every thread
-// takes whole rows: x * zscale (zero-point runs), the CTA's sum of
-// x * zoffset, and the B-operand table b = x * s * 2^E in three fp16 pieces
-// per (row, slice).  Epilogue: the slice outputs leave with one TMA bulk
-// store (split-K partials) or one bulk fixed-point add (cp.reduce.async.bulk
-// .add.u64), or -- reduce == 1 -- the last CTA of the column block sums the
-// partials in split order.
+// There is no producer warp: thread 0 issues the weight stream (cp.async.bulk
+// into a ring of stages, mbarrier per stage) and refills a stage once all 8
+// warps released it.
+//
+// Prologue: the x rows of the CTA arrive by one bulk copy per input array and
+// column (or are formed in place by the fused combine + LayerNorm), then every
+// thread takes whole rows: x * zscale (zero-point runs), the CTA's sum of
+// x * zoffset, and the B-operand table b = x * s * 2^E as four signed byte
+// digits per (row, slice).  Epilogue: the slice outputs leave with one TMA
+// bulk store (split-K partials) or one bulk fixed-point add
+// (cp.reduce.async.bulk .add.u64) per column, or -- reduce == 1, decode only
+// -- the last CTA of the column block sums the partials in split order.
 #pragma once
 
 #define MG_THREADS 256
@@ -25,21 +33,25 @@
 
 __host__ __device__ constexpr size_t mg_a16(size_t v) { return (v + 15) & ~(size_t)15; }
 __host__ __device__ constexpr size_t mg_a128(size_t v) { return (v + 127) & ~(size_t)127; }
+__host__ __device__ constexpr int mg_cols(int nm) { return nm == 1 ? 1 : 2 * nm; }
+__host__ __device__ constexpr int mg_tab_bytes(int nm) { return nm == 1 ? mt::BTAB : 2 * mt::BTAB; }
 
 // dynamic shared memory carve-up (host and device agree on it)
-//   xs [rows] x * 2^E, xz [rows] x * zscale * 2^100, zsm the zmeta slice, xin
-//   the raw x rows, scl [rows][<=8] f16 scales, wtab per warp the B tables of
-//   one stage [warp][UPS units][128 bytes], then the ring
+//   header (barriers, reduction scratch), then per input column: xs [rows]
+//   x * 2^E, xz [rows] x * zscale * 2^100; zsm the zmeta slice, xin the raw x
+//   rows (xin_cap bytes per column), scl [rows][<=8] f16 scales, wtab per warp
+//   the B tables of one stage [warp][UPS][NM][table], then the ring
 struct MgSmem {
   size_t xs, xz, zsm, xin, scl, wtab, ring;
-  __host__ __device__ MgSmem(int xs_cap, int zs_cap, int xin_cap) {
-    xs = 512;
-    xz = xs + (size_t)xs_cap * 4;
-    zsm = xz + (size_t)xs_cap * 4;
+  __host__ __device__ MgSmem(int xs_cap, int zs_cap, int xin_cap, int nm = 1) {
+    const int nc = mg_cols(nm);
+    xs = 1024;
+    xz = xs + (size_t)nc * xs_cap * 4;
+    zsm = xz + (size_t)nc * xs_cap * 4;
     xin = mg_a16(zsm + (size_t)zs_cap * 4);
-    scl = mg_a16(xin + (size_t)xin_cap);
+    scl = mg_a16(xin + (size_t)nc * xin_cap);
     wtab = scl + (size_t)xs_cap * 16;
-    ring = mg_a128(wtab + (size_t)MG_WARPS * 4 * mt::BTAB);
+    ring = mg_a128(wtab + (size_t)MG_WARPS * 4 * nm * mg_tab_bytes(nm));
   }
 };
 
@@ -61,26 +73,27 @@ MOE_DEV void load_scales(float (&sc)[8], const __half* p, int nsc) {
   for (int k = 0; k < 8; ++k) sc[k] = k < nsc ? __half2float(p[k]) : 0.f;
 }
 
-template <int B>
-__global__ void __launch_bounds__(MG_THREADS, 2)
+template <int B, int NM>
+__global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
     k_mgemv(const __grid_constant__ GLaunch P, int xs_cap, int zs_cap, int xin_cap, int nst,
             int stage_bytes) {
   constexpr int W = MG_WARPS, NT = MG_THREADS, UPS = mma_units(B);
+  constexpr int NC = mg_cols(NM), CPG = NM == 1 ? 1 : 2, TB = mg_tab_bytes(NM);
   extern __shared__ __align__(128) uint8_t smem[];
-  const MgSmem L(xs_cap, zs_cap, xin_cap);
+  const MgSmem L(xs_cap, zs_cap, xin_cap, NM);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
-  float* misc = reinterpret_cast<float*>(smem + 128);  // [32]
-  uint64_t* zbar = reinterpret_cast<uint64_t*>(smem + 256);
+  uint64_t* zbar = reinterpret_cast<uint64_t*>(smem + 128);
   uint64_t* xbar = zbar + 1;
   uint64_t* sbar = zbar + 2;
-  int* lastf = reinterpret_cast<int*>(smem + 288);
-  float* xs = reinterpret_cast<float*>(smem + L.xs);
-  float* xz = reinterpret_cast<float*>(smem + L.xz);
+  int* lastf = reinterpret_cast<int*>(smem + 160);
+  float* misc = reinterpret_cast<float*>(smem + 256);  // [2][NC][W] (<= 512 bytes)
+  float* xs = reinterpret_cast<float*>(smem + L.xs);   // [NC][xs_cap]
+  float* xz = reinterpret_cast<float*>(smem + L.xz);   // [NC][xs_cap]
   __half2* zsm = reinterpret_cast<__half2*>(smem + L.zsm);
   uint8_t* xin = smem + L.xin;
   __half* scl_s = reinterpret_cast<__half*>(smem + L.scl);
-  uint8_t* wtab = smem + L.wtab + warp_id() * UPS * mt::BTAB;
+  uint8_t* wtab = smem + L.wtab + warp_id() * UPS * NM * TB;
   uint8_t* ring = smem + L.ring;
 
   int ji = 0, cnt_base = 0;
@@ -88,9 +101,25 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
     if ((int)blockIdx.x >= P.j[i].blk0) ji = i;
   for (int i = 0; i < ji; ++i) cnt_base += P.j[i].M.ncb;
   const GJob& J = P.j[ji];
-  const int local = blockIdx.x - J.blk0;
-  const int cb = local / J.S, s = local % J.S;
   const MatDev& M = J.M;
+  const int local = blockIdx.x - J.blk0;
+  const int per_cg = M.ncb * J.S;
+  const int cg = local / per_cg, cb = (local % per_cg) / J.S, s = local % J.S;
+  // input columns of this CTA: (input index, output index) pairs
+  int nc = 1;
+  int cix[NC], cox[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) cix[c] = cox[c] = 0;
+  if (J.cols) {
+    nc = min(NC, J.ncol - cg * NC);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < nc) {
+        const int2 v = J.cols[cg * NC + c];
+        cix[c] = v.x;
+        cox[c] = v.y;
+      }
+  }
   const int qs = s * J.QPS, nun = max(min(M.nquads, qs + J.QPS) - qs, 0);  // k-steps
   const int nsl = mma_slices(M, cb), rb = mma_rec_bytes(M, cb);
   const int sb = mt::slice_bytes(B, 1 << M.g_log2);
@@ -105,6 +134,7 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
   const bool swiglu = J.xmode == X_SWIGLU, xcomb = J.xmode == X_COMBINE;
   const int xparts = J.xS > 1 ? J.xS : 1;
   const bool expert = J.rel_slot >= 0;
+  const RouteRec* route = P.route + J.rel_pos;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) {
@@ -122,7 +152,7 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
   int ebuf = 0;
   if (expert) {
     gemv::pdl_wait();  // the route is written by the previous kernel (tail)
-    ebuf = P.route->buf[J.rel_slot];
+    ebuf = route->buf[J.rel_slot];
     if (ebuf < 0) {  // expert parallel: another rank owns this expert
       float* zdst = J.reduce == 2 ? nullptr
                     : J.reduce == 1 ? (s == 0 ? J.out : nullptr)
@@ -142,16 +172,18 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
     gemv::bulk_g2s_hint(ring + (size_t)st * stage_bytes, src + (int64_t)it * UPS * rb, bytes,
                         full + st, pol);
   };
-  // x rows of the CTA: one bulk copy per input array (partials [xparts][rows])
+  // x rows of the CTA: one bulk copy per input array and column
+  // (xin [column][array][part][rows]; partials [xparts][rows])
   const bool xstage = !xcomb && nrows > 0;
   const int xbytes = nrows * 4;
+  const int narr = swiglu ? 2 : 1;
   if (threadIdx.x == 0) {
     const uint8_t* base = M.base;
     const __half2* zmeta = M.zmeta;
     const __half* scl = M.scl;
     if (expert) {
-      if (!P.route->ready[J.rel_slot])
-        wait_flag(P.flags + ebuf, P.route->gen[J.rel_slot], P.err, P.wait_ns);
+      if (!route->ready[J.rel_slot])
+        wait_flag(P.flags + ebuf, route->gen[J.rel_slot], P.err, P.wait_ns);
       const uint8_t* b = P.pool + (long long)ebuf * P.slot_stride;
       base = b + reinterpret_cast<size_t>(base);
       zmeta = reinterpret_cast<const __half2*>(b + reinterpret_cast<size_t>(zmeta));
@@ -173,16 +205,19 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
     }
     if (!expert) gemv::pdl_wait();  // x is the previous kernel's output
     if (xstage) {
-      gemv::mbar_arrive_tx(xbar, (swiglu ? 2u : 1u) * (uint32_t)xparts * (uint32_t)xbytes);
-      const uint8_t* a = reinterpret_cast<const uint8_t*>(swiglu ? J.up1 : J.x);
+      gemv::mbar_arrive_tx(xbar, (uint32_t)(nc * narr * xparts) * (uint32_t)xbytes);
       const size_t pstride = (size_t)J.xstride * 4;
-      for (int p = 0; p < xparts; ++p)
-        gemv::bulk_g2s(xin + (size_t)p * xbytes, a + p * pstride + (size_t)row0 * 4, xbytes, xbar);
-      if (swiglu)
-        for (int p = 0; p < xparts; ++p)
-          gemv::bulk_g2s(xin + (size_t)(xparts + p) * xbytes,
-                         reinterpret_cast<const uint8_t*>(J.up3) + p * pstride + (size_t)row0 * 4,
-                         xbytes, xbar);
+      for (int c = 0; c < nc; ++c) {
+        uint8_t* xc = xin + (size_t)c * xin_cap;
+        const size_t coff = (size_t)cix[c] * J.xcs * 4 + (size_t)row0 * 4;
+        for (int a = 0; a < narr; ++a) {
+          const uint8_t* arr = reinterpret_cast<const uint8_t*>(
+              swiglu ? (a ? J.up3 : J.up1) : J.x);
+          for (int p = 0; p < xparts; ++p)
+            gemv::bulk_g2s(xc + (size_t)(a * xparts + p) * xbytes, arr + p * pstride + coff,
+                           xbytes, xbar);
+        }
+      }
     }
   }
   if (!expert) gemv::pdl_wait();
@@ -195,10 +230,10 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
   }
 
   // ---------------------------------------------------- x rows -> xs (x * 2^100)
-  if (xcomb) {  // fused combine + LayerNorm of the previous layer's output
+  if (xcomb) {  // fused combine + LayerNorm of the previous layer's output (NC == 1)
     float* xf = reinterpret_cast<float*>(xin);  // the full residual [K]
     const int K = M.K;
-    const float w0 = P.route->w[0], w1 = J.ctop > 1 ? P.route->w[1] : 0.f;
+    const float w0 = route->w[0], w1 = J.ctop > 1 ? route->w[1] : 0.f;
     float sum = 0.f;
     for (int i0 = threadIdx.x; i0 < K; i0 += 8 * NT) {
       float hv[8];
@@ -239,22 +274,29 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
     }
   } else if (xstage) {
     gemv::mbar_wait(xbar, 0);
-    const float* xf = reinterpret_cast<const float*>(xin);
-    for (int i = threadIdx.x; i < nrows; i += NT) {
-      float a = 0.f, b = 0.f;
-      for (int p = 0; p < xparts; ++p) a += xf[p * nrows + i];  // producer splits, in order
-      float xv = a;
-      if (swiglu) {  // SwiGLU of the up projections (model.py:223-226)
-        for (int p = 0; p < xparts; ++p) b += xf[(xparts + p) * nrows + i];
-        xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
+    for (int c = 0; c < NC; ++c) {
+      const float* xf = reinterpret_cast<const float*>(xin + (size_t)c * xin_cap);
+      for (int i = threadIdx.x; i < nrows; i += NT) {
+        float xv = 0.f;
+        if (c < nc) {
+          float a = 0.f, b = 0.f;
+          for (int p = 0; p < xparts; ++p) a += xf[p * nrows + i];  // producer splits, in order
+          xv = a;
+          if (swiglu) {  // SwiGLU of the up projections (model.py:223-226)
+            for (int p = 0; p < xparts; ++p) b += xf[(xparts + p) * nrows + i];
+            xv = __fmul_rn(__fmul_rn(a, sigmoid_ref(a)), b);
+          }
+        }
+        xs[c * xs_cap + i] = xv;
       }
-      xs[i] = xv;
     }
   }
   tl_mark(P.site, 0);
 
   // ------------------- per row: x * zscale, sum x * zoffset, max |x * s| (E)
-  float zo_part = 0.f, mx = 0.f;
+  float zo_part[NC], mx[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) zo_part[c] = mx[c] = 0.f;
   const int nsc = mma_nsc(M, cb), spl = M.sg_log2 - 7;  // 2^spl slices per scale
   if (nrows > 0) {
     gemv::mbar_wait(zbar, 0);
@@ -265,46 +307,61 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
     for (int i = threadIdx.x; i < nrows; i += NT) {
       const int run = (int)(((int64_t)(row0 + i) * M.G + gcb0) >> M.sg_log2);
       const float2 zm = __half22float2(zsm[zlead + run - z0]);
-      const float xv = xs[i];
-      xz[i] = (xv * gemv::kXScale) * zm.x;  // the zero-code floats are 2^-149-scaled
-      zo_part = fmaf(xv, zm.y, zo_part);
       float sc[8];
       load_scales(sc, scl_s + (size_t)i * nsc, nsc);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) mx = fmaxf(mx, fabsf(xv * sc[c]));
+      for (int c = 0; c < NC; ++c) {
+        const float xv = xs[c * xs_cap + i];
+        xz[c * xs_cap + i] = (xv * gemv::kXScale) * zm.x;  // zero-code floats are 2^-149-scaled
+        zo_part[c] = fmaf(xv, zm.y, zo_part[c]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mx[c] = fmaxf(mx[c], fabsf(xv * sc[k]));
+      }
     }
   }
-  zo_part = warp_sum(zo_part);
-  mx = warp_max(mx);
-  if (lane == 0) {
-    misc[warp] = zo_part;
-    misc[W + warp] = mx;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    zo_part[c] = warp_sum(zo_part[c]);
+    mx[c] = warp_max(mx[c]);
+    if (lane == 0) {
+      misc[c * W + warp] = zo_part[c];
+      misc[(NC + c) * W + warp] = mx[c];
+    }
   }
   __syncthreads();
-  float zo_sum = 0.f;
-  mx = 0.f;
+  float zo_sum[NC];
+  int Eb[NC];
 #pragma unroll
-  for (int w = 0; w < W; ++w) {
-    zo_sum += misc[w];
-    mx = fmaxf(mx, misc[W + w]);
+  for (int c = 0; c < NC; ++c) {
+    float zsum = 0.f, m = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      zsum += misc[c * W + w];
+      m = fmaxf(m, misc[(NC + c) * W + w]);
+    }
+    zo_sum[c] = zsum;
+    // fixed point of b = x * s: |b| < 2^30; 2^(-E-6) must stay a normal float
+    Eb[c] = m > 0.f ? min(29 - ilogbf(m), 100) : 0;
   }
-  // fixed point of b = x * s: |b| < 2^30; 2^(-E-6) must stay a normal float
-  const int Eb = mx > 0.f ? min(29 - ilogbf(mx), 100) : 0;
-  {
-    const float p2 = __uint_as_float(gemv::pow2_bits(Eb));
-    for (int i = threadIdx.x; i < nrows; i += NT) xs[i] *= p2;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const float p2 = __uint_as_float(gemv::pow2_bits(Eb[c]));
+    for (int i = threadIdx.x; i < nrows; i += NT) xs[c * xs_cap + i] *= p2;
   }
   __syncthreads();
   tl_mark(P.site, 2);  // prologue done
 
   // ---------------------------------------------------- streaming loop
-  int D[8][4];
-  float zq[8];
+  int D[NM][8][4];
+  float zq[NC][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    D[i][0] = D[i][1] = D[i][2] = D[i][3] = 0;
-    zq[i] = 0.f;
-  }
+  for (int m = 0; m < NM; ++m)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) D[m][i][0] = D[m][i][1] = D[m][i][2] = D[m][i][3] = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) zq[c][i] = 0.f;
   {
     const int g = lane >> 2, t = lane & 3;
     const uint8_t* sl0 = ring + (size_t)warp * sb;
@@ -314,38 +371,44 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
     uint32_t ph = 0;
     for (int it = 0; it < nit; ++it) {
       const int u0 = it * UPS, nu = min(UPS, nun - u0);
-      uint2 bf[UPS];
+      uint2 bf[UPS][NM];
       if (active) {  // the B tables of the stage's units for this slice (row = lane)
 #pragma unroll
         for (int u = 0; u < UPS; ++u) {
           const int row = (u0 + u) * mt::KS + lane;
           const bool in = u < nu;
-          mg::put_digits(wtab + u * mt::BTAB, lane, in ? xs[row] : 0.f,
-                         in ? __half2float(scl_s[row * nsc + wsc]) : 0.f);
+          const float sc = in ? __half2float(scl_s[row * nsc + wsc]) : 0.f;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+            mg::put_digits(wtab + (u * NM + c / CPG) * TB + (c % CPG) * mt::BTAB, lane,
+                           in ? xs[c * xs_cap + row] : 0.f, sc);
         }
         __syncwarp();
 #pragma unroll
         for (int u = 0; u < UPS; ++u)
-          bf[u] = g < 4 ? reinterpret_cast<const uint2*>(wtab + u * mt::BTAB)[4 * g + t]
-                        : make_uint2(0u, 0u);
+#pragma unroll
+          for (int m = 0; m < NM; ++m)
+            bf[u][m] = (CPG == 2 || g < 4)
+                           ? reinterpret_cast<const uint2*>(wtab + (u * NM + m) * TB)[4 * g + t]
+                           : make_uint2(0u, 0u);
       }
       gemv::mbar_wait(full + st, ph);
       if (active) {
         const uint8_t* sl = sl0 + (size_t)st * stage_bytes;
         if (nu == UPS) {
-          mg::Unit<B> U[UPS];
+          mg::Unit<B, NC> U[UPS];
 #pragma unroll
           for (int u = 0; u < UPS; ++u)
-            mg::unit_load<B>(U[u], sl + u * rb, bf[u], xz + (u0 + u) * mt::KS, lane);
+            mg::unit_load<B, NC>(U[u], sl + u * rb, xz + (u0 + u) * mt::KS, xs_cap, lane);
 #pragma unroll
-          for (int u = 0; u < UPS; ++u) mg::unit_math<B>(D, zq, U[u]);
+          for (int u = 0; u < UPS; ++u) mg::unit_math<B, NM, NC>(D, zq, U[u], bf[u]);
         } else {
 #pragma unroll
           for (int u = 0; u < UPS; ++u)
             if (u < nu) {
-              mg::Unit<B> U;
-              mg::unit_load<B>(U, sl + u * rb, bf[u], xz + (u0 + u) * mt::KS, lane);
-              mg::unit_math<B>(D, zq, U);
+              mg::Unit<B, NC> U;
+              mg::unit_load<B, NC>(U, sl + u * rb, xz + (u0 + u) * mt::KS, xs_cap, lane);
+              mg::unit_math<B, NM, NC>(D, zq, U, bf[u]);
             }
         }
       }
@@ -365,37 +428,43 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
   cta_mark(1);
 
   // ---------------------------------------------------- epilogue
-  float* ymm = reinterpret_cast<float*>(ring);  // [1024] slice outputs
-  unsigned long long* fxs = reinterpret_cast<unsigned long long*>(ring + 4096);  // [1024]
+  float* ymm = reinterpret_cast<float*>(ring);  // [NC][1024] slice outputs
+  unsigned long long* fxs =
+      reinterpret_cast<unsigned long long*>(ring + (size_t)NC * 4096);  // [NC][1024]
   __syncthreads();  // every warp left the ring
-  if (warp < nsl) mg::finish<B>(D, zq, Eb, lane, ymm + warp * mt::SO);
+  if (warp < nsl) mg::finish<B, NM, CPG>(D, zq, Eb, lane, ymm + warp * mt::SO, mt::CBO);
   __syncthreads();
-  const float zo_out = zo_sum;  // x is unscaled here (only xz carries 2^100)
-  float* dst = (J.S == 1 && J.reduce) ? J.out : J.part + (size_t)s * M.N;
-  for (int t = threadIdx.x; t < nout; t += NT) {
-    const float a = ymm[t] + zo_out;
-    if (J.reduce == 2)
-      fxs[t] = fx_bits(a, P.err);
-    else if (J.reduce == 0)
-      ymm[t] = a;
-    else
-      dst[obase + t] = a;
+  for (int c = 0; c < nc; ++c) {
+    const float zo_out = zo_sum[c];  // x is unscaled here (only xz carries 2^100)
+    float* yc = ymm + (size_t)c * mt::CBO;
+    float* dst = (J.S == 1 && J.reduce) ? J.out : J.part + (size_t)cox[c] * J.ocs + (size_t)s * M.N;
+    for (int t = threadIdx.x; t < nout; t += NT) {
+      const float a = yc[t] + zo_out;
+      if (J.reduce == 2)
+        fxs[(size_t)c * mt::CBO + t] = fx_bits(a, P.err);
+      else if (J.reduce == 0)
+        yc[t] = a;
+      else
+        dst[obase + t] = a;
+    }
   }
-  if (J.reduce != 1) {  // one TMA operation per CTA
+  if (J.reduce != 1) {  // one TMA operation per CTA and column
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (J.reduce == 2)
-        asm volatile(
-            "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(
-                J.acc + obase),
-            "r"(gemv::smem_u32(fxs)), "r"((uint32_t)(nout * 8))
-            : "memory");
-      else
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                         dst + obase),
-                     "r"(gemv::smem_u32(ymm)), "r"((uint32_t)(nout * 4))
-                     : "memory");
+      for (int c = 0; c < nc; ++c) {
+        if (J.reduce == 2)
+          asm volatile(
+              "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(
+                  J.acc + (size_t)cox[c] * J.ocs + obase),
+              "r"(gemv::smem_u32(fxs + (size_t)c * mt::CBO)), "r"((uint32_t)(nout * 8))
+              : "memory");
+        else
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                           J.part + (size_t)cox[c] * J.ocs + (size_t)s * M.N + obase),
+                       "r"(gemv::smem_u32(ymm + (size_t)c * mt::CBO)), "r"((uint32_t)(nout * 4))
+                       : "memory");
+      }
       asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
     }
     cta_mark(2);
@@ -407,7 +476,8 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
     tl_end(P.site);
     return;
   }
-  // reduce == 1: the last CTA of this column block sums the S partials in order
+  // reduce == 1 (single column): the last CTA of this column block sums the S
+  // partials in order
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {

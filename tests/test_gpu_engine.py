@@ -252,3 +252,41 @@ def test_mixtral_width_decode_bitwise_reproducible():
     eng.close()
     assert runs[0][0] == runs[1][0]
     assert np.array_equal(runs[0][1], runs[1][1])
+
+
+@pytest.mark.parametrize("bits,n", [(3, 9), (2, 70)])
+def test_mixtral_width_batched_prefill_equals_per_position(bits, n, monkeypatch):
+    """Batched prefill (the positions as input columns of the tensor-core
+    GEMVs, one pass over each distinct expert per layer; engine.cu
+    prefill_batched) gives bit-identical logits, trace and store event log to
+    running the decode kernels once per position (MOE_PREFILL_BATCH=0), for a
+    ragged last column group (9 = 2 x 4 + 1) and a prompt longer than one
+    64-position chunk (70)."""
+    import bench
+    from paper_2312_17238_b200 import CacheConfig, OffloadEngine, SpeculationConfig
+    from paper_2312_17238_b200 import synthetic_model
+    cfg = dict(bench.MIXTRAL)
+    cfg["n_layers"] = 2
+    cobj = bench.cfg_obj(cfg)
+    prompt = [int(t) for t in np.random.default_rng(5).integers(0, cobj.vocab_size, n)]
+    outs = []
+    for batch in ("1", "0"):
+        monkeypatch.setenv("MOE_PREFILL_BATCH", batch)
+        eng = OffloadEngine(synthetic_model(cobj, 0), CacheConfig(k=2, b=4),
+                            SpeculationConfig(enabled=False), record_hidden=True,
+                            synth=(0, 4, bits), expert_bytes=bench.expert_bytes(bench.MIXTRAL, bits))
+        logits = eng.prefill(prompt)
+        r = eng.decode(2)
+        tr = eng.trace()
+        outs.append((np.asarray(logits).copy(), r.tokens, _ev_rows(eng.events),
+                     [(x.token_pos, x.layer, tuple(x.experts)) for x in tr.records],
+                     np.stack([x.hidden for x in tr.records]),
+                     np.stack([x.weights for x in tr.records])))
+        eng.close()
+    a, b = outs
+    assert np.array_equal(a[0], b[0])
+    assert a[1] == b[1]
+    assert a[2] == b[2]
+    assert a[3] == b[3]
+    assert np.array_equal(a[4], b[4])
+    assert np.array_equal(a[5], b[5])
