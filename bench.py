@@ -231,6 +231,20 @@ def timeline_of(eng, prompt, world, nl):
             kinds[nm] = {"avg_us": round(float(np.mean(d)), 2),
                          "median_us": round(float(np.median(d)), 2),
                          "sum_us": round(float(np.sum(d)), 1)}
+    # intra-kernel phase marks (block 0, thread 0; kernels.cu tl_mark): median
+    # offset of each recorded phase from the kernel's span start, per kind
+    marks = raw[2 * n.value:10 * n.value].reshape(n.value, 8)
+    for i, nm in enumerate(names):
+        if nm not in kinds:
+            continue
+        ph = {}
+        for p in range(8):
+            v = [(marks[j, p] - st[j]) / 1e3 for j in (1 + 8 * l + i for l in range(nl))
+                 if ok[j] and marks[j, p] > st[j]]
+            if v:
+                ph[str(p)] = round(float(np.median(v)), 2)
+        if ph:
+            kinds[nm]["phase_marks_us"] = ph
     for nm, j in (("embed", 0), ("lm_head", 1 + 8 * nl), ("logits", 2 + 8 * nl)):
         if ok[j]:
             kinds[nm] = {"avg_us": round((en[j] - st[j]) / 1e3, 2),

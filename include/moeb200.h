@@ -119,6 +119,23 @@ int moe_load_tensor(moe_engine* eng, const char* name, const moe_matrix* m);
 int moe_load_expert(moe_engine* eng, int32_t layer, int32_t expert, const moe_matrix* w_gate,
                     const moe_matrix* w_up, const moe_matrix* w_down);
 
+/* quant.deserialize_block (quant.py:364-421): parse one serialized block
+ * (quant.serialize_block bytes, e.g. read from disk) into a moe_matrix view of
+ * `buf`; the meta_bits-packed zero codes are unpacked into `zeros_out`
+ * (zeros_cap bytes).  zeros_out == NULL: validate and report the group count
+ * only.  Malformed input -> MOE_ERR_FORMAT with the reference's message.
+ * Host only (no GPU needed). */
+int moe_parse_block(const uint8_t* buf, int64_t len, moe_matrix* out, uint8_t* zeros_out,
+                    int64_t zeros_cap, int64_t* n_groups_out);
+
+/* moe_load_tensor / moe_load_expert from serialized blocks (the store's
+ * host-arena payloads loaded from their on-disk form, store.py:85-92). */
+int moe_load_tensor_serialized(moe_engine* eng, const char* name, const uint8_t* buf,
+                               int64_t len);
+int moe_load_expert_serialized(moe_engine* eng, int32_t layer, int32_t expert,
+                               const uint8_t* w_gate, int64_t n_gate, const uint8_t* w_up,
+                               int64_t n_up, const uint8_t* w_down, int64_t n_down);
+
 /* Device-side synthetic weights (counter hash, see oracle/model.py
  * synth_params), quantized on device with the reference quantizer
  * (quant.py:181-229); attn_bits/expert_bits in {2,3,4,32}. */

@@ -72,6 +72,9 @@ SIGNATURES = {
     "moe_load_expert": (I32, [P, I32, I32, C.POINTER(Matrix), C.POINTER(Matrix),
                               C.POINTER(Matrix)]),
     "moe_synth_model": (I32, [P, U64, I32, I32]),
+    "moe_parse_block": (I32, [P, I64, C.POINTER(Matrix), P, I64, C.POINTER(C.c_int64)]),
+    "moe_load_tensor_serialized": (I32, [P, C.c_char_p, P, I64]),
+    "moe_load_expert_serialized": (I32, [P, I32, I32, P, I64, P, I64, P, I64]),
     "moe_finalize": (I32, [P]),
     "moe_set_device": (I32, [I32]),
     "moe_measure_h2d": (I32, [P, I32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -8,7 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmoeb200.so")
-SOURCES = ["kernels.cu", "tile.cu", "engine.cu", "store_sim.cu"]
+SOURCES = ["kernels.cu", "tile.cu", "engine.cu", "store_sim.cu", "blockio.cu"]
 HEADERS = ["common.cuh", "gemv.cuh", "store_dev.cuh", "kernels.cuh", "copy_sched.h", "mma_layout.cuh",
            "mma_gemv.cuh", "mgemv_kernel.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -451,7 +451,7 @@ struct moe_engine {
   int run_copier();
   // batched prefill (tensor-core layout, one GPU): buffers for PB positions
   int PB = 0;
-  float *pf_xn = nullptr, *pf_ctx = nullptr, *pf_up = nullptr;
+  float *pf_xn = nullptr, *pf_ctx = nullptr, *pf_up = nullptr, *pf_q = nullptr;
   unsigned long long *pf_qkv_acc = nullptr, *pf_wo_acc = nullptr, *pf_dn_acc = nullptr;
   int2* pf_cols = nullptr;       // device: [PB] identity, then up / down column tables
   int2* pf_cols_h = nullptr;     // pinned staging of the expert column tables
@@ -516,7 +516,7 @@ moe_engine::~moe_engine() {
   if (mb_host) cudaFreeHost(mb_host);
   if (t0) cudaEventDestroy(t0);
   if (t1) cudaEventDestroy(t1);
-  for (void* p : {(void*)pf_xn, (void*)pf_ctx, (void*)pf_up, (void*)pf_qkv_acc,
+  for (void* p : {(void*)pf_xn, (void*)pf_ctx, (void*)pf_up, (void*)pf_q, (void*)pf_qkv_acc,
                   (void*)pf_wo_acc, (void*)pf_dn_acc, (void*)pf_cols})
     if (p) cudaFree(p);
   if (pf_cols_h) cudaFreeHost(pf_cols_h);
@@ -920,12 +920,17 @@ int moe_engine::prefill_alloc() {
   int rc;
   if ((rc = dalloc(&pf_xn, (size_t)pb * d))) return rc;
   if ((rc = dalloc(&pf_ctx, (size_t)pb * d))) return rc;
+  if ((rc = dalloc(&pf_q, (size_t)pb * d))) return rc;
   if ((rc = dalloc(&pf_up, (size_t)pb * topk * 2 * S_up * f))) return rc;
   if ((rc = dalloc(&pf_qkv_acc, (size_t)pb * 3 * d))) return rc;
   if ((rc = dalloc(&pf_wo_acc, (size_t)pb * d))) return rc;
   if ((rc = dalloc(&pf_dn_acc, (size_t)pb * topk * d))) return rc;
   if ((rc = dalloc(&pf_cols, (size_t)pb * (1 + 2 * topk)))) return rc;
-  CU(cudaHostAlloc(&pf_cols_h, (size_t)pb * 2 * topk * sizeof(int2), cudaHostAllocDefault));
+  // one staging region per chunk: a chunk's tables are still being copied
+  // (async, stream order) while the host fills the next chunk's
+  const int nchunk = (T + pb - 1) / pb;
+  CU(cudaHostAlloc(&pf_cols_h, (size_t)nchunk * pb * 2 * topk * sizeof(int2),
+                   cudaHostAllocDefault));
   CU(cudaHostAlloc(&pf_route_h, (size_t)T * sizeof(RouteRec), cudaHostAllocDefault));
   std::vector<int2> id(pb);
   for (int i = 0; i < pb; ++i) id[i] = make_int2(i, i);
@@ -965,21 +970,37 @@ int moe_engine::prefill_batched(int n) {
         dense_cols(q.j[i], nc, d, 3LL * d);
       }
       launch_gemv_cols(attn_bits, q, finalize_launch(q), s_comp);
-      for (int i = 0; i < nc; ++i) {
+      if (hd % 128 == 0) {  // all positions of the chunk in two launches
         AttnParams a{};
-        a.qkv_part = qkv_part;
-        a.S = S_qkv;
-        a.acc = pf_qkv_acc + (size_t)i * 3 * d;
+        a.acc = pf_qkv_acc;
+        a.qbuf = pf_q;
         a.kc = kc + (size_t)l * T * d;
         a.vc = vc + (size_t)l * T * d;
-        a.ctx = pf_ctx + (size_t)i * d;
+        a.ctx = pf_ctx;
         a.site = -1;
-        a.pos = c0 + i;
+        a.pos = c0;
         a.H = H;
         a.hd = hd;
         a.d = d;
         a.T_max = T;
-        launch_attention(a, s_comp, false);
+        launch_attention_rows(a, nc, s_comp);
+      } else {
+        for (int i = 0; i < nc; ++i) {
+          AttnParams a{};
+          a.qkv_part = qkv_part;
+          a.S = S_qkv;
+          a.acc = pf_qkv_acc + (size_t)i * 3 * d;
+          a.kc = kc + (size_t)l * T * d;
+          a.vc = vc + (size_t)l * T * d;
+          a.ctx = pf_ctx + (size_t)i * d;
+          a.site = -1;
+          a.pos = c0 + i;
+          a.H = H;
+          a.hd = hd;
+          a.d = d;
+          a.T_max = T;
+          launch_attention(a, s_comp, false);
+        }
       }
       GLaunch o{};
       o.nj = 1;
@@ -991,20 +1012,19 @@ int moe_engine::prefill_batched(int n) {
       o.j[0].acc = pf_wo_acc;
       dense_cols(o.j[0], nc, d, d);
       launch_gemv_cols(attn_bits, o, finalize_launch(o), s_comp);
-      for (int i = 0; i < nc; ++i) {
-        const int p = c0 + i;
+      {
         TailParams t{};
-        t.x = x + (size_t)p * d;
+        t.x = x + (size_t)c0 * d;
         t.part = wo_out;
         t.S = 1;
-        t.acc = pf_wo_acc + (size_t)i * d;
+        t.acc = pf_wo_acc;
         t.g2 = ln2g[l];
         t.b2 = ln2b[l];
         t.gate_l = gate[l];
         t.gh_l = gate_h[l];
         t.guess_layer = -1;
-        t.h = h + (size_t)p * d;
-        t.route = route + p;
+        t.h = h + (size_t)c0 * d;
+        t.route = route + c0;
         t.trace = trace;
         t.trace_hidden = rec_hidden ? trace_hidden : nullptr;
         t.n_layers = L;
@@ -1014,11 +1034,11 @@ int moe_engine::prefill_batched(int n) {
         t.E = E;
         t.top_k = topk;
         t.layer = l;
-        t.pos = p;
+        t.pos = c0;
         t.mode = 1;
         t.ep_size = 1;
         if (tail_smem_bytes(t) > 226 * 1024) t.gh_l = t.gh_g = nullptr;
-        launch_tail(t, s_comp, false);
+        launch_tail(t, s_comp, false, nc);  // one CTA per position
       }
       dbg("prefill attention", l, c0);
     }
@@ -1036,6 +1056,7 @@ int moe_engine::prefill_batched(int n) {
     // ---- the experts, grouped by buffer (= distinct expert), chunk by chunk
     for (int c0 = 0; c0 < n; c0 += PB) {
       const int nc = std::min(PB, n - c0);
+      int2* cols_h = pf_cols_h + (size_t)(c0 / PB) * PB * 2 * topk;
       std::vector<int> bufs;                 // distinct buffers in first-use order
       std::vector<std::vector<int2>> refs;   // per buffer: (position, slot)
       for (int i = 0; i < nc; ++i)
@@ -1057,15 +1078,15 @@ int moe_engine::prefill_batched(int n) {
         first[k] = (int)ncols;
         for (const int2& r : refs[k]) {
           const int q = (r.x - c0) * topk + r.y;
-          pf_cols_h[ncols] = make_int2(r.x, q);
-          pf_cols_h[(size_t)PB * topk + ncols] = make_int2(q, q);
+          cols_h[ncols] = make_int2(r.x, q);
+          cols_h[(size_t)PB * topk + ncols] = make_int2(q, q);
           ++ncols;
         }
       }
       if (ncols) {
-        CU(cudaMemcpyAsync(up_cols, pf_cols_h, ncols * sizeof(int2), cudaMemcpyHostToDevice,
+        CU(cudaMemcpyAsync(up_cols, cols_h, ncols * sizeof(int2), cudaMemcpyHostToDevice,
                            s_comp));
-        CU(cudaMemcpyAsync(dn_cols, pf_cols_h + (size_t)PB * topk, ncols * sizeof(int2),
+        CU(cudaMemcpyAsync(dn_cols, cols_h + (size_t)PB * topk, ncols * sizeof(int2),
                            cudaMemcpyHostToDevice, s_comp));
       }
       const long long upcs = 2LL * S_up * f;  // floats per (position, slot) of pf_up
@@ -1135,19 +1156,18 @@ int moe_engine::prefill_batched(int n) {
         }
         launch_gemv_cols(expert_bits, dn, finalize_launch(dn), s_comp);
       }
-      for (int i = 0; i < nc; ++i) {
-        const int p = c0 + i;
+      {
         CombineParams c{};
-        c.h = h + (size_t)p * d;
+        c.h = h + (size_t)c0 * d;
         c.part = dn_out;
         c.S = 1;
-        c.acc = pf_dn_acc + (size_t)i * topk * d;
-        c.route = route + p;
-        c.out = x + (size_t)p * d;
+        c.acc = pf_dn_acc;
+        c.route = route + c0;
+        c.out = x + (size_t)c0 * d;
         c.d = d;
         c.top_k = topk;
         c.site = -1;
-        launch_combine(c, s_comp, false);
+        launch_combine(c, s_comp, false, nc);  // grid.y = positions
       }
       dbg("prefill experts", l, c0);
     }
@@ -1343,6 +1363,7 @@ int moe_engine::finish_call(bool want_logits) {
 extern "C" {
 
 const char* moe_last_error(void) { return g_err.c_str(); }
+int moe_engine_fail(int code, const char* msg) { return fail(code, msg); }
 
 int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec_cfg* sc,
                int32_t device, int32_t record_hidden, moe_engine** out) {

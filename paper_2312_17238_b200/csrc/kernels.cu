@@ -862,15 +862,19 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
   }
   gemv::pdl_wait();
   tl_begin(P.site);
-  const int pos = P.ds ? P.ds->pos : P.pos;
+  const int pos = P.ds ? P.ds->pos : P.pos + (int)blockIdx.y;
   const int T = pos + 1;
   const float* qg = P.qkv_part + (size_t)h * HD;
   float* krow = P.kc + (size_t)pos * rstride + (size_t)h * HD;
   float* vrow = P.vc + (size_t)pos * rstride + (size_t)h * HD;
+  float* ctx = P.ctx + (size_t)blockIdx.y * d;
   // KV append (model.py:293, KVCache.append); the QKV GEMV leaves its split-K
   // partials [3][S][d] unreduced: summed here in split order
   const size_t sstride = (size_t)P.S * d;
-  if (P.acc) {  // fixed-point sums of the QKV GEMV: read, then reset for the next layer
+  if (P.qbuf) {  // batched prefill: K/V rows appended by k_kv_append, q converted there
+    const float* qs = P.qbuf + (size_t)blockIdx.y * d + (size_t)h * HD;
+    for (int i = tid; i < HD; i += blockDim.x) q[i] = qs[i];
+  } else if (P.acc) {  // fixed-point sums of the QKV GEMV: read, then reset for the next layer
     unsigned long long* qa = P.acc + (size_t)h * HD;
     for (int i = tid; i < HD; i += blockDim.x) {
       const unsigned long long a = __ldcg(qa + i), bk = __ldcg(qa + d + i),
@@ -967,8 +971,25 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
     }
   }
   __syncthreads();
-  for (int i = tid; i < HD; i += blockDim.x) P.ctx[h * HD + i] = half2buf[i] + half2buf[HD + i];
+  for (int i = tid; i < HD; i += blockDim.x) ctx[h * HD + i] = half2buf[i] + half2buf[HD + i];
   tl_end(P.site);
+}
+
+// batched prefill: the Q/K/V fixed-point sums of `rows` positions -> q rows
+// (qbuf) and the K/V cache rows of positions pos .. pos + rows - 1, sums reset
+// (the same fx_val conversion k_attention128 applies in decode)
+__global__ void __launch_bounds__(256) k_kv_append(AttnParams P) {
+  const int r = blockIdx.y, d = P.d;
+  unsigned long long* a = P.acc + (size_t)r * 3 * d;
+  float* kr = P.kc + (size_t)(P.pos + r) * d;
+  float* vr = P.vc + (size_t)(P.pos + r) * d;
+  float* qr = const_cast<float*>(P.qbuf) + (size_t)r * d;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) {
+    qr[i] = fx_val(__ldcg(a + i));
+    kr[i] = fx_val(__ldcg(a + d + i));
+    vr[i] = fx_val(__ldcg(a + 2 * d + i));
+    a[i] = a[d + i] = a[2 * d + i] = 0ull;
+  }
 }
 
 // ------------------------------------------------------------------ tail
@@ -981,16 +1002,17 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
 // tail: hs = x + Wo output (fp32 partial or fixed-point sums, reset after
 // the loads), V values per thread with every load in flight first
 template <int V, bool FX>
-MOE_DEV void residual_in(const TailParams& P, float* hs, int tid) {
+MOE_DEV void residual_in(const TailParams& P, const float* xin, unsigned long long* acc, float* hs,
+                         int tid) {
   const int d = P.d, nt = (int)blockDim.x;
   float xa[V], pa[V];
   unsigned long long qa[FX ? V : 1];
 #pragma unroll
   for (int u = 0; u < V; ++u) {
     const int i = tid + u * nt;
-    xa[u] = i < d ? __ldcg(P.x + i) : 0.f;
+    xa[u] = i < d ? __ldcg(xin + i) : 0.f;
     if constexpr (FX)
-      qa[u] = i < d ? __ldcg(P.acc + i) : 0ull;
+      qa[u] = i < d ? __ldcg(acc + i) : 0ull;
     else
       pa[u] = i < d ? __ldcg(P.part + i) : 0.f;
   }
@@ -1004,7 +1026,7 @@ MOE_DEV void residual_in(const TailParams& P, float* hs, int tid) {
 #pragma unroll
     for (int u = 0; u < V; ++u) {
       const int i = tid + u * nt;
-      if (i < d) P.acc[i] = 0ull;
+      if (i < d) acc[i] = 0ull;
     }
 }
 
@@ -1048,7 +1070,13 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   }
   gemv::pdl_wait();
   tl_begin(P.site);
-  const int pos = P.ds ? P.ds->pos : P.pos;
+  // batched prefill (mode 1): CTA r handles position P.pos + r
+  const int row = P.mode == 1 ? (int)blockIdx.x : 0;
+  const int pos = P.ds ? P.ds->pos : P.pos + row;
+  const float* xin = P.x + (size_t)row * d;
+  unsigned long long* accr = P.acc ? P.acc + (size_t)row * d : nullptr;
+  float* hout = P.h + (size_t)row * d;
+  RouteRec* route = P.route + row;
   const size_t slot = (size_t)pos * P.n_layers + P.layer;
   float* th = P.trace_hidden ? P.trace_hidden + slot * d : nullptr;
   StoreDev S = P.st;
@@ -1061,19 +1089,19 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
         fls[i] = ld_acquire_u32(const_cast<const uint32_t*>(P.st.flags) + i);
   }
   // residual: all loads first, then the stores (no load waits behind a store)
-  if (P.acc) {
+  if (accr) {
     if (d <= 4 * (int)blockDim.x)
-      residual_in<4, true>(P, hs, tid);
+      residual_in<4, true>(P, xin, accr, hs, tid);
     else
-      residual_in<8, true>(P, hs, tid);
+      residual_in<8, true>(P, xin, accr, hs, tid);
   } else {
-    residual_in<8, false>(P, hs, tid);  // d <= 8192 with 1024 threads
+    residual_in<8, false>(P, xin, accr, hs, tid);  // d <= 8192 with 1024 threads
   }
   tl_mark(P.site, 0);
   gemv::mbar_wait(&wbar, 0);
   __syncthreads();
   tl_mark(P.site, 1);
-  layernorm_block(hs, g2s, b2s, P.h, hs, d, reinterpret_cast<float*>(gpart));
+  layernorm_block(hs, g2s, b2s, hout, hs, d, reinterpret_cast<float*>(gpart));
   __syncthreads();
   tl_mark(P.site, 2);
   int bad = 0;
@@ -1222,8 +1250,8 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     const float wj = lane < k ? __fdiv_rn(ez, sum) : 0.f;
     const int ej = lane < k ? sel_sh[lane] : -1;
     if (lane < MOE_MAX_TOPK) {
-      P.route->e[lane] = ej;
-      P.route->w[lane] = wj;
+      route->e[lane] = ej;
+      route->w[lane] = wj;
     }
     TraceRecDev* tr = P.trace + slot;
     if (lane < 8) {
@@ -1244,7 +1272,13 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
     }
     if (bad) {
       atomicOr(P.st.err, MOE_ERRF_NONFINITE_GATE);
-      atomicCAS(P.st.err + 6, 0, pos + 1);  // first failing position (+1)
+      // first failing position (+1): the smallest over the CTAs of a batched prefill
+      int cur = *(volatile int*)(P.st.err + 6);
+      while (cur == 0 || cur > pos + 1) {
+        const int prev = atomicCAS(P.st.err + 6, cur, pos + 1);
+        if (prev == cur) break;
+        cur = prev;
+      }
     } else if (P.mode == 0) {
       const int m = (guess && P.m > 0) ? P.m : 0;
       store::resolve_token(S, P.layer, sel_sh, k, gsel_sh, m, m ? P.guess_layer : -1, pos, rbuf,
@@ -1253,9 +1287,9 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
 #pragma unroll
     for (int j = 0; j < MOE_MAX_TOPK; ++j) {
       const int b = rbuf[j];
-      P.route->buf[j] = b;
-      P.route->gen[j] = rgen[j];
-      P.route->ready[j] = (P.mode == 0 && P.st.flags && b >= 0 && j < k)
+      route->buf[j] = b;
+      route->gen[j] = rgen[j];
+      route->ready[j] = (P.mode == 0 && P.st.flags && b >= 0 && j < k)
                               ? (int)((int)(fls[b] - rgen[j]) >= 0) : 0;
     }
     tl_mark(P.site + 4, 1);  // store bookkeeping done
@@ -1356,8 +1390,13 @@ __global__ void __launch_bounds__(1024) k_combine(CombineParams P) {
   tl_begin(P.site);
   const float* part = P.part;
   if (P.ep_seq) part += (size_t)(*P.ep_seq & 1ull) * P.ep_slab;
+  // batched prefill: grid.y = positions (h, acc, route, out advance per row)
+  const int row = blockIdx.y;
+  const float* hin = P.h + (size_t)row * P.d;
+  unsigned long long* acc = P.acc ? P.acc + (size_t)row * P.top_k * P.d : nullptr;
+  float* outp = P.out + (size_t)row * P.d;
   float w[MOE_MAX_TOPK];
-  for (int j = 0; j < P.top_k; ++j) w[j] = P.route->w[j];
+  for (int j = 0; j < P.top_k; ++j) w[j] = P.route[row].w[j];
   const int step = P.xn ? blockDim.x : gridDim.x * blockDim.x;
   const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
   if (P.xn && (P.S == 1 || P.acc) && P.top_k <= 2) {  // decode fast path: all loads first
@@ -1369,17 +1408,17 @@ __global__ void __launch_bounds__(1024) k_combine(CombineParams P) {
       combine_fast<8, false>(P, part, w, osh, i0, step);  // d <= 8192 (one CTA)
   } else {
     for (int i = i0; i < P.d; i += step) {
-      float out = __ldcg(P.h + i);
+      float out = __ldcg(hin + i);
       for (int j = 0; j < P.top_k; ++j) {
         float y = 0.f;
-        if (P.acc) {
-          y = fx_val(__ldcg(P.acc + (size_t)j * P.d + i));
-          P.acc[(size_t)j * P.d + i] = 0ull;
+        if (acc) {
+          y = fx_val(__ldcg(acc + (size_t)j * P.d + i));
+          acc[(size_t)j * P.d + i] = 0ull;
         } else
           for (int s = 0; s < P.S; ++s) y += __ldcg(part + ((size_t)j * P.S + s) * P.d + i);
         out = __fadd_rn(out, __fmul_rn(w[j], y));  // model.py:251-254, reference order
       }
-      P.out[i] = out;
+      outp[i] = out;
       if (P.xn) osh[i] = out;
     }
   }
@@ -1560,7 +1599,8 @@ cudaError_t preload_kernels() {
                        (const void*)k_layernorm, (const void*)k_attention, (const void*)k_tail,
                        (const void*)k_prefill_bk, (const void*)k_begin_call,
                        (const void*)k_combine,   (const void*)k_logits, (const void*)k_wait_ready,
-                       (const void*)k_exchange, (const void*)k_mgemv<2, 1>,
+                       (const void*)k_exchange, (const void*)k_kv_append,
+                       (const void*)k_mgemv<2, 1>,
                        (const void*)k_mgemv<3, 1>, (const void*)k_mgemv<4, 1>,
                        (const void*)k_mgemv<2, MG_PREFILL_NM>,
                        (const void*)k_mgemv<3, MG_PREFILL_NM>,
@@ -1767,6 +1807,12 @@ void launch_layernorm(const float* x, const float* g, const float* b, float* y, 
   launch_small(k_layernorm, dim3(1), dim3(1024), 0, s, pdl, x, g, b, y, d);
 }
 
+void launch_attention_rows(const AttnParams& P, int rows, cudaStream_t s) {
+  launch_small(k_kv_append, dim3((P.d + 255) / 256, rows), dim3(256), 0, s, false, P);
+  launch_small(k_attention128, dim3(P.H, rows), dim3(256),
+               (size_t)(3 * P.hd + P.T_max) * sizeof(float), s, false, P);
+}
+
 void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl) {
   if (P.hd % 128 == 0) {
     launch_small(k_attention128, dim3(P.H), dim3(256),
@@ -1786,8 +1832,8 @@ int tail_smem_bytes(const TailParams& P) {
                (size_t)P.st.nbuf * 4);
 }
 
-void launch_tail(const TailParams& P, cudaStream_t s, bool pdl) {
-  launch_small(k_tail, dim3(1), dim3(1024), (size_t)tail_smem_bytes(P), s, pdl, P);
+void launch_tail(const TailParams& P, cudaStream_t s, bool pdl, int rows) {
+  launch_small(k_tail, dim3(rows), dim3(1024), (size_t)tail_smem_bytes(P), s, pdl, P);
 }
 
 void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s) {
@@ -1802,7 +1848,11 @@ void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int*
   g_launches.fetch_add(1);
 }
 
-void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl) {
+void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl, int rows) {
+  if (rows > 1) {  // batched prefill: no fused LayerNorm
+    launch_small(k_combine, dim3((P.d + 255) / 256, rows), dim3(256), 0, s, pdl, P);
+    return;
+  }
   if (P.xn)
     launch_small(k_combine, dim3(1), dim3(1024), (size_t)P.d * 12, s, pdl, P);
   else

@@ -15,13 +15,16 @@ __host__ __device__ constexpr int gemv_qs(int bits) { return MOE_GEMV_WARPS * ge
 #define MOE_GEMV_RING (80 * 1024)  // bytes of stage ring per CTA (2 CTAs / SM)
 #define MOE_XS_MAX 4096            // rows of x kept in smem per CTA
 #define MOE_GEMV_SMEM_CAP (112 * 1024)  // dynamic smem per CTA at 2 CTAs / SM
+#ifndef MOE_UPS24
+#define MOE_UPS24 2
+#endif
 #ifndef MOE_UPS3
-#define MOE_UPS3 1
+#define MOE_UPS3 2
 #endif
 #define MOE_MMA_UNITS_MAX 64       // k-steps per CTA in the tensor-core layout (B table)
 // k-steps per pipeline stage of the tensor-core layout (a compile-time count so
 // the consumer loop is unrolled and its shared-memory loads run ahead)
-__host__ __device__ constexpr int mma_units(int bits) { return bits == 3 ? MOE_UPS3 : 1; }
+__host__ __device__ constexpr int mma_units(int bits) { return bits == 3 ? MOE_UPS3 : MOE_UPS24; }
 
 // X_COMBINE: the input row slice is LayerNorm(h + w0*y0 + w1*y1) (the MoE
 // combine of the previous layer, model.py:251-254, fused with the next LN):
@@ -102,7 +105,8 @@ struct AttnParams {
   unsigned long long* acc;  // or: q/k/v as fixed-point sums [3][d] (read, then zeroed)
   float* kc;              // this layer's K cache [max_seq][H][hd]
   float* vc;
-  float* ctx;             // [d]
+  float* ctx;             // [d] (batched prefill: [rows][d])
+  const float* qbuf;      // batched prefill: q rows [rows][d] (K/V rows already appended)
   const DecodeState* ds;  // decode: position from here (else `pos`)
   int pos, H, hd, d, T_max;
   int site;  // timeline slot of this launch (profiling), -1 none
@@ -218,7 +222,9 @@ cudaError_t set_cta_trace(unsigned long long* buf);          // GEMV microbench 
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl);
 // batched prefill (tensor-core layout only): jobs with `cols`, MG_PREFILL_COLS
 // input columns per CTA
+#ifndef MG_PREFILL_NM
 #define MG_PREFILL_NM 2
+#endif
 #define MG_PREFILL_COLS (2 * MG_PREFILL_NM)
 void launch_gemv_cols(int bits, const GLaunch& P, int nblocks, cudaStream_t s);
 int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full, int* nstages,
@@ -229,11 +235,18 @@ void launch_layernorm(const float* x, const float* g, const float* b, float* y, 
 // one CTA per row: y[r] = LN(x[r]) for r < rows (batched prefill)
 void launch_layernorm_rows(const float* x, const float* g, const float* b, float* y, int d,
                            int rows, cudaStream_t s);
+// batched prefill (head_dim % 128 == 0): k_kv_append then attention with
+// grid (H, rows), positions pos .. pos + rows - 1
+void launch_attention_rows(const AttnParams& P, int rows, cudaStream_t s);
 void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl = false);
-void launch_tail(const TailParams& P, cudaStream_t s, bool pdl = false);
+// rows > 1 (batched prefill, mode 1 only): CTA r handles position pos + r
+// (x, acc, h, route advance by r rows)
+void launch_tail(const TailParams& P, cudaStream_t s, bool pdl = false, int rows = 1);
 int tail_smem_bytes(const TailParams& P);
 void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s);
-void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl = false);
+// rows > 1 (batched prefill, no fused LN): grid.y = positions (h, acc, route,
+// out advance per row)
+void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl = false, int rows = 1);
 void launch_exchange(const ExchangeParams& P, cudaStream_t s, bool pdl = false);
 void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int* err,
                        unsigned long long wait_ns, cudaStream_t s);

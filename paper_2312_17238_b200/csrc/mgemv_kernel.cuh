@@ -103,8 +103,10 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
   const GJob& J = P.j[ji];
   const MatDev& M = J.M;
   const int local = blockIdx.x - J.blk0;
-  const int per_cg = M.ncb * J.S;
-  const int cg = local / per_cg, cb = (local % per_cg) / J.S, s = local % J.S;
+  // column groups innermost: the CTAs streaming the same weight bytes for
+  // different input columns run together, so all but the first read hit L2
+  const int ncg = J.ncg > 1 ? J.ncg : 1;
+  const int cg = local % ncg, rest = local / ncg, cb = rest / J.S, s = rest % J.S;
   // input columns of this CTA: (input index, output index) pairs
   int nc = 1;
   int cix[NC], cox[NC];

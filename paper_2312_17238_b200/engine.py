@@ -29,8 +29,16 @@ def _is_block(w) -> bool:
     return hasattr(w, "packed_codes") and hasattr(w, "scheme")
 
 
+def _is_serialized(w) -> bool:
+    return isinstance(w, (bytes, bytearray, memoryview))
+
+
 def block_payload_nbytes(block) -> int:
-    """Serialized payload bytes (reference quant.py:332-343)."""
+    """Serialized payload bytes (reference quant.py:332-343); for a serialized
+    block (quant.serialize_block bytes) the bytes after its header."""
+    if _is_serialized(block):
+        ndim = bytes(block[11:12])[0] if len(block) >= 12 else 0
+        return len(block) - (12 + 4 * ndim + 4)
     if block.scheme.bits == 16:
         return len(block.packed_codes)
     zb = -(-np.asarray(block.zeros).size * block.scheme.meta_bits // 8)
@@ -58,7 +66,8 @@ def payload_nbytes(payload) -> int:
         return int(payload.nbytes)
     tot = 0
     for w in expert_triple(payload):
-        tot += block_payload_nbytes(w) if _is_block(w) else int(np.asarray(w).nbytes)
+        tot += (block_payload_nbytes(w) if _is_block(w) or _is_serialized(w)
+                else int(np.asarray(w).nbytes))
     return tot
 
 
@@ -245,6 +254,10 @@ class OffloadEngine:
         cfg, p, L = model.config, model.params, lib()
 
         def put(name, w, allow_half=False):
+            if _is_serialized(w):  # quant.serialize_block bytes (e.g. read from disk)
+                buf = bytes(w)
+                check(L.moe_load_tensor_serialized(self._h, name.encode(), buf, len(buf)))
+                return
             mk = _Marshal()
             m = mk.any(w, allow_half)
             check(L.moe_load_tensor(self._h, name.encode(), C.byref(m)))
@@ -271,8 +284,14 @@ class OffloadEngine:
             k = ExpertKey(*key)
             if owner_of(k.expert, cfg.n_experts, self.ep_world) != self.ep_rank:
                 continue  # another rank's expert
+            trip = expert_triple(payload)
+            if all(_is_serialized(w) for w in trip):  # serialized blocks, parsed in C++
+                bufs = [bytes(w) for w in trip]
+                check(L.moe_load_expert_serialized(self._h, k.layer, k.expert,
+                                                   *[a for b in bufs for a in (b, len(b))]))
+                continue
             mk = _Marshal()
-            ms = [mk.any(w) for w in expert_triple(payload)]
+            ms = [mk.any(w) for w in trip]
             check(L.moe_load_expert(self._h, k.layer, k.expert, *[C.byref(m) for m in ms]))
 
     # ------------------------------------------------------------ expert parallel

@@ -147,3 +147,36 @@ class DeviceStoreSim:
             l, e = keys[0]
             if phys["content"][b] != l * self.E + e:
                 raise AssertionError(f"buffer {b} does not hold {keys[0]}")
+
+
+def replay_device(trace, cache: CacheConfig, speculation=None):
+    """The reference ``replay`` (engine.py:263-313) driven through the engine's
+    device store code: prompt positions batched layer by layer (each distinct
+    expert acquired once per layer), generated positions token by token with
+    the speculative guesses re-evaluated from the recorded hidden states.
+    Returns the simulator (``.events`` is the log to compare with
+    ``replay(trace, cache, speculation).events``)."""
+    from moe_offload.engine import SpeculationConfig
+    from moe_offload.model import top_k_select
+    spec = speculation or SpeculationConfig()
+    m = spec.m if spec.enabled else 0
+    trace.validate()
+    sim = DeviceStoreSim(trace.n_layers, trace.n_experts, cache, top_k=trace.top_k, m=max(m, 1))
+    by_tok = {}
+    for r in trace.records:
+        by_tok.setdefault(r.token_pos, []).append(r)
+    prompt = [t for t in sorted(by_tok) if t < trace.prompt_len]
+    gen = [t for t in sorted(by_tok) if t >= trace.prompt_len]
+    if prompt:
+        for ell in range(trace.n_layers):
+            ex = np.array([next(r for r in by_tok[t] if r.layer == ell).experts for t in prompt],
+                          np.int32)
+            sim.resolve_prefill(ell, ex)
+    for t in gen:
+        for r in sorted(by_tok[t], key=lambda r: r.layer):
+            target = r.layer + spec.lookahead
+            guesses = ()
+            if m > 0 and target < trace.n_layers:
+                guesses = [int(e) for e in top_k_select(trace.gate_logits(target, r.hidden), m)]
+            sim.resolve_token(r.layer, t, list(r.experts), guesses, target if guesses else -1)
+    return sim

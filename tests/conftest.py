@@ -12,7 +12,13 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
 def pytest_sessionstart(session):
-    """(Re)build libmoeb200.so when a source is newer (no-op otherwise)."""
+    """Install the unmodified reference into baseline/_ref when it is missing
+    (the package imports its value types from moe_offload), then (re)build
+    libmoeb200.so when a source is newer (no-op otherwise)."""
+    if (not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "moe_offload"))
+            and os.path.isdir("/root/reference/pkg")):
+        import subprocess
+        subprocess.run(["bash", os.path.join(ROOT, "tools", "install_reference.sh")], check=True)
     from paper_2312_17238_b200 import build
     build.build()
 

@@ -290,3 +290,31 @@ def test_mixtral_width_batched_prefill_equals_per_position(bits, n, monkeypatch)
     assert a[3] == b[3]
     assert np.array_equal(a[4], b[4])
     assert np.array_equal(a[5], b[5])
+
+
+def test_engine_from_serialized_blocks_equals_engine_from_blocks(c1_models):
+    """§8(f)3: expert payloads and attention blocks handed over as the
+    reference's serialized bytes (quant.serialize_block, e.g. read from disk)
+    are parsed in C++ (csrc/blockio.cu) straight into the pinned arena and the
+    device weights; the engine then matches the one built from block objects
+    bit for bit (logits, tokens, store events)."""
+    from oracle import quant as OQ
+    from paper_2312_17238_b200 import CacheConfig, ExpertKey, OffloadEngine, SpeculationConfig
+    cfg, get = c1_models
+    model, pay, attn = get((4, 3))
+    pay = {ExpertKey(*k): v for k, v in pay.items()}
+    ser_pay = {k: tuple(OQ.serialize(b) for b in v) for k, v in pay.items()}
+    ser_attn = {k: OQ.serialize(v) for k, v in attn.items()}
+    prompt = make_prompt(3, 7, cfg.vocab_size)
+    outs = []
+    for p, a in ((pay, attn), (ser_pay, ser_attn)):
+        eng = OffloadEngine(model, CacheConfig(k=2, b=4), SpeculationConfig(True, 2),
+                            payloads=p, attn_blocks=a)
+        logits = np.asarray(eng.prefill(prompt)).copy()
+        r = eng.decode(6)
+        outs.append((logits, r.tokens, r.final_logits.copy(), _ev_rows(eng.events),
+                     eng.cache.expert_bytes))
+        eng.close()
+    a, b = outs
+    assert np.array_equal(a[0], b[0]) and a[1] == b[1] and np.array_equal(a[2], b[2])
+    assert a[3] == b[3] and a[4] == b[4]

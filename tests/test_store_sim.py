@@ -179,3 +179,31 @@ def test_copy_engine_policy_never_deadlocks(k, b, m, progress):
     assert rows(sim.events) == orows(ref.events)
     chunks = _lib.lib().moe_store_sim_chunks(sim._h)
     assert chunks <= 4 * sim.copies  # stale speculative jobs may be dropped, never duplicated
+
+
+def test_trace_replay_through_device_store_equals_reference_replay():
+    """§8(f)2: the reference ``replay`` of a recorded trace (engine.py:263-313)
+    and the same trace driven through the engine's device store code
+    (store_sim.replay_device) give identical event logs over a k x m grid,
+    speculation re-evaluated from the recorded hidden states."""
+    from moe_offload.engine import OffloadEngine as RefEngine, SpeculationConfig, replay
+    from moe_offload.model import build_model, toy_config
+    from paper_2312_17238_b200.store_sim import replay_device
+    cfg = toy_config(vocab_size=32, d_model=32, n_layers=4, n_heads=4, d_ffn=48, n_experts=8,
+                     max_seq_len=128)
+    model = build_model(cfg)
+    eng = RefEngine(model, CacheConfig(k=2, b=4), SpeculationConfig(True, 2))
+    prompt = [int(t) for t in np.random.default_rng(7).integers(0, 32, 6)]
+    eng.prefill(prompt)
+    eng.decode(20, sampler="categorical", sampler_seed=1)
+    tr = eng.trace()
+    for k in (0, 1, 2, 4, 8):
+        for m in (0, 1, 2, 4):
+            spec = SpeculationConfig(enabled=m > 0, m=max(m, 1))
+            cache = CacheConfig(k=k, b=4, expert_bytes=eng.store.config.expert_bytes)
+            ref = replay(tr, cache, spec).events
+            dev = replay_device(tr, cache, spec).events
+            assert dev == ref, (k, m)
+    live = replay(tr, CacheConfig(k=2, b=4, expert_bytes=eng.store.config.expert_bytes),
+                  SpeculationConfig(True, 2)).events
+    assert live == eng.events
