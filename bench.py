@@ -83,16 +83,9 @@ def measured_peaks():
 
 
 def ep_budget(k, b, m, n_experts, rank, world):
-    """Expert parallel under the single-GPU budget: the node-wide
-    cache of k experts per layer and b staging buffers is split over the ranks
-    (rank r gets floor(k/N) + (r < k % N) slots, capped by the experts it owns),
-    so the node never caches more than one GPU would and offloading stays forced
-    at every N.  A rank left with b_r = 0 staging buffers cannot prefetch."""
-    from paper_2312_17238_b200.expert_parallel import owned_experts
-    own = len(owned_experts(n_experts, rank, world))
-    kr = min(own, k // world + (1 if rank < k % world else 0))
-    br = b // world + (1 if rank < b % world else 0)
-    return kr, br, min(m, br)
+    """Per-rank budget of an expert-parallel run (expert_parallel.rank_budget)."""
+    from paper_2312_17238_b200.expert_parallel import rank_budget
+    return rank_budget(k, b, m, n_experts, rank, world)
 
 
 class ClockSampler:
@@ -371,10 +364,11 @@ def run_b200(args, rank, world):
     if os.path.exists(prof_path):
         with open(prof_path) as fh:
             prof = json.load(fh)
-        if f"<{xb}>" in prof.get("kernel", ""):  # the capture is of this config's kernel
+        if f"<{xb}," in prof.get("kernel", ""):  # the capture is of this config's kernel
             traffic = prof.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm",
-                "kernel": f"k_gemv<{xb}> expert up-projection (W1+W3 of 2 experts)",
+                "kernel": f"k_mgemv<{xb},1> expert up-projection (W1+W3 of 2 experts, "
+                          f"integer tensor-core dequant-GEMV)",
                 "achieved": round(up_gbs, 1) if up_gbs else None, "peak": hbm, "unit": "GB/s",
                 "frac": round(up_gbs / hbm, 4) if up_gbs else None, "traffic": traffic,
                 "algorithmic_bytes_per_launch": up_bytes,

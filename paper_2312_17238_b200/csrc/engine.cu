@@ -456,7 +456,7 @@ struct moe_engine {
   int2* pf_cols = nullptr;       // device: [PB] identity, then up / down column tables
   int2* pf_cols_h = nullptr;     // pinned staging of the expert column tables
   RouteRec* pf_route_h = nullptr;  // pinned: the layer's routes (read after bookkeeping)
-  bool batched_prefill_ok() const;
+  bool batched_prefill_ok(int n) const;
   int prefill_alloc();
   int prefill_batched(int n);
   int enq_attention(int l, int p, int mode);
@@ -902,10 +902,14 @@ int moe_engine::enq_experts(int l, int p) {
 // expert, the (position, slot) pairs that chose it.  Each column is computed
 // exactly like the decode kernel computes it (same split geometry and
 // fixed-point sums), so prefill equals teacher-forced decode bit for bit.
-bool moe_engine::batched_prefill_ok() const {
+bool moe_engine::batched_prefill_ok(int n) const {
   if (ep_world > 1 || !xl_set) return false;
-  if (const char* v = getenv("MOE_PREFILL_BATCH"))
+  int min_n = 4;  // shorter prompts: the per-position path is faster (profiles/r2_prefill.md)
+  if (const char* v = getenv("MOE_PREFILL_BATCH")) {
     if (atoi(v) == 0) return false;
+    min_n = 1;  // forced on (tests)
+  }
+  if (n < min_n) return false;
   if (attn_bits > 4 || expert_bits > 4) return false;
   for (int l = 0; l < L; ++l)
     if (!wq[l].M.mma || !wk[l].M.mma || !wv[l].M.mma || !wo[l].M.mma) return false;
@@ -1848,7 +1852,7 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
     ep.site = 0;
     launch_embed(ep, e->s_comp, e->pdl);
   }
-  if (e->batched_prefill_ok()) {
+  if (e->batched_prefill_ok(n)) {
     rc = e->prefill_batched(n);
     if (rc) return rc;
   } else {

@@ -36,15 +36,24 @@ def owned_mask(n_layers: int, n_experts: int, rank: int, world: int) -> np.ndarr
     return m
 
 
-def local_cache_k(k: int, n_experts: int, world: int) -> int:
-    """Per-rank LRU capacity under a node-wide budget of k experts per layer:
-    the budget is split evenly and capped by the experts a rank owns."""
-    return min(-(-k // world), len(owned_experts(n_experts, 0, world)))
+def rank_budget(k: int, b: int, m: int, n_experts: int, rank: int, world: int):
+    """(k_r, b_r, m_r) of rank r under the single-GPU budget: the
+    node-wide cache of k experts per layer and b staging buffers is split over
+    the ranks -- rank r gets floor(k/N) + (r < k % N) slots, capped by the
+    experts it owns, and floor(b/N) + (r < b % N) staging buffers -- so the node
+    never caches more than one GPU would and offloading stays forced at every N
+    (at N = 8, k = 4: four ranks cache one expert per layer, four cache none).
+    A rank left with b_r = 0 staging buffers cannot prefetch (m_r = 0)."""
+    own = len(owned_experts(n_experts, rank, world))
+    kr = min(own, k // world + (1 if rank < k % world else 0))
+    br = b // world + (1 if rank < b % world else 0)
+    return kr, br, min(m, br)
 
 
 def slot_exchange(slots_local: np.ndarray, all_reduce) -> np.ndarray:
     """Sum-exchange of the (top_k, d) slot buffer; ``all_reduce`` is the
-    collective (NCCL on the GPU engine, gloo in the CPU tests)."""
+    collective (gloo in the CPU tests).  The GPU engine does the same exchange
+    inside its decode graph with k_exchange over peer memory (CUDA IPC)."""
     out = np.ascontiguousarray(slots_local, np.float32).copy()
     all_reduce(out)
     return out

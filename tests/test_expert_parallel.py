@@ -13,7 +13,7 @@ import socket
 import numpy as np
 import pytest
 
-from paper_2312_17238_b200.expert_parallel import (local_cache_k, owned_experts, owned_keys,
+from paper_2312_17238_b200.expert_parallel import (rank_budget, owned_experts, owned_keys,
                                                    owned_mask, owner_of)
 
 
@@ -27,7 +27,13 @@ def test_partition_covers_every_expert_once():
             assert sorted(seen) == list(range(E))
             assert all(owner_of(e, E, N) in range(N) for e in range(E))
     assert owned_keys(2, 8, 1, 2) == {(l, e) for l in range(2) for e in (4, 5, 6, 7)}
-    assert local_cache_k(4, 8, 2) == 2 and local_cache_k(2, 8, 8) == 1
+    # the node-wide budget is split, never exceeded: sum over ranks == k (and b)
+    for world in (1, 2, 4, 8):
+        for k, b, m in ((4, 4, 0), (2, 4, 2), (0, 4, 2), (8, 4, 1)):
+            rb = [rank_budget(k, b, m, 8, r, world) for r in range(world)]
+            assert sum(x[0] for x in rb) == min(k, 8) and sum(x[1] for x in rb) == b
+            assert all(x[2] <= x[1] and x[2] <= m for x in rb)
+    assert rank_budget(4, 4, 0, 8, 0, 8) == (1, 1, 0) and rank_budget(4, 4, 0, 8, 7, 8) == (0, 0, 0)
 
 
 def _free_port():
