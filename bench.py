@@ -242,7 +242,20 @@ def timeline_of(eng, prompt, world, nl):
         if ok[j]:
             kinds[nm] = {"avg_us": round((en[j] - st[j]) / 1e3, 2),
                          "sum_us": round((en[j] - st[j]) / 1e3, 1)}
+    # gaps: start of each kernel minus the end of the one before it in stream
+    # order (embed, per layer qkv .. down, combine, lm_head, logits)
+    order = [0] + [1 + 8 * l + i for l in range(nl) for i in range(6)]
+    order += [1 + 8 * (nl - 1) + 6, 1 + 8 * nl, 2 + 8 * nl]
+    order = [j for j in order if ok[j]]
+    gaps = {}
+    for a, b in zip(order, order[1:]):
+        nm = "lm_head" if b == 1 + 8 * nl else "logits" if b == 2 + 8 * nl else (
+            names[(b - 1) % 8] if b else "embed")
+        gaps.setdefault(nm, []).append((st[b] - en[a]) / 1e3)
+    gap_stats = {nm: {"median_us": round(float(np.median(v)), 2),
+                      "sum_us": round(float(np.sum(v)), 1)} for nm, v in gaps.items()}
     return {"token_span_us": round(float((en[ok].max() - t0) / 1e3), 1),
+            "gaps_before": gap_stats,
             "busy_sum_us": round(float(sum(v["sum_us"] for v in kinds.values())), 1),
             "kernels": kinds,
             "how": "one decode token, graph + PDL; per kernel earliest CTA start (after "
@@ -379,6 +392,17 @@ def run_b200(args, rank, world):
                                "attn_qkv": gbs(3 * attn_block, 0) and round(gbs(3 * attn_block, 0), 1),
                                "lm_head": gbs(cfg["d_model"] * V * 2, 4)
                                and round(gbs(cfg["d_model"] * V * 2, 4), 1)}}
+    # the same launch back to back (PDL on) over 400 MB of rotated synthetic
+    # weights of this shape (moe_bench_gemv): the kernel's steady-state duration
+    try:
+        mus, mgbs = C.c_double(), C.c_double()
+        det = (C.c_double * 4)()
+        _lib.check(L.moe_bench_gemv(xb, cfg["d_model"], cfg["d_ffn"], 4, 50, 1, C.byref(mus),
+                                    C.byref(mgbs), det))
+        roofline["microbench_us"] = round(mus.value, 2)
+        roofline["frac_microbench"] = round(up_bytes / (mus.value * 1e-6) / 1e9 / hbm, 4)
+    except Exception as ex:  # profiling aid only
+        roofline["microbench_error"] = str(ex)
     try:
         up_med = timeline["kernels"]["expert_up"]["median_us"]
         roofline["timeline_median_us"] = up_med

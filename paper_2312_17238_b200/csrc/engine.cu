@@ -335,6 +335,7 @@ struct moe_engine {
   float *x = nullptr, *h = nullptr, *xn = nullptr, *ctx = nullptr, *logits = nullptr;
   unsigned int tok_seq = 0;  // decode tokens issued (DecodeState.seq)
   bool pend_comb = false;  // decode: layer l's combine + LN1(l+1) is fused into QKV(l+1)
+  bool pend_qkv_reset = false;  // Q/K/V sums read by the fused attention, reset by W2
   // fixed-point split-K sums (reduce == 2)
   unsigned long long *wo_acc = nullptr, *dn_acc = nullptr, *qkv_acc = nullptr;
   float *qkv_part = nullptr, *wo_part = nullptr, *up_part = nullptr, *dn_part = nullptr,
@@ -384,6 +385,8 @@ struct moe_engine {
   bool trace_copies = false;   // MOE_COPY_TRACE=1: copier log on stderr
   bool pdl = true;             // programmatic dependent launch (MOE_PDL=0 disables)
   bool use_graph = true;       // one CUDA graph per decode token (MOE_GRAPH=0 disables)
+  bool attn_fused = true;      // decode attention in the Wo GEMV prologue (MOE_ATTN_FUSED=0)
+  bool copy_park = true;       // park speculative copies of passed layers (MOE_COPY_PARK=0)
   bool capturing = false;
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;
@@ -538,7 +541,8 @@ int moe_engine::run_copier() {
     int buf;
   };
   CopySched sched;
-  sched.init(nbuf, xbytes, copy_chunk);
+  sched.init(nbuf, xbytes, copy_chunk, sc.lookahead);
+  sched.park = copy_park;
   std::deque<Inflight> dq, sq;                    // demand / speculative stream chunks
   std::vector<cudaEvent_t> last_ev(nbuf, nullptr);  // last chunk issued to each buffer
   std::vector<cudaStream_t> last_stream(nbuf, nullptr);
@@ -699,6 +703,16 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   launch_gemv(attn_bits, q, nq, s_comp, pdl && !prof);
   prof_end(K_QKV);
   dbg("qkv", l, p);
+  // decode attention fused into the Wo GEMV's prologue (each Wo CTA computes its
+  // head dims of the context) when a CTA's input rows lie inside one head
+  const int wo_rows = Q_wo * mt::KS;
+  const bool fuse_attn = attn_fused && wo[l].M.mma && hd % 128 == 0 && wo_rows <= hd &&
+                         hd % wo_rows == 0 && q.j[0].reduce == 2;
+  // the fused attention reads the Q/K/V sums; decode: this layer's W2 GEMV resets
+  // them, a slice per CTA; per-position prefill: the tail (the next position's
+  // QKV GEMV adds into them before any W2 runs)
+  pend_qkv_reset = fuse_attn && cur_ds;
+  if (!fuse_attn) {
   AttnParams a{};
   a.qkv_part = qkv_part;
   a.S = S_qkv;
@@ -715,6 +729,7 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   a.T_max = T;
   launch_attention(a, s_comp, pl);
   dbg("attn", l, p);
+  }
   GLaunch o{};
   o.nj = 1;
   o.cnt = cnt;
@@ -723,6 +738,16 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   o.j[0] = dense_job(wo[l], ctx, wo_part, wo_out, Q_wo);
   o.j[0].reduce = 2;  // fixed-point split-K sums, read (and reset) by the tail
   o.j[0].acc = wo_acc;
+  if (fuse_attn) {
+    o.j[0].xmode = X_ATTN;
+    o.att_acc = qkv_acc;
+    o.att_kc = kc + (size_t)l * T * d;
+    o.att_vc = vc + (size_t)l * T * d;
+    o.att_ds = cur_ds;
+    o.att_pos = p;
+    o.att_hd = hd;
+    o.att_T = T;
+  }
   const int no = finalize_launch(o);
   prof_begin(K_WO);
   launch_gemv(attn_bits, o, no, s_comp, pdl && !prof);
@@ -758,6 +783,10 @@ int moe_engine::enq_attention(int l, int p, int mode) {
   t.pos = p;
   t.mode = mode;
   t.ep_size = 1;
+  if (fuse_attn && !cur_ds) {
+    t.zero = qkv_acc;
+    t.zero_n = 3 * d;
+  }
   if (tail_smem_bytes(t) > 226 * 1024) t.gh_l = t.gh_g = nullptr;  // gates too big to stage
   launch_tail(t, s_comp, pl);
   dbg("tail", l, p);
@@ -817,6 +846,11 @@ int moe_engine::enq_experts(int l, int p) {
   }
   u.nj = 2 * topk;
   dn.nj = topk;
+  if (pend_qkv_reset) {  // the fused attention (Wo prologue) read them: reset, a slice per CTA
+    dn.zero = qkv_acc;
+    dn.zero_n = 3 * d;
+    pend_qkv_reset = false;
+  }
   if (pend_comb) {  // the fused combine read dn_acc: reset it before W2 adds
     u.zero = dn_acc;
     u.zero_n = topk * d;
@@ -1408,6 +1442,8 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* tv = getenv("MOE_COPY_TRACE")) e->trace_copies = atoi(tv) != 0;
   if (const char* pv = getenv("MOE_PDL")) e->pdl = atoi(pv) != 0;
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
+  if (const char* av = getenv("MOE_ATTN_FUSED")) e->attn_fused = atoi(av) != 0;
+  if (const char* cp = getenv("MOE_COPY_PARK")) e->copy_park = atoi(cp) != 0;
   for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (const char* w = getenv("MOE_WAIT_TIMEOUT_MS")) e->wait_ns = 1000000ull * atoll(w);
   if (const char* a = getenv("MOE_AHEAD")) e->ahead = std::max(1, atoi(a));

@@ -625,7 +625,6 @@ __global__ void __launch_bounds__(MOE_GEMV_THREADS, MOE_GEMV_MINB)
     tl_end(P.site);
 }
 
-#include "mgemv_kernel.cuh"
 
 // ------------------------------------------------------------------ wait
 // Blocks the compute stream until every expert buffer of this position's route
@@ -685,8 +684,8 @@ MOE_DEV float ln_sum256(float v, float* red) {  // blockDim >= 256, all threads 
   __syncthreads();
   return t;
 }
-MOE_DEV void layernorm_block(const float* x, const float* g, const float* b, float* y, float* ysh,
-                             int d, float* red) {
+// LN statistics (mu, sqrt(var + eps)) in that rounding structure
+MOE_DEV float2 layernorm_stats(const float* x, int d, float* red) {
   const bool lane256 = threadIdx.x < 256;
   float s = 0.f;
   if (lane256)
@@ -699,9 +698,16 @@ MOE_DEV void layernorm_block(const float* x, const float* g, const float* b, flo
       q = fmaf(t, t, q);
     }
   const float var = __fdiv_rn(ln_sum256(q, red), (float)d);
-  const float den = sqrtf(__fadd_rn(var, 1e-5f));
+  return make_float2(mu, sqrtf(__fadd_rn(var, 1e-5f)));
+}
+MOE_DEV float layernorm_elem(float x, float2 st, float g, float b) {
+  return __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(x, st.x), st.y), g), b);
+}
+MOE_DEV void layernorm_block(const float* x, const float* g, const float* b, float* y, float* ysh,
+                             int d, float* red) {
+  const float2 st = layernorm_stats(x, d, red);
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float v = __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(x[i], mu), den), g[i]), b[i]);
+    const float v = layernorm_elem(x[i], st, g[i], b[i]);
     if (y) y[i] = v;
     if (ysh) ysh[i] = v;
   }
@@ -836,70 +842,20 @@ __global__ void __launch_bounds__(256) k_attention(AttnParams P) {
   }
 }
 
-// Fast path for head_dim % 128 == 0: one CTA of 256 threads per head.  The
-// current k/v row is appended first; scores use 4 threads per position (a
-// quarter of the K row each, all loads in flight, quad shuffle reduce), then
-// softmax and alpha @ V with each head dimension split over two threads.
-__global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
-  extern __shared__ float asm_[];  // q [HD], scores [T_max], ctx halves [2][HD]
-  __shared__ float red[33];
-  const int HD = P.hd, h = blockIdx.x, d = P.d;
-  const int tid = threadIdx.x;
-  float* q = asm_;
-  float* sc = asm_ + HD;
-  float* half2buf = sc + P.T_max;
-  gemv::pdl_trigger();
-  const size_t rstride = (size_t)P.H * HD;
-  if (P.ds) {  // decode: this head's K/V rows of earlier tokens are final -> pull them
-    // into L2 while the QKV GEMV runs (they were evicted by the weight stream)
-    const int pp = P.ds->pos;
-    const int lines = HD * 4 / 128;  // 128-byte lines per row
-    for (int i = tid; i < 2 * pp * lines; i += blockDim.x) {
-      const int t = i / (2 * lines), r = i % (2 * lines);
-      const float* base = (r < lines ? P.kc : P.vc) + (size_t)t * rstride + (size_t)h * HD;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (r % lines) * 32));
-    }
-  }
-  gemv::pdl_wait();
-  tl_begin(P.site);
-  const int pos = P.ds ? P.ds->pos : P.pos + (int)blockIdx.y;
-  const int T = pos + 1;
-  const float* qg = P.qkv_part + (size_t)h * HD;
-  float* krow = P.kc + (size_t)pos * rstride + (size_t)h * HD;
-  float* vrow = P.vc + (size_t)pos * rstride + (size_t)h * HD;
-  float* ctx = P.ctx + (size_t)blockIdx.y * d;
-  // KV append (model.py:293, KVCache.append); the QKV GEMV leaves its split-K
-  // partials [3][S][d] unreduced: summed here in split order
-  const size_t sstride = (size_t)P.S * d;
-  if (P.qbuf) {  // batched prefill: K/V rows appended by k_kv_append, q converted there
-    const float* qs = P.qbuf + (size_t)blockIdx.y * d + (size_t)h * HD;
-    for (int i = tid; i < HD; i += blockDim.x) q[i] = qs[i];
-  } else if (P.acc) {  // fixed-point sums of the QKV GEMV: read, then reset for the next layer
-    unsigned long long* qa = P.acc + (size_t)h * HD;
-    for (int i = tid; i < HD; i += blockDim.x) {
-      const unsigned long long a = __ldcg(qa + i), bk = __ldcg(qa + d + i),
-                               bv = __ldcg(qa + 2 * d + i);
-      q[i] = fx_val(a);
-      krow[i] = fx_val(bk);
-      vrow[i] = fx_val(bv);
-      qa[i] = qa[d + i] = qa[2 * d + i] = 0ull;
-    }
-  } else {
-    for (int i = tid; i < HD; i += blockDim.x) {
-      float a = 0.f, bk = 0.f, bv = 0.f;
-#pragma unroll 4
-      for (int s = 0; s < P.S; ++s) {
-        a += __ldcg(qg + (size_t)s * d + i);
-        bk += __ldcg(qg + sstride + (size_t)s * d + i);
-        bv += __ldcg(qg + 2 * sstride + (size_t)s * d + i);
-      }
-      q[i] = a;
-      krow[i] = bk;
-      vrow[i] = bv;
-    }
-  }
-  __syncthreads();
-  tl_mark(P.site, 0);
+// Scores, softmax and alpha @ V of one head over positions 0..pos for a
+// 256-thread CTA (model.py:294-299): q and the current position's k / v rows
+// in shared memory, earlier rows from the KV cache (kc / vc point at this
+// head's columns, row t at + t * rstride).  Scores use 4 threads per position
+// (a quarter of the K row each, all loads in flight, quad shuffle reduce),
+// then softmax, then alpha @ V with each head dimension split over two
+// partial sums (even / odd positions).  Writes head dims [c0, c0 + nd) to
+// out[0 .. nd).  Shared by k_attention128 and the Wo GEMV's fused attention
+// prologue (X_ATTN), so every decode / prefill path rounds alike.
+// sc: >= pos + 1 floats, hb: 2 * nd floats, red: 33 floats (shared).
+__device__ __noinline__ void attend_head(const float* q, const float* kcur, const float* vcur, const float* kc,
+                         const float* vc, size_t rstride, int pos, int HD, int c0, int nd,
+                         float* sc, float* hb, float* red, float* out) {
+  const int tid = threadIdx.x, T = pos + 1;
   const float rs = sqrtf((float)HD);
   {
     const int g = tid & 3, nf = HD / 16;  // float4s per quarter row
@@ -909,13 +865,15 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
     for (int t0 = tw; t0 < T; t0 += step) {
       const int t = t0 + ((tid & 31) >> 2);
       const bool live = t < T;
-      const float4* kr = reinterpret_cast<const float4*>(
-                             P.kc + (size_t)(live ? t : 0) * rstride + (size_t)h * HD) + g * nf;
+      const bool cur = t == pos;  // the current row lives in shared memory
+      const float4* kr = reinterpret_cast<const float4*>(kc + (size_t)(live && !cur ? t : 0) *
+                                                              rstride) + g * nf;
+      const float4* ks = reinterpret_cast<const float4*>(kcur) + g * nf;
       float a0 = 0.f, a1 = 0.f;
       for (int c = 0; c < nf; c += 8) {
         float4 kv[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) kv[u] = __ldcg(kr + c + u);
+        for (int u = 0; u < 8; ++u) kv[u] = cur ? ks[c + u] : __ldcg(kr + c + u);
 #pragma unroll
         for (int u = 0; u < 8; u += 2) {
           const float4 x0 = q4[c + u], x1 = q4[c + u + 1];
@@ -931,7 +889,6 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
     }
   }
   __syncthreads();
-  tl_mark(P.site, 1);
   float mx = -INFINITY;
   for (int t = tid; t < T; t += blockDim.x) mx = fmaxf(mx, sc[t]);
   mx = warp_max(mx);
@@ -949,31 +906,105 @@ __global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
   su = block_sum_f(su, red);
   for (int t = tid; t < T; t += blockDim.x) sc[t] = __fdiv_rn(sc[t], su);
   __syncthreads();
-  tl_mark(P.site, 2);
-  {
-    const int half = tid / 128, i0 = tid & 127;
-    for (int i = i0; i < HD; i += 128) {
-      const float* vcol = P.vc + (size_t)h * HD + i;
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-      int t = half;
-      for (; t + 6 < T; t += 8) {
-        const float v0 = __ldcg(vcol + (size_t)t * rstride),
-                    v1 = __ldcg(vcol + (size_t)(t + 2) * rstride),
-                    v2 = __ldcg(vcol + (size_t)(t + 4) * rstride),
-                    v3 = __ldcg(vcol + (size_t)(t + 6) * rstride);
-        a0 = fmaf(sc[t], v0, a0);
-        a1 = fmaf(sc[t + 2], v1, a1);
-        a2 = fmaf(sc[t + 4], v2, a2);
-        a3 = fmaf(sc[t + 6], v3, a3);
+  // item (half, j): dim c0 + j summed over positions half, half + 2, ...
+  for (int w = tid; w < 2 * nd; w += blockDim.x) {
+    const int half = w / nd, j = w % nd, i = c0 + j;
+    const float* vcol = vc + i;
+    const float vp = vcur[i];
+    auto ld = [&](int t) { return t == pos ? vp : __ldcg(vcol + (size_t)t * rstride); };
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int t = half;
+    for (; t + 6 < T; t += 8) {
+      const float v0 = ld(t), v1 = ld(t + 2), v2 = ld(t + 4), v3 = ld(t + 6);
+      a0 = fmaf(sc[t], v0, a0);
+      a1 = fmaf(sc[t + 2], v1, a1);
+      a2 = fmaf(sc[t + 4], v2, a2);
+      a3 = fmaf(sc[t + 6], v3, a3);
+    }
+    for (; t < T; t += 2) a0 = fmaf(sc[t], ld(t), a0);
+    hb[half * nd + j] = (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
+  for (int j = tid; j < nd; j += blockDim.x) out[j] = hb[j] + hb[nd + j];
+}
+
+// pull a head's K/V cache rows of positions < pos into L2 (decode: they were
+// evicted by the weight stream) -- issued before griddepcontrol.wait
+MOE_DEV void prefetch_kv(const float* kc, const float* vc, size_t rstride, int pos, int HD) {
+  const int lines = HD * 4 / 128;  // 128-byte lines per row
+  for (int i = threadIdx.x; i < 2 * pos * lines; i += blockDim.x) {
+    const int t = i / (2 * lines), r = i % (2 * lines);
+    const float* base = (r < lines ? kc : vc) + (size_t)t * rstride;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (r % lines) * 32));
+  }
+}
+
+// Fast path for head_dim % 128 == 0: one CTA of 256 threads per head.  The
+// current k/v row is appended to the cache, then attend_head.
+__global__ void __launch_bounds__(256) k_attention128(AttnParams P) {
+  // q [HD], k / v of this position [HD] each, scores [T_max], ctx halves [2][HD]
+  extern __shared__ float asm_[];
+  __shared__ float red[33];
+  const int HD = P.hd, h = blockIdx.x, d = P.d;
+  const int tid = threadIdx.x;
+  float* q = asm_;
+  float* kcur = q + HD;
+  float* vcur = kcur + HD;
+  float* sc = vcur + HD;
+  float* half2buf = sc + P.T_max;
+  gemv::pdl_trigger();
+  const size_t rstride = (size_t)P.H * HD;
+  if (P.ds)
+    prefetch_kv(P.kc + (size_t)h * HD, P.vc + (size_t)h * HD, rstride, P.ds->pos, HD);
+  gemv::pdl_wait();
+  tl_begin(P.site);
+  const int pos = P.ds ? P.ds->pos : P.pos + (int)blockIdx.y;
+  const float* qg = P.qkv_part + (size_t)h * HD;
+  float* krow = P.kc + (size_t)pos * rstride + (size_t)h * HD;
+  float* vrow = P.vc + (size_t)pos * rstride + (size_t)h * HD;
+  float* ctx = P.ctx + (size_t)blockIdx.y * d;
+  // KV append (model.py:293, KVCache.append)
+  const size_t sstride = (size_t)P.S * d;
+  if (P.qbuf) {  // batched prefill: K/V rows appended by k_kv_append, q converted there
+    const float* qs = P.qbuf + (size_t)blockIdx.y * d + (size_t)h * HD;
+    for (int i = tid; i < HD; i += blockDim.x) {
+      q[i] = qs[i];
+      kcur[i] = krow[i];
+      vcur[i] = vrow[i];
+    }
+  } else if (P.acc) {  // fixed-point sums of the QKV GEMV: read, then reset for the next layer
+    unsigned long long* qa = P.acc + (size_t)h * HD;
+    for (int i = tid; i < HD; i += blockDim.x) {
+      const unsigned long long a = __ldcg(qa + i), bk = __ldcg(qa + d + i),
+                               bv = __ldcg(qa + 2 * d + i);
+      q[i] = fx_val(a);
+      kcur[i] = krow[i] = fx_val(bk);
+      vcur[i] = vrow[i] = fx_val(bv);
+      qa[i] = qa[d + i] = qa[2 * d + i] = 0ull;
+    }
+  } else {  // split-K partials [3][S][d], summed in split order
+    for (int i = tid; i < HD; i += blockDim.x) {
+      float a = 0.f, bk = 0.f, bv = 0.f;
+#pragma unroll 4
+      for (int s = 0; s < P.S; ++s) {
+        a += __ldcg(qg + (size_t)s * d + i);
+        bk += __ldcg(qg + sstride + (size_t)s * d + i);
+        bv += __ldcg(qg + 2 * sstride + (size_t)s * d + i);
       }
-      for (; t < T; t += 2) a0 = fmaf(sc[t], __ldcg(vcol + (size_t)t * rstride), a0);
-      half2buf[half * HD + i] = (a0 + a1) + (a2 + a3);
+      q[i] = a;
+      kcur[i] = krow[i] = bk;
+      vcur[i] = vrow[i] = bv;
     }
   }
   __syncthreads();
-  for (int i = tid; i < HD; i += blockDim.x) ctx[h * HD + i] = half2buf[i] + half2buf[HD + i];
+  tl_mark(P.site, 0);
+  attend_head(q, kcur, vcur, P.kc + (size_t)h * HD, P.vc + (size_t)h * HD, rstride, pos, HD, 0,
+              HD, sc, half2buf, red, ctx + (size_t)h * HD);
   tl_end(P.site);
 }
+
+// the tensor-core dequant-GEMV (uses attend_head for the fused decode attention)
+#include "mgemv_kernel.cuh"
 
 // batched prefill: the Q/K/V fixed-point sums of `rows` positions -> q rows
 // (qbuf) and the K/V cache rows of positions pos .. pos + rows - 1, sums reset
@@ -1001,9 +1032,9 @@ __global__ void __launch_bounds__(256) k_kv_append(AttnParams P) {
 // (engine.py:222-231).
 // tail: hs = x + Wo output (fp32 partial or fixed-point sums, reset after
 // the loads), V values per thread with every load in flight first
-template <int V, bool FX>
+template <int V, bool FX, class Mid>
 MOE_DEV void residual_in(const TailParams& P, const float* xin, unsigned long long* acc, float* hs,
-                         int tid) {
+                         int tid, Mid&& mid) {
   const int d = P.d, nt = (int)blockDim.x;
   float xa[V], pa[V];
   unsigned long long qa[FX ? V : 1];
@@ -1016,6 +1047,7 @@ MOE_DEV void residual_in(const TailParams& P, const float* xin, unsigned long lo
     else
       pa[u] = i < d ? __ldcg(P.part + i) : 0.f;
   }
+  mid();  // more independent loads (store state, flags) while these are in flight
 #pragma unroll
   for (int u = 0; u < V; ++u) {
     const int i = tid + u * nt;
@@ -1070,6 +1102,8 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   }
   gemv::pdl_wait();
   tl_begin(P.site);
+  if (P.zero)  // Q/K/V sums read by the Wo GEMV's fused attention: reset for the next layer
+    for (int i = tid; i < P.zero_n; i += blockDim.x) P.zero[i] = 0ull;
   // batched prefill (mode 1): CTA r handles position P.pos + r
   const int row = P.mode == 1 ? (int)blockIdx.x : 0;
   const int pos = P.ds ? P.ds->pos : P.pos + row;
@@ -1080,48 +1114,69 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   const size_t slot = (size_t)pos * P.n_layers + P.layer;
   float* th = P.trace_hidden ? P.trace_hidden + slot * d : nullptr;
   StoreDev S = P.st;
-  if (P.mode == 0) {
-    S = store::stage_in(P.st, sst);  // overlaps the residual loads
-    // snapshot of the buffers' published copy generations: a routed buffer
-    // whose copy had landed is marked ready, so the GEMVs skip the flag wait
-    if (P.st.flags)
-      for (int i = tid; i < P.st.nbuf; i += blockDim.x)
-        fls[i] = ld_acquire_u32(const_cast<const uint32_t*>(P.st.flags) + i);
-  }
+  // the store state and the copy-flag snapshot (decode) load while the
+  // residual's loads are in flight: one L2 round trip instead of three
+  auto stage = [&]() {
+    if (P.mode != 0) return;
+    const int n4 = P.st.state_ints >> 2;
+    if (n4 <= (int)blockDim.x && P.st.nbuf <= (int)blockDim.x) {
+      // one element per thread: every load is issued before any shared store
+      const int4* src = reinterpret_cast<const int4*>(P.st.state_base);
+      int4 v = make_int4(0, 0, 0, 0);
+      int vt = 0;
+      uint32_t fv = 0;
+      const int ti = 4 * n4 + tid;
+      if (tid < n4) v = __ldcg(src + tid);
+      if (ti < P.st.state_ints) vt = __ldcg(P.st.state_base + ti);
+      // snapshot of the buffers' published copy generations: a routed buffer
+      // whose copy had landed is marked ready, so the GEMVs skip the flag wait
+      if (P.st.flags && tid < P.st.nbuf)
+        fv = ld_acquire_u32(const_cast<const uint32_t*>(P.st.flags) + tid);
+      if (tid < n4) reinterpret_cast<int4*>(sst)[tid] = v;
+      if (ti < P.st.state_ints) sst[ti] = vt;
+      if (P.st.flags && tid < P.st.nbuf) fls[tid] = fv;
+      S = store::stage_view(P.st, sst);
+    } else {
+      S = store::stage_in(P.st, sst);
+      if (P.st.flags)
+        for (int i = tid; i < P.st.nbuf; i += blockDim.x)
+          fls[i] = ld_acquire_u32(const_cast<const uint32_t*>(P.st.flags) + i);
+    }
+  };
   // residual: all loads first, then the stores (no load waits behind a store)
   if (accr) {
     if (d <= 4 * (int)blockDim.x)
-      residual_in<4, true>(P, xin, accr, hs, tid);
+      residual_in<4, true>(P, xin, accr, hs, tid, stage);
     else
-      residual_in<8, true>(P, xin, accr, hs, tid);
+      residual_in<8, true>(P, xin, accr, hs, tid, stage);
   } else {
-    residual_in<8, false>(P, xin, accr, hs, tid);  // d <= 8192 with 1024 threads
+    residual_in<8, false>(P, xin, accr, hs, tid, stage);  // d <= 8192 with 1024 threads
   }
   tl_mark(P.site, 0);
   gemv::mbar_wait(&wbar, 0);
   __syncthreads();
   tl_mark(P.site, 1);
-  layernorm_block(hs, g2s, b2s, hout, hs, d, reinterpret_cast<float*>(gpart));
-  __syncthreads();
+  const float2 lst = layernorm_stats(hs, d, reinterpret_cast<float*>(gpart));
   tl_mark(P.site, 2);
-  int bad = 0;
-  for (int i = tid; i < d; i += blockDim.x) {
-    if (!isfinite(hs[i])) bad = 1;
-    if (th) th[i] = hs[i];
-  }
-  bad = __syncthreads_or(bad);
   // gate logits of this layer and the guessed layer on the same h (model.py:210,
-  // engine.py:60-68): thread t owns expert t % E over rows t/E, t/E + nt/E, ...
+  // engine.py:60-68)
   const int nt = (blockDim.x / E) * E;
   const bool gate8 = hg && E == 8;  // fast path: one 16-byte fp16 gate row per load
+  int bad = 0;
   if (gate8) {
-    // thread t takes rows t, t + nthreads, ... for all 8 experts (and the
-    // guessed layer's 8): fp32 partials, then double sums in a fixed order
+    // LN2 (model.py:300-301) fused with the gate partials: thread t normalizes
+    // rows t, t + nthreads, ... and accumulates them for all 8 experts (and the
+    // guessed layer's 8) in that order -- fp32 partials, then double sums in a
+    // fixed order
     float pa[8], pg[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) pa[e] = pg[e] = 0.f;
     for (int r = tid; r < d; r += blockDim.x) {
-      const float hv = hs[r];
+      const float hv = layernorm_elem(hs[r], lst, g2s[r], b2s[r]);
+      hout[r] = hv;
+      if (th) th[r] = hv;
+      if (!isfinite(hv)) bad = 1;
+      if (guess) hs[r] = hv;  // re-read by this thread for the guessed gate
       const uint4 gl4 = *reinterpret_cast<const uint4*>(gls + (size_t)r * 8);
       const __half2* gl2 = reinterpret_cast<const __half2*>(&gl4);
 #pragma unroll
@@ -1130,7 +1185,10 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
         pa[2 * e] = fmaf(hv, g.x, pa[2 * e]);
         pa[2 * e + 1] = fmaf(hv, g.y, pa[2 * e + 1]);
       }
-      if (guess) {
+    }
+    if (guess)  // same rows, same order (second pass keeps registers under 64)
+      for (int r = tid; r < d; r += blockDim.x) {
+        const float hv = hs[r];
         const uint4 gg4 = *reinterpret_cast<const uint4*>(ggs + (size_t)r * 8);
         const __half2* gg2 = reinterpret_cast<const __half2*>(&gg4);
 #pragma unroll
@@ -1140,7 +1198,6 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
           pg[2 * e + 1] = fmaf(hv, g.y, pg[2 * e + 1]);
         }
       }
-    }
     // fp32 butterfly sums of the 8 (16) partials, interleaved so the
     // shuffles of different logits overlap; warp sums go to double below
 #pragma unroll
@@ -1158,36 +1215,47 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
         gpart[warp * 16 + 8 + e] = (double)pg[e];
       }
     }
-  } else if (tid < nt) {
-    const int e = tid % E, rstep = nt / E;
-    // per-thread fp32 partials over 2 interleaved accumulators, combined in
-    // double across threads (fixed order below)
-    float a0 = 0.f, a1 = 0.f, g0 = 0.f, g1 = 0.f;
-    int r = tid / E;
-    if (hg) {
-      for (; r + rstep < d; r += 2 * rstep) {
-        const float h0 = hs[r], h1 = hs[r + rstep];
-        a0 = fmaf(h0, __half2float(gls[r * E + e]), a0);
-        a1 = fmaf(h1, __half2float(gls[(r + rstep) * E + e]), a1);
-        if (guess) {
-          g0 = fmaf(h0, __half2float(ggs[r * E + e]), g0);
-          g1 = fmaf(h1, __half2float(ggs[(r + rstep) * E + e]), g1);
+    bad = __syncthreads_or(bad);
+  } else {
+    for (int i = tid; i < d; i += blockDim.x) {
+      const float v = layernorm_elem(hs[i], lst, g2s[i], b2s[i]);
+      hout[i] = v;
+      if (th) th[i] = v;
+      if (!isfinite(v)) bad = 1;
+      hs[i] = v;
+    }
+    bad = __syncthreads_or(bad);
+    if (tid < nt) {
+      const int e = tid % E, rstep = nt / E;
+      // per-thread fp32 partials over 2 interleaved accumulators, combined in
+      // double across threads (fixed order below)
+      float a0 = 0.f, a1 = 0.f, g0 = 0.f, g1 = 0.f;
+      int r = tid / E;
+      if (hg) {
+        for (; r + rstep < d; r += 2 * rstep) {
+          const float h0 = hs[r], h1 = hs[r + rstep];
+          a0 = fmaf(h0, __half2float(gls[r * E + e]), a0);
+          a1 = fmaf(h1, __half2float(gls[(r + rstep) * E + e]), a1);
+          if (guess) {
+            g0 = fmaf(h0, __half2float(ggs[r * E + e]), g0);
+            g1 = fmaf(h1, __half2float(ggs[(r + rstep) * E + e]), g1);
+          }
+        }
+        if (r < d) {
+          a0 = fmaf(hs[r], __half2float(gls[r * E + e]), a0);
+          if (guess) g0 = fmaf(hs[r], __half2float(ggs[r * E + e]), g0);
+        }
+      } else {
+        for (; r < d; r += rstep) {
+          a0 = fmaf(hs[r], __ldg(P.gate_l + r * E + e), a0);
+          if (guess) g0 = fmaf(hs[r], __ldg(P.gate_g + r * E + e), g0);
         }
       }
-      if (r < d) {
-        a0 = fmaf(hs[r], __half2float(gls[r * E + e]), a0);
-        if (guess) g0 = fmaf(hs[r], __half2float(ggs[r * E + e]), g0);
-      }
-    } else {
-      for (; r < d; r += rstep) {
-        a0 = fmaf(hs[r], __ldg(P.gate_l + r * E + e), a0);
-        if (guess) g0 = fmaf(hs[r], __ldg(P.gate_g + r * E + e), g0);
-      }
+      gpart[tid] = (double)a0 + (double)a1;
+      gpart[blockDim.x + tid] = (double)g0 + (double)g1;
     }
-    gpart[tid] = (double)a0 + (double)a1;
-    gpart[blockDim.x + tid] = (double)g0 + (double)g1;
+    __syncthreads();
   }
-  __syncthreads();
   tl_mark(P.site, 3);
   const int nlog = guess ? 2 * E : E;
   if (gate8) {  // logit e: the warps' sums in warp order
@@ -1720,8 +1788,11 @@ static void launch_mgemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool p
     xs_cap = max(xs_cap, rows);
     rbf = max(rbf, J.M.rb_full);
     const int n = (J.xmode == X_SWIGLU ? 2 : 1) * (J.xS > 1 ? J.xS : 1);
-    xin_cap = max(xin_cap, J.xmode == X_COMBINE ? J.M.K * 4 : n * 4 * rows);
+    xin_cap = max(xin_cap, J.xmode == X_COMBINE ? J.M.K * 4
+                           : J.xmode == X_ATTN ? (3 * P.att_hd + P.att_T + 2 * rows + 40) * 4
+                                               : n * 4 * rows);
   }
+  xin_cap = (xin_cap + 15) & ~15;
   const int zs_cap = gemv_zs_cap(P, B, xs_cap, rbf, 1);
   const MgSmem L(xs_cap, zs_cap, xin_cap, NM);
   const int stage = mma_units(B) * rbf;
@@ -1810,13 +1881,13 @@ void launch_layernorm(const float* x, const float* g, const float* b, float* y, 
 void launch_attention_rows(const AttnParams& P, int rows, cudaStream_t s) {
   launch_small(k_kv_append, dim3((P.d + 255) / 256, rows), dim3(256), 0, s, false, P);
   launch_small(k_attention128, dim3(P.H, rows), dim3(256),
-               (size_t)(3 * P.hd + P.T_max) * sizeof(float), s, false, P);
+               (size_t)(5 * P.hd + P.T_max) * sizeof(float), s, false, P);
 }
 
 void launch_attention(const AttnParams& P, cudaStream_t s, bool pdl) {
   if (P.hd % 128 == 0) {
     launch_small(k_attention128, dim3(P.H), dim3(256),
-                 (size_t)(3 * P.hd + P.T_max) * sizeof(float), s, pdl, P);
+                 (size_t)(5 * P.hd + P.T_max) * sizeof(float), s, pdl, P);
     return;
   }
   const size_t smem = (size_t)(P.hd + P.T_max) * sizeof(float);

@@ -30,7 +30,10 @@ __host__ __device__ constexpr int mma_units(int bits) { return bits == 3 ? MOE_U
 // combine of the previous layer, model.py:251-254, fused with the next LN):
 // every CTA forms the full residual (fixed-point expert sums, reference
 // order) and its LN statistics; block 0 also stores the residual
-enum XMode { X_PLAIN = 0, X_SWIGLU = 1, X_COMBINE = 2 };
+// X_ATTN (decode Wo): the input rows are the CTA's head dims of the attention
+// context, computed in the prologue (attend_head, model.py:294-299) from the
+// QKV fixed-point sums and the KV cache; one CTA per head appends the k / v rows
+enum XMode { X_PLAIN = 0, X_SWIGLU = 1, X_COMBINE = 2, X_ATTN = 3 };
 
 struct GJob {
   MatDev M;            // absolute pointers, or byte offsets when rel_slot >= 0
@@ -80,6 +83,13 @@ struct GLaunch {
   int* err;
   unsigned long long wait_ns;
   int site;  // timeline slot of this launch (profiling), -1 none
+  // X_ATTN jobs: q/k/v sums [3][d] (reset later by the tail), this layer's KV
+  // cache [T][H][hd], the position (decode cursor, else att_pos)
+  const unsigned long long* att_acc;
+  float* att_kc;
+  float* att_vc;
+  const DecodeState* att_ds;
+  int att_pos, att_hd, att_T;
 };
 
 // Split-K by fixed-point atomics (GJob.reduce == 2): each CTA adds its fp32
@@ -133,6 +143,8 @@ struct TailParams {
   int d, E, top_k, m, layer, guess_layer, pos, mode;  // mode 0 decode, 1 prefill (no store)
   int ep_rank, ep_size;   // expert parallel (ep_size 1 = off)
   int site;  // timeline slot of this launch (profiling), -1 none
+  unsigned long long* zero;  // optional: sums consumed by the fused attention (Q/K/V), reset
+  int zero_n;
 };
 
 struct PrefillBKParams {

@@ -150,6 +150,12 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
   }
   __syncthreads();
   gemv::pdl_trigger();
+  const bool xattn = J.xmode == X_ATTN;
+  const int ahead = xattn ? row0 / P.att_hd : 0, ac0 = xattn ? row0 % P.att_hd : 0;
+  const bool awriter = xattn && cb == 0 && ac0 == 0;  // appends the head's k / v rows
+  if (awriter && P.att_ds)  // decode: earlier K/V rows were evicted by the weight streams
+    prefetch_kv(P.att_kc + (size_t)ahead * P.att_hd, P.att_vc + (size_t)ahead * P.att_hd, M.K,
+                P.att_ds->pos, P.att_hd);
 
   int ebuf = 0;
   if (expert) {
@@ -161,6 +167,11 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
                                     : J.part + (size_t)s * M.N;
       if (zdst)
         for (int t = threadIdx.x; t < nout; t += NT) zdst[obase + t] = 0.f;
+      if (P.zero) {  // this CTA's slice of the consumed sums (see below)
+        const int per = (P.zero_n + gridDim.x - 1) / gridDim.x;
+        const int a = blockIdx.x * per, e = min(P.zero_n, a + per);
+        for (int i = a + threadIdx.x; i < e; i += NT) P.zero[i] = 0ull;
+      }
       return;
     }
   }
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
   };
   // x rows of the CTA: one bulk copy per input array and column
   // (xin [column][array][part][rows]; partials [xparts][rows])
-  const bool xstage = !xcomb && nrows > 0;
+  const bool xstage = !xcomb && !xattn && nrows > 0;
   const int xbytes = nrows * 4;
   const int narr = swiglu ? 2 : 1;
   if (threadIdx.x == 0) {
@@ -274,6 +285,33 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
                                 __ldg(J.lnb + r));
       xs[i] = v;
     }
+  } else if (xattn && nrows > 0) {  // fused decode attention of this CTA's head dims
+    const int HD = P.att_hd, d = M.K;
+    float* q = reinterpret_cast<float*>(xin);
+    float* kcur = q + HD;
+    float* vcur = kcur + HD;
+    float* asc = vcur + HD;
+    float* hb = asc + P.att_T;
+    float* red = hb + 2 * nrows;
+    const int pos = P.att_ds ? P.att_ds->pos : P.att_pos;
+    const unsigned long long* qa = P.att_acc + (size_t)ahead * HD;
+    float* krow = P.att_kc + (size_t)pos * d + (size_t)ahead * HD;
+    float* vrow = P.att_vc + (size_t)pos * d + (size_t)ahead * HD;
+    for (int i = threadIdx.x; i < HD; i += NT) {
+      const unsigned long long a = __ldcg(qa + i), bk = __ldcg(qa + d + i),
+                               bv = __ldcg(qa + 2 * d + i);
+      q[i] = fx_val(a);
+      kcur[i] = fx_val(bk);
+      vcur[i] = fx_val(bv);
+      if (awriter) {  // KV append (model.py:293, KVCache.append)
+        krow[i] = kcur[i];
+        vrow[i] = vcur[i];
+      }
+    }
+    __syncthreads();
+    attend_head(q, kcur, vcur, P.att_kc + (size_t)ahead * HD, P.att_vc + (size_t)ahead * HD, d,
+                pos, HD, ac0, nrows, asc, hb, red, xs);
+    __syncthreads();
   } else if (xstage) {
     gemv::mbar_wait(xbar, 0);
     for (int c = 0; c < NC; ++c) {

@@ -304,14 +304,8 @@ __device__ __forceinline__ T* rebase(T* p, const int* from, int* to) {
                                reinterpret_cast<const char*>(from)));
 }
 
-// all threads: view of global store G backed by `sm` (16-byte aligned)
-__device__ __forceinline__ StoreDev stage_in(const StoreDev& G, int* sm) {
-  const int n4 = G.state_ints >> 2;
-  const int4* src = reinterpret_cast<const int4*>(G.state_base);
-  int4* dst = reinterpret_cast<int4*>(sm);
-  for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = __ldcg(src + i);
-  for (int i = 4 * n4 + threadIdx.x; i < G.state_ints; i += blockDim.x)
-    sm[i] = __ldcg(G.state_base + i);
+// the store G with every state pointer rebased into the shared copy `sm`
+__device__ __forceinline__ StoreDev stage_view(const StoreDev& G, int* sm) {
   StoreDev V = G;
   V.lru = rebase(G.lru, G.state_base, sm);
   V.lru_len = rebase(G.lru_len, G.state_base, sm);
@@ -325,7 +319,19 @@ __device__ __forceinline__ StoreDev stage_in(const StoreDev& G, int* sm) {
   V.free_stack = rebase(G.free_stack, G.state_base, sm);
   V.pending = rebase(G.pending, G.state_base, sm);
   V.gen = rebase(G.gen, G.state_base, sm);
-  return V;  // (caller synchronizes before use)
+  return V;
+}
+
+// all threads: copy the state of global store G to `sm` (16-byte aligned)
+// and return the view backed by it (caller synchronizes before use)
+__device__ __forceinline__ StoreDev stage_in(const StoreDev& G, int* sm) {
+  const int n4 = G.state_ints >> 2;
+  const int4* src = reinterpret_cast<const int4*>(G.state_base);
+  int4* dst = reinterpret_cast<int4*>(sm);
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = __ldcg(src + i);
+  for (int i = 4 * n4 + threadIdx.x; i < G.state_ints; i += blockDim.x)
+    sm[i] = __ldcg(G.state_base + i);
+  return stage_view(G, sm);
 }
 
 // all threads: write the staged state back

@@ -318,3 +318,32 @@ def test_engine_from_serialized_blocks_equals_engine_from_blocks(c1_models):
     a, b = outs
     assert np.array_equal(a[0], b[0]) and a[1] == b[1] and np.array_equal(a[2], b[2])
     assert a[3] == b[3] and a[4] == b[4]
+
+
+def test_mixtral_width_fused_attention_equals_attention_kernel(monkeypatch):
+    """The decode attention fused into the Wo GEMV prologue (X_ATTN: every Wo
+    CTA computes its head dims with attend_head) gives bit-identical logits,
+    tokens, trace and events to the separate per-head attention kernel
+    (MOE_ATTN_FUSED=0), including the KV rows later tokens read back."""
+    import bench
+    from paper_2312_17238_b200 import CacheConfig, OffloadEngine, SpeculationConfig
+    from paper_2312_17238_b200 import synthetic_model
+    cfg = dict(bench.MIXTRAL)
+    cfg["n_layers"] = 2
+    cobj = bench.cfg_obj(cfg)
+    prompt = [int(t) for t in np.random.default_rng(11).integers(0, cobj.vocab_size, 3)]
+    outs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("MOE_ATTN_FUSED", fused)
+        eng = OffloadEngine(synthetic_model(cobj, 0), CacheConfig(k=2, b=4),
+                            SpeculationConfig(enabled=True, m=2), record_hidden=True,
+                            synth=(0, 4, 3), expert_bytes=bench.expert_bytes(bench.MIXTRAL, 3))
+        logits = np.asarray(eng.prefill(prompt)).copy()
+        r = eng.decode(40)
+        tr = eng.trace()
+        outs.append((logits, r.tokens, r.final_logits.copy(), _ev_rows(eng.events),
+                     np.stack([x.hidden for x in tr.records])))
+        eng.close()
+    a, b = outs
+    assert np.array_equal(a[0], b[0]) and a[1] == b[1] and np.array_equal(a[2], b[2])
+    assert a[3] == b[3] and np.array_equal(a[4], b[4])
