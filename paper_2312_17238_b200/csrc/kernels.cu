@@ -13,9 +13,12 @@
 #include "gemv.cuh"
 #include "mma_gemv.cuh"
 
-__device__ TimelineSlot* g_timeline = nullptr;
-__device__ int g_timeline_n = 0;  // span slots; phase marks follow
-__device__ unsigned long long* g_cta_trace = nullptr;  // GEMV microbench: [cta][4]
+// profiling hooks in constant memory: every kernel tests them after
+// griddepcontrol.wait, where a global-memory pointer load would cost an L2
+// round trip on the critical path (a constant-cache hit costs a few cycles)
+__constant__ TimelineSlot* g_timeline = nullptr;
+__constant__ int g_timeline_n = 0;  // span slots; phase marks follow
+__constant__ unsigned long long* g_cta_trace = nullptr;  // GEMV microbench: [cta][4]
 
 namespace {
 
@@ -672,7 +675,7 @@ MOE_DEV float block_sum_f(float v, float* red) {
 // with separately rounded float32 ops.  x, g, b may live in shared memory.
 // The statistics are reduced over exactly 256 lanes (thread t sums x[t +
 // 256k] in k order, butterfly warp sums, then the 8 warp sums in order)
-// whatever the block size, so every LN site -- the 1024-thread kernels and
+// whatever the block size, so every LN site -- the 512/1024-thread kernels and
 // the QKV GEMV's fused combine + LN1 on its 8 consumer warps -- rounds alike.
 MOE_DEV float ln_sum256(float v, float* red) {  // blockDim >= 256, all threads call
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1033,9 +1036,9 @@ __global__ void __launch_bounds__(256) k_kv_append(AttnParams P) {
 // tail: hs = x + Wo output (fp32 partial or fixed-point sums, reset after
 // the loads), V values per thread with every load in flight first
 template <int V, bool FX, class Mid>
-MOE_DEV void residual_in(const TailParams& P, const float* xin, unsigned long long* acc, float* hs,
-                         int tid, Mid&& mid) {
-  const int d = P.d, nt = (int)blockDim.x;
+MOE_DEV void residual_in(const float* part, const float* xin, unsigned long long* acc, float* hs,
+                         int tid, Mid&& mid, int d) {
+  const int nt = (int)blockDim.x;
   float xa[V], pa[V];
   unsigned long long qa[FX ? V : 1];
 #pragma unroll
@@ -1045,7 +1048,7 @@ MOE_DEV void residual_in(const TailParams& P, const float* xin, unsigned long lo
     if constexpr (FX)
       qa[u] = i < d ? __ldcg(acc + i) : 0ull;
     else
-      pa[u] = i < d ? __ldcg(P.part + i) : 0.f;
+      pa[u] = i < d ? __ldcg(part + i) : 0.f;
   }
   mid();  // more independent loads (store state, flags) while these are in flight
 #pragma unroll
@@ -1062,7 +1065,23 @@ MOE_DEV void residual_in(const TailParams& P, const float* xin, unsigned long lo
     }
 }
 
-__global__ void __launch_bounds__(1024) k_tail(TailParams P) {
+// rows beyond 8 per thread (d > 8 * blockDim): further passes of 8
+template <bool FX, class Mid>
+MOE_DEV void residual_all(const TailParams& P, const float* xin, unsigned long long* acc,
+                          float* hs, int tid, Mid&& mid) {
+  const int d = P.d, span = 8 * (int)blockDim.x;
+  auto none = []() {};
+  for (int b = 0; b < d; b += span) {
+    if (b == 0)
+      residual_in<8, FX>(P.part, xin, acc, hs, tid, mid, min(span, d));
+    else
+      residual_in<8, FX>(P.part + b, xin + b, FX ? acc + b : acc, hs + b, tid, none,
+                         min(span, d - b));
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_tail(TailParams P) {
   extern __shared__ __align__(128) unsigned char tsm[];
   const int d = P.d, E = P.E;
   const bool guess = P.gate_g != nullptr;
@@ -1146,11 +1165,11 @@ __global__ void __launch_bounds__(1024) k_tail(TailParams P) {
   // residual: all loads first, then the stores (no load waits behind a store)
   if (accr) {
     if (d <= 4 * (int)blockDim.x)
-      residual_in<4, true>(P, xin, accr, hs, tid, stage);
+      residual_in<4, true>(P.part, xin, accr, hs, tid, stage, d);
     else
-      residual_in<8, true>(P, xin, accr, hs, tid, stage);
+      residual_all<true>(P, xin, accr, hs, tid, stage);
   } else {
-    residual_in<8, false>(P, xin, accr, hs, tid, stage);  // d <= 8192 with 1024 threads
+    residual_all<false>(P, xin, accr, hs, tid, stage);
   }
   tl_mark(P.site, 0);
   gemv::mbar_wait(&wbar, 0);
@@ -1664,7 +1683,8 @@ cudaError_t preload_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)k_gemv<2>,   (const void*)k_gemv<3>,  (const void*)k_gemv<4>,
                        (const void*)k_gemv<16>,  (const void*)k_gemv<32>, (const void*)k_embed,
-                       (const void*)k_layernorm, (const void*)k_attention, (const void*)k_tail,
+                       (const void*)k_layernorm, (const void*)k_attention,
+                       (const void*)k_tail<MOE_TAIL_THREADS>,
                        (const void*)k_prefill_bk, (const void*)k_begin_call,
                        (const void*)k_combine,   (const void*)k_logits, (const void*)k_wait_ready,
                        (const void*)k_exchange, (const void*)k_kv_append,
@@ -1695,7 +1715,8 @@ cudaError_t preload_kernels() {
   cudaError_t e = cudaFuncSetAttribute((const void*)k_attention,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute((const void*)k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute((const void*)k_tail<MOE_TAIL_THREADS>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                               226 * 1024);  // + static shared memory <= 227 KB
 }
 
@@ -1904,7 +1925,8 @@ int tail_smem_bytes(const TailParams& P) {
 }
 
 void launch_tail(const TailParams& P, cudaStream_t s, bool pdl, int rows) {
-  launch_small(k_tail, dim3(rows), dim3(1024), (size_t)tail_smem_bytes(P), s, pdl, P);
+  launch_small(k_tail<MOE_TAIL_THREADS>, dim3(rows), dim3(MOE_TAIL_THREADS),
+               (size_t)tail_smem_bytes(P), s, pdl, P);
 }
 
 void launch_prefill_bk(const PrefillBKParams& P, cudaStream_t s) {

@@ -21,6 +21,10 @@ __host__ __device__ constexpr int gemv_qs(int bits) { return MOE_GEMV_WARPS * ge
 #ifndef MOE_UPS3
 #define MOE_UPS3 2
 #endif
+// threads of the tail kernel (one CTA per position)
+#ifndef MOE_TAIL_THREADS
+#define MOE_TAIL_THREADS 512
+#endif
 #define MOE_MMA_UNITS_MAX 64       // k-steps per CTA in the tensor-core layout (B table)
 // k-steps per pipeline stage of the tensor-core layout (a compile-time count so
 // the consumer loop is unrolled and its shared-memory loads run ahead)
@@ -90,6 +94,10 @@ struct GLaunch {
   float* att_vc;
   const DecodeState* att_ds;
   int att_pos, att_hd, att_T;
+  // expert jobs: the route was final before this grid started (the previous
+  // launch is an expert GEMV, which triggers its dependents only after its own
+  // griddepcontrol.wait), so it is read, and the weights streamed, pre-wait
+  int route_early;
 };
 
 // Split-K by fixed-point atomics (GJob.reduce == 2): each CTA adds its fp32

@@ -149,7 +149,14 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
     gemv::mbar_fence_init();
   }
   __syncthreads();
-  gemv::pdl_trigger();
+  // dense jobs release the next kernel at once; expert jobs only once the
+  // route is final (below), so a successor may read it before its own wait
+  if (!expert) gemv::pdl_trigger();
+  // route_early: the route was final before this grid started (the previous
+  // kernel triggers only after its own wait on the route's producer), so the
+  // weight stream starts before griddepcontrol.wait -- during the previous
+  // kernel's last CTAs -- and only the x rows wait for it
+  const bool early = expert && P.route_early;
   const bool xattn = J.xmode == X_ATTN;
   const int ahead = xattn ? row0 / P.att_hd : 0, ac0 = xattn ? row0 % P.att_hd : 0;
   const bool awriter = xattn && cb == 0 && ac0 == 0;  // appends the head's k / v rows
@@ -159,9 +166,11 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
 
   int ebuf = 0;
   if (expert) {
-    gemv::pdl_wait();  // the route is written by the previous kernel (tail)
-    ebuf = route->buf[J.rel_slot];
+    if (!early) gemv::pdl_wait();  // the route is written by the previous kernel (tail)
+    ebuf = __ldcg(route->buf + J.rel_slot);
+    gemv::pdl_trigger();
     if (ebuf < 0) {  // expert parallel: another rank owns this expert
+      if (early) gemv::pdl_wait();
       float* zdst = J.reduce == 2 ? nullptr
                     : J.reduce == 1 ? (s == 0 ? J.out : nullptr)
                                     : J.part + (size_t)s * M.N;
@@ -195,8 +204,8 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
     const __half2* zmeta = M.zmeta;
     const __half* scl = M.scl;
     if (expert) {
-      if (!route->ready[J.rel_slot])
-        wait_flag(P.flags + ebuf, route->gen[J.rel_slot], P.err, P.wait_ns);
+      if (!__ldcg(route->ready + J.rel_slot))
+        wait_flag(P.flags + ebuf, __ldcg(route->gen + J.rel_slot), P.err, P.wait_ns);
       const uint8_t* b = P.pool + (long long)ebuf * P.slot_stride;
       base = b + reinterpret_cast<size_t>(base);
       zmeta = reinterpret_cast<const __half2*>(b + reinterpret_cast<size_t>(zmeta));
@@ -216,7 +225,7 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
       pol = gemv::policy_evict_first();
       for (int it = 0; it < min(nst, nit); ++it) issue(it);  // dense: before the wait
     }
-    if (!expert) gemv::pdl_wait();  // x is the previous kernel's output
+    if (!expert || early) gemv::pdl_wait();  // x is the previous kernel's output
     if (xstage) {
       gemv::mbar_arrive_tx(xbar, (uint32_t)(nc * narr * xparts) * (uint32_t)xbytes);
       const size_t pstride = (size_t)J.xstride * 4;
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
       }
     }
   }
-  if (!expert) gemv::pdl_wait();
+  if (!expert || early) gemv::pdl_wait();
   tl_begin(P.site);  // (after the wait: the span excludes the previous kernel)
   cta_mark(0);
   if (P.zero) {  // reset sums an earlier kernel consumed (a slice per CTA)
@@ -248,18 +257,20 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
     const int K = M.K;
     const float w0 = route->w[0], w1 = J.ctop > 1 ? route->w[1] : 0.f;
     float sum = 0.f;
-    for (int i0 = threadIdx.x; i0 < K; i0 += 8 * NT) {
-      float hv[8];
-      unsigned long long q0[8], q1[8];
+    // every load in flight at once (K <= 16 * NT: one round trip)
+    constexpr int CV = 16;
+    for (int i0 = threadIdx.x; i0 < K; i0 += CV * NT) {
+      float hv[CV];
+      unsigned long long q0[CV], q1[CV];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < CV; ++u) {
         const int i = i0 + u * NT;
         hv[u] = i < K ? __ldcg(J.x + i) : 0.f;
         q0[u] = i < K ? __ldcg(J.cacc + i) : 0ull;
         q1[u] = (i < K && J.ctop > 1) ? __ldcg(J.cacc + K + i) : 0ull;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < CV; ++u) {
         const int i = i0 + u * NT;
         if (i < K) {
           float o = __fadd_rn(hv[u], __fmul_rn(w0, fx_val(q0[u])));  // model.py:251-254

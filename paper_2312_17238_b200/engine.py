@@ -370,6 +370,8 @@ class OffloadEngine:
             fin = np.empty(V, np.float32)
             rc = lib().moe_decode_greedy(self._h, int(n_tokens), toks.ctypes.data_as(_lib.IP),
                                          fin.ctypes.data_as(_lib.FP))
+            if rc:  # e.g. past max_seq_len: the tokens that fit were decoded (reference order)
+                self._pos = int(lib().moe_num_trace(self._h)) // self.model.config.n_layers
             check(rc)
             self._pos += n_tokens
             self._last_logits = fin

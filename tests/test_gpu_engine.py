@@ -347,3 +347,35 @@ def test_mixtral_width_fused_attention_equals_attention_kernel(monkeypatch):
     a, b = outs
     assert np.array_equal(a[0], b[0]) and a[1] == b[1] and np.array_equal(a[2], b[2])
     assert a[3] == b[3] and np.array_equal(a[4], b[4])
+
+
+def test_decode_past_max_seq_len_matches_reference(c1_models):
+    """KVCache.append (model.py:265-268): decoding past max_seq_len decodes the
+    tokens that fit, then raises ValueError('position T exceeds max_seq_len=T');
+    the event log, trace and position match the reference engine's state after
+    the same exception."""
+    import dataclasses
+
+    from moe_offload.engine import OffloadEngine as RefEngine
+    from moe_offload.engine import SpeculationConfig as RSpec
+    from moe_offload.model import Model as RModel, ModelConfig as RConfig
+    from paper_2312_17238_b200 import CacheConfig
+    cfg, get = c1_models
+    model, pay, attn = get(None)
+    T = cfg.max_seq_len
+    prompt = make_prompt(9, T - 3, cfg.vocab_size)
+    rmodel = RModel(RConfig(**dataclasses.asdict(cfg)), model.params)  # the same weights
+    ref = RefEngine(rmodel, CacheConfig(k=2, b=4), RSpec(enabled=False))
+    ref.prefill(prompt)
+    with pytest.raises(ValueError) as re_:
+        ref.decode(6)
+    eng = _engine(model, pay, attn, 2, 4, 0)
+    eng.prefill(prompt)
+    with pytest.raises(ValueError) as ge:
+        eng.decode(6)
+    assert str(ge.value) == str(re_.value)
+    assert len(eng.trace().records) == len(ref.trace().records)
+    assert [r.experts for r in eng.trace().records] == [r.experts for r in ref.trace().records]
+    assert _ev_rows(eng.events) == _ev_rows(ref.events)
+    with pytest.raises(ValueError):
+        eng.prefill(make_prompt(9, T + 1, cfg.vocab_size))
