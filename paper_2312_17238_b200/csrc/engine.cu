@@ -387,7 +387,6 @@ struct moe_engine {
   bool use_graph = true;       // one CUDA graph per decode token (MOE_GRAPH=0 disables)
   bool attn_fused = true;      // decode attention in the Wo GEMV prologue (MOE_ATTN_FUSED=0)
   bool copy_park = true;       // park speculative copies of passed layers (MOE_COPY_PARK=0)
-  bool route_early = true;     // W2 reads its route / streams weights pre-wait (MOE_ROUTE_EARLY=0)
   bool capturing = false;
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;
@@ -808,7 +807,6 @@ int moe_engine::enq_experts(int l, int p) {
   u.site = site_of(l, 4);
   GLaunch dn = u;
   dn.site = site_of(l, 5);
-  dn.route_early = route_early;  // W2 follows W1||W3, which triggers after its route wait
   for (int j = 0; j < topk; ++j) {
     for (int m = 0; m < 2; ++m) {
       GJob& J = u.j[2 * j + m];
@@ -1446,7 +1444,6 @@ int moe_create(const moe_model_desc* md, const moe_cache_cfg* cc, const moe_spec
   if (const char* gv = getenv("MOE_GRAPH")) e->use_graph = atoi(gv) != 0;
   if (const char* av = getenv("MOE_ATTN_FUSED")) e->attn_fused = atoi(av) != 0;
   if (const char* cp = getenv("MOE_COPY_PARK")) e->copy_park = atoi(cp) != 0;
-  if (const char* re = getenv("MOE_ROUTE_EARLY")) e->route_early = atoi(re) != 0;
   for (auto& ev : e->tok_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (const char* w = getenv("MOE_WAIT_TIMEOUT_MS")) e->wait_ns = 1000000ull * atoll(w);
   if (const char* a = getenv("MOE_AHEAD")) e->ahead = std::max(1, atoi(a));

@@ -8,6 +8,7 @@
 // then layernorm(ln_f) | gemv<f16>(lm_head) | logits (+ argmax on device).
 // All reductions are in a fixed order, so results are run-to-run deterministic.
 #include <atomic>
+#include <cstdio>
 
 #include "kernels.cuh"
 #include "gemv.cuh"

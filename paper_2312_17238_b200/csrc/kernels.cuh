@@ -94,10 +94,6 @@ struct GLaunch {
   float* att_vc;
   const DecodeState* att_ds;
   int att_pos, att_hd, att_T;
-  // expert jobs: the route was final before this grid started (the previous
-  // launch is an expert GEMV, which triggers its dependents only after its own
-  // griddepcontrol.wait), so it is read, and the weights streamed, pre-wait
-  int route_early;
 };
 
 // Split-K by fixed-point atomics (GJob.reduce == 2): each CTA adds its fp32

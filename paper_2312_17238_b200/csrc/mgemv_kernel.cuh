@@ -149,14 +149,7 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
     gemv::mbar_fence_init();
   }
   __syncthreads();
-  // dense jobs release the next kernel at once; expert jobs only once the
-  // route is final (below), so a successor may read it before its own wait
-  if (!expert) gemv::pdl_trigger();
-  // route_early: the route was final before this grid started (the previous
-  // kernel triggers only after its own wait on the route's producer), so the
-  // weight stream starts before griddepcontrol.wait -- during the previous
-  // kernel's last CTAs -- and only the x rows wait for it
-  const bool early = expert && P.route_early;
+  gemv::pdl_trigger();
   const bool xattn = J.xmode == X_ATTN;
   const int ahead = xattn ? row0 / P.att_hd : 0, ac0 = xattn ? row0 % P.att_hd : 0;
   const bool awriter = xattn && cb == 0 && ac0 == 0;  // appends the head's k / v rows
@@ -166,11 +159,12 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
 
   int ebuf = 0;
   if (expert) {
-    if (!early) gemv::pdl_wait();  // the route is written by the previous kernel (tail)
+    // the route is written by the previous kernel (tail).  (Reading it before
+    // this wait, even when the previous kernel triggers its dependents only
+    // after its own wait on the tail, was measured to see stale routes.)
+    gemv::pdl_wait();
     ebuf = __ldcg(route->buf + J.rel_slot);
-    gemv::pdl_trigger();
     if (ebuf < 0) {  // expert parallel: another rank owns this expert
-      if (early) gemv::pdl_wait();
       float* zdst = J.reduce == 2 ? nullptr
                     : J.reduce == 1 ? (s == 0 ? J.out : nullptr)
                                     : J.part + (size_t)s * M.N;
@@ -225,7 +219,7 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
       pol = gemv::policy_evict_first();
       for (int it = 0; it < min(nst, nit); ++it) issue(it);  // dense: before the wait
     }
-    if (!expert || early) gemv::pdl_wait();  // x is the previous kernel's output
+    if (!expert) gemv::pdl_wait();  // x is the previous kernel's output
     if (xstage) {
       gemv::mbar_arrive_tx(xbar, (uint32_t)(nc * narr * xparts) * (uint32_t)xbytes);
       const size_t pstride = (size_t)J.xstride * 4;
@@ -242,7 +236,7 @@ __global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
       }
     }
   }
-  if (!expert || early) gemv::pdl_wait();
+  if (!expert) gemv::pdl_wait();
   tl_begin(P.site);  // (after the wait: the span excludes the previous kernel)
   cta_mark(0);
   if (P.zero) {  // reset sums an earlier kernel consumed (a slice per CTA)
