@@ -238,6 +238,18 @@ def timeline_of(eng, prompt, world, nl):
                 ph[str(p)] = round(float(np.median(v)), 2)
         if ph:
             kinds[nm]["phase_marks_us"] = ph
+    # the tail's store bookkeeping (thread 0; marks in the exchange slot, kind 7,
+    # relative to the tail's span start): 0 start, 1 begin_call, 2.. acquires,
+    # 6 speculation done, 7 route written
+    if "tail" in kinds and not any(ok[1 + 8 * l + 7] for l in range(nl)):
+        ph = {}
+        for p in range(8):
+            v = [(marks[1 + 8 * l + 7, p] - st[1 + 8 * l + 3]) / 1e3 for l in range(nl)
+                 if ok[1 + 8 * l + 3] and marks[1 + 8 * l + 7, p] > st[1 + 8 * l + 3]]
+            if v:
+                ph[str(p)] = round(float(np.median(v)), 2)
+        if ph:
+            kinds["tail"]["bookkeeping_marks_us"] = ph
     for nm, j in (("embed", 0), ("lm_head", 1 + 8 * nl), ("logits", 2 + 8 * nl)):
         if ok[j]:
             kinds[nm] = {"avg_us": round((en[j] - st[j]) / 1e3, 2),

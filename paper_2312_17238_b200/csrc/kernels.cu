@@ -1369,8 +1369,9 @@ __global__ void __launch_bounds__(NT, 1) k_tail(TailParams P) {
       }
     } else if (P.mode == 0) {
       const int m = (guess && P.m > 0) ? P.m : 0;
+      const int msite = P.site + 4;  // profiling marks in the (unused) exchange slot
       store::resolve_token(S, P.layer, sel_sh, k, gsel_sh, m, m ? P.guess_layer : -1, pos, rbuf,
-                           rgen);
+                           rgen, [msite](int i) { tl_mark(msite, i); });
     }
 #pragma unroll
     for (int j = 0; j < MOE_MAX_TOPK; ++j) {
@@ -1380,7 +1381,7 @@ __global__ void __launch_bounds__(NT, 1) k_tail(TailParams P) {
       route->ready[j] = (P.mode == 0 && P.st.flags && b >= 0 && j < k)
                               ? (int)((int)(fls[b] - rgen[j]) >= 0) : 0;
     }
-    tl_mark(P.site + 4, 1);  // store bookkeeping done
+    tl_mark(P.site + 4, 7);  // route written
   }
   tl_mark(P.site, 6);
   if (P.mode == 0) {

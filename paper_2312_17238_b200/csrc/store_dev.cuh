@@ -349,16 +349,26 @@ __device__ __forceinline__ void stage_out(const StoreDev& G, const int* sm) {
 // order, then speculative_load the top-m guesses for layer + lookahead.
 // bufs/gens receive the physical buffer (and its copy generation) of each
 // selected expert; -1 for experts another EP rank owns.
+struct NoMark {
+  MOE_HD void operator()(int) const {}
+};
+
+// mark(i) after each step (profiling: 1 begin_call, 2 + j acquire j, 6 speculation)
+template <class Mark = NoMark>
 MOE_HD void resolve_token(StoreDev& S, int layer, const int* sel, int k, const int* guesses,
-                          int m, int guess_layer, int pos, int* bufs, uint32_t* gens) {
+                          int m, int guess_layer, int pos, int* bufs, uint32_t* gens,
+                          Mark mark = Mark()) {
   begin_call(S);
+  mark(1);
   for (int j = 0; j < k; ++j) {
     const bool in_range = layer >= 0 && layer < S.L && sel[j] >= 0 && sel[j] < S.E;
     // out of range -> UnknownExpertError; in range but another rank's -> -1
     bufs[j] = (!in_range || key_ok(S, layer, sel[j])) ? acquire(S, layer, sel[j], pos) : -1;
+    mark(2 + (j < 3 ? j : 3));
   }
   if (guess_layer >= 0 && m > 0) speculative_load(S, guess_layer, guesses, m, pos, layer);
   for (int j = 0; j < k; ++j) gens[j] = bufs[j] >= 0 ? S.gen[bufs[j]] : 0u;
+  mark(6);
 }
 
 // One prefill layer (engine.py:233-240): every distinct expert acquired once,
