@@ -1690,11 +1690,11 @@ cudaError_t preload_kernels() {
                        (const void*)k_prefill_bk, (const void*)k_begin_call,
                        (const void*)k_combine,   (const void*)k_logits, (const void*)k_wait_ready,
                        (const void*)k_exchange, (const void*)k_kv_append,
-                       (const void*)k_mgemv<2, 1>,
-                       (const void*)k_mgemv<3, 1>, (const void*)k_mgemv<4, 1>,
-                       (const void*)k_mgemv<2, MG_PREFILL_NM>,
-                       (const void*)k_mgemv<3, MG_PREFILL_NM>,
-                       (const void*)k_mgemv<4, MG_PREFILL_NM>};
+                       (const void*)k_mgemv<2, 1, 1>,
+                       (const void*)k_mgemv<3, 1, 1>, (const void*)k_mgemv<4, 1, 1>,
+                       (const void*)k_mgemv<2, MG_PREFILL_NM, MG_PREFILL_CPG>,
+                       (const void*)k_mgemv<3, MG_PREFILL_NM, MG_PREFILL_CPG>,
+                       (const void*)k_mgemv<4, MG_PREFILL_NM, MG_PREFILL_CPG>};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -1705,11 +1705,11 @@ cudaError_t preload_kernels() {
     if (e != cudaSuccess) return e;
   }
   for (const void* f : {(const void*)k_embed, (const void*)k_combine,
-                        (const void*)k_attention128, (const void*)k_mgemv<2, 1>,
-                        (const void*)k_mgemv<3, 1>, (const void*)k_mgemv<4, 1>,
-                        (const void*)k_mgemv<2, MG_PREFILL_NM>,
-                        (const void*)k_mgemv<3, MG_PREFILL_NM>,
-                        (const void*)k_mgemv<4, MG_PREFILL_NM>}) {
+                        (const void*)k_attention128, (const void*)k_mgemv<2, 1, 1>,
+                        (const void*)k_mgemv<3, 1, 1>, (const void*)k_mgemv<4, 1, 1>,
+                        (const void*)k_mgemv<2, MG_PREFILL_NM, MG_PREFILL_CPG>,
+                        (const void*)k_mgemv<3, MG_PREFILL_NM, MG_PREFILL_CPG>,
+                        (const void*)k_mgemv<4, MG_PREFILL_NM, MG_PREFILL_CPG>}) {
     cudaError_t e2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           224 * 1024);
     if (e2 != cudaSuccess) return e2;
@@ -1801,9 +1801,9 @@ static void launch_gemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pd
 
 // tensor-core layout (k_mgemv): x staging for every job (the full residual for
 // the fused combine), the zmeta slice, scales + B table, then the ring
-template <int B, int NM>
+template <int B, int NM, int CPG>
 static void launch_mgemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
-  constexpr int NC = mg_cols(NM);
+  constexpr int NC = mg_cols(NM, CPG);
   int xs_cap = 0, rbf = 0, xin_cap = 0;
   for (int i = 0; i < P.nj; ++i) {
     const GJob& J = P.j[i];
@@ -1817,10 +1817,10 @@ static void launch_mgemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool p
   }
   xin_cap = (xin_cap + 15) & ~15;
   const int zs_cap = gemv_zs_cap(P, B, xs_cap, rbf, 1);
-  const MgSmem L(xs_cap, zs_cap, xin_cap, NM);
+  const MgSmem L(xs_cap, zs_cap, xin_cap, NM, CPG);
   const int stage = mma_units(B) * rbf;
   // 2 CTAs per SM for decode; the batched kernel runs 1 CTA per SM
-  const long long cap = NM == 1 ? MOE_GEMV_SMEM_CAP : 220 * 1024;
+  const long long cap = NM * CPG <= 2 ? MOE_GEMV_SMEM_CAP : 220 * 1024;
   int nst = (int)((cap - (long long)L.ring) / stage);
   nst = nst < 2 ? 2 : (nst > 8 ? 8 : nst);
   const int ring = max(nst * stage, NC * 12 * 1024);  // the epilogue reuses the ring
@@ -1834,16 +1834,16 @@ static void launch_mgemv_t(const GLaunch& P, int nblocks, cudaStream_t s, bool p
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_mgemv<B, NM>, P, xs_cap, zs_cap, xin_cap, nst, stage);
+  cudaLaunchKernelEx(&cfg, k_mgemv<B, NM, CPG>, P, xs_cap, zs_cap, xin_cap, nst, stage);
   g_launches.fetch_add(1);
 }
 
 void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool pdl) {
   if (bits <= 4 && P.j[0].M.mma) {
     switch (bits) {
-      case 2: launch_mgemv_t<2, 1>(P, nblocks, s, pdl); return;
-      case 3: launch_mgemv_t<3, 1>(P, nblocks, s, pdl); return;
-      default: launch_mgemv_t<4, 1>(P, nblocks, s, pdl); return;
+      case 2: launch_mgemv_t<2, 1, 1>(P, nblocks, s, pdl); return;
+      case 3: launch_mgemv_t<3, 1, 1>(P, nblocks, s, pdl); return;
+      default: launch_mgemv_t<4, 1, 1>(P, nblocks, s, pdl); return;
     }
   }
   switch (bits) {
@@ -1858,9 +1858,9 @@ void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool p
 // batched prefill: MG_PREFILL_NM column groups (2 columns each) per CTA
 void launch_gemv_cols(int bits, const GLaunch& P, int nblocks, cudaStream_t s) {
   switch (bits) {
-    case 2: launch_mgemv_t<2, MG_PREFILL_NM>(P, nblocks, s, false); return;
-    case 3: launch_mgemv_t<3, MG_PREFILL_NM>(P, nblocks, s, false); return;
-    default: launch_mgemv_t<4, MG_PREFILL_NM>(P, nblocks, s, false); return;
+    case 2: launch_mgemv_t<2, MG_PREFILL_NM, MG_PREFILL_CPG>(P, nblocks, s, false); return;
+    case 3: launch_mgemv_t<3, MG_PREFILL_NM, MG_PREFILL_CPG>(P, nblocks, s, false); return;
+    default: launch_mgemv_t<4, MG_PREFILL_NM, MG_PREFILL_CPG>(P, nblocks, s, false); return;
   }
 }
 

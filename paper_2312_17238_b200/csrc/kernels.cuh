@@ -239,9 +239,12 @@ void launch_gemv(int bits, const GLaunch& P, int nblocks, cudaStream_t s, bool p
 // batched prefill (tensor-core layout only): jobs with `cols`, MG_PREFILL_COLS
 // input columns per CTA
 #ifndef MG_PREFILL_NM
-#define MG_PREFILL_NM 2
+#define MG_PREFILL_NM 1
 #endif
-#define MG_PREFILL_COLS (2 * MG_PREFILL_NM)
+#ifndef MG_PREFILL_CPG
+#define MG_PREFILL_CPG 2
+#endif
+#define MG_PREFILL_COLS (MG_PREFILL_CPG * MG_PREFILL_NM)
 void launch_gemv_cols(int bits, const GLaunch& P, int nblocks, cudaStream_t s);
 int gemv_smem_bytes(int bits, int xs_rows, int zs_cap, int xin_cap, int rb_full, int* nstages,
                     int* stage_bytes);

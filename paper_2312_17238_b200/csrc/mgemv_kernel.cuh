@@ -33,8 +33,10 @@
 
 __host__ __device__ constexpr size_t mg_a16(size_t v) { return (v + 15) & ~(size_t)15; }
 __host__ __device__ constexpr size_t mg_a128(size_t v) { return (v + 127) & ~(size_t)127; }
-__host__ __device__ constexpr int mg_cols(int nm) { return nm == 1 ? 1 : 2 * nm; }
-__host__ __device__ constexpr int mg_tab_bytes(int nm) { return nm == 1 ? mt::BTAB : 2 * mt::BTAB; }
+// NM MMA column groups per k-step, CPG input columns per group (1: the digits
+// fill columns 0..3 of the n8 tile, 2: two inputs' digits fill all 8)
+__host__ __device__ constexpr int mg_cols(int nm, int cpg) { return nm * cpg; }
+__host__ __device__ constexpr int mg_tab_bytes(int cpg) { return cpg * mt::BTAB; }
 
 // dynamic shared memory carve-up (host and device agree on it)
 //   header (barriers, reduction scratch), then per input column: xs [rows]
@@ -43,15 +45,15 @@ __host__ __device__ constexpr int mg_tab_bytes(int nm) { return nm == 1 ? mt::BT
 //   the B tables of one stage [warp][UPS][NM][table], then the ring
 struct MgSmem {
   size_t xs, xz, zsm, xin, scl, wtab, ring;
-  __host__ __device__ MgSmem(int xs_cap, int zs_cap, int xin_cap, int nm = 1) {
-    const int nc = mg_cols(nm);
+  __host__ __device__ MgSmem(int xs_cap, int zs_cap, int xin_cap, int nm = 1, int cpg = 1) {
+    const int nc = mg_cols(nm, cpg);
     xs = 1024;
     xz = xs + (size_t)nc * xs_cap * 4;
     zsm = xz + (size_t)nc * xs_cap * 4;
     xin = mg_a16(zsm + (size_t)zs_cap * 4);
     scl = mg_a16(xin + (size_t)nc * xin_cap);
     wtab = scl + (size_t)xs_cap * 16;
-    ring = mg_a128(wtab + (size_t)MG_WARPS * 4 * nm * mg_tab_bytes(nm));
+    ring = mg_a128(wtab + (size_t)MG_WARPS * 4 * nm * mg_tab_bytes(cpg));
   }
 };
 
@@ -73,14 +75,14 @@ MOE_DEV void load_scales(float (&sc)[8], const __half* p, int nsc) {
   for (int k = 0; k < 8; ++k) sc[k] = k < nsc ? __half2float(p[k]) : 0.f;
 }
 
-template <int B, int NM>
-__global__ void __launch_bounds__(MG_THREADS, NM == 1 ? 2 : 1)
+template <int B, int NM, int CPG>
+__global__ void __launch_bounds__(MG_THREADS, NM * CPG <= 2 ? 2 : 1)
     k_mgemv(const __grid_constant__ GLaunch P, int xs_cap, int zs_cap, int xin_cap, int nst,
             int stage_bytes) {
   constexpr int W = MG_WARPS, NT = MG_THREADS, UPS = mma_units(B);
-  constexpr int NC = mg_cols(NM), CPG = NM == 1 ? 1 : 2, TB = mg_tab_bytes(NM);
+  constexpr int NC = mg_cols(NM, CPG), TB = mg_tab_bytes(CPG);
   extern __shared__ __align__(128) uint8_t smem[];
-  const MgSmem L(xs_cap, zs_cap, xin_cap, NM);
+  const MgSmem L(xs_cap, zs_cap, xin_cap, NM, CPG);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
   uint64_t* zbar = reinterpret_cast<uint64_t*>(smem + 128);
