@@ -918,6 +918,9 @@ __device__ __noinline__ void attend_head(const float* q, const float* kcur, cons
     auto ld = [&](int t) { return t == pos ? vp : __ldcg(vcol + (size_t)t * rstride); };
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     int t = half;
+    // (unrolled so the loads of several groups are in flight; the FMA order,
+    // hence the rounding, is the loop's)
+#pragma unroll 4
     for (; t + 6 < T; t += 8) {
       const float v0 = ld(t), v1 = ld(t + 2), v2 = ld(t + 4), v3 = ld(t + 6);
       a0 = fmaf(sc[t], v0, a0);
@@ -925,6 +928,7 @@ __device__ __noinline__ void attend_head(const float* q, const float* kcur, cons
       a2 = fmaf(sc[t + 4], v2, a2);
       a3 = fmaf(sc[t + 6], v3, a3);
     }
+#pragma unroll 4
     for (; t < T; t += 2) a0 = fmaf(sc[t], ld(t), a0);
     hb[half * nd + j] = (a0 + a1) + (a2 + a3);
   }
