@@ -159,13 +159,17 @@ __global__ void __launch_bounds__(MG_THREADS, NM * CPG <= 2 ? 2 : 1)
     prefetch_kv(P.att_kc + (size_t)ahead * P.att_hd, P.att_vc + (size_t)ahead * P.att_hd, M.K,
                 P.att_ds->pos, P.att_hd);
 
-  int ebuf = 0;
+  int ebuf = 0, eready = 1;
+  uint32_t egen = 0;
   if (expert) {
     // the route is written by the previous kernel (tail).  (Reading it before
     // this wait, even when the previous kernel triggers its dependents only
     // after its own wait on the tail, was measured to see stale routes.)
     gemv::pdl_wait();
+    // one L2 round trip for the whole route entry (buffer, ready, generation)
     ebuf = __ldcg(route->buf + J.rel_slot);
+    eready = __ldcg(route->ready + J.rel_slot);
+    egen = __ldcg(route->gen + J.rel_slot);
     if (ebuf < 0) {  // expert parallel: another rank owns this expert
       float* zdst = J.reduce == 2 ? nullptr
                     : J.reduce == 1 ? (s == 0 ? J.out : nullptr)
@@ -200,8 +204,7 @@ __global__ void __launch_bounds__(MG_THREADS, NM * CPG <= 2 ? 2 : 1)
     const __half2* zmeta = M.zmeta;
     const __half* scl = M.scl;
     if (expert) {
-      if (!__ldcg(route->ready + J.rel_slot))
-        wait_flag(P.flags + ebuf, __ldcg(route->gen + J.rel_slot), P.err, P.wait_ns);
+      if (!eready) wait_flag(P.flags + ebuf, egen, P.err, P.wait_ns);
       const uint8_t* b = P.pool + (long long)ebuf * P.slot_stride;
       base = b + reinterpret_cast<size_t>(base);
       zmeta = reinterpret_cast<const __half2*>(b + reinterpret_cast<size_t>(zmeta));
