@@ -567,7 +567,7 @@ def main():
     ap.add_argument("--k", type=int, default=None, help="sweep: override the LRU cache size")
     ap.add_argument("--m", type=int, default=None, help="sweep: override the prefetch depth")
     args = ap.parse_args()
-    if os.environ.get("CUDA_INJECTION64_PATH"):
+    if os.environ.get("CUDA_INJECTION64_PATH") or os.environ.get("NV_COMPUTE_PROFILER_PERFWORKS_DIR"):
         # under ncu / compute-sanitizer the numbers are not bench values: keep the
         # run short (no host reference sample, no five-prompt pass, no e2e pass)
         args.no_cpu_baseline = args.no_prompts = args.no_e2e = True
