@@ -222,7 +222,11 @@ __global__ void __launch_bounds__(MG_THREADS, NM * CPG <= 2 ? 2 : 1)
       gemv::bulk_g2s(zsm, reinterpret_cast<const void*>(za - lead), zbytes, zbar);
       src = base + cb_offset(M, cb) + (int64_t)qs * rb;
       pol = gemv::policy_evict_first();
-      for (int it = 0; it < min(nst, nit); ++it) issue(it);  // dense: before the wait
+      // dense: the weight stream starts before the wait (x is the previous
+      // kernel's output); expert: x is ready, so its copies go first and the
+      // prologue does not wait behind the first weight stages
+      if (!expert)
+        for (int it = 0; it < min(nst, nit); ++it) issue(it);
     }
     if (!expert) gemv::pdl_wait();  // x is the previous kernel's output
     if (xstage) {
@@ -240,6 +244,8 @@ __global__ void __launch_bounds__(MG_THREADS, NM * CPG <= 2 ? 2 : 1)
         }
       }
     }
+    if (expert && nrows > 0)
+      for (int it = 0; it < min(nst, nit); ++it) issue(it);
   }
   if (!expert) gemv::pdl_wait();
   tl_begin(P.site);  // (after the wait: the span excludes the previous kernel)
