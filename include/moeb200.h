@@ -274,6 +274,10 @@ int64_t moe_store_sim_copies(moe_store_sim* s);
 int moe_store_sim_copy_policy(moe_store_sim* s, int64_t job_bytes, int64_t chunk_bytes,
                               int32_t progress);
 int64_t moe_store_sim_chunks(moe_store_sim* s);
+/* speculative jobs parked so far (their target layer had passed), and the
+ * parking switch of the simulated copy engine (engine: MOE_COPY_PARK) */
+int64_t moe_store_sim_parked(moe_store_sim* s);
+int moe_store_sim_set_park(moe_store_sim* s, int32_t on);
 const char* moe_store_sim_last_error(void);
 int moe_store_sim_destroy(moe_store_sim* s);
 

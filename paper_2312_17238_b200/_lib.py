@@ -112,6 +112,8 @@ SIGNATURES = {
     "moe_store_sim_copies": (I64, [P]),
     "moe_store_sim_copy_policy": (I32, [P, I64, I64, I32]),
     "moe_store_sim_chunks": (I64, [P]),
+    "moe_store_sim_parked": (I64, [P]),
+    "moe_store_sim_set_park": (I32, [P, I32]),
     "moe_store_sim_last_error": (C.c_char_p, []),
     "moe_store_sim_destroy": (I32, [P]),
 }

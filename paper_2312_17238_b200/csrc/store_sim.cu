@@ -235,6 +235,14 @@ int moe_store_sim_copy_policy(moe_store_sim* s, int64_t job_bytes, int64_t chunk
 
 int64_t moe_store_sim_chunks(moe_store_sim* s) { return s ? s->chunks : 0; }
 
+int64_t moe_store_sim_parked(moe_store_sim* s) { return s ? s->sched.n_parked : 0; }
+
+int moe_store_sim_set_park(moe_store_sim* s, int32_t on) {
+  if (!s) return sfail(MOE_ERR_VALUE, "null simulator");
+  s->sched.park = on != 0;
+  return MOE_OK;
+}
+
 const char* moe_store_sim_last_error(void) { return s_err.c_str(); }
 
 int moe_store_sim_destroy(moe_store_sim* s) {

@@ -207,3 +207,40 @@ def test_trace_replay_through_device_store_equals_reference_replay():
     live = replay(tr, CacheConfig(k=2, b=4, expert_bytes=eng.store.config.expert_bytes),
                   SpeculationConfig(True, 2)).events
     assert live == eng.events
+
+
+@pytest.mark.parametrize("k,b,m", [(1, 2, 1), (2, 4, 2), (0, 4, 2)])
+def test_copy_engine_parks_passed_speculation(k, b, m):
+    """copy_sched.h parking: with no copy progress between bookkeeping calls,
+    speculative jobs whose target layer the decode has passed are parked
+    (not copied further) -- every routed buffer is still published with the
+    right contents (a staging hit promotes a parked job), the event log still
+    equals the reference store's, and no more chunks are copied than without
+    parking."""
+    from paper_2312_17238_b200 import _lib
+    L, E, T = 4, 8, 30
+    chunks = {}
+    for park in (1, 0):
+        rng = np.random.default_rng(7 * k + b + m)
+        sim = DeviceStoreSim(L, E, CacheConfig(k, b, 4096), top_k=2, m=m)
+        lib = _lib.lib()
+        assert lib.moe_store_sim_copy_policy(sim._h, 4096, 1024, 0) == 0
+        assert lib.moe_store_sim_set_park(sim._h, park) == 0
+        ref = ExpertStore(L, E, OCache(k, b, 4096))
+        for pos in range(T):
+            for l in range(L):
+                ex = [int(x) for x in rng.choice(E, 2, replace=False)]
+                g = [int(x) for x in rng.choice(E, m, replace=False)]
+                gl = l + 1 if l + 1 < L else -1
+                bufs = sim.resolve_token(l, pos, ex, g if gl >= 0 else [], gl)
+                for e in ex:
+                    ref.acquire(l, e, pos)
+                if gl >= 0:
+                    ref.speculative_load([(gl, x) for x in g], pos, current_layer=l)
+                content = sim.buffers()["content"]
+                for e, bf in zip(ex, bufs):
+                    assert content[bf] == l * E + e
+        assert rows(sim.events) == orows(ref.events)
+        chunks[park] = (lib.moe_store_sim_chunks(sim._h), lib.moe_store_sim_parked(sim._h))
+    assert chunks[1][1] > 0 and chunks[0][1] == 0
+    assert chunks[1][0] <= chunks[0][0]
