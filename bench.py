@@ -194,7 +194,7 @@ def build_engine(args, rank, world):
                             expert_bytes=expert_bytes(cfg, xb), **kw)
         host = (model, attn, experts)
     if world > 1:
-        connect(eng)
+        connect(eng, transport=args.ep_transport)
     return eng, host, (k, b, m)
 
 
@@ -277,7 +277,10 @@ def timeline_of(eng, prompt, world, nl):
 def kernel_event_times(eng, prompt, kp):
     """Per-kernel CUDA-event timing pass: events around every launch of the
     decode token on the compute stream (this disables PDL overlap, so the
-    per-launch durations include launch latency)."""
+    per-launch durations include the kernel's own launch latency).  Before each
+    start event the engine parks the stream on a short k_hold, so the host has
+    enqueued "event, kernel, event" by the time the stream reaches the start
+    event: no host-side gap is counted in a kernel's span."""
     import ctypes as C
 
     from paper_2312_17238_b200 import _lib
@@ -296,6 +299,7 @@ def run_b200(args, rank, world):
     import ctypes as C
 
     from paper_2312_17238_b200 import _lib
+    from paper_2312_17238_b200.expert_parallel import transport_of
     cfg = dict(MIXTRAL)
     ab, xb, k, m = CONFIGS[args.config]
     V, nl = cfg["vocab_size"], cfg["n_layers"]
@@ -399,7 +403,9 @@ def run_b200(args, rank, world):
                 "algorithmic_bytes_per_launch": up_bytes,
                 "avg_launch_us": round(avg_ms[2] * 1e3, 2), "peak_kind": peak_kind,
                 "timing": f"CUDA events around each launch on the compute stream over a "
-                          f"{kp}-token pass ({prof_ms_step:.3f} ms/token with events)",
+                          f"{kp}-token pass, the stream held 40 us before each start event so "
+                          f"no host launch gap falls inside a span ({prof_ms_step:.3f} "
+                          f"ms/token with events and holds)",
                 "others_gbs": {"expert_down": gbs(dn_bytes, 3) and round(gbs(dn_bytes, 3), 1),
                                "attn_qkv": gbs(3 * attn_block, 0) and round(gbs(3 * attn_block, 0), 1),
                                "lm_head": gbs(cfg["d_model"] * V * 2, 4)
@@ -463,7 +469,8 @@ def run_b200(args, rank, world):
                        f"ep{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (5.9 GB of weights read per token)",
                    "expert_bytes": expert_bytes(cfg, xb), "weights": args.weights,
-                   "rank_budget": {"k": kr, "b": br, "m": mr}},
+                   "rank_budget": {"k": kr, "b": br, "m": mr},
+                   "ep_transport": transport_of(args.ep_transport) if world > 1 else None},
         "hit_rate": win["hit_rate"], "hit_rate_device_only": win["hit_rate_device_only"],
         "h2d_gbs": round(h2d_gbs, 2) if h2d_gbs else None,
         "miss_loads_per_token": win["miss_loads"] / args.steps,
@@ -560,6 +567,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=list(CONFIGS))
     ap.add_argument("--weights", default="reference", choices=["reference", "hash"])
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--ep-transport", default=None, choices=["ipc", "nccl"],
+                    help="expert-parallel slot exchange (N > 1): peer-memory k_exchange "
+                         "(default) or ncclAllGather; MOE_EP_TRANSPORT sets the default")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-prompts", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -195,6 +195,19 @@ int moe_ep_configure(moe_engine* eng, int32_t rank, int32_t world);
 int moe_ep_handle(moe_engine* eng, void* out64);
 int moe_ep_connect(moe_engine* eng, const void* handles);
 
+/* Expert parallel over NCCL instead of peer memory (north_star: "hidden states
+ * exchanged by NCCL all-to-all over NVLink").  Rank 0 calls
+ * moe_nccl_unique_id, the 128-byte id reaches every rank out of band
+ * (torch.distributed broadcast), and every rank calls moe_ep_connect_nccl
+ * after finalize and before its first decode.  The per-layer slot exchange is
+ * then one ncclAllGather of the (top_k x d) slot buffers on the compute stream
+ * (captured in the decode graph), summed in rank order by the combine: the
+ * same exact sum as the peer-memory exchange.  NCCL is resolved at run time
+ * (libnccl.so.2).  world = 1 is allowed (a one-rank all-gather), which is how
+ * the transport is tested on one GPU. */
+int moe_nccl_unique_id(void* out128);
+int moe_ep_connect_nccl(moe_engine* eng, const void* id128);
+
 /* Profiling: when on, every GEMV launch is bracketed by CUDA events on the
  * compute stream; moe_kernel_times returns summed milliseconds and launch
  * counts per class [qkv, wo, expert_up, expert_down, lm_head] (5 entries). */

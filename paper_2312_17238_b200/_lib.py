@@ -91,6 +91,8 @@ SIGNATURES = {
     "moe_ep_configure": (I32, [P, I32, I32]),
     "moe_ep_handle": (I32, [P, C.c_void_p]),
     "moe_ep_connect": (I32, [P, C.c_void_p]),
+    "moe_nccl_unique_id": (I32, [C.c_void_p]),
+    "moe_ep_connect_nccl": (I32, [P, C.c_void_p]),
     "moe_set_profiling": (I32, [P, I32]),
     "moe_kernel_times": (I32, [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "moe_profiler_range": (I32, [I32]),

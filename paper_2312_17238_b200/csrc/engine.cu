@@ -7,6 +7,9 @@
 // marks each buffer ready with cuStreamWriteValue32 (kernels wait on it).
 #include <cuda.h>
 #include <cuda_profiler_api.h>
+#include <nvtx3/nvToolsExt.h>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <atomic>
 #include <chrono>
 #include <algorithm>
@@ -22,6 +25,48 @@
 
 #include "copy_sched.h"
 #include "kernels.cuh"
+
+namespace {
+// NCCL, resolved at run time (the process's libnccl.so.2: torch's bundled one
+// when torch is loaded) so the library has no link-time NCCL dependency; only
+// the expert-parallel NCCL transport (moe_ep_connect_nccl) uses it.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) unique_id = nullptr;
+  decltype(&ncclCommInitRank) init_rank = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  std::string why;
+};
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      a.why = std::string("libnccl.so.2 not loadable: ") + (e ? e : "?");
+      return a;
+    }
+    a.unique_id = reinterpret_cast<decltype(a.unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!a.unique_id || !a.init_rank || !a.all_gather || !a.destroy || !a.error_string)
+      a.why = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+// NVTX range over one C-ABI call (header-only nvtx3: a no-op unless a tool
+// such as nsys / ncu --nvtx injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -324,6 +369,11 @@ struct moe_engine {
   unsigned long long* peer_flag[MOE_EP_MAX] = {};
   std::vector<void*> ipc_opened;
   bool ep_connected = false;
+  // NCCL transport (moe_ep_connect_nccl): one ncclAllGather of the slot
+  // buffers per layer and position on the compute stream (graph-captured)
+  bool ep_nccl = false;
+  ncclComm_t nccl_comm = nullptr;
+  float* nrecv = nullptr;  // [N][topk][d] all-gather output (rank-major)
   size_t arena_off(int l, int x) const { return (size_t)arena_idx[(size_t)l * E + x] * xbytes; }
   bool owns(int l, int x) const { return arena_idx[(size_t)l * E + x] >= 0; }
   std::vector<bool> loaded;
@@ -409,6 +459,7 @@ struct moe_engine {
   // per-class GEMV timing with CUDA events on the compute stream (profiling)
   enum { K_QKV = 0, K_WO, K_UP, K_DOWN, K_LM, K_N };
   bool prof = false;
+  unsigned long long prof_hold_ns = 40000;
   std::vector<cudaEvent_t> pev;  // pairs
   std::vector<int> pcls;
   size_t pused = 0;
@@ -423,6 +474,7 @@ struct moe_engine {
       for (size_t i = old; i < pev.size(); ++i) cudaEventCreate(&pev[i]);
     }
     pcls[pused / 2] = c;
+    launch_hold(prof_hold_ns, s_comp);  // stream busy while the host enqueues the span
     cudaEventRecord(pev[pused], s_comp);
   }
   void prof_end(int) {
@@ -516,6 +568,8 @@ moe_engine::~moe_engine() {
   for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
   if (owned_dev) cudaFree(owned_dev);
   if (xch) cudaFree(xch);
+  if (nccl_comm) nccl_api().destroy(nccl_comm);
+  if (nrecv) cudaFree(nrecv);
   if (mb_host) cudaFreeHost(mb_host);
   if (t0) cudaEventDestroy(t0);
   if (t1) cudaEventDestroy(t1);
@@ -605,6 +659,7 @@ int moe_engine::run_copier() {
       f.bytes = (int64_t)c.bytes;
       f.buf = c.buf;
       cudaEventRecord(f.a, st);
+      nvtxMarkA(c.last ? "copy chunk (last)" : "copy chunk");
       cudaMemcpyAsync(dst, src, c.bytes, cudaMemcpyHostToDevice, st);
       cudaEventRecord(f.b, st);
       last_ev[c.buf] = f.b;
@@ -839,7 +894,7 @@ int moe_engine::enq_experts(int l, int p) {
     J.out = dn_out + (size_t)j * d;
     // single GPU: fixed-point split-K sums read (and reset) by the combine;
     // expert parallel: reduced in-kernel, the exchange ships dn_out
-    J.reduce = ep_world > 1 ? 1 : 2;
+    J.reduce = (ep_world > 1 || ep_nccl) ? 1 : 2;
     J.acc = dn_acc + (size_t)j * d;
     J.QPS = Q_dn;
     J.S = S_dn;
@@ -884,7 +939,15 @@ int moe_engine::enq_experts(int l, int p) {
   c.part = dn_out;
   c.S = 1;
   c.acc = dn.j[0].reduce == 2 ? dn_acc : nullptr;
-  if (ep_world > 1) {  // sum-exchange of the slot buffers over peer memory
+  if (ep_nccl) {  // NCCL transport: all-gather of the slot buffers (rank-major)
+    const ncclResult_t r = nccl_api().all_gather(dn_out, nrecv, (size_t)topk * d, ncclFloat32,
+                                                 nccl_comm, s_comp);
+    if (r != ncclSuccess) return fail(MOE_ERR_CUDA, std::string("ncclAllGather: ") +
+                                                        nccl_api().error_string(r));
+    c.part = nrecv;
+    c.S = ep_world;
+    c.rank_major = 1;
+  } else if (ep_world > 1) {  // sum-exchange of the slot buffers over peer memory
     ExchangeParams xp{};
     xp.src = dn_out;
     for (int r = 0; r < ep_world; ++r) {
@@ -916,7 +979,7 @@ int moe_engine::enq_experts(int l, int p) {
     c.ln_b = l + 1 < L ? ln1b[l + 1] : lnfb;
     c.xn = xn;
   }
-  if (cur_ds && ep_world == 1 && c.acc && l + 1 < L) {
+  if (cur_ds && ep_world == 1 && !ep_nccl && c.acc && l + 1 < L) {
     pend_comb = true;  // QKV(l+1) forms the residual and LN1 itself
   } else {
     launch_combine(c, s_comp, pdl && !prof);
@@ -937,7 +1000,7 @@ int moe_engine::enq_experts(int l, int p) {
 // exactly like the decode kernel computes it (same split geometry and
 // fixed-point sums), so prefill equals teacher-forced decode bit for bit.
 bool moe_engine::batched_prefill_ok(int n) const {
-  if (ep_world > 1 || !xl_set) return false;
+  if (ep_world > 1 || ep_nccl || !xl_set) return false;
   int min_n = 4;  // shorter prompts: the per-position path is faster (profiles/r2_prefill.md)
   if (const char* v = getenv("MOE_PREFILL_BATCH")) {
     if (atoi(v) == 0) return false;
@@ -1845,7 +1908,7 @@ int moe_finalize(moe_engine* e) {
 static int check_ready(moe_engine* e, bool need_peers = false) {
   if (!e) return fail(MOE_ERR_VALUE, "null engine");
   if (!e->finalized) return fail(MOE_ERR_RUNTIME, "engine not finalized (weights not loaded)");
-  if (need_peers && e->ep_world > 1 && !e->ep_connected)
+  if (need_peers && e->ep_world > 1 && !e->ep_connected && !e->ep_nccl)
     return fail(MOE_ERR_RUNTIME, "expert parallel engine not connected to its peers");
   cudaSetDevice(e->dev);
   return MOE_OK;
@@ -1860,6 +1923,7 @@ int moe_reset_session(moe_engine* e) {
 }
 
 int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_out) {
+  NvtxRange nvtx("moe_prefill");
   int rc = check_ready(e, true);
   if (rc) return rc;
   e->pos = 0;  // reset_session (engine.py:149): KV and trace, not the store
@@ -1921,6 +1985,7 @@ int moe_prefill(moe_engine* e, const int32_t* tokens, int32_t n, float* logits_o
 }
 
 int moe_step(moe_engine* e, int32_t token, float* logits_out) {
+  NvtxRange nvtx("moe_step");
   int rc = check_ready(e, true);
   if (rc) return rc;
   if (token < 0 || token >= e->V)
@@ -1947,6 +2012,7 @@ int moe_step(moe_engine* e, int32_t token, float* logits_out) {
 }
 
 int moe_decode_greedy(moe_engine* e, int32_t n, int32_t* tokens_out, float* final_logits_out) {
+  NvtxRange nvtx("moe_decode_greedy");
   int rc = check_ready(e, true);
   if (rc) return rc;
   if (n < 1) return fail(MOE_ERR_VALUE, "n_tokens must be >= 1");
@@ -2166,6 +2232,41 @@ int moe_ep_connect(moe_engine* e, const void* handles) {
     e->peer_flag[r] = reinterpret_cast<unsigned long long*>(base + recv_bytes);
   }
   e->ep_connected = true;
+  return MOE_OK;
+}
+
+int moe_nccl_unique_id(void* out128) {
+  if (!out128) return fail(MOE_ERR_VALUE, "null argument");
+  const NcclApi& n = nccl_api();
+  if (!n.why.empty()) return fail(MOE_ERR_RUNTIME, n.why);
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  const ncclResult_t r = n.unique_id(&id);
+  if (r != ncclSuccess) return fail(MOE_ERR_CUDA, std::string("ncclGetUniqueId: ") + n.error_string(r));
+  memcpy(out128, &id, sizeof(id));
+  return MOE_OK;
+}
+
+int moe_ep_connect_nccl(moe_engine* e, const void* id128) {
+  if (!e || !id128) return fail(MOE_ERR_VALUE, "null argument");
+  if (!e->finalized) return fail(MOE_ERR_RUNTIME, "engine not finalized (weights not loaded)");
+  if (e->ep_connected || e->ep_nccl) return fail(MOE_ERR_RUNTIME, "expert parallel already connected");
+  if (e->gexec) return fail(MOE_ERR_RUNTIME, "connect before the first decode");
+  const NcclApi& n = nccl_api();
+  if (!n.why.empty()) return fail(MOE_ERR_RUNTIME, n.why);
+  cudaSetDevice(e->dev);
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  const ncclResult_t r = n.init_rank(&e->nccl_comm, e->ep_world, id, e->ep_rank);
+  if (r != ncclSuccess) {
+    e->nccl_comm = nullptr;
+    return fail(MOE_ERR_CUDA, std::string("ncclCommInitRank: ") + n.error_string(r));
+  }
+  const size_t bytes = (size_t)e->ep_world * e->topk * e->d * sizeof(float);
+  CU(cudaMalloc(&e->nrecv, bytes));
+  CU(cudaMemset(e->nrecv, 0, bytes));
+  e->dev_bytes += bytes;
+  e->ep_nccl = true;
   return MOE_OK;
 }
 

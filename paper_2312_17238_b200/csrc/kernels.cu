@@ -653,6 +653,15 @@ __global__ void k_wait_ready(const RouteRec* route, int n, const uint32_t* flags
   }
 }
 
+// Event-timing pass only: one thread idles the compute stream for `ns` so the
+// host has enqueued "start event, kernel, end event" before the stream reaches
+// the start event.  Without it the GPU drains the stream between host launches
+// and every event-timed span includes the host's launch gap.
+__global__ void k_hold(unsigned long long ns) {
+  const unsigned long long t0 = globaltimer();
+  while (globaltimer() - t0 < ns) __nanosleep(1000);
+}
+
 // Block-wide fp32 sum in a fixed order (per-thread, warp tree, warp 0 over
 // the warp sums): deterministic.  `red` needs 33 floats.
 MOE_DEV float block_sum_f(float v, float* red) {
@@ -1508,7 +1517,9 @@ __global__ void __launch_bounds__(1024) k_combine(CombineParams P) {
           y = fx_val(__ldcg(acc + (size_t)j * P.d + i));
           acc[(size_t)j * P.d + i] = 0ull;
         } else
-          for (int s = 0; s < P.S; ++s) y += __ldcg(part + ((size_t)j * P.S + s) * P.d + i);
+          for (int s = 0; s < P.S; ++s)
+            y += __ldcg(part + (P.rank_major ? (size_t)s * P.top_k + j : (size_t)j * P.S + s) *
+                                   P.d + i);
         out = __fadd_rn(out, __fmul_rn(w[j], y));  // model.py:251-254, reference order
       }
       outp[i] = out;
@@ -1944,6 +1955,11 @@ void launch_begin_call(StoreDev st, cudaStream_t s) { k_begin_call<<<1, 32, 0, s
 void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int* err,
                        unsigned long long wait_ns, cudaStream_t s) {
   k_wait_ready<<<1, 32, 0, s>>>(route, n, flags, err, wait_ns);
+  g_launches.fetch_add(1);
+}
+
+void launch_hold(unsigned long long ns, cudaStream_t s) {
+  k_hold<<<1, 1, 0, s>>>(ns);
   g_launches.fetch_add(1);
 }
 

@@ -169,6 +169,9 @@ struct CombineParams {
   // the half in use is picked by the exchange counter's parity
   const unsigned long long* ep_seq;
   long long ep_slab;
+  // expert parallel over NCCL: `part` is the all-gather output [S=N][top_k][d]
+  // (rank-major); summed in rank order like the peer-memory layout
+  int rank_major;
   // optional fused LayerNorm of `out` (next layer's LN1, or LN_f after the
   // last layer): one CTA, xn = LN(out)
   const float* ln_g;
@@ -270,6 +273,7 @@ void launch_exchange(const ExchangeParams& P, cudaStream_t s, bool pdl = false);
 void launch_wait_ready(const RouteRec* route, int n, const uint32_t* flags, int* err,
                        unsigned long long wait_ns, cudaStream_t s);
 void launch_logits(const LogitsParams& P, cudaStream_t s, bool pdl = false);
+void launch_hold(unsigned long long ns, cudaStream_t s);  // event-timing pass only
 void launch_begin_call(StoreDev st, cudaStream_t s);
 cudaError_t preload_kernels();
 long long launch_count();  // kernels launched (or captured) by this process

@@ -308,6 +308,14 @@ class OffloadEngine:
             raise ValueError("need one 64-byte handle per rank")
         check(lib().moe_ep_connect(self._h, C.c_char_p(blob)))
 
+    def ep_connect_nccl(self, unique_id: bytes) -> None:
+        """NCCL transport: join the communicator named by rank 0's 128-byte
+        ``nccl_unique_id()``; the slot exchange becomes one ncclAllGather per
+        layer and position (include/moeb200.h)."""
+        if len(unique_id) != 128:
+            raise ValueError("an NCCL unique id is 128 bytes")
+        check(lib().moe_ep_connect_nccl(self._h, C.c_char_p(unique_id)))
+
     def close(self):
         if self._h is not None:
             lib().moe_destroy(self._h)

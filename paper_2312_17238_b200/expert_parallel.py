@@ -53,7 +53,8 @@ def rank_budget(k: int, b: int, m: int, n_experts: int, rank: int, world: int):
 def slot_exchange(slots_local: np.ndarray, all_reduce) -> np.ndarray:
     """Sum-exchange of the (top_k, d) slot buffer; ``all_reduce`` is the
     collective (gloo in the CPU tests).  The GPU engine does the same exchange
-    inside its decode graph with k_exchange over peer memory (CUDA IPC)."""
+    inside its decode graph: k_exchange over peer memory (CUDA IPC), or one
+    ncclAllGather whose rank-major output the combine sums in rank order."""
     out = np.ascontiguousarray(slots_local, np.float32).copy()
     all_reduce(out)
     return out
@@ -67,10 +68,64 @@ def combine(h: np.ndarray, weights, slots: np.ndarray) -> np.ndarray:
     return out
 
 
-def connect(engine, group=None) -> None:
-    """Exchange the engines' IPC handles over torch.distributed and connect
-    every rank's engine to its peers (all ranks call this collectively)."""
+TRANSPORTS = ("ipc", "nccl")
+
+
+def transport_of(transport=None) -> str:
+    """The slot-exchange transport: ``ipc`` (default: k_exchange, peer-memory
+    stores and flags inside the decode graph) or ``nccl`` (one ncclAllGather
+    per layer and position); ``MOE_EP_TRANSPORT`` overrides the default."""
+    import os
+    t = (transport or os.environ.get("MOE_EP_TRANSPORT") or "ipc").lower()
+    if t not in TRANSPORTS:
+        raise ValueError(f"unknown expert-parallel transport {t!r} (one of {TRANSPORTS})")
+    return t
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (rank 0 makes it, every rank joins)."""
+    import ctypes as C
+
+    from ._lib import check, lib
+    buf = C.create_string_buffer(128)
+    check(lib().moe_nccl_unique_id(buf))
+    return buf.raw
+
+
+def share_nccl_id(group=None) -> bytes:
+    """Rank 0's NCCL unique id on every rank of ``group`` (torch.distributed
+    broadcast: the process group only carries the 128 bytes)."""
     import torch.distributed as dist
+    box = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                               group=group)
+    return box[0]
+
+
+def gather_combine(h: np.ndarray, weights, gathered: np.ndarray) -> np.ndarray:
+    """The NCCL transport's combine: ``gathered`` is the all-gather output
+    [N][top_k][d] (rank-major); slot j's contributions are summed in rank
+    order, then the reference-ordered mixture (k_combine, rank_major)."""
+    g = np.asarray(gathered, np.float32)
+    slots = g[0].copy()
+    for r in range(1, g.shape[0]):
+        slots = slots + g[r]
+    return combine(h, weights, slots)
+
+
+def connect(engine, group=None, transport=None) -> str:
+    """Connect every rank's engine to its peers over torch.distributed (all
+    ranks call this collectively); returns the transport used.
+
+    ``ipc``: all-gather the engines' CUDA IPC handles and open them.
+    ``nccl``: rank 0's NCCL unique id is broadcast and every rank joins the
+    communicator (the torch process group only carries the id)."""
+    import torch.distributed as dist
+    t = transport_of(transport)
+    if t == "nccl":
+        engine.ep_connect_nccl(share_nccl_id(group))
+        return t
     handles = [None] * dist.get_world_size(group)
     dist.all_gather_object(handles, engine.ep_handle(), group=group)
     engine.ep_connect(handles)
+    return t

@@ -131,3 +131,46 @@ def test_ep_world2_matches_reference():
                     if keys:
                         st.speculative_load(keys, t, current_layer=l)
         assert ev == st.events, f"rank {rank}"
+
+
+@pytest.mark.timeout(300)
+def test_nccl_transport_world1_matches_reference():
+    """The NCCL transport (moe_ep_connect_nccl: one ncclAllGather per layer and
+    position, captured in the decode graph, rank-major combine) on a one-rank
+    communicator -- the only NCCL shape one GPU can run.  Tokens equal the
+    reference golden, the event log equals the single-GPU engine's, logits
+    within the parity tolerance."""
+    import json
+
+    from oracle import engine as OE
+    from oracle import model as OM
+    from paper_2312_17238_b200 import CacheConfig, ExpertKey, OffloadEngine, SpeculationConfig
+    from paper_2312_17238_b200.expert_parallel import nccl_unique_id
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "tests", "golden", "engine_cases.json")) as fh:
+        meta = json.load(fh)
+    cfg = OM.ModelConfig(**meta["config"])
+    name, qb, k, b, m, ntok = next(c for c in meta["cases"] if c[0] == CASE)
+    fq, pay, attn = OE.build_mixed_quant(OM.init_params(cfg), cfg, *qb)
+    data = np.load(os.path.join(root, "tests", "golden", "engine_golden.npz"))
+    prompt = [int(t) for t in data["prompt"]]
+    out = []
+    for nccl in (False, True):
+        eng = OffloadEngine(OM.Model(cfg, fq), CacheConfig(k, b),
+                            SpeculationConfig(enabled=m > 0, m=max(m, 1)),
+                            payloads={ExpertKey(*kk): v for kk, v in pay.items()},
+                            record_hidden=False, attn_blocks=attn, device=0)
+        if nccl:
+            eng.ep_connect_nccl(nccl_unique_id())
+        eng.prefill(prompt)
+        res = eng.decode(ntok)
+        ev = [(e.seq, e.kind, e.key.layer, e.key.expert, e.token_pos, e.bytes_moved)
+              for e in eng.events]
+        out.append((res.tokens, res.final_logits, ev))
+        eng.close()
+    gold = [int(t) for t in data[f"{CASE}/tokens"]]
+    ref = data[f"{CASE}/final_logits"].astype(np.float64)
+    (t0, l0, e0), (t1, l1, e1) = out
+    assert t0 == gold and t1 == gold
+    assert e1 == e0
+    assert np.abs(l1 - ref).max() <= 2e-3 * np.abs(ref).max() + 1e-4
