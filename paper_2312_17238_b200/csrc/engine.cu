@@ -100,8 +100,8 @@ struct DevMat {  // one tiled matrix in device memory
 // split the quad range of every job so one launch is ~2 CTAs per SM
 // (MOE_GEMV_THREADS threads, ~100 KB smem each); QPS is a multiple of the
 // pipeline stage so every bulk copy stays 16-byte aligned
-int plan_qps(int total_cb, int nquads, int qs, bool mma = false) {
-  const int waves = MOE_GEMV_MINB;  // CTAs per SM: one resident wave
+int plan_qps(int total_cb, int nquads, int qs, bool mma = false, int nwaves = 1) {
+  const int waves = MOE_GEMV_MINB * nwaves;  // CTAs per SM x resident waves
   // splits need not be whole pipeline stages (the last stage of a split is
   // partial), so S is the largest split count that fits the resident wave:
   // every SM gets the same number of CTAs whenever total_cb * S == target
@@ -1782,15 +1782,20 @@ int moe_finalize(moe_engine* e) {
   if ((rc = e->dalloc(&e->logits, (size_t)T * V))) return rc;
   // split planning in storage units (MatDev.nqp: quads, or k-steps for the
   // tensor-core layout) over column blocks (MatDev.ncb)
-  auto plan = [](int njobs, const MatDev& M, int* Q, int* S) {
-    *Q = plan_qps(njobs * M.ncb, M.nqp, gemv_qs(M.bits), M.mma != 0);
+  // MOE_MG_WAVES="qkv,wo,up,down": resident waves per launch (experiment;
+  // default one wave each)
+  int waves_of[4] = {1, 1, 1, 1};
+  if (const char* w = getenv("MOE_MG_WAVES"))
+    sscanf(w, "%d,%d,%d,%d", &waves_of[0], &waves_of[1], &waves_of[2], &waves_of[3]);
+  auto plan = [](int njobs, const MatDev& M, int* Q, int* S, int nw = 1) {
+    *Q = plan_qps(njobs * M.ncb, M.nqp, gemv_qs(M.bits), M.mma != 0, std::max(nw, 1));
     *S = (M.nqp + *Q - 1) / *Q;
   };
   const MatDev xm0 = matdev_from(e->xl[0], nullptr), xm2 = matdev_from(e->xl[2], nullptr);
-  plan(3, e->wq[0].M, &e->Q_qkv, &e->S_qkv);
-  plan(1, e->wo[0].M, &e->Q_wo, &e->S_wo);
-  plan(2 * e->topk, xm0, &e->Q_up, &e->S_up);
-  plan(e->topk, xm2, &e->Q_dn, &e->S_dn);
+  plan(3, e->wq[0].M, &e->Q_qkv, &e->S_qkv, waves_of[0]);
+  plan(1, e->wo[0].M, &e->Q_wo, &e->S_wo, waves_of[1]);
+  plan(2 * e->topk, xm0, &e->Q_up, &e->S_up, waves_of[2]);
+  plan(e->topk, xm2, &e->Q_dn, &e->S_dn, waves_of[3]);
   plan(1, e->lm_head.M, &e->Q_lm, &e->S_lm);
   if ((rc = e->dalloc(&e->qkv_part, (size_t)3 * e->S_qkv * d))) return rc;
   if ((rc = e->dalloc(&e->wo_part, (size_t)e->S_wo * d))) return rc;
