@@ -190,7 +190,9 @@ int moe_measure_h2d(moe_engine* eng, int32_t reps, double* best_gbs, double* med
  * cache and store, store.py restricted to the owned keys).  After finalize,
  * exchange every rank's 64-byte handle (moe_ep_handle) and moe_ep_connect
  * with all of them, in rank order: the per-layer slot exchange then runs
- * over peer memory (NVLink P2P / CUDA IPC) inside the decode graph. */
+ * over peer memory (NVLink P2P / CUDA IPC) inside the decode graph, fused
+ * into the down-projection GEMV (each completed column block is stored into
+ * every rank's receive buffer and counted there). */
 int moe_ep_configure(moe_engine* eng, int32_t rank, int32_t world);
 int moe_ep_handle(moe_engine* eng, void* out64);
 int moe_ep_connect(moe_engine* eng, const void* handles);

@@ -930,6 +930,19 @@ int moe_engine::enq_experts(int l, int p) {
   launch_gemv(expert_bits, u, nu, s_comp, pdl && !prof);
   prof_end(K_UP);
   dbg("up", -1, p);
+  // expert parallel over peer memory: the exchange is fused into the down
+  // GEMV (tensor-core layout; the CUDA-core layout keeps k_exchange)
+  const bool epx = ep_world > 1 && !ep_nccl && dn.j[0].M.mma != 0;
+  if (epx) {
+    dn.ep_n = ep_world;
+    dn.ep_rank = ep_rank;
+    dn.ep_topk = topk;
+    dn.ep_seq = xseq;
+    for (int r = 0; r < ep_world; ++r) {
+      dn.ep_recv[r] = peer_recv[r];
+      dn.ep_flag[r] = peer_flag[r];
+    }
+  }
   prof_begin(K_DOWN);
   launch_gemv(expert_bits, dn, ndn, s_comp, pdl && !prof);
   prof_end(K_DOWN);
@@ -947,6 +960,16 @@ int moe_engine::enq_experts(int l, int p) {
     c.part = nrecv;
     c.S = ep_world;
     c.rank_major = 1;
+  } else if (epx) {  // the down GEMV stored the slots into every rank's receive buffer
+    c.part = xrecv;
+    c.S = ep_world;
+    c.ep_seq = xseq;
+    c.ep_seq_w = xseq;
+    c.ep_flags = xflag;
+    c.ep_ncbt = (long long)topk * dn.j[0].M.ncb;
+    c.ep_slab = (long long)topk * ep_world * d;
+    c.err = err;
+    c.wait_ns = wait_ns;
   } else if (ep_world > 1) {  // sum-exchange of the slot buffers over peer memory
     ExchangeParams xp{};
     xp.src = dn_out;

@@ -1477,6 +1477,15 @@ MOE_DEV void combine_fast(const CombineParams& P, const float* part, const float
 }
 
 // out = h + w0*y0 + w1*y1 in descending-weight order (model.py:251-254)
+MOE_DEV unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+MOE_DEV void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(1024) k_combine(CombineParams P) {
   __shared__ float red[33];
   extern __shared__ float osh[];  // out [d], then LN gamma / beta [d] each
@@ -1491,7 +1500,28 @@ __global__ void __launch_bounds__(1024) k_combine(CombineParams P) {
   gemv::pdl_wait();
   tl_begin(P.site);
   const float* part = P.part;
-  if (P.ep_seq) part += (size_t)(*P.ep_seq & 1ull) * P.ep_slab;
+  if (P.ep_flags) {  // fused exchange: wait for every rank's column blocks of this exchange
+    __shared__ unsigned long long sq_sh;
+    if (threadIdx.x == 0) {
+      const unsigned long long sq = __ldcg(P.ep_seq) + 1ull;
+      const unsigned long long want = sq * (unsigned long long)P.ep_ncbt;
+      const unsigned long long t0 = globaltimer();
+      for (int r = 0; r < P.S; ++r)
+        while (ld_acquire_sys_u64(P.ep_flags + r) < want) {
+          __nanosleep(64);
+          if (globaltimer() - t0 > P.wait_ns) {
+            atomicOr(P.err, MOE_ERRF_TIMEOUT);
+            break;
+          }
+        }
+      sq_sh = sq;
+    }
+    __syncthreads();
+    part += (size_t)(sq_sh & 1ull) * P.ep_slab;
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) *P.ep_seq_w = sq_sh;
+  } else if (P.ep_seq) {
+    part += (size_t)(*P.ep_seq & 1ull) * P.ep_slab;
+  }
   // batched prefill: grid.y = positions (h, acc, route, out advance per row)
   const int row = blockIdx.y;
   const float* hin = P.h + (size_t)row * P.d;
@@ -1537,15 +1567,6 @@ __global__ void __launch_bounds__(1024) k_combine(CombineParams P) {
   }
   tl_mark(P.site, 2);
   tl_end(P.site);
-}
-
-MOE_DEV unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-MOE_DEV void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __global__ void __launch_bounds__(1024) k_exchange(ExchangeParams P) {
@@ -1970,6 +1991,8 @@ void launch_combine(const CombineParams& P, cudaStream_t s, bool pdl, int rows) 
   }
   if (P.xn)
     launch_small(k_combine, dim3(1), dim3(1024), (size_t)P.d * 12, s, pdl, P);
+  else if (P.ep_flags)  // fused exchange: one CTA reads and then advances the counter
+    launch_small(k_combine, dim3(1), dim3(1024), 0, s, pdl, P);
   else
     launch_small(k_combine, dim3((P.d + 255) / 256), dim3(256), 0, s, pdl, P);
 }

@@ -11,6 +11,7 @@
 __host__ __device__ constexpr int gemv_qpw(int bits) { return bits <= 4 ? 2 : 1; }
 __host__ __device__ constexpr int gemv_qs(int bits) { return MOE_GEMV_WARPS * gemv_qpw(bits); }
 #define MOE_GEMV_MAXJOBS 8
+#define MOE_EP_MAX 8
 #define MOE_GEMV_MINB 2            // CTAs per SM the kernel is register-limited for
 #define MOE_GEMV_RING (80 * 1024)  // bytes of stage ring per CTA (2 CTAs / SM)
 #define MOE_XS_MAX 4096            // rows of x kept in smem per CTA
@@ -94,6 +95,16 @@ struct GLaunch {
   float* att_vc;
   const DecodeState* att_ds;
   int att_pos, att_hd, att_T;
+  // expert parallel, exchange fused into the down GEMV (reduce == 1 jobs,
+  // ep_n > 1): the CTA that completes a column block of slot j stores those
+  // outputs straight into every rank's receive buffer [2][top_k][N][d] at
+  // (j, ep_rank) over peer memory, then bumps that rank's arrival counter
+  // ep_flag[r][ep_rank] (system scope).  ep_seq: exchanges completed so far
+  // (advanced by the combine that consumes this one).
+  float* ep_recv[MOE_EP_MAX];
+  unsigned long long* ep_flag[MOE_EP_MAX];
+  const unsigned long long* ep_seq;
+  int ep_rank, ep_n, ep_topk;
 };
 
 // Split-K by fixed-point atomics (GJob.reduce == 2): each CTA adds its fp32
@@ -169,6 +180,13 @@ struct CombineParams {
   // the half in use is picked by the exchange counter's parity
   const unsigned long long* ep_seq;
   long long ep_slab;
+  // fused exchange (GLaunch.ep_*): wait until every rank's arrival counter
+  // ep_flags[r] reaches (exchange number) x ep_ncbt, then advance *ep_seq_w
+  const unsigned long long* ep_flags;
+  unsigned long long* ep_seq_w;
+  long long ep_ncbt;
+  int* err;
+  unsigned long long wait_ns;
   // expert parallel over NCCL: `part` is the all-gather output [S=N][top_k][d]
   // (rank-major); summed in rank order like the peer-memory layout
   int rank_major;
@@ -188,7 +206,6 @@ struct CombineParams {
 // memory (NVLink P2P / CUDA IPC), then raises its flag on every rank and
 // waits for all flags.  Receive buffers are double-buffered by the exchange
 // sequence number (a rank can be at most one exchange ahead of any other).
-#define MOE_EP_MAX 8
 struct ExchangeParams {
   const float* src;                      // [top_k][d]
   float* recv[MOE_EP_MAX];               // per rank: its receive buffer [2][top_k][N][d]

@@ -75,6 +75,25 @@ MOE_DEV void load_scales(float (&sc)[8], const __half* p, int nsc) {
   for (int k = 0; k < 8; ++k) sc[k] = k < nsc ? __half2float(p[k]) : 0.f;
 }
 
+// Expert parallel, exchange fused into the down GEMV (GLaunch.ep_*): the
+// receive-buffer row of (slot, this rank) in rank r's buffer, for the
+// exchange now in flight (double-buffered by its parity)
+MOE_DEV float* ep_dst(const GLaunch& P, int r, int slot, int d) {
+  const unsigned long long sq = __ldcg(P.ep_seq) + 1ull;
+  const size_t slab = (size_t)P.ep_topk * P.ep_n * d;
+  return P.ep_recv[r] + (size_t)(sq & 1ull) * slab + ((size_t)slot * P.ep_n + P.ep_rank) * d;
+}
+// every thread's peer stores of this column block are issued: make them
+// visible system-wide, then count the block on every rank (one per block)
+MOE_DEV void ep_arrive(const GLaunch& P) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int r = 0; r < P.ep_n; ++r) atomicAdd_system(P.ep_flag[r] + P.ep_rank, 1ull);
+  }
+}
+
 template <int B, int NM, int CPG>
 __global__ void __launch_bounds__(MG_THREADS, NM * CPG <= 2 ? 2 : 1)
     k_mgemv(const __grid_constant__ GLaunch P, int xs_cap, int zs_cap, int xin_cap, int nst,
@@ -176,6 +195,13 @@ __global__ void __launch_bounds__(MG_THREADS, NM * CPG <= 2 ? 2 : 1)
                                     : J.part + (size_t)s * M.N;
       if (zdst)
         for (int t = threadIdx.x; t < nout; t += NT) zdst[obase + t] = 0.f;
+      if (P.ep_n > 1 && J.reduce == 1 && s == 0) {  // fused exchange: this slot is zero here
+        for (int r = 0; r < P.ep_n; ++r) {
+          float* dst = ep_dst(P, r, J.rel_slot, M.N) + obase;
+          for (int t = threadIdx.x; t < nout; t += NT) dst[t] = 0.f;
+        }
+        ep_arrive(P);
+      }
       if (P.zero) {  // this CTA's slice of the consumed sums (see below)
         const int per = (P.zero_n + gridDim.x - 1) / gridDim.x;
         const int a = blockIdx.x * per, e = min(P.zero_n, a + per);
@@ -527,7 +553,16 @@ __global__ void __launch_bounds__(MG_THREADS, NM * CPG <= 2 ? 2 : 1)
     tl_end(P.site);
     return;
   }
+  const bool epx = P.ep_n > 1 && expert;  // fused exchange (reduce == 1 here)
   if (J.S == 1) {
+    if (epx) {  // single split: this CTA completes its column block
+      __syncthreads();
+      for (int r = 0; r < P.ep_n; ++r) {
+        float* dst = ep_dst(P, r, J.rel_slot, M.N) + obase;
+        for (int t = threadIdx.x; t < nout; t += NT) dst[t] = J.out[obase + t];
+      }
+      ep_arrive(P);
+    }
     cta_mark(2);
     tl_end(P.site);
     return;
@@ -564,9 +599,15 @@ __global__ void __launch_bounds__(MG_THREADS, NM * CPG <= 2 ? 2 : 1)
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (t0 + u * NT < nout) J.out[obase + t0 + u * NT] = a[u];
+        if (t0 + u * NT < nout) {
+          J.out[obase + t0 + u * NT] = a[u];
+          if (epx)  // fused exchange: straight into every rank's receive buffer
+            for (int r = 0; r < P.ep_n; ++r)
+              ep_dst(P, r, J.rel_slot, M.N)[obase + t0 + u * NT] = a[u];
+        }
     }
     if (threadIdx.x == 0) P.cnt[cnt_base + cb] = 0;
+    if (epx) ep_arrive(P);
   }
   cta_mark(2);
   tl_end(P.site);
