@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, q):
+def _rank(rank, world, port, q, case=CASE):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -42,12 +42,15 @@ def _rank(rank, world, port, q):
         with open(os.path.join(root, "tests", "golden", "engine_cases.json")) as fh:
             meta = json.load(fh)
         cfg = OM.ModelConfig(**meta["config"])
-        name, qb, k, b, m, ntok = next(c for c in meta["cases"] if c[0] == CASE)
-        fq, pay, attn = OE.build_mixed_quant(OM.init_params(cfg), cfg, *qb)
+        name, qb, k, b, m, ntok = next(c for c in meta["cases"] if c[0] == case)
+        if qb:
+            fq, pay, attn = OE.build_mixed_quant(OM.init_params(cfg), cfg, *qb)
+            pay = {ExpertKey(*kk): v for kk, v in pay.items()}
+        else:  # fp32 experts: CUDA-core GEMV layout, exchange by k_exchange
+            fq, pay, attn = OM.init_params(cfg), None, None
         eng = OffloadEngine(OM.Model(cfg, fq), CacheConfig(k, b),
                             SpeculationConfig(enabled=m > 0, m=max(m, 1)),
-                            payloads={ExpertKey(*kk): v for kk, v in pay.items()},
-                            record_hidden=True, attn_blocks=attn, device=0,
+                            payloads=pay, record_hidden=True, attn_blocks=attn, device=0,
                             ep_rank=rank, ep_world=world)
         connect(eng)
         data = np.load(os.path.join(root, "tests", "golden", "engine_golden.npz"))
@@ -66,7 +69,10 @@ def _rank(rank, world, port, q):
 
 
 @pytest.mark.timeout(600)
-def test_ep_world2_matches_reference():
+@pytest.mark.parametrize("case", [CASE, "fp32_k2_m2"])
+def test_ep_world2_matches_reference(case):
+    """mq42 (tensor-core layout): the exchange fused into the down GEMV;
+    fp32 experts (CUDA-core layout): the separate k_exchange kernel."""
     import torch.multiprocessing as mp
 
     from oracle import engine as OE
@@ -76,7 +82,7 @@ def test_ep_world2_matches_reference():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q, case)) for r in range(2)]
     for p in procs:
         p.start()
     outs = sorted([q.get(timeout=540) for _ in procs], key=lambda o: o[0])
@@ -90,11 +96,11 @@ def test_ep_world2_matches_reference():
     with open(os.path.join(root, "tests", "golden", "engine_cases.json")) as fh:
         meta = json.load(fh)
     cfg = OM.ModelConfig(**meta["config"])
-    name, qb, k, b, m, ntok = next(c for c in meta["cases"] if c[0] == CASE)
-    gold = [int(t) for t in data[f"{CASE}/tokens"]]
+    name, qb, k, b, m, ntok = next(c for c in meta["cases"] if c[0] == case)
+    gold = [int(t) for t in data[f"{case}/tokens"]]
     for rank, toks, logits, ev, recs, _ in outs:
         assert toks == gold
-        ref = data[f"{CASE}/final_logits"].astype(np.float64)
+        ref = data[f"{case}/final_logits"].astype(np.float64)
         assert np.abs(logits - ref).max() <= 2e-3 * np.abs(ref).max() + 1e-4
     # both ranks saw identical routing and hidden states (replicated dense path)
     r0, r1 = outs[0][4], outs[1][4]
@@ -102,9 +108,13 @@ def test_ep_world2_matches_reference():
     # each rank's events == oracle store on its keys, driven by that routing
     L, E = cfg.n_layers, cfg.n_experts
     plen = len(data["prompt"])
-    fq, pay, _ = OE.build_mixed_quant(OM.init_params(cfg), cfg, *qb)
+    if qb:
+        fq, pay, _ = OE.build_mixed_quant(OM.init_params(cfg), cfg, *qb)
+        ebytes = OE.payload_bytes(pay[(0, 0)])
+    else:
+        fq = OM.init_params(cfg)
+        ebytes = OE.payload_bytes(OM.Model(cfg, fq).expert(0, 0))
     gates = [fq[f"layers.{l}.gate"] for l in range(L)]
-    ebytes = OE.payload_bytes(pay[(0, 0)])
     for rank, toks, logits, ev, recs, _ in outs:
         own = owned_keys(L, E, rank, 2)
         st = ExpertStore(L, E, CacheConfig(k, b, ebytes), owned=own)
