@@ -18,7 +18,9 @@ engine's compute stream around K device-greedy decode steps (inputs resident:
 weights in the pinned arena / HBM cache, L2 irrelevant -- 5.9 GB read per
 token); ``e2e`` = the same through the public API with a host sampler (per
 step: H2D token, D2H logits); ``prompts`` = tokens/s, hit rate and prefill time
-for the five §8(d) prompts, 32 tokens each, on the same engine.
+for the five §8(d) prompts, 32 tokens each, on the same engine;
+``secondary`` (C2 at N=1) = the metric's k=2 half, C3 (2-bit experts, k=2,
+prefetch m=2), measured by this script in a fresh process.
 
 ``--impl reference``: the unmodified reference ``moe_offload.OffloadEngine`` on
 the host cores, same weights, same prompt, same metric (oracle/refarm.py; no
@@ -574,13 +576,15 @@ def main():
     ap.add_argument("--no-prompts", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="C2 at N=1: skip the C3 (k=2) line measured in a fresh process")
     ap.add_argument("--k", type=int, default=None, help="sweep: override the LRU cache size")
     ap.add_argument("--m", type=int, default=None, help="sweep: override the prefetch depth")
     args = ap.parse_args()
     if os.environ.get("CUDA_INJECTION64_PATH") or os.environ.get("NV_COMPUTE_PROFILER_PERFWORKS_DIR"):
         # under ncu / compute-sanitizer the numbers are not bench values: keep the
         # run short (no host reference sample, no five-prompt pass, no e2e pass)
-        args.no_cpu_baseline = args.no_prompts = args.no_e2e = True
+        args.no_cpu_baseline = args.no_prompts = args.no_e2e = args.no_secondary = True
     if args.k is not None or args.m is not None:  # C5 sweep point derived from --config
         ab, xb, k, m = CONFIGS[args.config]
         k = k if args.k is None else args.k
@@ -632,8 +636,34 @@ def main():
             "sample": f"{args.cpu_steps} greedy tokens through all 32 layers of the unmodified "
                       f"moe_offload.OffloadEngine on the same weights after a 1-token prefill "
                       f"(materialize = C dequantize, bit-identical; build {t_build:.0f}s untimed)"}
+    if rank == 0 and world == 1 and args.config == "c2" and not args.no_secondary:
+        line["secondary"] = run_secondary(args)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def run_secondary(args):
+    """The metric's k=2 half (C3: 2-bit experts, k=2, prefetch m=2), measured by
+    the same bench code in a fresh process (its own engine and HBM), so the
+    default run reports both cache sizes the metric names."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--config", "c3", "--steps",
+           str(args.steps), "--warmup", str(args.warmup), "--weights", args.weights,
+           "--no-cpu-baseline", "--no-prompts", "--no-secondary"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        got = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if r.returncode != 0 or not got:
+            return {"error": f"rc={r.returncode}: {r.stderr.strip()[-300:]}"}
+        d = json.loads(got[-1])
+    except Exception as ex:  # reported, never fatal for the headline line
+        return {"error": repr(ex)[:300]}
+    keys = ("value", "unit", "ms_per_step", "steps", "warmup", "hit_rate", "h2d_gbs",
+            "miss_loads_per_token", "spec_loads_per_token", "clocks", "gpu_launches")
+    out = {"config": d["config"]}
+    out.update({k: d.get(k) for k in keys})
+    out["e2e"] = d.get("e2e")
+    out["roofline_e2e"] = d.get("roofline_e2e")
+    return out
 
 
 if __name__ == "__main__":
