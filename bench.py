@@ -612,6 +612,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo")
     line, host = run_b200(args, rank, world)
+    if world == 1:
+        line["gpus_active"] = 1
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -622,6 +624,14 @@ def main():
         # throughput is that sequence's tokens/s on the slowest rank's clock
         line["value"] = round(1e3 / line["ms_per_step"], 3)
         line["scaling"] = "weak"
+        # distinct physical GPUs behind the ranks (MOE_BENCH_DEVICE test runs share one)
+        try:
+            uid = str(torch.cuda.get_device_properties(args.device).uuid)
+        except Exception:
+            uid = f"device{args.device}"
+        uids = [None] * world
+        dist.all_gather_object(uids, uid)
+        line["gpus_active"] = len(set(uids))
         if line.get("e2e"):
             e = torch.tensor([line["e2e"]["value"]], dtype=torch.float64)
             dist.all_reduce(e, op=dist.ReduceOp.MIN)
